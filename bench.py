@@ -1,0 +1,317 @@
+#!/usr/bin/env python
+"""Benchmark of the two-level IGA iteration (Algorithm 1) on B200.
+
+Workload (BASELINE.json configs[1], "C2"): 2D Poisson on the unit square, uniform knots,
+maximally smooth B-splines of degree p in {3, 4, 5} on 256x256 elements, fp64, b = (f, φ_i) with
+f = 2π² sin(πx) sin(πy), x0 ~ U[-1,1] seed 0, second level q = 1 on H = 2h approximated by one
+V(1,1) cycle, Schwarz block 3x3 (p = 3, 4) / 5x5 (p = 5).  One bench STEP = one two-level
+iteration of each of the three problems (the three p of the config), inputs resident in HBM.
+
+metric value = DOF-iterations per second over the whole job = Σ_p N_p / step time (x n_gpus).
+L2 is flushed (a 256 MiB write) before every timed step; the flush is outside the event pair.
+
+--impl reference runs the CPU oracle (oracle/, the parity reference) as the reference arm.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "two-level iterations/s and DOF/s per p; HBM roofline fraction; conv. factor"
+UNIT = "DOF*it/s"
+WORKLOAD = "C2: 2D Poisson, p in {3,4,5}, 256x256 elements, q=1 V(1,1) at H=2h, fp64"
+PS = (3, 4, 5)
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # SMs x FP64 FMA/clk/SM x 2 x max SM clock
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms while the timed region runs."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                f = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(f) == 6:
+                    self.rows.append(f)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_ctx(pkg, torch, p, stream):
+    s = 3 if p <= 4 else 5
+    return pkg.Context(2, p, 1, 256, s, coarse_mode=pkg.COARSE_VCYCLE, coarse_h_factor=2, stream=stream)
+
+
+def cpu_baseline_sample(p=3, colours_timed=2):
+    """The oracle, as it stands, on a bounded sample of the workload: full-size C2 (p=3), the
+    first `colours_timed` of the D^2 Schwarz colours timed and scaled to the whole sweep, plus the
+    complete defect / restriction / V(1,1) / prolongation; setup (assembly, factorisations of the
+    timed blocks) excluded.  Returns (DOF*it/s, seconds of CPU work, description)."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle.schwarz import colour_of
+    from oracle.twolevel import TwoLevel
+    from oracle.assembly import load_sine
+    from synthetic_inputs import initial_guess
+    t_all = time.perf_counter()
+    tl = TwoLevel(2, p, 1, 256, s=3, coarse="vcycle", h_factor=2, order="multicolour")
+    D = tl.s + p
+    b = load_sine(p, 256, 2)
+    x = initial_guess(tl.N)
+    sel = [c for c in tl.smoother.seq if colour_of(c, D) < colours_timed]
+    for c in sel:                                   # factorisations = setup (not timed)
+        tl.smoother._factor(c)
+    t0 = time.perf_counter()
+    tl.smoother.sweep(x, b, sel)
+    t_sw = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    dq = tl.R @ (b - tl.A @ x)
+    e = tl._csolve(dq)
+    x += tl.RT @ e
+    t_rest = time.perf_counter() - t0
+    t_iter = t_sw * (D * D) / colours_timed + t_rest
+    desc = (f"oracle (NumPy/SciPy, 1 thread) on full-size C2 p={p}: {colours_timed}/{D*D} Schwarz colours timed "
+            f"and scaled x{D*D/colours_timed:.0f}, plus full defect+restriction+V(1,1)+prolongation; "
+            f"setup excluded; {time.perf_counter() - t_all:.1f} s wall incl. setup")
+    return tl.N / t_iter, t_iter, desc
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    vals = []
+    for _ in range(args.warmup if args.warmup < 1 else 0):
+        pass
+    t_cpu = 0.0
+    desc = ""
+    for k in range(max(args.steps, 1)):
+        v, t, desc = cpu_baseline_sample()
+        vals.append(v)
+        t_cpu += t
+    value = float(np.median(vals))
+    ms = float(1e3 * 66049 / value)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD + " (reference arm: oracle, p=3 sample)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2009_01499_b200 as pkg
+    from synthetic_inputs import initial_guess
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+
+    ctxs, bs, xs, Ns = [], [], [], []
+    for p in PS:
+        c = make_ctx(pkg, torch, p, sh)
+        b = torch.empty(c.N, dtype=torch.float64, device=dev)
+        c.rhs_sine(b)                                          # b = (f, φ_i) computed on the GPU
+        x = torch.tensor(initial_guess(c.N), device=dev)
+        ctxs.append(c); bs.append(b); xs.append(x); Ns.append(c.N)
+    x0s = [x.clone() for x in xs]
+    info = [c.info() for c in ctxs]
+
+    def step():
+        for c, b, x in zip(ctxs, bs, xs):
+            c.iterate(b, x, 1)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_wall = time.perf_counter()
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            evs[k][0].record(stream)
+            step()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms_per_step = float(tot.item()) / args.steps
+    value = world * sum(Ns) / (ms_per_step / 1e3)
+
+    # per-p iteration rate (same protocol, each problem alone)
+    per_p = {}
+    for p, c, b, x in zip(PS, ctxs, bs, xs):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(args.steps, 5)
+        ms = 0.0
+        for _ in range(reps):
+            flush.fill_(1.0)
+            e0.record(stream)
+            c.iterate(b, x, 1)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
+        ms /= reps
+        per_p[f"p{p}"] = {"N": c.N, "it_per_s": 1e3 / ms, "dof_per_s": c.N * 1e3 / ms, "ms_per_iter": ms}
+
+    # dominant kernel: the Schwarz colour kernel (all D^2 launches of one sweep), timed live
+    sw_ms_tot, sw_flops_tot, sw_launches = 0.0, 0.0, 0
+    for c, b, x, inf in zip(ctxs, bs, xs, info):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(args.steps, 5)
+        ms = 0.0
+        for _ in range(reps):
+            flush.fill_(2.0)
+            e0.record(stream)
+            c.sweep(b, x)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
+        sw_ms_tot += ms / reps
+        sw_flops_tot += inf.sweep_flops
+        sw_launches += inf.colours
+    achieved = sw_flops_tot / (sw_ms_tot / 1e3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "schwarz_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "kernel": "k_schwarz (one launch per colour)",
+                "note": "FP64 FMA pipe; peak derived 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md); "
+                        f"achieved = SURVEY 8(d) sweep flops / CUDA-event sweep time over {sw_launches} launches"}
+
+    # convergence factor (b = 0, 20 iterations, last 10 ratios) and iterations to 1e-8
+    conv = {}
+    for p, c, b in zip(PS, ctxs, bs):
+        z = torch.zeros(c.N, dtype=torch.float64, device=dev)
+        x = torch.tensor(initial_guess(c.N), device=dev)
+        hist = np.zeros(21)
+        c.iterate(z, x, 20, hist)
+        rho = float(np.exp(np.mean(np.log(hist[11:] / hist[10:-1]))))
+        x = torch.tensor(initial_guess(c.N), device=dev)
+        its, rr, ok = c.solve(b, x, 1e-8, 100)
+        conv[f"p{p}"] = {"rho": rho, "its_to_1e-8": its}
+
+    # e2e: through the C-ABI with HOST (pinned) buffers: H2D of b and x, iteration, D2H of x
+    hb = [b.cpu().pin_memory() for b in bs]
+    hx = [x.cpu().pin_memory() for x in x0s]
+    h2d = sum(2 * 8 * n for n in Ns)
+    d2h = sum(8 * n for n in Ns)
+    for c, b_, x_ in zip(ctxs, hb, hx):
+        c.iterate(b_, x_, 1)
+    e2e_ms = 0.0
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for _ in range(args.steps):
+        flush.fill_(3.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for c, b_, x_ in zip(ctxs, hb, hx):
+            c.iterate(b_, x_, 1)                             # returns after the D2H copy completed
+        e2e_ms += (time.perf_counter() - t0) * 1e3
+    e2e_t = torch.tensor([e2e_ms / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = world * sum(Ns) / (float(e2e_t.item()) / 1e3)
+
+    launches = sum(i.launches_per_iter for i in info) * args.steps
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "global_batch": world * 3, "dofs": Ns,
+                       "l2": "flushed before every timed step (256 MiB write)",
+                       "parallelism": "replicas" if world > 1 else "single-gpu",
+                       "graph": "one CUDA graph per iteration"},
+            "per_p": per_p, "conv": conv, "roofline": roofline,
+            "clocks": clk.summary(), "gpu_launches": launches,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "wall_s_timed": t_wall}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, t, desc = cpu_baseline_sample()
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+                                "host_cores_available": len(os.sched_getaffinity(0))}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    for c in ctxs:
+        c.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

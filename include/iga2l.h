@@ -1,0 +1,158 @@
+/*
+ * iga2l — B200-native two-level solver for maximally smooth B-spline (IGA) Galerkin
+ * discretizations of the Poisson problem on the unit square / cube.
+ *
+ * This header is the C-ABI boundary of libiga2l.so.  It follows the paper's problem statement
+ * (arXiv 2009.01499, /root/reference/PAPER.md, cited P:<line>):
+ *   -Δu = f in Ω = (0,1)^d, u = 0 on ∂Ω; Galerkin system A_p u_p = b_p with
+ *   A_p = (a(φ_j, φ_i)), b_p = ((f, φ_i)); φ = tensor-product B-splines of degree p with
+ *   maximal smoothness C^{p-1} on a uniform open knot vector with m spans per axis, Dirichlet
+ *   functions removed: n1 = m + p - 2 unknowns per axis.
+ * and it runs the paper's Algorithm 1: one overlapping multiplicative Schwarz sweep,
+ * defect, L2-projection restriction to degree q (lumped mass), second-level solve
+ * (exact, or one V(1,1) h-multigrid cycle; optionally on H = 2h),
+ * prolongation.  Readings of the paper where it is silent are listed in DESIGN.md (A1..A26).
+ *
+ * Data layout of every vector (x, b, y): N = n1^d fp64 values, x-fastest:
+ *     index(i_0, i_1[, i_2]) = i_0 + n1 * (i_1 + n1 * i_2),   0 <= i_a < n1,
+ * constrained index i_a is the paper's basis function N_{i_a + 2}.
+ *
+ * Pointers.  Every vector argument may be a DEVICE pointer (cudaMalloc / PyTorch CUDA tensor on
+ * the context's device) or a HOST pointer (pageable or pinned).  Device pointers are used in place,
+ * stream-ordered on the context stream.  Host pointers are staged through context-owned device
+ * buffers (H2D before, D2H after for outputs) and the call returns after the D2H copy completed.
+ * The caller owns all vectors; the library never retains a caller pointer after a call returns.
+ * Device-pointer calls are asynchronous w.r.t. the host unless stated otherwise.
+ *
+ * Errors.  Every int-returning function returns an iga2l_status.  On a non-OK return
+ * iga2l_last_error() gives a thread-local one-line message naming the offending field / call.
+ * Calls never abort the process.  A context serves one stream at a time (not thread-safe).
+ */
+#ifndef IGA2L_H
+#define IGA2L_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct iga2l_ctx iga2l_ctx;
+
+typedef enum {
+  IGA2L_OK = 0,
+  IGA2L_EPARAM = 1,    /* invalid argument; message names the field                         */
+  IGA2L_ENUMERIC = 2,  /* NaN/Inf residual, or a non-SPD local/coarse matrix during setup   */
+  IGA2L_NOTCONV = 3,   /* iga2l_solve hit maxit; outputs are valid (non-fatal)  */
+  IGA2L_ECUDA = 4,     /* CUDA runtime error (no device, launch failure, ...)               */
+  IGA2L_ENCCL = 5,     /* NCCL error (multi-GPU)                                            */
+  IGA2L_ENOMEM = 6     /* device or host allocation failed                                  */
+} iga2l_status;
+
+typedef enum {
+  IGA2L_COARSE_EXACT = 0,  /* A_q e = d_q solved exactly (dense Cholesky inverse; Nc <= 4096)  */
+  IGA2L_COARSE_VCYCLE = 1  /* one V(1,1) h-multigrid cycle, zero initial guess     */
+} iga2l_coarse_mode;
+
+typedef struct {
+  int coarse_mode;       /* iga2l_coarse_mode; default VCYCLE                                    */
+  int coarse_h_factor;   /* 1: q-level on the same mesh h (Algorithm 1); 2: aggressive   */
+                         /*    H = 2h.  Default 2.                                       */
+  int vcycle_coarsest_m; /* V-cycle coarsens while m > this (must be >= 1); default 8    */
+  void *stream;          /* cudaStream_t for all work; NULL = the context creates its own       */
+  int use_graph;         /* 1 (default): iterations are replayed from a captured CUDA graph      */
+  int nranks, rank;      /* slab partition along the last axis; must be 1, 0 in this version    */
+  const void *nccl_id;   /* reserved for nranks > 1 (128-byte ncclUniqueId); must be NULL now   */
+} iga2l_opts;
+
+/* Fill *o with the defaults above. */
+void iga2l_default_opts(iga2l_opts *o);
+
+/*
+ * Build a context (host setup + upload), P:90-113 and P:186-220:
+ *   dim     2 or 3 (the paper is 2D; 3D is the tensor generalisation, reading A25)
+ *   p       fine degree, 1..8
+ *   q       second-level degree, 1 <= q <= min(p, 2) ("linear/quadratic")
+ *   n       m = number of uniform spans per axis (h = 1/m), n >= 1, n1 = n + p - 2 >= 1
+ *   block   Schwarz block side s in {1,3,5,7} (s^d unknowns per block; paper: 3 for p<=4,
+ *           5 for p=5,6, 7 for p=7,8), s <= n1
+ *   overlap must be s - 1 (maximal overlap: one block per grid point)
+ * Aggressive coarsening / V-cycle need m divisible by 2 as required; violations -> EPARAM.
+ * On success *out owns all device memory it allocated; free with iga2l_destroy.
+ */
+int iga2l_setup(int dim, int p, int q, int64_t n, int block, int overlap, iga2l_ctx **out);
+int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap,
+                   const iga2l_opts *opts, iga2l_ctx **out);
+
+/* Sizes: n_local = N (unknowns held by this rank), slab [z0, z1) along the last axis, n1. */
+int iga2l_sizes(const iga2l_ctx *ctx, int64_t *n_local, int64_t *z0, int64_t *z1, int64_t *n1);
+
+/* b_i = (f, φ_i) for f = d π² ∏ sin(π x_a) (exact solution u = ∏ sin(π x_a); P:397-405 for d=2),
+ * Gauss quadrature with p+3 points per span (reading A17).  b: N fp64 (output). */
+int iga2l_rhs_sine(iga2l_ctx *ctx, double *b);
+
+/* y = A_p x, matrix-free ((2p+1)^d-point operator).  x, y: N fp64, must not alias. */
+int iga2l_apply(iga2l_ctx *ctx, const double *x, double *y);
+
+/* *out = ||b - A_p x||_2 (reading A15).  Synchronises the context stream. */
+int iga2l_residual_norm(iga2l_ctx *ctx, const double *b, const double *x, double *out);
+
+/*
+ * `iters` two-level iterations of Algorithm 1 (ν1 = 1, ν2 = 0; reading A14) on x in place.
+ * Schwarz order: multicolour, colour(c) = Σ_a (c_a mod D) D^a, D = s + p, ascending (reading A4).
+ * res_hist: NULL, or a HOST array of iters+1 doubles receiving ||b - A x_k||_2 for k = 0..iters
+ * (then the call synchronises).  iters >= 0.
+ */
+int iga2l_iterate(iga2l_ctx *ctx, const double *b, double *x, int iters, double *res_hist);
+
+/*
+ * Iterate until ||b - A x_k|| <= rtol ||b - A x_0|| or maxit iterations.
+ * iters_out / relres_out (host, may be NULL) receive the count and ||r_k||/||r_0||.
+ * Returns IGA2L_NOTCONV (outputs valid) if maxit was reached, IGA2L_ENUMERIC on NaN/Inf.
+ */
+int iga2l_solve(iga2l_ctx *ctx, const double *b, double *x, double rtol, int maxit,
+                int *iters_out, double *relres_out);
+
+/* ---- single phases of Algorithm 1 (same layouts; used by parity tests and the bench) ---- */
+
+/* Schwarz colours [colour_begin, colour_end) of the multicolour sweep on x in place
+ * (0 <= begin <= end <= D^d).  One full sweep = [0, D^d). */
+int iga2l_sweep(iga2l_ctx *ctx, const double *b, double *x, int colour_begin, int colour_end);
+
+/* dq = I_p^q (b - A_p x): defect + restriction.  dq: Nc = n1c^d fp64. */
+int iga2l_defect_restrict(iga2l_ctx *ctx, const double *b, const double *x, double *dq);
+
+/* e = second-level solve of A_q e = dq (exact or one V(1,1), per opts).  dq, e: Nc fp64. */
+int iga2l_coarse_solve(iga2l_ctx *ctx, const double *dq, double *e);
+
+/* x += I_q^p e (prolongation = adjoint of the restriction). */
+int iga2l_prolong_add(iga2l_ctx *ctx, const double *e, double *x);
+
+/* ---- introspection ---- */
+typedef struct {
+  int64_t n1, N, n1c, Nc;       /* fine / second-level sizes                                    */
+  int colours;                  /* D^d                                                          */
+  int levels;                   /* second-level V-cycle depth (1 = direct)                      */
+  int launches_per_iter;        /* kernel launches in one iteration (graph nodes of ours)      */
+  double sweep_flops;           /* algorithmic FP64 flops of one sweep           */
+  double iter_hbm_bytes;        /* algorithmic HBM bytes of one iteration outside the sweep    */
+} iga2l_info;
+int iga2l_get_info(const iga2l_ctx *ctx, iga2l_info *out);
+
+/* Host-only helper (no GPU needed): the 1D constrained band tables of degree p on m spans as
+ * used by the device path: K[i*(2p+1) + t+p] = ∫ N_{i+2}' N_{i+2+t}', M likewise (0 outside).
+ * K, M: host arrays of (m+p-2)*(2p+1) doubles. */
+int iga2l_host_band_tables(int p, int64_t m, double *K, double *M);
+
+/* Host-only helper: 1D transfer operator used for the restriction, as a dense row-major
+ * (n1c x n1) host matrix (h_factor 1: D^{-1} M_c; 2: P_mesh^T D^{-1} M_c). */
+int iga2l_host_restriction_1d(int p, int q, int64_t m, int h_factor, double *R);
+
+int iga2l_destroy(iga2l_ctx *ctx);
+const char *iga2l_last_error(void);
+const char *iga2l_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IGA2L_H */

@@ -67,7 +67,9 @@ class Schwarz:
         self.order = order
         self.seq = ordered_centres(n1, d, s, p, order)
         self._fac = {}
-        self.cache = n1 ** d <= 70000     # per-block (rows, factor) cache; setup-like, not method
+        k = s ** d
+        # per-block (rows, factor) cache (setup-like, not part of the method), bounded in memory
+        self.cache = n1 ** d * k * min(2 * p + 1, n1) ** d <= 3e7
 
     def _factor(self, c):
         f = self._fac.get(c)

@@ -1,0 +1,616 @@
+// C-ABI of libiga2l (layer L2): context setup, the Algorithm 1 schedule, CUDA-graph replay.
+// Contract: include/iga2l.h.  Paper: arXiv 2009.01499 (P:<line> = /root/reference/PAPER.md).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/iga2l.h"
+#include "host_setup.h"
+#include "kernels.cuh"
+
+using namespace iga2l;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(call)                                                                            \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      return fail(e_ == cudaErrorMemoryAllocation ? IGA2L_ENOMEM : IGA2L_ECUDA,             \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                      \
+    }                                                                                       \
+  } while (0)
+
+struct DevBand {
+  Band1D b{};
+  int *lo = nullptr;
+  double *c = nullptr;
+};
+
+struct Level {
+  int64_t m = 0;
+  int n = 0;          // unknowns per axis
+  int64_t N = 0;      // n^d
+  double *K = nullptr, *M = nullptr;   // band tables [n][2q+1]
+  double *x = nullptr, *b = nullptr, *r = nullptr, *t1 = nullptr, *t2 = nullptr;
+  DevBand P, PT;      // to the next coarser level: P (n x n_c), PT (n_c x n)
+  double *inv = nullptr;               // dense inverse at the coarsest level
+};
+
+}  // namespace
+
+struct iga2l_ctx {
+  int dim = 2, p = 1, q = 1, s = 1, w = 0, D = 1, colours = 1;
+  int64_t m = 0, n1 = 0, N = 0;
+  iga2l_opts opts{};
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  double *K1 = nullptr, *M1 = nullptr, *V = nullptr, *lam = nullptr, *g1 = nullptr;
+  DevBand R, RT;
+  std::vector<Level> lev;
+  double *r = nullptr, *t1 = nullptr, *t2 = nullptr;   // fine scratch, N each
+  double *partial = nullptr, *norm = nullptr, *hist = nullptr;
+  int *hist_count = nullptr;
+  int npartial = 0, hist_cap = 0;
+  double *hb = nullptr, *hx = nullptr, *hy = nullptr;  // staging for host pointers (fine)
+  double *hcb = nullptr, *hcx = nullptr;                // staging for host pointers (coarse)
+  double *pinned = nullptr;
+  // graph cache: key (b, x, with_norm)
+  struct G {
+    const double *b = nullptr;
+    double *x = nullptr;
+    int norm = -1;
+    cudaGraphExec_t exec = nullptr;
+  } graphs[4];
+  int next_graph = 0;
+  int launch_counter = 0;
+  int launches_per_iter = 0;
+  std::vector<void *> allocs;
+};
+
+namespace {
+
+template <typename T>
+int dalloc(iga2l_ctx *c, T **ptr, size_t count) {
+  void *p = nullptr;
+  cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+  if (e != cudaSuccess) return fail(IGA2L_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  c->allocs.push_back(p);
+  *ptr = static_cast<T *>(p);
+  return IGA2L_OK;
+}
+
+template <typename T>
+int upload(iga2l_ctx *c, T **ptr, const std::vector<T> &v) {
+  int rc = dalloc(c, ptr, v.size());
+  if (rc) return rc;
+  CU(cudaMemcpy(*ptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return IGA2L_OK;
+}
+
+int upload_band(iga2l_ctx *c, DevBand &d, const BandOp &h) {
+  int rc = upload(c, &d.lo, h.lo);
+  if (!rc) rc = upload(c, &d.c, h.c);
+  d.b = Band1D{h.rows, h.cols, h.W, d.lo, d.c};
+  return rc;
+}
+
+int64_t ipow(int64_t a, int d) {
+  int64_t r = 1;
+  for (int i = 0; i < d; ++i) r *= a;
+  return r;
+}
+
+bool is_device_ptr(const void *p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ---- launch helpers (count our kernel launches) ----
+void L_apply(iga2l_ctx *c, const double *x, const double *b, double *y, double *partial, int mode) {
+  launch_apply(c->dim, c->p, c->n1, c->K1, c->M1, x, b, y, partial, mode, c->st, nullptr);
+  c->launch_counter++;
+}
+
+// Tensor-product transform out = (⊗_a B) in (all axes the same 1D band B), passes axis 0, 1, 2.
+// n_in per axis = B.cols, n_out = B.rows.  acc: add into out on the last pass.
+void L_tensor(iga2l_ctx *c, int dim, const Band1D &B, const double *in, double *out, double *t1, double *t2,
+              int acc) {
+  const double *src = in;
+  for (int a = 0; a < dim; ++a) {
+    const bool last = (a == dim - 1);
+    double *dst = last ? out : (a % 2 == 0 ? t1 : t2);
+    const int64_t inner = ipow(B.rows, a), outer = ipow(B.cols, dim - 1 - a);
+    launch_band_axis(src, dst, outer, B.cols, inner, B, last ? acc : 0, c->st);
+    c->launch_counter++;
+    src = dst;
+  }
+}
+
+void L_vcycle(iga2l_ctx *c, size_t l) {
+  Level &L = c->lev[l];
+  if (L.inv) {
+    launch_dense_mv(int(L.N), L.inv, L.b, L.x, c->st);
+    c->launch_counter++;
+    return;
+  }
+  const int ncol = int(ipow(c->q + 1, c->dim));
+  cudaMemsetAsync(L.x, 0, L.N * sizeof(double), c->st);   // zero initial guess (reading A13)
+  for (int col = 0; col < ncol; ++col) {                 // pre-smoothing: (q+1)^d-colour GS (A11)
+    launch_q_gs_colour(c->dim, c->q, L.n, L.K, L.M, L.b, L.x, col, c->st);
+    c->launch_counter++;
+  }
+  launch_q_residual(c->dim, c->q, L.n, L.K, L.M, L.b, L.x, L.r, c->st);
+  c->launch_counter++;
+  Level &C = c->lev[l + 1];
+  L_tensor(c, c->dim, L.PT.b, L.r, C.b, L.t1, L.t2, 0);   // restriction P^T (reading A8)
+  L_vcycle(c, l + 1);
+  L_tensor(c, c->dim, L.P.b, C.x, L.x, L.t1, L.t2, 1);    // x += P e
+  for (int col = 0; col < ncol; ++col) {                 // post-smoothing, same order
+    launch_q_gs_colour(c->dim, c->q, L.n, L.K, L.M, L.b, L.x, col, c->st);
+    c->launch_counter++;
+  }
+}
+
+void L_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
+  for (int col = c0; col < c1; ++col) {
+    launch_schwarz_colour(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st);
+    c->launch_counter++;
+  }
+}
+
+// One iteration of Algorithm 1, ν1 = 1, ν2 = 0.
+void L_iteration(iga2l_ctx *c, const double *b, double *x, bool with_norm) {
+  L_sweep(c, b, x, 0, c->colours);                           // u^1 = u^0 + S_p(b - A_p u^0)
+  L_apply(c, x, b, c->r, nullptr, 1);                        // d_p = b - A_p u^1
+  L_tensor(c, c->dim, c->R.b, c->r, c->lev[0].b, c->t1, c->t2, 0);   // d_q = I_p^q d_p
+  L_vcycle(c, 0);                                            // A_q e_q = d_q (exact or one V(1,1))
+  L_tensor(c, c->dim, c->RT.b, c->lev[0].x, x, c->t1, c->t2, 1);     // u^1 += I_q^p e_q
+  if (with_norm) {
+    L_apply(c, x, b, c->r, c->partial, 1);
+    launch_sum_partials(c->partial, c->npartial, c->norm, c->hist, c->hist_count, c->hist_cap, c->st);
+    c->launch_counter++;
+  }
+}
+
+int check_ctx(const iga2l_ctx *c) {
+  if (!c) return fail(IGA2L_EPARAM, "ctx is NULL");
+  return IGA2L_OK;
+}
+
+// device view of a caller vector: device pointers pass through; host pointers are staged
+struct Staged {
+  const double *ptr;
+  bool host;
+};
+
+int stage_in(iga2l_ctx *c, const double *user, double *buf, int64_t n, Staged *out) {
+  if (!user) return fail(IGA2L_EPARAM, "vector argument is NULL");
+  if (is_device_ptr(user)) {
+    *out = {user, false};
+    return IGA2L_OK;
+  }
+  CU(cudaMemcpyAsync(buf, user, n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  *out = {buf, true};
+  return IGA2L_OK;
+}
+
+int stage_out(iga2l_ctx *c, double *user, const Staged &s, int64_t n) {
+  if (s.host) {
+    CU(cudaMemcpyAsync(user, s.ptr, n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+  }
+  return IGA2L_OK;
+}
+
+int run_iterations(iga2l_ctx *c, const double *b, double *x, int iters, bool with_norm) {
+  if (iters <= 0) return IGA2L_OK;
+  if (!c->opts.use_graph) {
+    for (int k = 0; k < iters; ++k) L_iteration(c, b, x, with_norm);
+    CU(cudaGetLastError());
+    return IGA2L_OK;
+  }
+  iga2l_ctx::G *g = nullptr;
+  for (auto &gg : c->graphs)
+    if (gg.exec && gg.b == b && gg.x == x && gg.norm == int(with_norm)) g = &gg;
+  if (!g) {
+    g = &c->graphs[c->next_graph];
+    c->next_graph = (c->next_graph + 1) % 4;
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    g->exec = nullptr;
+    cudaGraph_t graph;
+    CU(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+    c->launch_counter = 0;
+    L_iteration(c, b, x, with_norm);
+    cudaError_t e = cudaStreamEndCapture(c->st, &graph);
+    if (e != cudaSuccess) return fail(IGA2L_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    if (!with_norm) c->launches_per_iter = c->launch_counter;
+    CU(cudaGraphInstantiate(&g->exec, graph, 0));
+    cudaGraphDestroy(graph);
+    g->b = b;
+    g->x = x;
+    g->norm = int(with_norm);
+  }
+  for (int k = 0; k < iters; ++k) CU(cudaGraphLaunch(g->exec, c->st));
+  return IGA2L_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *iga2l_last_error(void) { return g_err.c_str(); }
+const char *iga2l_version(void) { return "iga2l 0.1 (sm_100a)"; }
+
+void iga2l_default_opts(iga2l_opts *o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->coarse_mode = IGA2L_COARSE_VCYCLE;
+  o->coarse_h_factor = 2;
+  o->vcycle_coarsest_m = 8;
+  o->stream = nullptr;
+  o->use_graph = 1;
+  o->nranks = 1;
+  o->rank = 0;
+  o->nccl_id = nullptr;
+}
+
+int iga2l_setup(int dim, int p, int q, int64_t n, int block, int overlap, iga2l_ctx **out) {
+  iga2l_opts o;
+  iga2l_default_opts(&o);
+  return iga2l_setup_ex(dim, p, q, n, block, overlap, &o, out);
+}
+
+int iga2l_destroy(iga2l_ctx *c) {
+  if (!c) return IGA2L_OK;
+  for (auto &g : c->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (void *p : c->allocs) cudaFree(p);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+  delete c;
+  return IGA2L_OK;
+}
+
+int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, const iga2l_opts *opts,
+                   iga2l_ctx **out) {
+  if (!out) return fail(IGA2L_EPARAM, "out is NULL");
+  *out = nullptr;
+  iga2l_opts o;
+  if (opts) o = *opts; else iga2l_default_opts(&o);
+  if (dim != 2 && dim != 3) return fail(IGA2L_EPARAM, "dim must be 2 or 3");
+  if (p < 1 || p > 8) return fail(IGA2L_EPARAM, "p must be in 1..8 (P:194)");
+  if (q < 1 || q > 2 || q > p) return fail(IGA2L_EPARAM, "q must satisfy 1 <= q <= min(p, 2) (P:165)");
+  if (n < 1 || n > 100000) return fail(IGA2L_EPARAM, "n (spans per axis) must be >= 1");
+  const int64_t n1 = n + p - 2;
+  if (n1 < 1) return fail(IGA2L_EPARAM, "n + p - 2 must be >= 1");
+  if (block != 1 && block != 3 && block != 5 && block != 7) return fail(IGA2L_EPARAM, "block must be 1, 3, 5 or 7");
+  if (block > n1) return fail(IGA2L_EPARAM, "block must be <= n + p - 2");
+  if (overlap != block - 1) return fail(IGA2L_EPARAM, "overlap must be block - 1 (maximal overlap, P:186)");
+  if (o.coarse_mode != IGA2L_COARSE_EXACT && o.coarse_mode != IGA2L_COARSE_VCYCLE)
+    return fail(IGA2L_EPARAM, "opts.coarse_mode");
+  if (o.coarse_h_factor != 1 && o.coarse_h_factor != 2) return fail(IGA2L_EPARAM, "opts.coarse_h_factor must be 1 or 2");
+  if (o.coarse_h_factor == 2 && n % 2) return fail(IGA2L_EPARAM, "aggressive coarsening needs n even (S:358)");
+  if (o.vcycle_coarsest_m < 1) return fail(IGA2L_EPARAM, "opts.vcycle_coarsest_m must be >= 1");
+  if (o.nranks != 1 || o.rank != 0 || o.nccl_id) return fail(IGA2L_EPARAM, "opts.nranks must be 1 in this build");
+  const int64_t mc = n / o.coarse_h_factor;
+  if (mc + q - 2 < 1) return fail(IGA2L_EPARAM, "second level is empty (n too small)");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(IGA2L_ECUDA, "no CUDA device available");
+  }
+  const int64_t N = ipow(n1, dim);
+  if (N > (int64_t)1 << 31) return fail(IGA2L_EPARAM, "problem too large");
+
+  iga2l_ctx *c = new iga2l_ctx();
+  c->dim = dim; c->p = p; c->q = q; c->s = block; c->w = (block - 1) / 2; c->D = block + p;
+  c->colours = int(ipow(c->D, dim));
+  c->m = n; c->n1 = n1; c->N = N; c->opts = o;
+  auto bail = [&](int rc) { iga2l_destroy(c); return rc; };
+  if (o.stream) c->st = static_cast<cudaStream_t>(o.stream);
+  else {
+    if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess)
+      return bail(fail(IGA2L_ECUDA, "cudaStreamCreate failed"));
+    c->own_stream = true;
+  }
+  int rc;
+  // fine level tables (P:83 via Gauss quadrature on Cox–de Boor)
+  std::vector<double> K, M, V, lam;
+  band_tables(p, n, K, M);
+  if (!fd_tables(p, block, n1, K, M, V, lam)) return bail(fail(IGA2L_ENUMERIC, "Schwarz block matrix not SPD"));
+  if ((rc = upload(c, &c->K1, K)) || (rc = upload(c, &c->M1, M)) || (rc = upload(c, &c->V, V)) ||
+      (rc = upload(c, &c->lam, lam)) || (rc = upload(c, &c->g1, load_1d_sine(p, n))))
+    return bail(rc);
+  // transfers (aggressive P:263)
+  BandOp R1 = degree_restriction(p, q, n);
+  if (o.coarse_h_factor == 2) R1 = multiply(transpose(mesh_prolongation(q, mc)), R1);
+  if ((rc = upload_band(c, c->R, R1)) || (rc = upload_band(c, c->RT, transpose(R1)))) return bail(rc);
+  // second-level hierarchy
+  int64_t ml = mc;
+  while (true) {
+    Level L;
+    L.m = ml;
+    L.n = int(ml + q - 2);
+    L.N = ipow(L.n, dim);
+    std::vector<double> Kq, Mq;
+    band_tables(q, ml, Kq, Mq);
+    if ((rc = upload(c, &L.K, Kq)) || (rc = upload(c, &L.M, Mq)) || (rc = dalloc(c, &L.x, L.N)) ||
+        (rc = dalloc(c, &L.b, L.N)) || (rc = dalloc(c, &L.r, L.N)) || (rc = dalloc(c, &L.t1, L.N)) ||
+        (rc = dalloc(c, &L.t2, L.N)))
+      return bail(rc);
+    const bool direct = (o.coarse_mode == IGA2L_COARSE_EXACT) || ml <= o.vcycle_coarsest_m;
+    if (direct) {
+      if (L.N > 4096) return bail(fail(IGA2L_EPARAM, "exact second level limited to 4096 unknowns in this build"));
+      std::vector<double> inv;
+      if (!dense_kron_inverse(dim, q, L.n, Kq, Mq, inv)) return bail(fail(IGA2L_ENUMERIC, "coarse matrix not SPD"));
+      if ((rc = upload(c, &L.inv, inv))) return bail(rc);
+      c->lev.push_back(L);
+      break;
+    }
+    if (ml % 2) return bail(fail(IGA2L_EPARAM, "V-cycle needs the second-level m divisible by 2 down to opts.vcycle_coarsest_m"));
+    BandOp P = mesh_prolongation(q, ml / 2);
+    if ((rc = upload_band(c, L.P, P)) || (rc = upload_band(c, L.PT, transpose(P)))) return bail(rc);
+    c->lev.push_back(L);
+    ml /= 2;
+  }
+  c->npartial = apply_num_partials(dim, p, n1);
+  if ((rc = dalloc(c, &c->r, N)) || (rc = dalloc(c, &c->t1, N)) || (rc = dalloc(c, &c->t2, N)) ||
+      (rc = dalloc(c, &c->partial, c->npartial)) || (rc = dalloc(c, &c->norm, 1)) ||
+      (rc = dalloc(c, &c->hist_count, 1)) || (rc = dalloc(c, &c->hist, 4096)))
+    return bail(rc);
+  c->hist_cap = 4096;
+  if (cudaMemset(c->hist_count, 0, sizeof(int)) != cudaSuccess) return bail(fail(IGA2L_ECUDA, "cudaMemset"));
+  if (cudaMallocHost(&c->pinned, 64 * sizeof(double)) != cudaSuccess) return bail(fail(IGA2L_ENOMEM, "cudaMallocHost"));
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return bail(fail(IGA2L_ECUDA, std::string("setup: ") + cudaGetErrorString(e)));
+  {  // count our kernel launches in one iteration: capture (nothing executes) and discard
+    cudaGraph_t graph;
+    if (cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+      return bail(fail(IGA2L_ECUDA, "capture for launch count"));
+    c->launch_counter = 0;
+    L_iteration(c, c->t1, c->t2, false);
+    if (cudaStreamEndCapture(c->st, &graph) != cudaSuccess) return bail(fail(IGA2L_ECUDA, "end capture"));
+    cudaGraphDestroy(graph);
+    c->launches_per_iter = c->launch_counter;
+  }
+  *out = c;
+  return IGA2L_OK;
+}
+
+int iga2l_sizes(const iga2l_ctx *c, int64_t *n_local, int64_t *z0, int64_t *z1, int64_t *n1) {
+  if (int rc = check_ctx(c)) return rc;
+  if (n_local) *n_local = c->N;
+  if (z0) *z0 = 0;
+  if (z1) *z1 = c->n1;
+  if (n1) *n1 = c->n1;
+  return IGA2L_OK;
+}
+
+int iga2l_get_info(const iga2l_ctx *c, iga2l_info *o) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!o) return fail(IGA2L_EPARAM, "out is NULL");
+  o->n1 = c->n1;
+  o->N = c->N;
+  o->n1c = c->lev[0].n;
+  o->Nc = c->lev[0].N;
+  o->colours = c->colours;
+  o->levels = int(c->lev.size());
+  o->launches_per_iter = c->launches_per_iter;
+  // sweep = N (2k^2 + 2 SF(p,s,d)) flops, SF = sum-factorised block residual MACs,
+  // or the full-stencil k (2p+1)^d where smaller.
+  const double k = double(ipow(c->s, c->dim)), s = c->s, p = c->p, Wn = s + 2 * p, tp = 2 * p + 1;
+  double SF = c->dim == 2 ? tp * (2 * s * Wn + 2 * s * s) : tp * (2 * s * Wn * Wn + 3 * s * s * Wn + 3 * s * s * s);
+  SF = std::min(SF, k * std::pow(tp, c->dim));
+  o->sweep_flops = double(c->N) * (2 * k * k + 2 * SF);
+  // residual+restriction 16 B + prolongation+norm 24 B per fine DOF, ~64 B per coarse DOF
+  double coarse = 0;
+  for (auto &L : c->lev) coarse += double(L.N);
+  o->iter_hbm_bytes = 40.0 * double(c->N) + 64.0 * coarse;
+  return IGA2L_OK;
+}
+
+int iga2l_rhs_sine(iga2l_ctx *c, double *b) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!b) return fail(IGA2L_EPARAM, "b is NULL");
+  const double pi = 3.14159265358979323846;
+  const bool dev = is_device_ptr(b);
+  if (!dev && !c->hy && dalloc(c, &c->hy, c->N)) return IGA2L_ENOMEM;
+  double *dst = dev ? b : c->hy;
+  launch_tensor_rhs(c->dim, c->n1, c->g1, c->dim * pi * pi, dst, c->st);
+  CU(cudaGetLastError());
+  if (!dev) {
+    CU(cudaMemcpyAsync(b, dst, c->N * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+  }
+  return IGA2L_OK;
+}
+
+static int ensure_staging(iga2l_ctx *c) {
+  int rc;
+  if (!c->hb && (rc = dalloc(c, &c->hb, c->N))) return rc;
+  if (!c->hx && (rc = dalloc(c, &c->hx, c->N))) return rc;
+  if (!c->hy && (rc = dalloc(c, &c->hy, c->N))) return rc;
+  if (!c->hcb && (rc = dalloc(c, &c->hcb, c->lev[0].N))) return rc;
+  if (!c->hcx && (rc = dalloc(c, &c->hcx, c->lev[0].N))) return rc;
+  return IGA2L_OK;
+}
+
+int iga2l_apply(iga2l_ctx *c, const double *x, double *y) {
+  if (int rc = check_ctx(c)) return rc;
+  if (x == y) return fail(IGA2L_EPARAM, "apply: x and y must not alias");
+  if (int rc = ensure_staging(c)) return rc;
+  Staged sx, sy;
+  if (int rc = stage_in(c, x, c->hx, c->N, &sx)) return rc;
+  if (!y) return fail(IGA2L_EPARAM, "y is NULL");
+  sy = {is_device_ptr(y) ? y : c->hy, !is_device_ptr(y)};
+  L_apply(c, sx.ptr, nullptr, const_cast<double *>(sy.ptr), nullptr, 0);
+  CU(cudaGetLastError());
+  return stage_out(c, y, sy, c->N);
+}
+
+int iga2l_residual_norm(iga2l_ctx *c, const double *b, const double *x, double *out) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!out) return fail(IGA2L_EPARAM, "out is NULL");
+  if (int rc = ensure_staging(c)) return rc;
+  Staged sb, sx;
+  if (int rc = stage_in(c, b, c->hb, c->N, &sb)) return rc;
+  if (int rc = stage_in(c, x, c->hx, c->N, &sx)) return rc;
+  L_apply(c, sx.ptr, sb.ptr, c->r, c->partial, 1);
+  launch_sum_partials(c->partial, c->npartial, c->norm, nullptr, nullptr, 0, c->st);
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(c->pinned, c->norm, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  *out = std::sqrt(c->pinned[0]);
+  if (!std::isfinite(*out)) return fail(IGA2L_ENUMERIC, "residual norm is not finite");
+  return IGA2L_OK;
+}
+
+int iga2l_iterate(iga2l_ctx *c, const double *b, double *x, int iters, double *res_hist) {
+  if (int rc = check_ctx(c)) return rc;
+  if (iters < 0) return fail(IGA2L_EPARAM, "iters must be >= 0");
+  if (int rc = ensure_staging(c)) return rc;
+  Staged sb, sx;
+  if (int rc = stage_in(c, b, c->hb, c->N, &sb)) return rc;
+  if (int rc = stage_in(c, x, c->hx, c->N, &sx)) return rc;
+  double *xd = const_cast<double *>(sx.ptr);
+  if (res_hist) {
+    if (iters + 1 > c->hist_cap) return fail(IGA2L_EPARAM, "res_hist supports at most 4095 iterations per call");
+    CU(cudaMemsetAsync(c->hist_count, 0, sizeof(int), c->st));
+    L_apply(c, xd, sb.ptr, c->r, c->partial, 1);
+    launch_sum_partials(c->partial, c->npartial, c->norm, c->hist, c->hist_count, c->hist_cap, c->st);
+  }
+  if (int rc = run_iterations(c, sb.ptr, xd, iters, res_hist != nullptr)) return rc;
+  CU(cudaGetLastError());
+  if (res_hist) {
+    CU(cudaMemcpyAsync(res_hist, c->hist, (iters + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    for (int k = 0; k <= iters; ++k)
+      if (!std::isfinite(res_hist[k])) return fail(IGA2L_ENUMERIC, "residual norm is not finite");
+  }
+  return stage_out(c, x, sx, c->N);
+}
+
+int iga2l_solve(iga2l_ctx *c, const double *b, double *x, double rtol, int maxit, int *iters_out,
+                double *relres_out) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!(rtol > 0.0) || maxit < 0) return fail(IGA2L_EPARAM, "rtol must be > 0 and maxit >= 0");
+  if (int rc = ensure_staging(c)) return rc;
+  Staged sb, sx;
+  if (int rc = stage_in(c, b, c->hb, c->N, &sb)) return rc;
+  if (int rc = stage_in(c, x, c->hx, c->N, &sx)) return rc;
+  double *xd = const_cast<double *>(sx.ptr);
+  CU(cudaMemsetAsync(c->hist_count, 0, sizeof(int), c->st));
+  L_apply(c, xd, sb.ptr, c->r, c->partial, 1);
+  launch_sum_partials(c->partial, c->npartial, c->norm, nullptr, nullptr, 0, c->st);
+  CU(cudaMemcpyAsync(c->pinned, c->norm, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  const double r0 = std::sqrt(c->pinned[0]);
+  if (!std::isfinite(r0)) return fail(IGA2L_ENUMERIC, "initial residual is not finite");
+  double rk = r0;
+  int it = 0;
+  while (it < maxit && rk > rtol * r0) {    // stop at ||r_k|| <= rtol ||r_0||
+    if (int rc = run_iterations(c, sb.ptr, xd, 1, true)) return rc;
+    CU(cudaMemcpyAsync(c->pinned, c->norm, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    rk = std::sqrt(c->pinned[0]);
+    ++it;
+    if (!std::isfinite(rk)) return fail(IGA2L_ENUMERIC, "residual norm is not finite");
+  }
+  if (iters_out) *iters_out = it;
+  if (relres_out) *relres_out = (r0 > 0) ? rk / r0 : 0.0;
+  if (int rc = stage_out(c, x, sx, c->N)) return rc;
+  if (rk > rtol * r0) return fail(IGA2L_NOTCONV, "maxit reached before rtol");
+  return IGA2L_OK;
+}
+
+int iga2l_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
+  if (int rc = check_ctx(c)) return rc;
+  if (c0 < 0 || c1 < c0 || c1 > c->colours) return fail(IGA2L_EPARAM, "colour range must satisfy 0 <= begin <= end <= D^d");
+  if (int rc = ensure_staging(c)) return rc;
+  Staged sb, sx;
+  if (int rc = stage_in(c, b, c->hb, c->N, &sb)) return rc;
+  if (int rc = stage_in(c, x, c->hx, c->N, &sx)) return rc;
+  L_sweep(c, sb.ptr, const_cast<double *>(sx.ptr), c0, c1);
+  CU(cudaGetLastError());
+  return stage_out(c, x, sx, c->N);
+}
+
+int iga2l_defect_restrict(iga2l_ctx *c, const double *b, const double *x, double *dq) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = ensure_staging(c)) return rc;
+  Staged sb, sx;
+  if (int rc = stage_in(c, b, c->hb, c->N, &sb)) return rc;
+  if (int rc = stage_in(c, x, c->hx, c->N, &sx)) return rc;
+  if (!dq) return fail(IGA2L_EPARAM, "dq is NULL");
+  const bool dev = is_device_ptr(dq);
+  double *dst = dev ? dq : c->hcb;
+  L_apply(c, sx.ptr, sb.ptr, c->r, nullptr, 1);
+  L_tensor(c, c->dim, c->R.b, c->r, dst, c->t1, c->t2, 0);
+  CU(cudaGetLastError());
+  return stage_out(c, dq, Staged{dst, !dev}, c->lev[0].N);
+}
+
+int iga2l_coarse_solve(iga2l_ctx *c, const double *dq, double *e) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = ensure_staging(c)) return rc;
+  if (!dq || !e) return fail(IGA2L_EPARAM, "NULL vector");
+  Level &L0 = c->lev[0];
+  const bool din = is_device_ptr(dq);
+  CU(cudaMemcpyAsync(L0.b, dq, L0.N * sizeof(double), din ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
+  L_vcycle(c, 0);
+  const bool dout = is_device_ptr(e);
+  CU(cudaMemcpyAsync(e, L0.x, L0.N * sizeof(double), dout ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
+  CU(cudaGetLastError());
+  if (!dout) CU(cudaStreamSynchronize(c->st));
+  return IGA2L_OK;
+}
+
+int iga2l_prolong_add(iga2l_ctx *c, const double *e, double *x) {
+  if (int rc = check_ctx(c)) return rc;
+  if (int rc = ensure_staging(c)) return rc;
+  Staged se, sx;
+  if (int rc = stage_in(c, e, c->hcx, c->lev[0].N, &se)) return rc;
+  if (int rc = stage_in(c, x, c->hx, c->N, &sx)) return rc;
+  L_tensor(c, c->dim, c->RT.b, se.ptr, const_cast<double *>(sx.ptr), c->t1, c->t2, 1);
+  CU(cudaGetLastError());
+  return stage_out(c, x, sx, c->N);
+}
+
+int iga2l_host_band_tables(int p, int64_t m, double *K, double *M) {
+  if (p < 0 || p > 8 || m < 1 || m + p - 2 < 1 || !K || !M) return fail(IGA2L_EPARAM, "host_band_tables arguments");
+  std::vector<double> k, mm;
+  band_tables(p, m, k, mm);
+  std::memcpy(K, k.data(), k.size() * sizeof(double));
+  std::memcpy(M, mm.data(), mm.size() * sizeof(double));
+  return IGA2L_OK;
+}
+
+int iga2l_host_restriction_1d(int p, int q, int64_t m, int h_factor, double *R) {
+  if (p < 1 || p > 8 || q < 1 || q > p || m < 2 || (h_factor != 1 && h_factor != 2) || !R ||
+      (h_factor == 2 && m % 2))
+    return fail(IGA2L_EPARAM, "host_restriction_1d arguments");
+  BandOp R1 = degree_restriction(p, q, m);
+  if (h_factor == 2) R1 = multiply(transpose(mesh_prolongation(q, m / 2)), R1);
+  for (int r = 0; r < R1.rows; ++r)
+    for (int col = 0; col < R1.cols; ++col) R[(size_t)r * R1.cols + col] = R1.at(r, col);
+  return IGA2L_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,567 @@
+// Device kernels of libiga2l (layer L1), sm_100a.  See kernels.cuh for the contracts.
+#include "kernels.cuh"
+
+#include <algorithm>
+#include <cstdio>
+
+namespace iga2l {
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// deterministic block reduction (fixed tree); result valid in thread 0
+__device__ double block_sum(double v, double *scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    r = (lane < nw) ? scratch[lane] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;
+}
+
+// ============================ fine operator: apply / residual ============================
+// 2D tile TX x TY outputs; window (TX+2p) x (TY+2p) staged in shared memory.
+template <int TX, int TY>
+__global__ void __launch_bounds__(256) k_apply2d(int p, int n1, const double *__restrict__ K,
+                                                 const double *__restrict__ M, const double *__restrict__ x,
+                                                 const double *__restrict__ b, double *__restrict__ y,
+                                                 double *__restrict__ partial, int mode) {
+  extern __shared__ double sm[];
+  const int W = 2 * p + 1, WX = TX + 2 * p, WY = TY + 2 * p;
+  double *X = sm;              // [WY][WX]
+  double *Tk = X + WX * WY;    // [WY][TX]
+  double *Tm = Tk + WY * TX;   // [WY][TX]
+  __shared__ double red[32];
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  for (int i = threadIdx.x; i < WX * WY; i += blockDim.x) {
+    const int wy = i / WX, wx = i - wy * WX;
+    const int gx = x0 - p + wx, gy = y0 - p + wy;
+    X[i] = (gx >= 0 && gx < n1 && gy >= 0 && gy < n1) ? x[(int64_t)gy * n1 + gx] : 0.0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < WY * TX; i += blockDim.x) {   // pass along x: K_x X, M_x X
+    const int wy = i / TX, lx = i - wy * TX, gx = x0 + lx;
+    double sk = 0.0, sm_ = 0.0;
+    if (gx < n1) {
+      const double *kr = K + (int64_t)gx * W, *mr = M + (int64_t)gx * W, *xr = X + wy * WX + lx;
+      for (int t = 0; t < W; ++t) {
+        sk = fma(kr[t], xr[t], sk);
+        sm_ = fma(mr[t], xr[t], sm_);
+      }
+    }
+    Tk[i] = sk;
+    Tm[i] = sm_;
+  }
+  __syncthreads();
+  double sq = 0.0;
+  for (int i = threadIdx.x; i < TY * TX; i += blockDim.x) {   // pass along y: M_y Tk + K_y Tm
+    const int ly = i / TX, lx = i - ly * TX, gx = x0 + lx, gy = y0 + ly;
+    if (gx >= n1 || gy >= n1) continue;
+    const double *kr = K + (int64_t)gy * W, *mr = M + (int64_t)gy * W;
+    double acc = 0.0;
+    for (int u = 0; u < W; ++u) {
+      acc = fma(mr[u], Tk[(ly + u) * TX + lx], acc);
+      acc = fma(kr[u], Tm[(ly + u) * TX + lx], acc);
+    }
+    const int64_t g = (int64_t)gy * n1 + gx;
+    const double out = mode ? b[g] - acc : acc;
+    y[g] = out;
+    sq = fma(out, out, sq);
+  }
+  if (partial) {
+    const double t = block_sum(sq, red);
+    if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+// 3D tile TX x TY x TZ outputs.
+template <int TX, int TY, int TZ>
+__global__ void __launch_bounds__(256) k_apply3d(int p, int n1, const double *__restrict__ K,
+                                                 const double *__restrict__ M, const double *__restrict__ x,
+                                                 const double *__restrict__ b, double *__restrict__ y,
+                                                 double *__restrict__ partial, int mode) {
+  extern __shared__ double sm[];
+  const int W = 2 * p + 1, WX = TX + 2 * p, WY = TY + 2 * p, WZ = TZ + 2 * p;
+  double *X = sm;                       // [WZ][WY][WX]
+  double *Pa = X + WX * WY * WZ;        // [WZ][WY][TX]  K_x X
+  double *Pb = Pa + TX * WY * WZ;       // [WZ][WY][TX]  M_x X
+  double *Pc = Pb + TX * WY * WZ;       // [WZ][TY][TX]
+  double *Pe = Pc + TX * TY * WZ;
+  __shared__ double red[32];
+  const int nbx = (n1 + TX - 1) / TX;
+  const int x0 = (blockIdx.x % nbx) * TX, y0 = (blockIdx.x / nbx) * TY, z0 = blockIdx.y * TZ;
+  for (int i = threadIdx.x; i < WX * WY * WZ; i += blockDim.x) {
+    const int wx = i % WX, wy = (i / WX) % WY, wz = i / (WX * WY);
+    const int gx = x0 - p + wx, gy = y0 - p + wy, gz = z0 - p + wz;
+    X[i] = (gx >= 0 && gx < n1 && gy >= 0 && gy < n1 && gz >= 0 && gz < n1)
+               ? x[((int64_t)gz * n1 + gy) * n1 + gx] : 0.0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < TX * WY * WZ; i += blockDim.x) {
+    const int lx = i % TX, wyz = i / TX, gx = x0 + lx;
+    double sa = 0.0, sb = 0.0;
+    if (gx < n1) {
+      const double *kr = K + (int64_t)gx * W, *mr = M + (int64_t)gx * W, *xr = X + wyz * WX + lx;
+      for (int t = 0; t < W; ++t) {
+        sa = fma(kr[t], xr[t], sa);
+        sb = fma(mr[t], xr[t], sb);
+      }
+    }
+    Pa[i] = sa;
+    Pb[i] = sb;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < TX * TY * WZ; i += blockDim.x) {
+    const int lx = i % TX, ly = (i / TX) % TY, wz = i / (TX * TY), gy = y0 + ly;
+    double sc = 0.0, se = 0.0;
+    if (gy < n1) {
+      const double *kr = K + (int64_t)gy * W, *mr = M + (int64_t)gy * W;
+      for (int u = 0; u < W; ++u) {
+        const int j = (wz * WY + ly + u) * TX + lx;
+        sc = fma(mr[u], Pa[j], sc);
+        sc = fma(kr[u], Pb[j], sc);
+        se = fma(mr[u], Pb[j], se);
+      }
+    }
+    Pc[i] = sc;
+    Pe[i] = se;
+  }
+  __syncthreads();
+  double sq = 0.0;
+  for (int i = threadIdx.x; i < TX * TY * TZ; i += blockDim.x) {
+    const int lx = i % TX, ly = (i / TX) % TY, lz = i / (TX * TY);
+    const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
+    if (gx >= n1 || gy >= n1 || gz >= n1) continue;
+    const double *kr = K + (int64_t)gz * W, *mr = M + (int64_t)gz * W;
+    double acc = 0.0;
+    for (int v = 0; v < W; ++v) {
+      const int j = ((lz + v) * TY + ly) * TX + lx;
+      acc = fma(mr[v], Pc[j], acc);
+      acc = fma(kr[v], Pe[j], acc);
+    }
+    const int64_t g = ((int64_t)gz * n1 + gy) * n1 + gx;
+    const double out = mode ? b[g] - acc : acc;
+    y[g] = out;
+    sq = fma(out, out, sq);
+  }
+  if (partial) {
+    const double t = block_sum(sq, red);
+    if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+constexpr int A2X = 32, A2Y = 8, A3X = 8, A3Y = 8, A3Z = 4;
+
+// =============================== Schwarz colour kernel ====================================
+// contract one axis of a [s]^DIM array (first index fastest) with an s x s matrix V[l*s + j]:
+//   transposed: out[.., j, ..] = Σ_l V[l][j] in[.., l, ..];  else out[.., l, ..] = Σ_j V[l][j] in[.., j, ..]
+template <int DIM>
+__device__ __forceinline__ void fd_contract(const double *in, double *out, const double *V, int s, int axis,
+                                            bool transposed) {
+  int tot = s * s;
+  if (DIM == 3) tot *= s;
+  const int stride = (axis == 0) ? 1 : (axis == 1 ? s : s * s);
+  for (int i = threadIdx.x; i < tot; i += blockDim.x) {
+    const int o = (i / stride) % s;
+    const int base = i - o * stride;
+    double acc = 0.0;
+    for (int l = 0; l < s; ++l) {
+      const double v = transposed ? V[l * s + o] : V[o * s + l];
+      acc = fma(v, in[base + l * stride], acc);
+    }
+    out[i] = acc;
+  }
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(128) k_schwarz(int p, int s, int n1, const double *__restrict__ K,
+                                                 const double *__restrict__ M, const double *__restrict__ Vt,
+                                                 const double *__restrict__ lamt, const double *__restrict__ b,
+                                                 double *__restrict__ x, int c0, int c1, int c2, int D, int nb0,
+                                                 int nb1) {
+  extern __shared__ double sm[];
+  const int w = (s - 1) / 2, Wn = s + 2 * p, W = 2 * p + 1;
+  const int bid = blockIdx.x;
+  const int j0 = bid % nb0, j1 = (bid / nb0) % nb1, j2 = bid / (nb0 * nb1);
+  const int cx = c0 + D * j0, cy = c1 + D * j1, cz = (DIM == 3) ? c2 + D * j2 : 0;
+  const int ox = cx - w - p, oy = cy - w - p, oz = cz - w - p;   // window origin
+  const int bx = cx - w, by = cy - w, bz = cz - w;                // block origin
+  const int s2 = s * s, sd = (DIM == 3) ? s2 * s : s2;
+  double *X = sm;
+  const int nX = (DIM == 3) ? Wn * Wn * Wn : Wn * Wn;
+  double *Pa = X + nX;
+  const int nP = (DIM == 3) ? s * Wn * Wn : s * Wn;
+  double *Pb = Pa + nP;
+  double *Pc = Pb + nP;                   // 3D only: [Wn][s][s]
+  const int nC = (DIM == 3) ? s2 * Wn : 0;
+  double *Pe = Pc + nC;
+  double *R = Pe + nC;                    // [s]^DIM
+  double *Q0 = R + sd, *Q1 = Q0 + sd;
+  double *Vx = Q1 + sd, *Vy = Vx + s2, *Vz = Vy + s2;
+  double *Lx = Vz + s2, *Ly = Lx + s, *Lz = Ly + s;
+
+  for (int i = threadIdx.x; i < s2; i += blockDim.x) {
+    Vx[i] = Vt[(int64_t)cx * s2 + i];
+    Vy[i] = Vt[(int64_t)cy * s2 + i];
+    if (DIM == 3) Vz[i] = Vt[(int64_t)cz * s2 + i];
+  }
+  for (int i = threadIdx.x; i < s; i += blockDim.x) {
+    Lx[i] = lamt[(int64_t)cx * s + i];
+    Ly[i] = lamt[(int64_t)cy * s + i];
+    if (DIM == 3) Lz[i] = lamt[(int64_t)cz * s + i];
+  }
+  // window of x (zero outside the domain: the band tables vanish there too)
+  for (int i = threadIdx.x; i < nX; i += blockDim.x) {
+    const int wx = i % Wn, wy = (i / Wn) % Wn, wz = (DIM == 3) ? i / (Wn * Wn) : 0;
+    const int gx = ox + wx, gy = oy + wy, gz = oz + wz;
+    bool ok = gx >= 0 && gx < n1 && gy >= 0 && gy < n1;
+    if (DIM == 3) ok = ok && gz >= 0 && gz < n1;
+    X[i] = ok ? x[((int64_t)gz * n1 + gy) * n1 + gx] : 0.0;
+  }
+  __syncthreads();
+  // pass x over (lx in block) x (rest of window)
+  for (int i = threadIdx.x; i < nP; i += blockDim.x) {
+    const int lx = i % s, rest = i / s, gx = bx + lx;
+    double sa = 0.0, sb = 0.0;
+    if (gx >= 0 && gx < n1) {
+      const double *kr = K + (int64_t)gx * W, *mr = M + (int64_t)gx * W, *xr = X + rest * Wn + lx;
+      for (int t = 0; t < W; ++t) {
+        sa = fma(kr[t], xr[t], sa);
+        sb = fma(mr[t], xr[t], sb);
+      }
+    }
+    Pa[i] = sa;   // [rest][lx], rest = wy (2D) or wz*Wn + wy (3D)
+    Pb[i] = sb;
+  }
+  __syncthreads();
+  if (DIM == 2) {
+    for (int i = threadIdx.x; i < s2; i += blockDim.x) {
+      const int lx = i % s, ly = i / s, gx = bx + lx, gy = by + ly;
+      double r = 0.0;
+      if (gx >= 0 && gx < n1 && gy >= 0 && gy < n1) {
+        const double *kr = K + (int64_t)gy * W, *mr = M + (int64_t)gy * W;
+        double acc = 0.0;
+        for (int u = 0; u < W; ++u) {
+          acc = fma(mr[u], Pa[(ly + u) * s + lx], acc);
+          acc = fma(kr[u], Pb[(ly + u) * s + lx], acc);
+        }
+        r = b[(int64_t)gy * n1 + gx] - acc;
+      }
+      R[i] = r;
+    }
+  } else {
+    for (int i = threadIdx.x; i < nC; i += blockDim.x) {   // pass y over (lx, ly) x wz
+      const int lx = i % s, ly = (i / s) % s, wz = i / s2, gy = by + ly;
+      double sc = 0.0, se = 0.0;
+      if (gy >= 0 && gy < n1) {
+        const double *kr = K + (int64_t)gy * W, *mr = M + (int64_t)gy * W;
+        for (int u = 0; u < W; ++u) {
+          const int j = (wz * Wn + ly + u) * s + lx;
+          sc = fma(mr[u], Pa[j], sc);
+          sc = fma(kr[u], Pb[j], sc);
+          se = fma(mr[u], Pb[j], se);
+        }
+      }
+      Pc[i] = sc;
+      Pe[i] = se;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < sd; i += blockDim.x) {   // pass z
+      const int lx = i % s, ly = (i / s) % s, lz = i / s2;
+      const int gx = bx + lx, gy = by + ly, gz = bz + lz;
+      double r = 0.0;
+      if (gx >= 0 && gx < n1 && gy >= 0 && gy < n1 && gz >= 0 && gz < n1) {
+        const double *kr = K + (int64_t)gz * W, *mr = M + (int64_t)gz * W;
+        double acc = 0.0;
+        for (int v = 0; v < W; ++v) {
+          const int j = ((lz + v) * s + ly) * s + lx;
+          acc = fma(mr[v], Pc[j], acc);
+          acc = fma(kr[v], Pe[j], acc);
+        }
+        r = b[((int64_t)gz * n1 + gy) * n1 + gx] - acc;
+      }
+      R[i] = r;
+    }
+  }
+  __syncthreads();
+  // δ = (⊗V) Λ^{-1} (⊗V)^T r  (fast diagonalisation of the Kronecker-sum block matrix)
+  fd_contract<DIM>(R, Q0, Vx, s, 0, true);
+  __syncthreads();
+  fd_contract<DIM>(Q0, Q1, Vy, s, 1, true);
+  __syncthreads();
+  double *cur = Q1, *oth = Q0;
+  if (DIM == 3) {
+    fd_contract<DIM>(Q1, Q0, Vz, s, 2, true);
+    __syncthreads();
+    cur = Q0;
+    oth = Q1;
+  }
+  for (int i = threadIdx.x; i < sd; i += blockDim.x) {
+    const int j = i % s, k = (i / s) % s, l = (DIM == 3) ? i / s2 : 0;
+    double den = Lx[j] + Ly[k];
+    if (DIM == 3) den += Lz[l];
+    cur[i] /= den;
+  }
+  __syncthreads();
+  if (DIM == 3) {
+    fd_contract<DIM>(cur, oth, Vz, s, 2, false);
+    __syncthreads();
+    double *t = cur; cur = oth; oth = t;
+  }
+  fd_contract<DIM>(cur, oth, Vy, s, 1, false);
+  __syncthreads();
+  fd_contract<DIM>(oth, R, Vx, s, 0, false);
+  __syncthreads();
+  for (int i = threadIdx.x; i < sd; i += blockDim.x) {
+    const int lx = i % s, ly = (i / s) % s, lz = (DIM == 3) ? i / s2 : 0;
+    const int gx = bx + lx, gy = by + ly, gz = bz + lz;
+    bool ok = gx >= 0 && gx < n1 && gy >= 0 && gy < n1;
+    if (DIM == 3) ok = ok && gz >= 0 && gz < n1;
+    if (ok) x[((int64_t)gz * n1 + gy) * n1 + gx] += R[i];
+  }
+}
+
+// =============================== band transform along one axis ===========================
+__global__ void k_band_axis(const double *__restrict__ in, double *__restrict__ out, int64_t outer, int nin,
+                            int64_t inner, int rows, int W, const int *__restrict__ lo,
+                            const double *__restrict__ c, int acc) {
+  const int64_t total = outer * rows * inner;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % inner;
+    const int r = int((idx / inner) % rows);
+    const int64_t o = idx / (inner * rows);
+    const int l0 = lo[r];
+    double s = 0.0;
+    for (int k = 0; k < W; ++k) {
+      const int col = l0 + k;
+      if (col >= 0 && col < nin) s = fma(c[(int64_t)r * W + k], in[(o * nin + col) * inner + i], s);
+    }
+    out[idx] = acc ? out[idx] + s : s;
+  }
+}
+
+// =============================== q-level kernels ==========================================
+template <int DIM>
+__device__ __forceinline__ double q_apply_point(int q, int n, const double *K, const double *M, const double *x,
+                                                int ix, int iy, int iz, double *diag) {
+  const int W = 2 * q + 1;
+  double acc = 0.0;
+  const double *kx = K + (int64_t)ix * W, *mx = M + (int64_t)ix * W;
+  const double *ky = K + (int64_t)iy * W, *my = M + (int64_t)iy * W;
+  if (DIM == 2) {
+    for (int u = 0; u < W; ++u) {
+      const int jy = iy + u - q;
+      if (jy < 0 || jy >= n) continue;
+      for (int t = 0; t < W; ++t) {
+        const int jx = ix + t - q;
+        if (jx < 0 || jx >= n) continue;
+        acc = fma(kx[t] * my[u] + mx[t] * ky[u], x[(int64_t)jy * n + jx], acc);
+      }
+    }
+    *diag = kx[q] * my[q] + mx[q] * ky[q];
+  } else {
+    const double *kz = K + (int64_t)iz * W, *mz = M + (int64_t)iz * W;
+    for (int v = 0; v < W; ++v) {
+      const int jz = iz + v - q;
+      if (jz < 0 || jz >= n) continue;
+      for (int u = 0; u < W; ++u) {
+        const int jy = iy + u - q;
+        if (jy < 0 || jy >= n) continue;
+        for (int t = 0; t < W; ++t) {
+          const int jx = ix + t - q;
+          if (jx < 0 || jx >= n) continue;
+          const double a = kx[t] * my[u] * mz[v] + mx[t] * ky[u] * mz[v] + mx[t] * my[u] * kz[v];
+          acc = fma(a, x[((int64_t)jz * n + jy) * n + jx], acc);
+        }
+      }
+    }
+    *diag = kx[q] * my[q] * mz[q] + mx[q] * ky[q] * mz[q] + mx[q] * my[q] * kz[q];
+  }
+  return acc;
+}
+
+template <int DIM>
+__global__ void k_q_gs(int q, int n, const double *__restrict__ K, const double *__restrict__ M,
+                       const double *__restrict__ b, double *__restrict__ x, int c0, int c1, int c2, int na0,
+                       int na1, int64_t total) {
+  const int st = q + 1;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int ix = c0 + st * int(idx % na0);
+    const int iy = c1 + st * int((idx / na0) % na1);
+    const int iz = (DIM == 3) ? c2 + st * int(idx / ((int64_t)na0 * na1)) : 0;
+    double dg;
+    const double ax = q_apply_point<DIM>(q, n, K, M, x, ix, iy, iz, &dg);
+    const int64_t g = ((int64_t)iz * n + iy) * n + ix;
+    x[g] += (b[g] - ax) / dg;
+  }
+}
+
+template <int DIM>
+__global__ void k_q_resid(int q, int n, const double *__restrict__ K, const double *__restrict__ M,
+                          const double *__restrict__ b, const double *__restrict__ x, double *__restrict__ r,
+                          int64_t total) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int ix = int(idx % n), iy = int((idx / n) % n), iz = (DIM == 3) ? int(idx / ((int64_t)n * n)) : 0;
+    double dg;
+    r[idx] = b[idx] - q_apply_point<DIM>(q, n, K, M, x, ix, iy, iz, &dg);
+  }
+}
+
+__global__ void k_dense_mv(int N, const double *__restrict__ A, const double *__restrict__ b, double *__restrict__ x) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= N) return;
+  double s = 0.0;
+  for (int j = lane; j < N; j += 32) s = fma(A[(int64_t)warp * N + j], b[j], s);
+  s = warp_sum(s);
+  if (lane == 0) x[warp] = s;
+}
+
+__global__ void k_sum_partials(const double *__restrict__ partial, int n, double *out, double *hist, int *count,
+                               int cap) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += partial[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) {
+    out[0] = s;
+    if (hist && *count < cap) {
+      hist[*count] = sqrt(s);
+      *count += 1;
+    }
+  }
+}
+
+__global__ void k_tensor_rhs(int dim, int64_t n1, const double *__restrict__ g, double scale, double *__restrict__ b,
+                             int64_t total) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    double v = scale * g[idx % n1] * g[(idx / n1) % n1];
+    if (dim == 3) v *= g[idx / (n1 * n1)];
+    b[idx] = v;
+  }
+}
+
+inline int grid_for(int64_t total, int bs) {
+  int64_t g = (total + bs - 1) / bs;
+  return int(std::min<int64_t>(std::max<int64_t>(g, 1), 148 * 32));
+}
+
+size_t apply_smem(int dim, int p) {
+  if (dim == 2) return sizeof(double) * ((A2X + 2 * p) * (A2Y + 2 * p) + 2 * (A2Y + 2 * p) * A2X);
+  const size_t wx = A3X + 2 * p, wy = A3Y + 2 * p, wz = A3Z + 2 * p;
+  return sizeof(double) * (wx * wy * wz + 2 * A3X * wy * wz + 2 * A3X * A3Y * wz);
+}
+
+size_t schwarz_smem(int dim, int p, int s) {
+  const size_t Wn = s + 2 * p, s2 = s * s, sd = dim == 3 ? s2 * s : s2;
+  const size_t nX = dim == 3 ? Wn * Wn * Wn : Wn * Wn;
+  const size_t nP = dim == 3 ? s * Wn * Wn : s * Wn;
+  const size_t nC = dim == 3 ? s2 * Wn : 0;
+  return sizeof(double) * (nX + 2 * nP + 2 * nC + 3 * sd + 3 * s2 + 3 * s);
+}
+
+template <typename F>
+void ensure_smem(F *kernel, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+}
+
+}  // namespace
+
+int apply_num_partials(int dim, int p, int64_t n1) {
+  (void)p;
+  if (dim == 2) return int(((n1 + A2X - 1) / A2X) * ((n1 + A2Y - 1) / A2Y));
+  return int(((n1 + A3X - 1) / A3X) * ((n1 + A3Y - 1) / A3Y) * ((n1 + A3Z - 1) / A3Z));
+}
+
+void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, const double *x, const double *b,
+                  double *y, double *partial, int mode, cudaStream_t st, int *nparts) {
+  const size_t sm = apply_smem(dim, p);
+  if (dim == 2) {
+    dim3 grid((unsigned)((n1 + A2X - 1) / A2X), (unsigned)((n1 + A2Y - 1) / A2Y));
+    ensure_smem(k_apply2d<A2X, A2Y>, sm);
+    k_apply2d<A2X, A2Y><<<grid, 256, sm, st>>>(p, int(n1), K, M, x, b, y, partial, mode);
+    if (nparts) *nparts = int(grid.x * grid.y);
+  } else {
+    const unsigned nbx = unsigned((n1 + A3X - 1) / A3X), nby = unsigned((n1 + A3Y - 1) / A3Y);
+    dim3 grid(nbx * nby, (unsigned)((n1 + A3Z - 1) / A3Z));
+    ensure_smem(k_apply3d<A3X, A3Y, A3Z>, sm);
+    k_apply3d<A3X, A3Y, A3Z><<<grid, 256, sm, st>>>(p, int(n1), K, M, x, b, y, partial, mode);
+    if (nparts) *nparts = int(grid.x * grid.y);
+  }
+}
+
+void launch_schwarz_colour(int dim, int p, int s, int64_t n1, const double *K, const double *M, const double *V,
+                           const double *lam, const double *b, double *x, int colour, int D, cudaStream_t st) {
+  const int c0 = colour % D, c1 = (colour / D) % D, c2 = (dim == 3) ? colour / (D * D) : 0;
+  if (c0 >= n1 || c1 >= n1 || c2 >= n1) return;
+  const int nb0 = int((n1 - c0 + D - 1) / D), nb1 = int((n1 - c1 + D - 1) / D);
+  const int nb2 = (dim == 3) ? int((n1 - c2 + D - 1) / D) : 1;
+  const size_t sm = schwarz_smem(dim, p, s);
+  const unsigned nblk = unsigned(nb0) * unsigned(nb1) * unsigned(nb2);
+  if (dim == 2) {
+    ensure_smem(k_schwarz<2>, sm);
+    k_schwarz<2><<<nblk, 128, sm, st>>>(p, s, int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1);
+  } else {
+    ensure_smem(k_schwarz<3>, sm);
+    k_schwarz<3><<<nblk, 128, sm, st>>>(p, s, int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1);
+  }
+}
+
+void launch_band_axis(const double *in, double *out, int64_t outer, int nin, int64_t inner, const Band1D &B,
+                      int accumulate, cudaStream_t st) {
+  const int64_t total = outer * B.rows * inner;
+  k_band_axis<<<grid_for(total, 256), 256, 0, st>>>(in, out, outer, nin, inner, B.rows, B.W, B.lo, B.c, accumulate);
+}
+
+void launch_q_gs_colour(int dim, int q, int n, const double *K, const double *M, const double *b, double *x,
+                        int colour, cudaStream_t st) {
+  const int st_ = q + 1;
+  const int c0 = colour % st_, c1 = (colour / st_) % st_, c2 = (dim == 3) ? colour / (st_ * st_) : 0;
+  if (c0 >= n || c1 >= n || c2 >= n) return;
+  const int na0 = (n - c0 + q) / st_, na1 = (n - c1 + q) / st_, na2 = (dim == 3) ? (n - c2 + q) / st_ : 1;
+  const int64_t total = (int64_t)na0 * na1 * na2;
+  if (dim == 2)
+    k_q_gs<2><<<grid_for(total, 128), 128, 0, st>>>(q, n, K, M, b, x, c0, c1, c2, na0, na1, total);
+  else
+    k_q_gs<3><<<grid_for(total, 128), 128, 0, st>>>(q, n, K, M, b, x, c0, c1, c2, na0, na1, total);
+}
+
+void launch_q_residual(int dim, int q, int n, const double *K, const double *M, const double *b, const double *x,
+                       double *r, cudaStream_t st) {
+  int64_t total = (int64_t)n * n;
+  if (dim == 3) total *= n;
+  if (dim == 2)
+    k_q_resid<2><<<grid_for(total, 128), 128, 0, st>>>(q, n, K, M, b, x, r, total);
+  else
+    k_q_resid<3><<<grid_for(total, 128), 128, 0, st>>>(q, n, K, M, b, x, r, total);
+}
+
+void launch_dense_mv(int N, const double *Ainv, const double *b, double *x, cudaStream_t st) {
+  const int warps_per_block = 8;
+  k_dense_mv<<<(N + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(N, Ainv, b, x);
+}
+
+void launch_sum_partials(const double *partial, int n, double *out, double *hist, int *count, int cap,
+                         cudaStream_t st) {
+  k_sum_partials<<<1, 256, 0, st>>>(partial, n, out, hist, count, cap);
+}
+
+void launch_tensor_rhs(int dim, int64_t n1, const double *g, double scale, double *b, cudaStream_t st) {
+  int64_t total = n1 * n1;
+  if (dim == 3) total *= n1;
+  k_tensor_rhs<<<grid_for(total, 256), 256, 0, st>>>(dim, n1, g, scale, b, total);
+}
+
+}  // namespace iga2l

@@ -1,0 +1,56 @@
+// Device kernels of libiga2l (layer L1), sm_100a.  All arithmetic is IEEE fp64.
+//
+// Operator: the degree-p stiffness on the tensor basis is
+//     A = Σ_a ⊗_b X_b,  X_b = K (1D stiffness) if b == a else M (1D mass),
+// applied matrix-free from per-row 1D band tables K[i*(2p+1) + t+p] (row i, column i+t; zero
+// outside the domain), by sum factorisation: one 1D pass per axis over a tile staged in shared
+// memory (2D: 4(2p+1) FMAs/DOF; 3D: 7(2p+1) FMAs/DOF).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace iga2l {
+
+struct Band1D {          // banded 1D transfer: row r uses columns lo[r] .. lo[r]+W-1
+  int rows, cols, W;
+  const int *lo;
+  const double *c;
+};
+
+// ---- fine operator: apply / residual -------------------------------------------------------
+// mode 0: y = A x;  mode 1: y = b - A x.  If partial != nullptr, partial[cta] = Σ y^2 over the tile.
+void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, const double *x,
+                  const double *b, double *y, double *partial, int mode, cudaStream_t st, int *nparts);
+int apply_num_partials(int dim, int p, int64_t n1);
+
+// ---- multicolour Schwarz: one colour ---------------------------------------------------------
+// Blocks centred at c = col + D*j (per axis) are solved in parallel (A-decoupled, reading A4):
+// r_B = b_B - (A x)_B; δ = A_B^{-1} r_B by fast diagonalisation with per-centre 1D tables V, lam;
+// x_B += δ.
+void launch_schwarz_colour(int dim, int p, int s, int64_t n1, const double *K, const double *M,
+                           const double *V, const double *lam, const double *b, double *x,
+                           int colour, int D, cudaStream_t st);
+
+// ---- tensor-product band transform along one axis ------------------------------------------
+// in: [outer][nin][inner]  ->  out: [outer][B.rows][inner],  out (+)= Σ_k B.c[r,k] in[.., lo[r]+k, ..]
+void launch_band_axis(const double *in, double *out, int64_t outer, int nin, int64_t inner,
+                      const Band1D &B, int accumulate, cudaStream_t st);
+
+// ---- q-level (V-cycle) kernels, direct (2q+1)^d stencil --------------------------------------
+void launch_q_gs_colour(int dim, int q, int n, const double *K, const double *M, const double *b,
+                        double *x, int colour, cudaStream_t st);
+void launch_q_residual(int dim, int q, int n, const double *K, const double *M, const double *b,
+                       const double *x, double *r, cudaStream_t st);
+
+// x = Ainv b (dense, N <= 4096), one warp per row.
+void launch_dense_mv(int N, const double *Ainv, const double *b, double *x, cudaStream_t st);
+
+// out[0] = Σ partial[0..n) (deterministic, single CTA); if hist/count given and *count < cap,
+// also hist[*count] = sqrt(out[0]), ++*count.
+void launch_sum_partials(const double *partial, int n, double *out, double *hist, int *count, int cap,
+                         cudaStream_t st);
+
+// b[idx] = scale * ∏_a g[i_a]
+void launch_tensor_rhs(int dim, int64_t n1, const double *g, double scale, double *b, cudaStream_t st);
+
+}  // namespace iga2l

@@ -1,0 +1,232 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star):
+  * operator/phase outputs (apply, rhs, one sweep, defect+restriction, coarse solve, prolongation):
+    max |gpu - oracle| <= 1e-12 * max |oracle| (fp64, summation order differs);
+  * 5 two-level iterations: ||x_gpu - x_oracle|| / ||x_oracle|| <= 1e-10;
+  * measured convergence factor within 2% of the oracle's.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2009_01499_b200 as pkg  # noqa: E402
+from oracle.assembly import load_sine  # noqa: E402
+from oracle.sampled import RowOracle  # noqa: E402
+from oracle.twolevel import TwoLevel  # noqa: E402
+from synthetic_inputs import CONFIGS, initial_guess, random_rhs  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+# (name, d, p, q, m, s, coarse, h_factor): parity sizes the oracle finishes in seconds, each with
+# several tiles/colours and a ragged tail (n1 not a multiple of D nor of the tile sizes).
+PAR = [
+    ("C1", 2, 2, 1, 16, 3, "exact", 1),
+    ("2d_p1", 2, 1, 1, 16, 3, "exact", 1),
+    ("2d_p3_vc", 2, 3, 1, 48, 3, "vcycle", 2),
+    ("2d_p4_vc", 2, 4, 1, 40, 3, "vcycle", 2),
+    ("2d_p5_vc", 2, 5, 1, 32, 5, "vcycle", 2),
+    ("2d_p8_q2", 2, 8, 2, 32, 7, "vcycle", 2),
+    ("2d_p2_sameh_vc", 2, 2, 1, 32, 3, "vcycle", 1),
+    ("3d_p3_vc", 3, 3, 1, 20, 3, "vcycle", 2),
+    ("3d_p5_q2", 3, 5, 2, 10, 5, "vcycle", 2),
+    ("2d_tiny", 2, 2, 1, 3, 3, "exact", 1),
+]
+
+_oracles = {}
+
+
+def oracle_for(name, d, p, q, m, s, coarse, hf):
+    key = (d, p, q, m, s, coarse, hf)
+    if key not in _oracles:
+        _oracles[key] = TwoLevel(d, p, q, m, s=s, coarse=coarse, h_factor=hf, order="multicolour")
+    return _oracles[key]
+
+
+def make_ctx(d, p, q, m, s, coarse, hf, **kw):
+    return pkg.Context(d, p, q, m, s, coarse_mode=pkg.COARSE_EXACT if coarse == "exact" else pkg.COARSE_VCYCLE,
+                       coarse_h_factor=hf, stream=torch.cuda.current_stream(DEV).cuda_stream, **kw)
+
+
+def cu(a):
+    return torch.tensor(a, dtype=torch.float64, device=DEV)
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def close(got, ref, tol=1e-12):
+    scale = max(np.abs(ref).max(), 1e-300)
+    err = np.abs(got - ref).max() / scale
+    assert err <= tol, f"max rel err {err:.3e} > {tol:.1e}"
+
+
+@pytest.mark.parametrize("cfg", PAR, ids=[c[0] for c in PAR])
+def test_apply_and_rhs(cfg):
+    name, d, p, q, m, s, coarse, hf = cfg
+    ctx = make_ctx(d, p, q, m, s, coarse, hf)
+    ora = oracle_for(*cfg)
+    x = initial_guess(ctx.N)
+    y = torch.empty(ctx.N, dtype=torch.float64, device=DEV)
+    ctx.apply(cu(x), y)
+    close(host(y), ora.A @ x, 1e-13)
+    b = torch.empty_like(y)
+    ctx.rhs_sine(b)
+    close(host(b), load_sine(p, m, d), 1e-14)
+
+
+@pytest.mark.parametrize("cfg", PAR, ids=[c[0] for c in PAR])
+def test_one_sweep_and_phases(cfg):
+    name, d, p, q, m, s, coarse, hf = cfg
+    ctx = make_ctx(d, p, q, m, s, coarse, hf)
+    ora = oracle_for(*cfg)
+    b, x0 = random_rhs(ctx.N), initial_guess(ctx.N)
+    xg = cu(x0)
+    ctx.sweep(cu(b), xg)
+    xo = ora.smoother.sweep(x0.copy(), b)
+    close(host(xg), xo)
+    # defect + restriction
+    dq = torch.empty(ctx.Nc, dtype=torch.float64, device=DEV)
+    ctx.defect_restrict(cu(b), cu(xo), dq)
+    dqo = ora.R @ (b - ora.A @ xo)
+    close(host(dq), dqo)
+    # second-level solve (exact or one V(1,1))
+    e = torch.empty_like(dq)
+    ctx.coarse_solve(cu(dqo), e)
+    eo = ora._csolve(dqo)
+    close(host(e), eo, 1e-11)
+    # prolongation x += R^T e
+    xp = cu(xo)
+    ctx.prolong_add(cu(eo), xp)
+    close(host(xp), xo + ora.RT @ eo)
+
+
+@pytest.mark.parametrize("cfg", PAR, ids=[c[0] for c in PAR])
+def test_five_iterations(cfg):
+    name, d, p, q, m, s, coarse, hf = cfg
+    ctx = make_ctx(d, p, q, m, s, coarse, hf)
+    ora = oracle_for(*cfg)
+    b, x0 = random_rhs(ctx.N), initial_guess(ctx.N)
+    xg = cu(x0)
+    hist = np.zeros(6)
+    ctx.iterate(cu(b), xg, iters=5, res_hist=hist)
+    xo = x0.copy()
+    ho = [np.linalg.norm(b - ora.A @ xo)]
+    for _ in range(5):
+        ora.iterate(xo, b)
+        ho.append(np.linalg.norm(b - ora.A @ xo))
+    rel = np.linalg.norm(host(xg) - xo) / np.linalg.norm(xo)
+    assert rel <= 1e-10, rel
+    assert np.allclose(hist, ho, rtol=1e-8, atol=0)
+
+
+def test_iters_zero_is_noop_and_deterministic():
+    ctx = make_ctx(2, 3, 1, 48, 3, "vcycle", 2)
+    b, x0 = cu(random_rhs(ctx.N)), cu(initial_guess(ctx.N))
+    x = x0.clone()
+    ctx.iterate(b, x, iters=0)
+    assert torch.equal(x, x0)
+    x1, x2 = x0.clone(), x0.clone()
+    ctx.iterate(b, x1, iters=3)
+    ctx.iterate(b, x2, iters=3)
+    assert torch.equal(x1, x2)                      # bitwise, no atomics on value paths
+    # graph replay == eager launches
+    ctx_e = make_ctx(2, 3, 1, 48, 3, "vcycle", 2, use_graph=False)
+    x3 = x0.clone()
+    ctx_e.iterate(b, x3, iters=3)
+    assert torch.equal(x1, x3)
+
+
+def test_host_pointers_match_device():
+    ctx = make_ctx(2, 4, 1, 40, 3, "vcycle", 2)
+    b, x0 = random_rhs(ctx.N), initial_guess(ctx.N)
+    xd = cu(x0)
+    ctx.iterate(cu(b), xd, iters=2)
+    xh = x0.copy()
+    ctx.iterate(b, xh, iters=2)                    # numpy (host) buffers, staged by the library
+    assert np.array_equal(host(xd), xh)
+
+
+@pytest.mark.parametrize("cfg", [PAR[0], PAR[3], PAR[7]], ids=["C1", "2d_p4", "3d_p3"])
+def test_convergence_factor_within_2pct(cfg):
+    name, d, p, q, m, s, coarse, hf = cfg
+    ctx = make_ctx(d, p, q, m, s, coarse, hf)
+    ora = oracle_for(*cfg)
+    x0 = initial_guess(ctx.N)
+    rate_o, _ = ora.rate(x0, iters=25)
+    hist = np.zeros(26)
+    ctx.iterate(cu(np.zeros(ctx.N)), cu(x0), iters=25, res_hist=hist)
+    ratios = hist[1:] / hist[:-1]
+    rate_g = float(np.exp(np.mean(np.log(ratios[-10:]))))
+    assert abs(rate_g - rate_o) <= 0.02 * rate_o, (rate_g, rate_o)
+
+
+@pytest.mark.parametrize("cfg", [PAR[0], PAR[2]], ids=["C1", "2d_p3"])
+def test_solve_matches_oracle(cfg):
+    name, d, p, q, m, s, coarse, hf = cfg
+    ctx = make_ctx(d, p, q, m, s, coarse, hf)
+    ora = oracle_for(*cfg)
+    b = load_sine(p, m, d)
+    x0 = initial_guess(ctx.N)
+    xg = cu(x0)
+    it, rr, ok = ctx.solve(cu(b), xg, rtol=1e-8, maxit=50)
+    xo, ito, ho = ora.solve(b, x0, rtol=1e-8)
+    assert ok and it == ito
+    assert rr <= 1e-8
+    assert np.linalg.norm(host(xg) - xo) <= 1e-9 * np.linalg.norm(xo)
+
+
+# ---- full BASELINE sizes, in the launch configuration bench.py times: sampled outputs ----
+FULL = ["C2p3", "C2p4", "C2p5", "C3", "C4", "C5"]
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_full_size_sampled(name):
+    cfg = CONFIGS[name]
+    d, p, q, m, s = cfg["d"], cfg["p"], cfg["q"], cfg["m"], cfg["s"]
+    ctx = make_ctx(d, p, q, m, s, cfg["coarse"], cfg["h_factor"])
+    N, n1, D = ctx.N, ctx.n1, s + p
+    ro = RowOracle(p, m, d)
+    rng = np.random.default_rng(7)
+    x0, b = initial_guess(N), random_rhs(N)
+    # apply on sampled rows (first, last, random)
+    y = torch.empty(N, dtype=torch.float64, device=DEV)
+    ctx.apply(cu(x0), y)
+    rows = np.concatenate([[0, N - 1, n1 - 1], rng.integers(0, N, 40)])
+    ref = ro.apply_rows(x0, rows)
+    got = host(y)[rows]
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+    # colour 0 then colour 1 of the sweep; sampled blocks checked one by one
+    xg = cu(x0)
+    bg = cu(b)
+    ctx.sweep(bg, xg, 0, 1)
+    x1 = host(xg)
+    for _ in range(4):
+        centre = tuple(int(D * rng.integers(0, (n1 - 1) // D + 1)) for _ in range(d))
+        B, dB = ro.block_update(x0, b, centre, s)
+        assert np.abs(x1[B] - (x0[B] + dB)).max() <= 1e-11 * max(np.abs(dB).max(), 1.0)
+    touched = np.zeros(N, bool)
+    idx = np.arange(N)
+    inblk = np.ones(N, bool)
+    for a in range(d):
+        c = (idx // n1 ** a) % n1
+        w = (s - 1) // 2
+        inblk &= ((c + w) % D) <= 2 * w
+    touched |= inblk
+    assert np.array_equal(x1[~touched], x0[~touched])       # only colour-0 blocks changed
+    ctx.sweep(bg, xg, 1, 2)
+    x2 = host(xg)
+    centre = (1,) + tuple(0 for _ in range(d - 1))
+    B, dB = ro.block_update(x1, b, centre, s)
+    assert np.abs(x2[B] - (x1[B] + dB)).max() <= 1e-11 * max(np.abs(dB).max(), 1.0)
+    # a full iteration reduces the residual (property at any size)
+    hist = np.zeros(3)
+    ctx.iterate(bg, xg, iters=2, res_hist=hist)
+    assert hist[2] < 0.9 * hist[1] < 0.9 * hist[0]

@@ -1,0 +1,73 @@
+"""CPU-only tests of the C-ABI library: it loads, exports every symbol include/iga2l.h declares,
+its host-side setup (L0) agrees with the oracle, and it reports errors (no GPU here)."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_2009_01499_b200 as pkg
+from oracle.assembly import matrices_1d
+from oracle.transfer import degree_restriction_1d, mesh_prolongation_1d
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+def test_exports_every_header_symbol():
+    L = pkg.lib()
+    syms = pkg.header_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(L, s), s
+    assert b"iga2l" in L.iga2l_version()
+
+
+def _dense_from_band(B, p):
+    n1 = B.shape[0]
+    D = np.zeros((n1, n1))
+    for i in range(n1):
+        for t in range(-p, p + 1):
+            if 0 <= i + t < n1:
+                D[i, i + t] = B[i, t + p]
+    return D
+
+
+@pytest.mark.parametrize("p,m", [(1, 4), (2, 5), (3, 7), (5, 16), (8, 24), (8, 9)])
+def test_host_band_tables_match_oracle(p, m):
+    K, M = pkg.host_band_tables(p, m)
+    Ko, Mo = matrices_1d(p, m)
+    assert np.abs(_dense_from_band(K, p) - Ko).max() <= 1e-14 * np.abs(Ko).max()
+    assert np.abs(_dense_from_band(M, p) - Mo).max() <= 1e-14 * np.abs(Mo).max()
+    # entries pointing outside the constrained range are exactly zero
+    assert np.all(K[0, :p] == 0) and np.all(M[-1, p + 1:] == 0)
+
+
+@pytest.mark.parametrize("p,q,m,hf", [(2, 1, 16, 1), (3, 1, 8, 1), (3, 1, 16, 2), (5, 2, 16, 2), (8, 2, 32, 2), (4, 2, 12, 2)])
+def test_host_restriction_matches_oracle(p, q, m, hf):
+    R = pkg.host_restriction_1d(p, q, m, hf)
+    Ro = degree_restriction_1d(p, q, m)
+    if hf == 2:
+        Ro = mesh_prolongation_1d(q, m // 2).T @ Ro
+    assert R.shape == Ro.shape
+    assert np.abs(R - Ro).max() <= 1e-14 * np.abs(Ro).max()
+
+
+def test_setup_errors_without_gpu_or_bad_params():
+    h = ctypes.c_void_p()
+    L = pkg.lib()
+    # bad parameters are rejected before any device work, naming the field
+    for args, word in [((4, 2, 1, 16, 3, 2), "dim"), ((2, 9, 1, 16, 3, 2), "p"), ((2, 3, 3, 16, 3, 2), "q"),
+                       ((2, 3, 1, 16, 4, 3), "block"), ((2, 3, 1, 16, 3, 1), "overlap"),
+                       ((2, 3, 1, 15, 3, 2), "n even")]:
+        rc = L.iga2l_setup(*args, ctypes.byref(h))
+        assert rc == pkg.EPARAM, (args, rc)
+        assert word in L.iga2l_last_error().decode()
+    import torch
+    if not torch.cuda.is_available():
+        rc = L.iga2l_setup(2, 2, 1, 16, 3, 2, ctypes.byref(h))
+        assert rc == pkg.ECUDA and b"no CUDA device" in L.iga2l_last_error()
+        with pytest.raises(pkg.IgaError):
+            pkg.Context(2, 2, 1, 16, 3)
