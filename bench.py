@@ -164,7 +164,8 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)         # one stream for torch ops, library calls and events
+    torch.cuda.set_stream(stream)
     sh = stream.cuda_stream
 
     ctxs, bs, xs, Ns = [], [], [], []

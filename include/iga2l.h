@@ -60,6 +60,7 @@ typedef struct {
                          /*    H = 2h.  Default 2.                                       */
   int vcycle_coarsest_m; /* V-cycle coarsens while m > this (must be >= 1); default 8    */
   void *stream;          /* cudaStream_t for all work; NULL = the context creates its own       */
+                         /*    blocking stream (ordered w.r.t. the legacy default stream)      */
   int use_graph;         /* 1 (default): iterations are replayed from a captured CUDA graph      */
   int nranks, rank;      /* slab partition along the last axis; must be 1, 0 in this version    */
   const void *nccl_id;   /* reserved for nranks > 1 (128-byte ncclUniqueId); must be NULL now   */

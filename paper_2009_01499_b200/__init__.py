@@ -134,7 +134,13 @@ class Context:
         L.iga2l_default_opts(ctypes.byref(o))
         o.coarse_mode, o.coarse_h_factor, o.vcycle_coarsest_m = coarse_mode, coarse_h_factor, vcycle_coarsest_m
         o.use_graph = int(bool(use_graph))
-        o.stream = stream
+        if stream is None:          # default: torch's current stream (0 = legacy -> library's own blocking stream)
+            try:
+                import torch
+                stream = torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else None
+            except Exception:
+                stream = None
+        o.stream = stream or None
         self._h = ctypes.c_void_p()
         ov = block - 1 if overlap is None else overlap
         _check(L.iga2l_setup_ex(dim, p, q, m, block, ov, ctypes.byref(o), ctypes.byref(self._h)))

@@ -74,6 +74,8 @@ struct iga2l_ctx {
     cudaGraphExec_t exec = nullptr;
   } graphs[4];
   int next_graph = 0;
+  QLevelDev *levdev = nullptr;   // device copy of the level table (single-CTA V-cycle tail)
+  int l_cta = -1;                // first level handled by the single-CTA tail kernel
   int launch_counter = 0;
   int launches_per_iter = 0;
   std::vector<void *> allocs;
@@ -132,6 +134,11 @@ void L_apply(iga2l_ctx *c, const double *x, const double *b, double *y, double *
 // n_in per axis = B.cols, n_out = B.rows.  acc: add into out on the last pass.
 void L_tensor(iga2l_ctx *c, int dim, const Band1D &B, const double *in, double *out, double *t1, double *t2,
               int acc) {
+  if (dim == 2) {            // one direct launch: out (+)= (B ⊗ B) in
+    launch_tensor2d(in, out, B, acc, c->st);
+    c->launch_counter++;
+    return;
+  }
   const double *src = in;
   for (int a = 0; a < dim; ++a) {
     const bool last = (a == dim - 1);
@@ -145,6 +152,11 @@ void L_tensor(iga2l_ctx *c, int dim, const Band1D &B, const double *in, double *
 
 void L_vcycle(iga2l_ctx *c, size_t l) {
   Level &L = c->lev[l];
+  if (int(l) == c->l_cta && c->levdev) {   // small tail levels: the whole rest of the cycle in one CTA
+    launch_vcycle_cta(c->dim, c->levdev, int(l), int(c->lev.size()), c->q, c->st);
+    c->launch_counter++;
+    return;
+  }
   if (L.inv) {
     launch_dense_mv(int(L.N), L.inv, L.b, L.x, c->st);
     c->launch_counter++;
@@ -170,7 +182,8 @@ void L_vcycle(iga2l_ctx *c, size_t l) {
 
 void L_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
   for (int col = c0; col < c1; ++col) {
-    launch_schwarz_colour(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st);
+    if (!launch_schwarz_colour_fast(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st))
+      launch_schwarz_colour(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st);
     c->launch_counter++;
   }
 }
@@ -326,7 +339,8 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
   auto bail = [&](int rc) { iga2l_destroy(c); return rc; };
   if (o.stream) c->st = static_cast<cudaStream_t>(o.stream);
   else {
-    if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess)
+    // blocking stream: ordered after work on the legacy default stream (safe with torch's default)
+    if (cudaStreamCreate(&c->st) != cudaSuccess)
       return bail(fail(IGA2L_ECUDA, "cudaStreamCreate failed"));
     c->own_stream = true;
   }
@@ -369,6 +383,17 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
     if ((rc = upload_band(c, L.P, P)) || (rc = upload_band(c, L.PT, transpose(P)))) return bail(rc);
     c->lev.push_back(L);
     ml /= 2;
+  }
+  {  // device level table for the single-CTA V-cycle tail (levels with <= kCtaTailMax unknowns)
+    constexpr int64_t kCtaTailMax = 20000;
+    std::vector<QLevelDev> tab(c->lev.size());
+    for (size_t l = 0; l < c->lev.size(); ++l) {
+      const Level &L = c->lev[l];
+      tab[l] = QLevelDev{L.n, L.N, L.K, L.M, L.x, L.b, L.r, L.t1, L.t2, L.P.b, L.PT.b, L.inv};
+      if (c->l_cta < 0 && L.N <= kCtaTailMax && c->lev.size() > 1) c->l_cta = int(l);
+    }
+    if (c->l_cta >= 0 && (rc = upload(c, &c->levdev, tab))) return bail(rc);
+    if (c->l_cta >= 0) vcycle_cluster_size(dim);   // probe outside any stream capture
   }
   c->npartial = apply_num_partials(dim, p, n1);
   if ((rc = dalloc(c, &c->r, N)) || (rc = dalloc(c, &c->t1, N)) || (rc = dalloc(c, &c->t2, N)) ||

@@ -4,6 +4,9 @@
 #include <algorithm>
 #include <cstdio>
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace iga2l {
 
 namespace {
@@ -193,8 +196,8 @@ __global__ void __launch_bounds__(128) k_schwarz(int p, int s, int n1, const dou
   const int bid = blockIdx.x;
   const int j0 = bid % nb0, j1 = (bid / nb0) % nb1, j2 = bid / (nb0 * nb1);
   const int cx = c0 + D * j0, cy = c1 + D * j1, cz = (DIM == 3) ? c2 + D * j2 : 0;
-  const int ox = cx - w - p, oy = cy - w - p, oz = cz - w - p;   // window origin
-  const int bx = cx - w, by = cy - w, bz = cz - w;                // block origin
+  const int ox = cx - w - p, oy = cy - w - p, oz = (DIM == 3) ? cz - w - p : 0;   // window origin
+  const int bx = cx - w, by = cy - w, bz = (DIM == 3) ? cz - w : 0;                // block origin
   const int s2 = s * s, sd = (DIM == 3) ? s2 * s : s2;
   double *X = sm;
   const int nX = (DIM == 3) ? Wn * Wn * Wn : Wn * Wn;
@@ -562,6 +565,353 @@ void launch_tensor_rhs(int dim, int64_t n1, const double *g, double scale, doubl
   int64_t total = n1 * n1;
   if (dim == 3) total *= n1;
   k_tensor_rhs<<<grid_for(total, 256), 256, 0, st>>>(dim, n1, g, scale, b, total);
+}
+
+}  // namespace iga2l
+
+// ============================================================================================
+// Optimised paths (v2): warp-per-block 2D Schwarz colour kernel (compile-time p, s), single-CTA
+// V-cycle tail, direct 2D tensor transfers.
+// ============================================================================================
+namespace iga2l {
+namespace {
+
+// One warp per Schwarz block; WPB blocks (warps) per CTA; only __syncwarp inside (blocks of one
+// colour are independent).  Same arithmetic as k_schwarz<2>, compile-time sizes.  Everything the
+// block needs (x window, b_B, the 1D band rows of its rows/columns, its FD tables) is fetched in
+// ONE round of independent loads into shared memory, so the kernel costs one L2 round trip.
+template <int P, int S, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_schwarz2d_w(int n1, const double *__restrict__ K,
+                                                         const double *__restrict__ M, const double *__restrict__ Vt,
+                                                         const double *__restrict__ lamt,
+                                                         const double *__restrict__ b, double *__restrict__ x,
+                                                         int c0, int c1, int D, int nb0, int nblk) {
+  constexpr int W = 2 * P + 1, Wn = S + 2 * P, w = (S - 1) / 2, S2 = S * S;
+  constexpr int PER = Wn * Wn + 2 * S * Wn + 3 * S2 + 4 * S * W + 2 * S2 + 2 * S;
+  extern __shared__ double sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bid = blockIdx.x * WPB + warp;
+  if (bid >= nblk) return;
+  double *X = sm + warp * PER, *Pa = X + Wn * Wn, *Pb = Pa + S * Wn, *R = Pb + S * Wn, *Q = R + S2;
+  double *Bb = Q + S2;                                   // b_B
+  double *Kx = Bb + S2, *Mx = Kx + S * W, *Ky = Mx + S * W, *My = Ky + S * W;   // band rows
+  double *Vx = My + S * W, *Vy = Vx + S2, *Lx = Vy + S2, *Ly = Lx + S;
+  const int j1 = bid / nb0, j0 = bid - j1 * nb0;
+  const int cx = c0 + D * j0, cy = c1 + D * j1;
+  const int ox = cx - w - P, oy = cy - w - P, bx = cx - w, by = cy - w;
+  const unsigned un = unsigned(n1);
+  // ---- one round of independent loads ----
+  for (int i = lane; i < Wn * Wn; i += 32) {
+    const int wy = i / Wn, wx = i - wy * Wn;
+    const int gx = ox + wx, gy = oy + wy;
+    X[i] = (unsigned(gx) < un && unsigned(gy) < un) ? x[(int64_t)gy * n1 + gx] : 0.0;
+  }
+  for (int i = lane; i < S * W; i += 32) {
+    const int l = i / W, t = i - l * W;
+    const int gx = bx + l, gy = by + l;
+    const bool okx = unsigned(gx) < un, oky = unsigned(gy) < un;
+    Kx[i] = okx ? K[(int64_t)gx * W + t] : 0.0;
+    Mx[i] = okx ? M[(int64_t)gx * W + t] : 0.0;
+    Ky[i] = oky ? K[(int64_t)gy * W + t] : 0.0;
+    My[i] = oky ? M[(int64_t)gy * W + t] : 0.0;
+  }
+  for (int i = lane; i < S2; i += 32) {
+    const int ly = i / S, lx = i - ly * S, gx = bx + lx, gy = by + ly;
+    Bb[i] = (unsigned(gx) < un && unsigned(gy) < un) ? b[(int64_t)gy * n1 + gx] : 0.0;
+    Vx[i] = Vt[(int64_t)cx * S2 + i];
+    Vy[i] = Vt[(int64_t)cy * S2 + i];
+  }
+  if (lane < S) {
+    Lx[lane] = lamt[(int64_t)cx * S + lane];
+    Ly[lane] = lamt[(int64_t)cy * S + lane];
+  }
+  __syncwarp();
+  for (int i = lane; i < S * Wn; i += 32) {          // pass x: K_x X, M_x X on the block columns
+    const int wy = i / S, lx = i - wy * S;
+    const double *kr = Kx + lx * W, *mr = Mx + lx * W, *xr = X + wy * Wn + lx;
+    double sa = 0.0, sb = 0.0;
+#pragma unroll
+    for (int t = 0; t < W; ++t) {
+      sa = fma(kr[t], xr[t], sa);
+      sb = fma(mr[t], xr[t], sb);
+    }
+    Pa[i] = sa;
+    Pb[i] = sb;
+  }
+  __syncwarp();
+  for (int i = lane; i < S2; i += 32) {              // pass y, block residual r_B = b_B - (A x)_B
+    const int ly = i / S, lx = i - ly * S;
+    const double *kr = Ky + ly * W, *mr = My + ly * W;
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+      acc = fma(mr[u], Pa[(ly + u) * S + lx], acc);
+      acc = fma(kr[u], Pb[(ly + u) * S + lx], acc);
+    }
+    R[i] = Bb[i] - acc;                              // rows/cols outside the grid: band rows are 0
+  }
+  __syncwarp();
+  for (int i = lane; i < S2; i += 32) {              // Q[ly][j] = Σ_lx Vx[lx][j] R[ly][lx]
+    const int ly = i / S, j = i - ly * S;
+    double a = 0.0;
+#pragma unroll
+    for (int l = 0; l < S; ++l) a = fma(Vx[l * S + j], R[ly * S + l], a);
+    Q[i] = a;
+  }
+  __syncwarp();
+  for (int i = lane; i < S2; i += 32) {              // R[k][j] = Σ_ly Vy[ly][k] Q[ly][j] / (λx_j + λy_k)
+    const int k = i / S, j = i - k * S;
+    double a = 0.0;
+#pragma unroll
+    for (int l = 0; l < S; ++l) a = fma(Vy[l * S + k], Q[l * S + j], a);
+    R[i] = a / (Lx[j] + Ly[k]);
+  }
+  __syncwarp();
+  for (int i = lane; i < S2; i += 32) {              // Q[ly][j] = Σ_k Vy[ly][k] R[k][j]
+    const int ly = i / S, j = i - ly * S;
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < S; ++k) a = fma(Vy[ly * S + k], R[k * S + j], a);
+    Q[i] = a;
+  }
+  __syncwarp();
+  for (int i = lane; i < S2; i += 32) {              // δ[ly][lx] = Σ_j Vx[lx][j] Q[ly][j];  x_B += δ
+    const int ly = i / S, lx = i - ly * S, gx = bx + lx, gy = by + ly;
+    double a = 0.0;
+#pragma unroll
+    for (int j = 0; j < S; ++j) a = fma(Vx[lx * S + j], Q[ly * S + j], a);
+    if (unsigned(gx) < un && unsigned(gy) < un) x[(int64_t)gy * n1 + gx] = X[(ly + P) * Wn + lx + P] + a;
+  }
+}
+
+template <int P, int S, int WPB>
+bool try_schwarz2d(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
+                   const double *b, double *x, int c0, int c1, int D, int nb0, int nblk, cudaStream_t st) {
+  if (p != P || s != S) return false;
+  constexpr int Wn = S + 2 * P;
+  constexpr int W = 2 * P + 1;
+  constexpr size_t sm = sizeof(double) * WPB * (Wn * Wn + 2 * S * Wn + 5 * S * S + 4 * S * W + 2 * S);
+  ensure_smem(k_schwarz2d_w<P, S, WPB>, sm);
+  k_schwarz2d_w<P, S, WPB><<<(nblk + WPB - 1) / WPB, WPB * 32, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, D,
+                                                                         nb0, nblk);
+  return true;
+}
+
+// 2D tensor transfer, direct: out[ry][rx] (+)= Σ_{ky,kx} c[ry][ky] c[rx][kx] in[lo[ry]+ky][lo[rx]+kx]
+__global__ void k_tensor2d(const double *__restrict__ in, double *__restrict__ out, int nin, int rows, int W,
+                           const int *__restrict__ lo, const double *__restrict__ c, int acc) {
+  const int64_t total = (int64_t)rows * rows;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int ry = int(idx / rows), rx = int(idx - (int64_t)ry * rows);
+    const int ly = lo[ry], lx = lo[rx];
+    double s = 0.0;
+    for (int ky = 0; ky < W; ++ky) {
+      const int iy = ly + ky;
+      if (unsigned(iy) >= unsigned(nin)) continue;
+      const double cy = c[(int64_t)ry * W + ky];
+      double t = 0.0;
+      for (int kx = 0; kx < W; ++kx) {
+        const int ix = lx + kx;
+        if (unsigned(ix) < unsigned(nin)) t = fma(c[(int64_t)rx * W + kx], in[(int64_t)iy * nin + ix], t);
+      }
+      s = fma(cy, t, s);
+    }
+    out[idx] = acc ? out[idx] + s : s;
+  }
+}
+
+// ---------------- V-cycle over the small tail levels in ONE thread-block cluster -------------
+// All CTAs of the cluster share the loops; phases are separated by barrier.cluster (release /
+// acquire at cluster scope; it also invalidates L1, so plain loads see the other SMs' stores).
+struct Team {
+  int64_t tid, nthr;
+  __device__ void sync() const { cg::this_cluster().sync(); }
+};
+
+__device__ void team_band_axis(const Team &tm, const double *in, double *out, int64_t outer, int nin, int64_t inner,
+                               const Band1D &B, int acc) {
+  const int64_t total = outer * B.rows * inner;
+  for (int64_t idx = tm.tid; idx < total; idx += tm.nthr) {
+    const int64_t i = idx % inner;
+    const int r = int((idx / inner) % B.rows);
+    const int64_t o = idx / (inner * B.rows);
+    const int l0 = B.lo[r];
+    double s = 0.0;
+    for (int k = 0; k < B.W; ++k) {
+      const int col = l0 + k;
+      if (col >= 0 && col < nin) s = fma(B.c[(int64_t)r * B.W + k], in[(o * nin + col) * inner + i], s);
+    }
+    out[idx] = acc ? out[idx] + s : s;
+  }
+}
+
+__device__ void team_tensor2d(const Team &tm, const Band1D &B, const double *in, double *out, int acc) {
+  const int64_t total = (int64_t)B.rows * B.rows;
+  for (int64_t idx = tm.tid; idx < total; idx += tm.nthr) {
+    const int ry = int(idx / B.rows), rx = int(idx - (int64_t)ry * B.rows);
+    const int ly = B.lo[ry], lx = B.lo[rx];
+    double s = 0.0;
+    for (int ky = 0; ky < B.W; ++ky) {
+      const int iy = ly + ky;
+      if (unsigned(iy) >= unsigned(B.cols)) continue;
+      double t = 0.0;
+      for (int kx = 0; kx < B.W; ++kx) {
+        const int ix = lx + kx;
+        if (unsigned(ix) < unsigned(B.cols)) t = fma(B.c[(int64_t)rx * B.W + kx], in[(int64_t)iy * B.cols + ix], t);
+      }
+      s = fma(B.c[(int64_t)ry * B.W + ky], t, s);
+    }
+    out[idx] = acc ? out[idx] + s : s;
+  }
+}
+
+template <int DIM>
+__device__ void team_tensor(const Team &tm, const Band1D &B, const double *in, double *out, double *t1, double *t2,
+                            int acc) {
+  if (DIM == 2) {
+    team_tensor2d(tm, B, in, out, acc);
+    tm.sync();
+    return;
+  }
+  const double *src = in;
+  int64_t inner = 1, outer = 1;
+  for (int a = 1; a < DIM; ++a) outer *= B.cols;
+  for (int a = 0; a < DIM; ++a) {
+    const bool last = (a == DIM - 1);
+    double *dst = last ? out : (a % 2 == 0 ? t1 : t2);
+    team_band_axis(tm, src, dst, outer, B.cols, inner, B, last ? acc : 0);
+    tm.sync();
+    src = dst;
+    inner *= B.rows;
+    if (a + 1 < DIM) outer /= B.cols;
+  }
+}
+
+template <int DIM>
+__device__ void team_gs(const Team &tm, const QLevelDev &L, int q) {
+  const int st = q + 1;
+  int ncol = 1;
+  for (int a = 0; a < DIM; ++a) ncol *= st;
+  for (int col = 0; col < ncol; ++col) {
+    const int c0 = col % st, c1 = (col / st) % st, c2 = (DIM == 3) ? col / (st * st) : 0;
+    const int na0 = (L.n - c0 + q) / st, na1 = (L.n - c1 + q) / st, na2 = (DIM == 3) ? (L.n - c2 + q) / st : 1;
+    const int64_t tot = (c0 < L.n && c1 < L.n && c2 < L.n) ? (int64_t)na0 * na1 * na2 : 0;
+    for (int64_t idx = tm.tid; idx < tot; idx += tm.nthr) {
+      const int ix = c0 + st * int(idx % na0), iy = c1 + st * int((idx / na0) % na1);
+      const int iz = (DIM == 3) ? c2 + st * int(idx / ((int64_t)na0 * na1)) : 0;
+      double dg;
+      const double ax = q_apply_point<DIM>(q, L.n, L.K, L.M, L.x, ix, iy, iz, &dg);
+      const int64_t g = ((int64_t)iz * L.n + iy) * L.n + ix;
+      L.x[g] += (L.b[g] - ax) / dg;
+    }
+    tm.sync();
+  }
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(1024) k_vcycle_cluster(const QLevelDev *__restrict__ levs, int l0, int nlev, int q) {
+  cg::cluster_group cl = cg::this_cluster();
+  const Team tm{(int64_t)cl.block_rank() * blockDim.x + threadIdx.x, (int64_t)cl.num_blocks() * blockDim.x};
+  for (int l = l0; l < nlev - 1; ++l) {
+    const QLevelDev L = levs[l];
+    for (int64_t i = tm.tid; i < L.N; i += tm.nthr) L.x[i] = 0.0;          // zero initial guess (A13)
+    tm.sync();
+    team_gs<DIM>(tm, L, q);                                                  // pre-smoothing (A11)
+    for (int64_t idx = tm.tid; idx < L.N; idx += tm.nthr) {                  // residual
+      const int ix = int(idx % L.n), iy = int((idx / L.n) % L.n), iz = (DIM == 3) ? int(idx / ((int64_t)L.n * L.n)) : 0;
+      double dg;
+      L.r[idx] = L.b[idx] - q_apply_point<DIM>(q, L.n, L.K, L.M, L.x, ix, iy, iz, &dg);
+    }
+    tm.sync();
+    team_tensor<DIM>(tm, L.PT, L.r, levs[l + 1].b, L.t1, L.t2, 0);          // restriction P^T (A8)
+  }
+  {                                                                          // coarsest: x = A^{-1} b
+    const QLevelDev C = levs[nlev - 1];
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = tm.tid >> 5, nw = tm.nthr >> 5;
+    for (int64_t row = gw; row < C.N; row += nw) {
+      double s = 0.0;
+      for (int64_t j = lane; j < C.N; j += 32) s = fma(C.inv[row * C.N + j], C.b[j], s);
+      s = warp_sum(s);
+      if (lane == 0) C.x[row] = s;
+    }
+    tm.sync();
+  }
+  for (int l = nlev - 2; l >= l0; --l) {
+    const QLevelDev L = levs[l];
+    team_tensor<DIM>(tm, L.P, levs[l + 1].x, L.x, L.t1, L.t2, 1);           // x += P e
+    team_gs<DIM>(tm, L, q);                                                  // post-smoothing
+  }
+}
+
+}  // namespace
+
+bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M, const double *V,
+                                const double *lam, const double *b, double *x, int colour, int D, cudaStream_t st) {
+  if (dim != 2) return false;
+  const int c0 = colour % D, c1 = (colour / D) % D;
+  if (c0 >= n1 || c1 >= n1) return true;   // empty colour
+  const int nb0 = int((n1 - c0 + D - 1) / D), nb1 = int((n1 - c1 + D - 1) / D), nblk = nb0 * nb1;
+  return try_schwarz2d<1, 3, 8>(p, s, n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, st) ||
+         try_schwarz2d<2, 3, 8>(p, s, n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, st) ||
+         try_schwarz2d<3, 3, 8>(p, s, n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, st) ||
+         try_schwarz2d<4, 3, 8>(p, s, n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, st) ||
+         try_schwarz2d<5, 5, 4>(p, s, n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, st) ||
+         try_schwarz2d<6, 5, 4>(p, s, n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, st) ||
+         try_schwarz2d<7, 7, 4>(p, s, n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, st) ||
+         try_schwarz2d<8, 7, 4>(p, s, n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, st);
+}
+
+void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumulate, cudaStream_t st) {
+  const int64_t total = (int64_t)B.rows * B.rows;
+  k_tensor2d<<<grid_for(total, 256), 256, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate);
+}
+
+static int g_vc_cluster[4] = {0, 0, 0, 0};
+
+int vcycle_cluster_size(int dim) {   // largest schedulable cluster (16 non-portable, else 8, 4, 2)
+  int &c = g_vc_cluster[dim];
+  if (c) return c;
+  auto kern = dim == 2 ? k_vcycle_cluster<2> : k_vcycle_cluster<3>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  for (int cs = 16; cs >= 1; cs /= 2) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs, 1, 1);
+    cfg.blockDim = dim3(1024, 1, 1);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) {
+      c = cs;
+      return c;
+    }
+    cudaGetLastError();
+  }
+  c = 1;
+  return c;
+}
+
+void launch_vcycle_cta(int dim, const QLevelDev *levs_dev, int l0, int nlev, int q, cudaStream_t st) {
+  const int cs = vcycle_cluster_size(dim);
+  auto kern = dim == 2 ? k_vcycle_cluster<2> : k_vcycle_cluster<3>;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs, 1, 1);
+  cfg.blockDim = dim3(1024, 1, 1);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, levs_dev, l0, nlev, q);
 }
 
 }  // namespace iga2l

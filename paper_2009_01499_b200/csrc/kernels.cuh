@@ -50,6 +50,29 @@ void launch_dense_mv(int N, const double *Ainv, const double *b, double *x, cuda
 void launch_sum_partials(const double *partial, int n, double *out, double *hist, int *count, int cap,
                          cudaStream_t st);
 
+// ---- optimised paths ------------------------------------------------------------------------
+// Warp-per-block 2D Schwarz colour kernel for the paper's (p, s) pairs; false = not specialised.
+bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M,
+                                const double *V, const double *lam, const double *b, double *x, int colour,
+                                int D, cudaStream_t st);
+// 2D tensor transfer out (+)= (B ⊗ B) in in one launch (in: B.cols^2, out: B.rows^2).
+void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumulate, cudaStream_t st);
+
+// One q-level of the V-cycle hierarchy, as seen by the single-CTA tail kernel (device array).
+struct QLevelDev {
+  int n;
+  int64_t N;
+  const double *K, *M;
+  double *x, *b, *r, *t1, *t2;
+  Band1D P, PT;          // to the next coarser level (unused at the coarsest)
+  const double *inv;     // dense inverse at the coarsest level
+};
+// V-cycle levels l0 .. nlev-1 (down-sweep, dense coarsest solve, up-sweep) in ONE thread-block
+// cluster (phases separated by cluster barriers).  vcycle_cluster_size() must be called once
+// outside stream capture (it probes the largest schedulable cluster).
+int vcycle_cluster_size(int dim);
+void launch_vcycle_cta(int dim, const QLevelDev *levs_dev, int l0, int nlev, int q, cudaStream_t st);
+
 // b[idx] = scale * ∏_a g[i_a]
 void launch_tensor_rhs(int dim, int64_t n1, const double *g, double scale, double *b, cudaStream_t st);
 
