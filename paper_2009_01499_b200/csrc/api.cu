@@ -355,7 +355,11 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
   // transfers (aggressive P:263)
   BandOp R1 = degree_restriction(p, q, n);
   if (o.coarse_h_factor == 2) R1 = multiply(transpose(mesh_prolongation(q, mc)), R1);
-  if ((rc = upload_band(c, c->R, R1)) || (rc = upload_band(c, c->RT, transpose(R1)))) return bail(rc);
+  {
+    const BandOp R1T = transpose(R1);
+    if (R1.W > 16 || R1T.W > 16) return bail(fail(IGA2L_EPARAM, "transfer bandwidth > 16 (p + q too large)"));
+    if ((rc = upload_band(c, c->R, R1)) || (rc = upload_band(c, c->RT, R1T))) return bail(rc);
+  }
   // second-level hierarchy
   int64_t ml = mc;
   while (true) {

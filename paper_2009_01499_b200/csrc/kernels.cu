@@ -344,11 +344,15 @@ __global__ void k_band_axis(const double *__restrict__ in, double *__restrict__ 
     const int r = int((idx / inner) % rows);
     const int64_t o = idx / (inner * rows);
     const int l0 = lo[r];
-    double s = 0.0;
-    for (int k = 0; k < W; ++k) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {            // all gathers independent (W <= 16 checked at setup)
       const int col = l0 + k;
-      if (col >= 0 && col < nin) s = fma(c[(int64_t)r * W + k], in[(o * nin + col) * inner + i], s);
+      const bool ok = k < W && col >= 0 && col < nin;
+      const double v = ok ? c[(int64_t)r * W + k] * in[(o * nin + col) * inner + i] : 0.0;
+      if (k & 1) s1 += v; else s0 += v;
     }
+    const double s = s0 + s1;
     out[idx] = acc ? out[idx] + s : s;
   }
 }
@@ -579,7 +583,9 @@ namespace {
 // One warp per Schwarz block; WPB blocks (warps) per CTA; only __syncwarp inside (blocks of one
 // colour are independent).  Same arithmetic as k_schwarz<2>, compile-time sizes.  Everything the
 // block needs (x window, b_B, the 1D band rows of its rows/columns, its FD tables) is fetched in
-// ONE round of independent loads into shared memory, so the kernel costs one L2 round trip.
+// ONE round of independent loads into shared memory; then four dependent phases:
+//   pass x (K_x X, M_x X), pass y (r_B = b_B - (A x)_B), Z = (Vx^T R Vy) ./ (λx + λy),
+//   δ = Vx Z Vy^T and x_B += δ.   FMA chains are split over two accumulators.
 template <int P, int S, int WPB>
 __global__ void __launch_bounds__(WPB * 32) k_schwarz2d_w(int n1, const double *__restrict__ K,
                                                          const double *__restrict__ M, const double *__restrict__ Vt,
@@ -600,12 +606,10 @@ __global__ void __launch_bounds__(WPB * 32) k_schwarz2d_w(int n1, const double *
   const int cx = c0 + D * j0, cy = c1 + D * j1;
   const int ox = cx - w - P, oy = cy - w - P, bx = cx - w, by = cy - w;
   const unsigned un = unsigned(n1);
-  // ---- one round of independent loads ----
-  for (int i = lane; i < Wn * Wn; i += 32) {
-    const int wy = i / Wn, wx = i - wy * Wn;
-    const int gx = ox + wx, gy = oy + wy;
-    X[i] = (unsigned(gx) < un && unsigned(gy) < un) ? x[(int64_t)gy * n1 + gx] : 0.0;
-  }
+  // Programmatic dependent launch: let the next colour's grid start now; everything that does not
+  // depend on the previous colour (band rows, FD tables, b_B) is loaded before griddepcontrol.wait.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#pragma unroll
   for (int i = lane; i < S * W; i += 32) {
     const int l = i / W, t = i - l * W;
     const int gx = bx + l, gy = by + l;
@@ -615,6 +619,7 @@ __global__ void __launch_bounds__(WPB * 32) k_schwarz2d_w(int n1, const double *
     Ky[i] = oky ? K[(int64_t)gy * W + t] : 0.0;
     My[i] = oky ? M[(int64_t)gy * W + t] : 0.0;
   }
+#pragma unroll
   for (int i = lane; i < S2; i += 32) {
     const int ly = i / S, lx = i - ly * S, gx = bx + lx, gy = by + ly;
     Bb[i] = (unsigned(gx) < un && unsigned(gy) < un) ? b[(int64_t)gy * n1 + gx] : 0.0;
@@ -625,64 +630,75 @@ __global__ void __launch_bounds__(WPB * 32) k_schwarz2d_w(int n1, const double *
     Lx[lane] = lamt[(int64_t)cx * S + lane];
     Ly[lane] = lamt[(int64_t)cy * S + lane];
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // previous colour complete and visible
+#pragma unroll
+  for (int i = lane; i < Wn * Wn; i += 32) {
+    const int wy = i / Wn, wx = i - wy * Wn;
+    const int gx = ox + wx, gy = oy + wy;
+    X[i] = (unsigned(gx) < un && unsigned(gy) < un) ? x[(int64_t)gy * n1 + gx] : 0.0;
+  }
   __syncwarp();
+#pragma unroll
   for (int i = lane; i < S * Wn; i += 32) {          // pass x: K_x X, M_x X on the block columns
     const int wy = i / S, lx = i - wy * S;
     const double *kr = Kx + lx * W, *mr = Mx + lx * W, *xr = X + wy * Wn + lx;
-    double sa = 0.0, sb = 0.0;
+    double sa0 = 0.0, sb0 = 0.0, sa1 = 0.0, sb1 = 0.0;
 #pragma unroll
-    for (int t = 0; t < W; ++t) {
-      sa = fma(kr[t], xr[t], sa);
-      sb = fma(mr[t], xr[t], sb);
+    for (int t = 0; t + 1 < W; t += 2) {
+      sa0 = fma(kr[t], xr[t], sa0);
+      sb0 = fma(mr[t], xr[t], sb0);
+      sa1 = fma(kr[t + 1], xr[t + 1], sa1);
+      sb1 = fma(mr[t + 1], xr[t + 1], sb1);
     }
-    Pa[i] = sa;
-    Pb[i] = sb;
+    sa0 = fma(kr[W - 1], xr[W - 1], sa0);            // W = 2P+1 is odd
+    sb0 = fma(mr[W - 1], xr[W - 1], sb0);
+    Pa[i] = sa0 + sa1;
+    Pb[i] = sb0 + sb1;
   }
   __syncwarp();
+#pragma unroll
   for (int i = lane; i < S2; i += 32) {              // pass y, block residual r_B = b_B - (A x)_B
     const int ly = i / S, lx = i - ly * S;
     const double *kr = Ky + ly * W, *mr = My + ly * W;
-    double acc = 0.0;
+    double a0 = 0.0, a1 = 0.0;
 #pragma unroll
     for (int u = 0; u < W; ++u) {
-      acc = fma(mr[u], Pa[(ly + u) * S + lx], acc);
-      acc = fma(kr[u], Pb[(ly + u) * S + lx], acc);
+      a0 = fma(mr[u], Pa[(ly + u) * S + lx], a0);
+      a1 = fma(kr[u], Pb[(ly + u) * S + lx], a1);
     }
-    R[i] = Bb[i] - acc;                              // rows/cols outside the grid: band rows are 0
+    R[i] = Bb[i] - (a0 + a1);                        // rows/cols outside the grid: band rows are 0
   }
   __syncwarp();
-  for (int i = lane; i < S2; i += 32) {              // Q[ly][j] = Σ_lx Vx[lx][j] R[ly][lx]
-    const int ly = i / S, j = i - ly * S;
-    double a = 0.0;
 #pragma unroll
-    for (int l = 0; l < S; ++l) a = fma(Vx[l * S + j], R[ly * S + l], a);
-    Q[i] = a;
-  }
-  __syncwarp();
-  for (int i = lane; i < S2; i += 32) {              // R[k][j] = Σ_ly Vy[ly][k] Q[ly][j] / (λx_j + λy_k)
+  for (int i = lane; i < S2; i += 32) {              // Z[k][j] = Σ_{ly,lx} Vx[lx][j] R[ly][lx] Vy[ly][k] / (λx_j + λy_k)
     const int k = i / S, j = i - k * S;
-    double a = 0.0;
+    double z0 = 0.0, z1 = 0.0;
 #pragma unroll
-    for (int l = 0; l < S; ++l) a = fma(Vy[l * S + k], Q[l * S + j], a);
-    R[i] = a / (Lx[j] + Ly[k]);
+    for (int ly = 0; ly < S; ++ly) {
+      double t = 0.0;
+#pragma unroll
+      for (int lx = 0; lx < S; ++lx) t = fma(Vx[lx * S + j], R[ly * S + lx], t);
+      if (ly & 1) z1 = fma(Vy[ly * S + k], t, z1); else z0 = fma(Vy[ly * S + k], t, z0);
+    }
+    Q[i] = (z0 + z1) / (Lx[j] + Ly[k]);
   }
   __syncwarp();
-  for (int i = lane; i < S2; i += 32) {              // Q[ly][j] = Σ_k Vy[ly][k] R[k][j]
-    const int ly = i / S, j = i - ly * S;
-    double a = 0.0;
 #pragma unroll
-    for (int k = 0; k < S; ++k) a = fma(Vy[ly * S + k], R[k * S + j], a);
-    Q[i] = a;
-  }
-  __syncwarp();
-  for (int i = lane; i < S2; i += 32) {              // δ[ly][lx] = Σ_j Vx[lx][j] Q[ly][j];  x_B += δ
+  for (int i = lane; i < S2; i += 32) {              // δ[ly][lx] = Σ_{k,j} Vy[ly][k] Vx[lx][j] Z[k][j];  x_B += δ
     const int ly = i / S, lx = i - ly * S, gx = bx + lx, gy = by + ly;
-    double a = 0.0;
+    double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-    for (int j = 0; j < S; ++j) a = fma(Vx[lx * S + j], Q[ly * S + j], a);
-    if (unsigned(gx) < un && unsigned(gy) < un) x[(int64_t)gy * n1 + gx] = X[(ly + P) * Wn + lx + P] + a;
+    for (int k = 0; k < S; ++k) {
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < S; ++j) t = fma(Vx[lx * S + j], Q[k * S + j], t);
+      if (k & 1) d1 = fma(Vy[ly * S + k], t, d1); else d0 = fma(Vy[ly * S + k], t, d0);
+    }
+    if (unsigned(gx) < un && unsigned(gy) < un) x[(int64_t)gy * n1 + gx] = X[(ly + P) * Wn + lx + P] + (d0 + d1);
   }
 }
+
+int g_use_pdl = 0;   // programmatic dependent launch between colour kernels (measured slower: off)
 
 template <int P, int S, int WPB>
 bool try_schwarz2d(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
@@ -692,31 +708,57 @@ bool try_schwarz2d(int p, int s, int64_t n1, const double *K, const double *M, c
   constexpr int W = 2 * P + 1;
   constexpr size_t sm = sizeof(double) * WPB * (Wn * Wn + 2 * S * Wn + 5 * S * S + 4 * S * W + 2 * S);
   ensure_smem(k_schwarz2d_w<P, S, WPB>, sm);
-  k_schwarz2d_w<P, S, WPB><<<(nblk + WPB - 1) / WPB, WPB * 32, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, D,
-                                                                         nb0, nblk);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((nblk + WPB - 1) / WPB);
+  cfg.blockDim = dim3(WPB * 32);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_use_pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_schwarz2d_w<P, S, WPB>, int(n1), K, M, V, lam, b, x, c0, c1, D, nb0, nblk);
   return true;
 }
 
-// 2D tensor transfer, direct: out[ry][rx] (+)= Σ_{ky,kx} c[ry][ky] c[rx][kx] in[lo[ry]+ky][lo[rx]+kx]
+// 2D tensor transfer, direct: out[ry][rx] (+)= Σ_{ky,kx} c[ry][ky] c[rx][kx] in[lo[ry]+ky][lo[rx]+kx].
+// The band loops are unrolled to a compile-time bound so that all W^2 gathers of an output are
+// independent loads (one L2 round trip instead of W^2 dependent ones).
+template <int WMAX>
+__device__ __forceinline__ double tensor2d_point(const double *__restrict__ in, int nin, int W, const int *__restrict__ lo,
+                                                 const double *__restrict__ c, int ry, int rx) {
+  const int ly = lo[ry], lx = lo[rx];
+  double cy[WMAX], cx[WMAX];
+#pragma unroll
+  for (int k = 0; k < WMAX; ++k) {
+    const bool oky = k < W && unsigned(ly + k) < unsigned(nin), okx = k < W && unsigned(lx + k) < unsigned(nin);
+    cy[k] = oky ? c[(int64_t)ry * W + k] : 0.0;
+    cx[k] = okx ? c[(int64_t)rx * W + k] : 0.0;
+  }
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+  for (int ky = 0; ky < WMAX; ++ky) {
+    double t = 0.0;
+#pragma unroll
+    for (int kx = 0; kx < WMAX; ++kx) {
+      const bool ok = cy[ky] != 0.0 && cx[kx] != 0.0;
+      const double v = ok ? in[(int64_t)(ly + ky) * nin + (lx + kx)] : 0.0;
+      t = fma(cx[kx], v, t);
+    }
+    if (ky & 1) s1 = fma(cy[ky], t, s1); else s0 = fma(cy[ky], t, s0);
+  }
+  return s0 + s1;
+}
+
+template <int WMAX>
 __global__ void k_tensor2d(const double *__restrict__ in, double *__restrict__ out, int nin, int rows, int W,
                            const int *__restrict__ lo, const double *__restrict__ c, int acc) {
   const int64_t total = (int64_t)rows * rows;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int ry = int(idx / rows), rx = int(idx - (int64_t)ry * rows);
-    const int ly = lo[ry], lx = lo[rx];
-    double s = 0.0;
-    for (int ky = 0; ky < W; ++ky) {
-      const int iy = ly + ky;
-      if (unsigned(iy) >= unsigned(nin)) continue;
-      const double cy = c[(int64_t)ry * W + ky];
-      double t = 0.0;
-      for (int kx = 0; kx < W; ++kx) {
-        const int ix = lx + kx;
-        if (unsigned(ix) < unsigned(nin)) t = fma(c[(int64_t)rx * W + kx], in[(int64_t)iy * nin + ix], t);
-      }
-      s = fma(cy, t, s);
-    }
+    const double s = tensor2d_point<WMAX>(in, nin, W, lo, c, ry, rx);
     out[idx] = acc ? out[idx] + s : s;
   }
 }
@@ -724,13 +766,79 @@ __global__ void k_tensor2d(const double *__restrict__ in, double *__restrict__ o
 // ---------------- V-cycle over the small tail levels in ONE thread-block cluster -------------
 // All CTAs of the cluster share the loops; phases are separated by barrier.cluster (release /
 // acquire at cluster scope; it also invalidates L1, so plain loads see the other SMs' stores).
+// Each CTA stages the current level's 1D band tables K_q, M_q in shared memory.
+__device__ unsigned long long *g_vc_trace = nullptr;   // optional phase timestamps (debug builds)
+__device__ int g_vc_trace_n = 0;
+
 struct Team {
   int64_t tid, nthr;
-  __device__ void sync() const { cg::this_cluster().sync(); }
+  __device__ void sync() const {
+    cg::this_cluster().sync();
+    if (g_vc_trace && tid == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g_vc_trace[g_vc_trace_n++ & 1023] = t;
+    }
+  }
 };
 
-__device__ void team_band_axis(const Team &tm, const double *in, double *out, int64_t outer, int nin, int64_t inner,
-                               const Band1D &B, int acc) {
+constexpr int kVcMaxN = 160;   // tail levels have <= 20000 unknowns: n <= 141 (2D), 27 (3D)
+
+template <int DIM, int Q>
+__device__ __forceinline__ double q_point(int n, const double *sK, const double *sM, const double *x, int ix, int iy,
+                                          int iz, double *diag) {
+  constexpr int W = 2 * Q + 1;
+  const unsigned un = unsigned(n);
+  double kx[W], mx[W], ky[W], my[W];
+#pragma unroll
+  for (int t = 0; t < W; ++t) {
+    kx[t] = sK[ix * W + t]; mx[t] = sM[ix * W + t];
+    ky[t] = sK[iy * W + t]; my[t] = sM[iy * W + t];
+  }
+  double acc0 = 0.0, acc1 = 0.0;
+  if (DIM == 2) {
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+      const int jy = iy + u - Q;
+      const bool oky = unsigned(jy) < un;
+#pragma unroll
+      for (int t = 0; t < W; ++t) {
+        const int jx = ix + t - Q;
+        const double xv = (oky && unsigned(jx) < un) ? x[(int64_t)jy * n + jx] : 0.0;
+        if (t & 1) acc1 = fma(kx[t] * my[u] + mx[t] * ky[u], xv, acc1);
+        else acc0 = fma(kx[t] * my[u] + mx[t] * ky[u], xv, acc0);
+      }
+    }
+    *diag = kx[Q] * my[Q] + mx[Q] * ky[Q];
+  } else {
+    double kz[W], mz[W];
+#pragma unroll
+    for (int t = 0; t < W; ++t) { kz[t] = sK[iz * W + t]; mz[t] = sM[iz * W + t]; }
+#pragma unroll
+    for (int v = 0; v < W; ++v) {
+      const int jz = iz + v - Q;
+      const bool okz = unsigned(jz) < un;
+#pragma unroll
+      for (int u = 0; u < W; ++u) {
+        const int jy = iy + u - Q;
+        const bool oky = okz && unsigned(jy) < un;
+        const double cyz_k = my[u] * mz[v], cyz_m = ky[u] * mz[v] + my[u] * kz[v];
+#pragma unroll
+        for (int t = 0; t < W; ++t) {
+          const int jx = ix + t - Q;
+          const double xv = (oky && unsigned(jx) < un) ? x[((int64_t)jz * n + jy) * n + jx] : 0.0;
+          if (t & 1) acc1 = fma(kx[t] * cyz_k + mx[t] * cyz_m, xv, acc1);
+          else acc0 = fma(kx[t] * cyz_k + mx[t] * cyz_m, xv, acc0);
+        }
+      }
+    }
+    *diag = kx[Q] * my[Q] * mz[Q] + mx[Q] * ky[Q] * mz[Q] + mx[Q] * my[Q] * kz[Q];
+  }
+  return acc0 + acc1;
+}
+
+__device__ __forceinline__ void team_band_axis(const Team tm, const double *in, double *out, int64_t outer, int nin,
+                                               int64_t inner, const Band1D B, int acc) {
   const int64_t total = outer * B.rows * inner;
   for (int64_t idx = tm.tid; idx < total; idx += tm.nthr) {
     const int64_t i = idx % inner;
@@ -746,29 +854,19 @@ __device__ void team_band_axis(const Team &tm, const double *in, double *out, in
   }
 }
 
-__device__ void team_tensor2d(const Team &tm, const Band1D &B, const double *in, double *out, int acc) {
+__device__ __forceinline__ void team_tensor2d(const Team tm, const Band1D B, const double *in, double *out, int acc) {
   const int64_t total = (int64_t)B.rows * B.rows;
   for (int64_t idx = tm.tid; idx < total; idx += tm.nthr) {
     const int ry = int(idx / B.rows), rx = int(idx - (int64_t)ry * B.rows);
-    const int ly = B.lo[ry], lx = B.lo[rx];
-    double s = 0.0;
-    for (int ky = 0; ky < B.W; ++ky) {
-      const int iy = ly + ky;
-      if (unsigned(iy) >= unsigned(B.cols)) continue;
-      double t = 0.0;
-      for (int kx = 0; kx < B.W; ++kx) {
-        const int ix = lx + kx;
-        if (unsigned(ix) < unsigned(B.cols)) t = fma(B.c[(int64_t)rx * B.W + kx], in[(int64_t)iy * B.cols + ix], t);
-      }
-      s = fma(B.c[(int64_t)ry * B.W + ky], t, s);
-    }
+    const double s = B.W <= 4 ? tensor2d_point<4>(in, B.cols, B.W, B.lo, B.c, ry, rx)
+                              : tensor2d_point<8>(in, B.cols, B.W, B.lo, B.c, ry, rx);
     out[idx] = acc ? out[idx] + s : s;
   }
 }
 
 template <int DIM>
-__device__ void team_tensor(const Team &tm, const Band1D &B, const double *in, double *out, double *t1, double *t2,
-                            int acc) {
+__device__ __forceinline__ void team_tensor(const Team tm, const Band1D B, const double *in, double *out, double *t1,
+                                            double *t2, int acc) {
   if (DIM == 2) {
     team_tensor2d(tm, B, in, out, acc);
     tm.sync();
@@ -788,60 +886,84 @@ __device__ void team_tensor(const Team &tm, const Band1D &B, const double *in, d
   }
 }
 
-template <int DIM>
-__device__ void team_gs(const Team &tm, const QLevelDev &L, int q) {
-  const int st = q + 1;
-  int ncol = 1;
-  for (int a = 0; a < DIM; ++a) ncol *= st;
+template <int DIM, int Q>
+__device__ __forceinline__ void team_gs(const Team tm, const int n, double *__restrict__ x,
+                                        const double *__restrict__ bb, const double *sK, const double *sM) {
+  constexpr int st = Q + 1;
+  constexpr int ncol = (DIM == 3) ? st * st * st : st * st;
+#pragma unroll 1
   for (int col = 0; col < ncol; ++col) {
     const int c0 = col % st, c1 = (col / st) % st, c2 = (DIM == 3) ? col / (st * st) : 0;
-    const int na0 = (L.n - c0 + q) / st, na1 = (L.n - c1 + q) / st, na2 = (DIM == 3) ? (L.n - c2 + q) / st : 1;
-    const int64_t tot = (c0 < L.n && c1 < L.n && c2 < L.n) ? (int64_t)na0 * na1 * na2 : 0;
-    for (int64_t idx = tm.tid; idx < tot; idx += tm.nthr) {
-      const int ix = c0 + st * int(idx % na0), iy = c1 + st * int((idx / na0) % na1);
-      const int iz = (DIM == 3) ? c2 + st * int(idx / ((int64_t)na0 * na1)) : 0;
+    const int na0 = (n - c0 + Q) / st, na1 = (n - c1 + Q) / st, na2 = (DIM == 3) ? (n - c2 + Q) / st : 1;
+    const int tot = (c0 < n && c1 < n && c2 < n) ? na0 * na1 * na2 : 0;
+    for (int idx = int(tm.tid); idx < tot; idx += int(tm.nthr)) {
+      const int ix = c0 + st * (idx % na0), iy = c1 + st * ((idx / na0) % na1);
+      const int iz = (DIM == 3) ? c2 + st * (idx / (na0 * na1)) : 0;
       double dg;
-      const double ax = q_apply_point<DIM>(q, L.n, L.K, L.M, L.x, ix, iy, iz, &dg);
-      const int64_t g = ((int64_t)iz * L.n + iy) * L.n + ix;
-      L.x[g] += (L.b[g] - ax) / dg;
+      const double ax = q_point<DIM, Q>(n, sK, sM, x, ix, iy, iz, &dg);
+      const int g = (iz * n + iy) * n + ix;
+      x[g] += (bb[g] - ax) / dg;
     }
     tm.sync();
   }
 }
 
-template <int DIM>
-__global__ void __launch_bounds__(1024) k_vcycle_cluster(const QLevelDev *__restrict__ levs, int l0, int nlev, int q) {
+template <int Q>
+__device__ __forceinline__ void stage_tables(const int n, const double *K, const double *M, double *sK, double *sM) {
+  constexpr int W = 2 * Q + 1;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n * W; i += blockDim.x) {
+    sK[i] = K[i];
+    sM[i] = M[i];
+  }
+  __syncthreads();
+}
+
+template <int DIM, int Q>
+__global__ void __launch_bounds__(512) k_vcycle_cluster(const QLevelDev *__restrict__ levs, int l0, int nlev) {
+  __shared__ double sK[kVcMaxN * (2 * Q + 1)], sM[kVcMaxN * (2 * Q + 1)];
   cg::cluster_group cl = cg::this_cluster();
   const Team tm{(int64_t)cl.block_rank() * blockDim.x + threadIdx.x, (int64_t)cl.num_blocks() * blockDim.x};
   for (int l = l0; l < nlev - 1; ++l) {
-    const QLevelDev L = levs[l];
-    for (int64_t i = tm.tid; i < L.N; i += tm.nthr) L.x[i] = 0.0;          // zero initial guess (A13)
+    const int n = levs[l].n, N = int(levs[l].N);
+    double *x = levs[l].x, *r = levs[l].r, *t1 = levs[l].t1, *t2 = levs[l].t2;
+    const double *bb = levs[l].b;
+    const Band1D PT = levs[l].PT;
+    double *bnext = levs[l + 1].b;
+    stage_tables<Q>(n, levs[l].K, levs[l].M, sK, sM);
+    for (int i = int(tm.tid); i < N; i += int(tm.nthr)) x[i] = 0.0;        // zero initial guess (A13)
     tm.sync();
-    team_gs<DIM>(tm, L, q);                                                  // pre-smoothing (A11)
-    for (int64_t idx = tm.tid; idx < L.N; idx += tm.nthr) {                  // residual
-      const int ix = int(idx % L.n), iy = int((idx / L.n) % L.n), iz = (DIM == 3) ? int(idx / ((int64_t)L.n * L.n)) : 0;
+    team_gs<DIM, Q>(tm, n, x, bb, sK, sM);                                   // pre-smoothing (A11)
+    for (int idx = int(tm.tid); idx < N; idx += int(tm.nthr)) {              // residual
+      const int ix = idx % n, iy = (idx / n) % n, iz = (DIM == 3) ? idx / (n * n) : 0;
       double dg;
-      L.r[idx] = L.b[idx] - q_apply_point<DIM>(q, L.n, L.K, L.M, L.x, ix, iy, iz, &dg);
+      r[idx] = bb[idx] - q_point<DIM, Q>(n, sK, sM, x, ix, iy, iz, &dg);
     }
     tm.sync();
-    team_tensor<DIM>(tm, L.PT, L.r, levs[l + 1].b, L.t1, L.t2, 0);          // restriction P^T (A8)
+    team_tensor<DIM>(tm, PT, r, bnext, t1, t2, 0);                           // restriction P^T (A8)
   }
   {                                                                          // coarsest: x = A^{-1} b
-    const QLevelDev C = levs[nlev - 1];
+    const int NC = int(levs[nlev - 1].N);
+    const double *inv = levs[nlev - 1].inv, *bc = levs[nlev - 1].b;
+    double *xc = levs[nlev - 1].x;
     const int lane = threadIdx.x & 31;
-    const int64_t gw = tm.tid >> 5, nw = tm.nthr >> 5;
-    for (int64_t row = gw; row < C.N; row += nw) {
+    const int gw = int(tm.tid >> 5), nw = int(tm.nthr >> 5);
+    for (int row = gw; row < NC; row += nw) {
       double s = 0.0;
-      for (int64_t j = lane; j < C.N; j += 32) s = fma(C.inv[row * C.N + j], C.b[j], s);
+      for (int j = lane; j < NC; j += 32) s = fma(inv[(int64_t)row * NC + j], bc[j], s);
       s = warp_sum(s);
-      if (lane == 0) C.x[row] = s;
+      if (lane == 0) xc[row] = s;
     }
     tm.sync();
   }
   for (int l = nlev - 2; l >= l0; --l) {
-    const QLevelDev L = levs[l];
-    team_tensor<DIM>(tm, L.P, levs[l + 1].x, L.x, L.t1, L.t2, 1);           // x += P e
-    team_gs<DIM>(tm, L, q);                                                  // post-smoothing
+    const int n = levs[l].n;
+    double *x = levs[l].x, *t1 = levs[l].t1, *t2 = levs[l].t2;
+    const double *bb = levs[l].b, *xnext = levs[l + 1].x;
+    const Band1D P = levs[l].P;
+    stage_tables<Q>(n, levs[l].K, levs[l].M, sK, sM);
+    team_tensor<DIM>(tm, P, xnext, x, t1, t2, 1);                            // x += P e
+    team_gs<DIM, Q>(tm, n, x, bb, sK, sM);                                   // post-smoothing
   }
 }
 
@@ -865,20 +987,34 @@ bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double 
 
 void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumulate, cudaStream_t st) {
   const int64_t total = (int64_t)B.rows * B.rows;
-  k_tensor2d<<<grid_for(total, 256), 256, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate);
+  const int g = grid_for(total, 128);
+  if (B.W <= 4)
+    k_tensor2d<4><<<g, 128, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate);
+  else if (B.W <= 8)
+    k_tensor2d<8><<<g, 128, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate);
+  else
+    k_tensor2d<16><<<g, 128, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate);
 }
 
 static int g_vc_cluster[4] = {0, 0, 0, 0};
 
+void vcycle_trace_enable(unsigned long long *dev_buf) {
+  cudaMemcpyToSymbol(g_vc_trace, &dev_buf, sizeof(dev_buf));
+  int z = 0;
+  cudaMemcpyToSymbol(g_vc_trace_n, &z, sizeof(z));
+}
+
 int vcycle_cluster_size(int dim) {   // largest schedulable cluster (16 non-portable, else 8, 4, 2)
   int &c = g_vc_cluster[dim];
   if (c) return c;
-  auto kern = dim == 2 ? k_vcycle_cluster<2> : k_vcycle_cluster<3>;
+  auto kern = dim == 2 ? k_vcycle_cluster<2, 2> : k_vcycle_cluster<3, 2>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  for (auto k2 : {k_vcycle_cluster<2, 1>, k_vcycle_cluster<3, 1>, k_vcycle_cluster<2, 2>, k_vcycle_cluster<3, 2>})
+    cudaFuncSetAttribute(k2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   for (int cs = 16; cs >= 1; cs /= 2) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs, 1, 1);
-    cfg.blockDim = dim3(1024, 1, 1);
+    cfg.blockDim = dim3(512, 1, 1);
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = cs;
@@ -899,10 +1035,11 @@ int vcycle_cluster_size(int dim) {   // largest schedulable cluster (16 non-port
 
 void launch_vcycle_cta(int dim, const QLevelDev *levs_dev, int l0, int nlev, int q, cudaStream_t st) {
   const int cs = vcycle_cluster_size(dim);
-  auto kern = dim == 2 ? k_vcycle_cluster<2> : k_vcycle_cluster<3>;
+  auto kern = dim == 2 ? (q == 1 ? k_vcycle_cluster<2, 1> : k_vcycle_cluster<2, 2>)
+                       : (q == 1 ? k_vcycle_cluster<3, 1> : k_vcycle_cluster<3, 2>);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs, 1, 1);
-  cfg.blockDim = dim3(1024, 1, 1);
+  cfg.blockDim = dim3(512, 1, 1);
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -911,7 +1048,7 @@ void launch_vcycle_cta(int dim, const QLevelDev *levs_dev, int l0, int nlev, int
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, levs_dev, l0, nlev, q);
+  cudaLaunchKernelEx(&cfg, kern, levs_dev, l0, nlev);
 }
 
 }  // namespace iga2l
