@@ -62,8 +62,15 @@ typedef struct {
   void *stream;          /* cudaStream_t for all work; NULL = the context creates its own       */
                          /*    blocking stream (ordered w.r.t. the legacy default stream)      */
   int use_graph;         /* 1 (default): iterations are replayed from a captured CUDA graph      */
-  int nranks, rank;      /* slab partition along the last axis; must be 1, 0 in this version    */
-  const void *nccl_id;   /* reserved for nranks > 1 (128-byte ncclUniqueId); must be NULL now   */
+  int nranks, rank;      /* slab partition along the last axis:                  */
+                         /*   nranks == 1: one domain (rank 0);                                 */
+                         /*   nranks  > 1, rank in [0, nranks): this process owns slab `rank`;  */
+                         /*     vectors are its owned planes [z0, z1) (iga2l_sizes); halos and  */
+                         /*     reductions over NCCL (nccl_id required);                         */
+                         /*   nranks  > 1, rank == -1: all slabs in this process on this device */
+                         /*     (global vectors; halo exchange by device copies; nccl_id NULL)   */
+  const void *nccl_id;   /* 128-byte ncclUniqueId from iga2l_nccl_unique_id() on one rank,       */
+                         /*   broadcast by the caller (NULL unless rank >= 0 and nranks > 1)     */
 } iga2l_opts;
 
 /* Fill *o with the defaults above. */
@@ -144,6 +151,14 @@ int iga2l_get_info(const iga2l_ctx *ctx, iga2l_info *out);
  * used by the device path: K[i*(2p+1) + t+p] = ∫ N_{i+2}' N_{i+2+t}', M likewise (0 outside).
  * K, M: host arrays of (m+p-2)*(2p+1) doubles. */
 int iga2l_host_band_tables(int p, int64_t m, double *K, double *M);
+
+/* 128-byte NCCL unique id (call on one rank, broadcast to all, pass as opts.nccl_id). */
+int iga2l_nccl_unique_id(void *out128);
+
+/* Host-only helper: the slab plan of `rank` among `nranks` for the last axis of n1 = m+p-2 points:
+ * out8 = {z0, z1 (owned planes), za, zb (stored planes incl. halo), first / end block centre handled,
+ *         halo H = block-1+p, feasible (z1-z0 >= H)}. */
+int iga2l_host_slab_plan(int dim, int p, int block, int64_t m, int nranks, int rank, int64_t *out8);
 
 /* Host-only helper: 1D transfer operator used for the restriction, as a dense row-major
  * (n1c x n1) host matrix (h_factor 1: D^{-1} M_c; 2: P_mesh^T D^{-1} M_c). */

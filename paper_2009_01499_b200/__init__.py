@@ -67,6 +67,8 @@ def lib():
         "iga2l_get_info": (i, [vp, P(Info)]),
         "iga2l_host_band_tables": (i, [i, i64, vp, vp]),
         "iga2l_host_restriction_1d": (i, [i, i, i64, i, vp]),
+        "iga2l_host_slab_plan": (i, [i, i, i, i64, i, i, vp]),
+        "iga2l_nccl_unique_id": (i, [vp]),
         "iga2l_destroy": (i, [vp]),
         "iga2l_last_error": (ctypes.c_char_p, []),
         "iga2l_version": (ctypes.c_char_p, []),
@@ -115,6 +117,20 @@ def host_band_tables(p, m):
     return K.reshape(n1, 2 * p + 1), M.reshape(n1, 2 * p + 1)
 
 
+def host_slab_plan(dim, p, block, m, nranks, rank):
+    """Slab plan (z0, z1, za, zb, centre_lo, centre_hi, H, feasible) of `rank` (host-only)."""
+    import numpy as np
+    out = np.zeros(8, dtype=np.int64)
+    _check(lib().iga2l_host_slab_plan(dim, p, block, m, nranks, rank, ctypes.c_void_p(out.ctypes.data)))
+    return dict(zip(["z0", "z1", "za", "zb", "c_lo", "c_hi", "H", "feasible"], [int(v) for v in out]))
+
+
+def nccl_unique_id():
+    buf = (ctypes.c_char * 128)()
+    _check(lib().iga2l_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return bytes(buf)
+
+
 def host_restriction_1d(p, q, m, h_factor):
     import numpy as np
     n1 = m + p - 2
@@ -128,7 +144,7 @@ class Context:
     """One iga2l context (iga2l_setup_ex).  Methods mirror the C entry points."""
 
     def __init__(self, dim, p, q, m, block, overlap=None, coarse_mode=COARSE_VCYCLE, coarse_h_factor=2,
-                 vcycle_coarsest_m=8, stream=None, use_graph=True):
+                 vcycle_coarsest_m=8, stream=None, use_graph=True, nranks=1, rank=0, nccl_id=None):
         L = lib()
         o = Opts()
         L.iga2l_default_opts(ctypes.byref(o))
@@ -141,12 +157,20 @@ class Context:
             except Exception:
                 stream = None
         o.stream = stream or None
+        o.nranks, o.rank = nranks, rank
+        self._id = None
+        if nccl_id is not None:
+            self._id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            o.nccl_id = ctypes.cast(self._id, ctypes.c_void_p)
         self._h = ctypes.c_void_p()
         ov = block - 1 if overlap is None else overlap
         _check(L.iga2l_setup_ex(dim, p, q, m, block, ov, ctypes.byref(o), ctypes.byref(self._h)))
         self.dim, self.p, self.q, self.m, self.s = dim, p, q, m, block
         info = self.info()
         self.n1, self.N, self.n1c, self.Nc = info.n1, info.N, info.n1c, info.Nc
+        nl, z0, z1 = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(L.iga2l_sizes(self._h, ctypes.byref(nl), ctypes.byref(z0), ctypes.byref(z1), None))
+        self.N_local, self.z0, self.z1 = nl.value, z0.value, z1.value
 
     def info(self):
         inf = Info()

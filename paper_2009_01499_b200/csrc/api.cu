@@ -1,7 +1,10 @@
 // C-ABI of libiga2l (layer L2): context setup, the Algorithm 1 schedule, CUDA-graph replay.
 // Contract: include/iga2l.h.  Paper: arXiv 2009.01499 (P:<line> = /root/reference/PAPER.md).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>   // types only; the library is dlopen'ed (the process may already hold torch's copy)
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -79,6 +82,20 @@ struct iga2l_ctx {
   int launch_counter = 0;
   int launches_per_iter = 0;
   std::vector<void *> allocs;
+  // ---- slab decomposition along the last axis; nranks > 1 ----
+  // rank >= 0: one slab per process, halos / reductions over NCCL; rank == -1: all slabs live in
+  // this process on this device (halo exchange = device copies) — the one-GPU test of the same path.
+  int nranks = 1, rank = 0, H = 0;
+  int64_t plane = 0;        // n1^{d-1}
+  struct Slab {
+    int z0 = 0, z1 = 0, za = 0, zb = 0;          // owned [z0, z1), stored [za, zb) (halo H each side)
+    double *xp = nullptr, *bp = nullptr, *rp = nullptr, *cpart = nullptr, *t1 = nullptr, *t2 = nullptr;
+    double *partial = nullptr;
+    int npart = 0;
+  };
+  std::vector<Slab> slabs;
+  void *comm = nullptr;     // ncclComm_t
+  double *normparts = nullptr, *normred = nullptr;
 };
 
 namespace {
@@ -264,6 +281,210 @@ int run_iterations(iga2l_ctx *c, const double *b, double *x, int iters, bool wit
   return IGA2L_OK;
 }
 
+// ------------------------------- NCCL (loaded at run time) ---------------------------------
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  const char *(*errStr)(ncclResult_t) = nullptr;
+};
+
+NcclApi &nccl() {
+  static NcclApi a;
+  static bool tried = false;
+  if (tried) return a;
+  tried = true;
+  void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return a;
+#define NCCL_SYM(field, name) a.field = reinterpret_cast<decltype(a.field)>(dlsym(h, name))
+  NCCL_SYM(getUniqueId, "ncclGetUniqueId");
+  NCCL_SYM(commInitRank, "ncclCommInitRank");
+  NCCL_SYM(commDestroy, "ncclCommDestroy");
+  NCCL_SYM(allReduce, "ncclAllReduce");
+  NCCL_SYM(send, "ncclSend");
+  NCCL_SYM(recv, "ncclRecv");
+  NCCL_SYM(groupStart, "ncclGroupStart");
+  NCCL_SYM(groupEnd, "ncclGroupEnd");
+  NCCL_SYM(errStr, "ncclGetErrorString");
+#undef NCCL_SYM
+  a.ok = a.getUniqueId && a.commInitRank && a.commDestroy && a.allReduce && a.send && a.recv && a.groupStart &&
+         a.groupEnd && a.errStr;
+  return a;
+}
+
+#define NC(call)                                                                                   \
+  do {                                                                                             \
+    ncclResult_t r_ = (call);                                                                      \
+    if (r_ != ncclSuccess) return fail(IGA2L_ENCCL, std::string(#call) + ": " + nccl().errStr(r_)); \
+  } while (0)
+
+// ------------------------------- slab decomposition ----------------------------------------
+// Slab bounds: balanced contiguous planes of the last axis; halo H = s - 1 + p = 2w + p planes.
+void slab_bounds(int64_t n1, int R, int r, int H, int *z0, int *z1, int *za, int *zb) {
+  *z0 = int(n1 * r / R);
+  *z1 = int(n1 * (r + 1) / R);
+  *za = std::max(0, *z0 - H);
+  *zb = int(std::min<int64_t>(n1, *z1 + H));
+}
+
+// Halo exchange of a per-slab padded buffer (x or b): own boundary H planes -> neighbour halos.
+int S_exchange(iga2l_ctx *c, bool which_b) {
+  const int H = c->H;
+  const size_t pb = size_t(c->plane) * sizeof(double);
+  auto buf = [&](iga2l_ctx::Slab &s) { return which_b ? s.bp : s.xp; };
+  if (c->rank < 0) {   // local mode: device copies between neighbouring slabs
+    for (size_t r = 0; r + 1 < c->slabs.size(); ++r) {
+      auto &A = c->slabs[r], &B = c->slabs[r + 1];
+      CU(cudaMemcpyAsync(buf(B) + size_t(B.za - B.za) * c->plane, buf(A) + size_t(A.z1 - H - A.za) * c->plane,
+                         H * pb, cudaMemcpyDeviceToDevice, c->st));   // A's top owned planes -> B's lower halo
+      CU(cudaMemcpyAsync(buf(A) + size_t(A.z1 - A.za) * c->plane, buf(B) + size_t(B.z0 - B.za) * c->plane,
+                         H * pb, cudaMemcpyDeviceToDevice, c->st));   // B's bottom owned planes -> A's upper halo
+    }
+    return IGA2L_OK;
+  }
+  auto &S = c->slabs[0];
+  ncclComm_t comm = static_cast<ncclComm_t>(c->comm);
+  const size_t cnt = size_t(H) * c->plane;
+  NC(nccl().groupStart());
+  if (c->rank > 0) {
+    NC(nccl().send(buf(S) + size_t(S.z0 - S.za) * c->plane, cnt, ncclDouble, c->rank - 1, comm, c->st));
+    NC(nccl().recv(buf(S), cnt, ncclDouble, c->rank - 1, comm, c->st));
+  }
+  if (c->rank < c->nranks - 1) {
+    NC(nccl().send(buf(S) + size_t(S.z1 - H - S.za) * c->plane, cnt, ncclDouble, c->rank + 1, comm, c->st));
+    NC(nccl().recv(buf(S) + size_t(S.z1 - S.za) * c->plane, cnt, ncclDouble, c->rank + 1, comm, c->st));
+  }
+  NC(nccl().groupEnd());
+  return IGA2L_OK;
+}
+
+SlabView sv_owned(const iga2l_ctx::Slab &s) { return SlabView{s.za, s.z0, s.z1}; }
+
+// ||b - A x||^2 over all slabs -> c->norm (and hist if given); deterministic order.
+int S_norm(iga2l_ctx *c, bool push_hist) {
+  for (size_t r = 0; r < c->slabs.size(); ++r) {
+    auto &S = c->slabs[r];
+    launch_apply(c->dim, c->p, c->n1, c->K1, c->M1, S.xp, S.bp, S.rp, S.partial, 1, c->st, &S.npart, sv_owned(S));
+    launch_sum_partials(S.partial, S.npart, c->normparts + r, nullptr, nullptr, 0, c->st);
+    c->launch_counter += 2;
+  }
+  const double *src = c->normparts;
+  int n = int(c->slabs.size());
+  if (c->rank >= 0 && c->nranks > 1) {
+    NC(nccl().allReduce(c->normparts, c->normred, 1, ncclDouble, ncclSum, static_cast<ncclComm_t>(c->comm), c->st));
+    src = c->normred;
+    n = 1;
+  }
+  launch_sum_partials(src, n, c->norm, push_hist ? c->hist : nullptr, push_hist ? c->hist_count : nullptr,
+                      c->hist_cap, c->st);
+  c->launch_counter++;
+  return IGA2L_OK;
+}
+
+// One iteration of Algorithm 1 on the slab decomposition.
+int S_iteration(iga2l_ctx *c, bool with_norm) {
+  const int n1 = int(c->n1), d = c->dim;
+  const int per_class = int(ipow(c->D, d - 1));   // colours of one last-axis class (class outermost, A5)
+  for (int zc = 0; zc < c->D; ++zc) {
+    if (zc > 0)
+      if (int rc = S_exchange(c, false)) return rc;   // halos current at the start of every class
+    for (int k = 0; k < per_class; ++k) {
+      const int col = zc * per_class + k;
+      for (auto &S : c->slabs) {
+        const SlabView sv{S.za, std::max(0, S.z0 - c->w), std::min(n1, S.z1 + c->w)};
+        if (!launch_schwarz_colour_fast(d, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, S.bp, S.xp, col, c->D,
+                                        c->st, sv))
+          launch_schwarz_colour(d, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, S.bp, S.xp, col, c->D, c->st, sv);
+        c->launch_counter++;
+      }
+    }
+  }
+  if (int rc = S_exchange(c, false)) return rc;        // halos for the residual
+  const Band1D &R = c->R.b;
+  const int nc = R.rows;
+  for (auto &S : c->slabs) {                           // d_p = b - A x on owned planes; partial d_q
+    launch_apply(d, c->p, c->n1, c->K1, c->M1, S.xp, S.bp, S.rp, nullptr, 1, c->st, nullptr, sv_owned(S));
+    c->launch_counter++;
+    if (d == 2) {
+      launch_tensor2d(S.rp, S.cpart, R, 0, c->st, S.z0, S.z1, S.za, 0, nc, 0);
+      c->launch_counter++;
+    } else {
+      const int nz = S.z1 - S.z0;
+      launch_band_axis(S.rp + size_t(S.z0 - S.za) * c->plane, S.t1, int64_t(nz) * n1, n1, 1, R, 0, c->st);
+      launch_band_axis(S.t1, S.t2, nz, n1, nc, R, 0, c->st);
+      launch_band_axis(S.t2, S.cpart, 1, nz, int64_t(nc) * nc, R, 0, c->st, S.z0, S.z1, S.z0);
+      c->launch_counter += 3;
+    }
+  }
+  Level &L0 = c->lev[0];
+  if (c->rank < 0) {                                   // sum the slab partials in a fixed order
+    CU(cudaMemcpyAsync(L0.b, c->slabs[0].cpart, L0.N * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    for (size_t r = 1; r < c->slabs.size(); ++r) {
+      launch_axpy(L0.b, c->slabs[r].cpart, L0.N, c->st);
+      c->launch_counter++;
+    }
+  } else {
+    NC(nccl().allReduce(c->slabs[0].cpart, L0.b, L0.N, ncclDouble, ncclSum, static_cast<ncclComm_t>(c->comm), c->st));
+  }
+  L_vcycle(c, 0);                                      // replicated second level
+  for (auto &S : c->slabs) {                           // x += R^T e on owned AND halo planes
+    if (d == 2) {
+      launch_tensor2d(L0.x, S.xp, c->RT.b, 1, c->st, 0, nc, 0, S.za, S.zb, S.za);
+      c->launch_counter++;
+    } else {
+      const Band1D &RT = c->RT.b;
+      const int nz = S.zb - S.za;
+      launch_band_axis(L0.x, S.t1, 1, nc, int64_t(nc) * nc, RT, 0, c->st, 0, -1, 0, S.za, S.zb);
+      launch_band_axis(S.t1, S.t2, nz, nc, nc, RT, 0, c->st);
+      launch_band_axis(S.t2, S.xp, int64_t(nz) * n1, nc, 1, RT, 1, c->st);
+      c->launch_counter += 3;
+    }
+  }
+  if (with_norm)
+    if (int rc = S_norm(c, true)) return rc;
+  CU(cudaGetLastError());
+  return IGA2L_OK;
+}
+
+// Caller vectors -> slab buffers.  Local mode: the caller passes the GLOBAL vectors (device);
+// NCCL mode: the caller passes its owned planes [z0, z1) only; halos are then exchanged.
+int S_scatter(iga2l_ctx *c, const double *b, const double *x) {
+  const size_t pl = size_t(c->plane);
+  for (auto &S : c->slabs) {
+    if (c->rank < 0) {
+      if (b) CU(cudaMemcpyAsync(S.bp, b + size_t(S.za) * pl, size_t(S.zb - S.za) * pl * 8, cudaMemcpyDeviceToDevice, c->st));
+      if (x) CU(cudaMemcpyAsync(S.xp, x + size_t(S.za) * pl, size_t(S.zb - S.za) * pl * 8, cudaMemcpyDeviceToDevice, c->st));
+    } else {
+      if (b) CU(cudaMemcpyAsync(S.bp + size_t(S.z0 - S.za) * pl, b, size_t(S.z1 - S.z0) * pl * 8, cudaMemcpyDeviceToDevice, c->st));
+      if (x) CU(cudaMemcpyAsync(S.xp + size_t(S.z0 - S.za) * pl, x, size_t(S.z1 - S.z0) * pl * 8, cudaMemcpyDeviceToDevice, c->st));
+    }
+  }
+  if (c->rank >= 0) {
+    if (b)
+      if (int rc = S_exchange(c, true)) return rc;
+    if (x)
+      if (int rc = S_exchange(c, false)) return rc;
+  }
+  return IGA2L_OK;
+}
+
+int S_gather(iga2l_ctx *c, double *x) {
+  const size_t pl = size_t(c->plane);
+  for (auto &S : c->slabs) {
+    double *dst = (c->rank < 0) ? x + size_t(S.z0) * pl : x;
+    CU(cudaMemcpyAsync(dst, S.xp + size_t(S.z0 - S.za) * pl, size_t(S.z1 - S.z0) * pl * 8, cudaMemcpyDeviceToDevice,
+                       c->st));
+  }
+  return IGA2L_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -294,6 +515,7 @@ int iga2l_destroy(iga2l_ctx *c) {
   if (!c) return IGA2L_OK;
   for (auto &g : c->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (c->comm) nccl().commDestroy(static_cast<ncclComm_t>(c->comm));
   for (void *p : c->allocs) cudaFree(p);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
@@ -321,7 +543,18 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
   if (o.coarse_h_factor != 1 && o.coarse_h_factor != 2) return fail(IGA2L_EPARAM, "opts.coarse_h_factor must be 1 or 2");
   if (o.coarse_h_factor == 2 && n % 2) return fail(IGA2L_EPARAM, "aggressive coarsening needs n even (S:358)");
   if (o.vcycle_coarsest_m < 1) return fail(IGA2L_EPARAM, "opts.vcycle_coarsest_m must be >= 1");
-  if (o.nranks != 1 || o.rank != 0 || o.nccl_id) return fail(IGA2L_EPARAM, "opts.nranks must be 1 in this build");
+  if (o.nranks < 1) return fail(IGA2L_EPARAM, "opts.nranks must be >= 1");
+  if (o.nranks == 1 && (o.rank != 0 || o.nccl_id)) return fail(IGA2L_EPARAM, "opts.rank must be 0 and opts.nccl_id NULL when nranks == 1");
+  if (o.nranks > 1 && !((o.rank == -1 && !o.nccl_id) || (o.rank >= 0 && o.rank < o.nranks && o.nccl_id)))
+    return fail(IGA2L_EPARAM, "opts.rank: -1 (all slabs in this process, nccl_id NULL) or 0..nranks-1 with nccl_id");
+  if (o.nranks > 1) {
+    const int H = block - 1 + p;
+    for (int r = 0; r < o.nranks; ++r) {
+      int z0, z1, za, zb;
+      slab_bounds(n + p - 2, o.nranks, r, H, &z0, &z1, &za, &zb);
+      if (z1 - z0 < H) return fail(IGA2L_EPARAM, "opts.nranks: every slab needs >= s - 1 + p planes (SURVEY 8(e))");
+    }
+  }
   const int64_t mc = n / o.coarse_h_factor;
   if (mc + q - 2 < 1) return fail(IGA2L_EPARAM, "second level is empty (n too small)");
   int ndev = 0;
@@ -336,6 +569,11 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
   c->dim = dim; c->p = p; c->q = q; c->s = block; c->w = (block - 1) / 2; c->D = block + p;
   c->colours = int(ipow(c->D, dim));
   c->m = n; c->n1 = n1; c->N = N; c->opts = o;
+  c->nranks = o.nranks;
+  c->rank = o.nranks > 1 ? o.rank : 0;
+  c->H = block - 1 + p;
+  c->plane = ipow(n1, dim - 1);
+  if (o.nranks > 1) c->opts.use_graph = 0;   // slab path: eager launches (NCCL calls in the schedule)
   auto bail = [&](int rc) { iga2l_destroy(c); return rc; };
   if (o.stream) c->st = static_cast<cudaStream_t>(o.stream);
   else {
@@ -400,6 +638,31 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
     if (c->l_cta >= 0) vcycle_cluster_size(dim);   // probe outside any stream capture
   }
   c->npartial = apply_num_partials(dim, p, n1);
+  if (c->nranks > 1) {   // slab buffers (padded with H halo planes) and the communicator
+    const int first = c->rank < 0 ? 0 : c->rank, last = c->rank < 0 ? c->nranks - 1 : c->rank;
+    for (int r = first; r <= last; ++r) {
+      iga2l_ctx::Slab S;
+      slab_bounds(n1, c->nranks, r, c->H, &S.z0, &S.z1, &S.za, &S.zb);
+      const int64_t np = int64_t(S.zb - S.za) * c->plane;
+      if ((rc = dalloc(c, &S.xp, np)) || (rc = dalloc(c, &S.bp, np)) || (rc = dalloc(c, &S.rp, np)) ||
+          (rc = dalloc(c, &S.t1, np)) || (rc = dalloc(c, &S.t2, np)) || (rc = dalloc(c, &S.cpart, c->lev[0].N)) ||
+          (rc = dalloc(c, &S.partial, c->npartial)))
+        return bail(rc);
+      c->slabs.push_back(S);
+    }
+    if ((rc = dalloc(c, &c->normparts, c->nranks)) || (rc = dalloc(c, &c->normred, 1))) return bail(rc);
+    if (c->rank >= 0) {
+      NcclApi &nc = nccl();
+      if (!nc.ok) return bail(fail(IGA2L_ENCCL, "libnccl.so.2 not loadable"));
+      ncclUniqueId id;
+      std::memcpy(&id, o.nccl_id, sizeof(id));
+      ncclComm_t comm;
+      ncclResult_t r = nc.commInitRank(&comm, c->nranks, id, c->rank);
+      if (r != ncclSuccess) return bail(fail(IGA2L_ENCCL, std::string("ncclCommInitRank: ") + nc.errStr(r)));
+      c->comm = comm;
+      c->N = int64_t(c->slabs[0].z1 - c->slabs[0].z0) * c->plane;   // caller vectors: owned planes only
+    }
+  }
   if ((rc = dalloc(c, &c->r, N)) || (rc = dalloc(c, &c->t1, N)) || (rc = dalloc(c, &c->t2, N)) ||
       (rc = dalloc(c, &c->partial, c->npartial)) || (rc = dalloc(c, &c->norm, 1)) ||
       (rc = dalloc(c, &c->hist_count, 1)) || (rc = dalloc(c, &c->hist, 4096)))
@@ -409,7 +672,7 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
   if (cudaMallocHost(&c->pinned, 64 * sizeof(double)) != cudaSuccess) return bail(fail(IGA2L_ENOMEM, "cudaMallocHost"));
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return bail(fail(IGA2L_ECUDA, std::string("setup: ") + cudaGetErrorString(e)));
-  {  // count our kernel launches in one iteration: capture (nothing executes) and discard
+  if (c->nranks == 1) {  // count our kernel launches in one iteration: capture (nothing executes) and discard
     cudaGraph_t graph;
     if (cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
       return bail(fail(IGA2L_ECUDA, "capture for launch count"));
@@ -425,9 +688,10 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
 
 int iga2l_sizes(const iga2l_ctx *c, int64_t *n_local, int64_t *z0, int64_t *z1, int64_t *n1) {
   if (int rc = check_ctx(c)) return rc;
+  const bool one = c->nranks > 1 && c->rank >= 0;
   if (n_local) *n_local = c->N;
-  if (z0) *z0 = 0;
-  if (z1) *z1 = c->n1;
+  if (z0) *z0 = one ? c->slabs[0].z0 : 0;
+  if (z1) *z1 = one ? c->slabs[0].z1 : c->n1;
   if (n1) *n1 = c->n1;
   return IGA2L_OK;
 }
@@ -462,7 +726,18 @@ int iga2l_rhs_sine(iga2l_ctx *c, double *b) {
   const bool dev = is_device_ptr(b);
   if (!dev && !c->hy && dalloc(c, &c->hy, c->N)) return IGA2L_ENOMEM;
   double *dst = dev ? b : c->hy;
-  launch_tensor_rhs(c->dim, c->n1, c->g1, c->dim * pi * pi, dst, c->st);
+  if (c->nranks > 1 && c->rank >= 0) {   // owned planes of the global load vector
+    double *full = nullptr;
+    if (int rc = dalloc(c, &full, ipow(c->n1, c->dim))) return rc;
+    launch_tensor_rhs(c->dim, c->n1, c->g1, c->dim * pi * pi, full, c->st);
+    CU(cudaMemcpyAsync(dst, full + size_t(c->slabs[0].z0) * c->plane, c->N * sizeof(double), cudaMemcpyDeviceToDevice,
+                       c->st));
+    CU(cudaStreamSynchronize(c->st));
+    c->allocs.erase(std::find(c->allocs.begin(), c->allocs.end(), (void *)full));
+    cudaFree(full);
+  } else {
+    launch_tensor_rhs(c->dim, c->n1, c->g1, c->dim * pi * pi, dst, c->st);
+  }
   CU(cudaGetLastError());
   if (!dev) {
     CU(cudaMemcpyAsync(b, dst, c->N * sizeof(double), cudaMemcpyDeviceToHost, c->st));
@@ -489,6 +764,17 @@ int iga2l_apply(iga2l_ctx *c, const double *x, double *y) {
   if (int rc = stage_in(c, x, c->hx, c->N, &sx)) return rc;
   if (!y) return fail(IGA2L_EPARAM, "y is NULL");
   sy = {is_device_ptr(y) ? y : c->hy, !is_device_ptr(y)};
+  if (c->nranks > 1) {
+    if (int rc = S_scatter(c, nullptr, sx.ptr)) return rc;
+    for (auto &S : c->slabs) {
+      launch_apply(c->dim, c->p, c->n1, c->K1, c->M1, S.xp, nullptr, S.rp, nullptr, 0, c->st, nullptr, sv_owned(S));
+      double *dst = const_cast<double *>(sy.ptr) + (c->rank < 0 ? size_t(S.z0) * c->plane : 0);
+      CU(cudaMemcpyAsync(dst, S.rp + size_t(S.z0 - S.za) * c->plane, size_t(S.z1 - S.z0) * c->plane * 8,
+                         cudaMemcpyDeviceToDevice, c->st));
+    }
+    CU(cudaGetLastError());
+    return stage_out(c, y, sy, c->N);
+  }
   L_apply(c, sx.ptr, nullptr, const_cast<double *>(sy.ptr), nullptr, 0);
   CU(cudaGetLastError());
   return stage_out(c, y, sy, c->N);
@@ -501,8 +787,13 @@ int iga2l_residual_norm(iga2l_ctx *c, const double *b, const double *x, double *
   Staged sb, sx;
   if (int rc = stage_in(c, b, c->hb, c->N, &sb)) return rc;
   if (int rc = stage_in(c, x, c->hx, c->N, &sx)) return rc;
-  L_apply(c, sx.ptr, sb.ptr, c->r, c->partial, 1);
-  launch_sum_partials(c->partial, c->npartial, c->norm, nullptr, nullptr, 0, c->st);
+  if (c->nranks > 1) {
+    if (int rc = S_scatter(c, sb.ptr, sx.ptr)) return rc;
+    if (int rc = S_norm(c, false)) return rc;
+  } else {
+    L_apply(c, sx.ptr, sb.ptr, c->r, c->partial, 1);
+    launch_sum_partials(c->partial, c->npartial, c->norm, nullptr, nullptr, 0, c->st);
+  }
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(c->pinned, c->norm, sizeof(double), cudaMemcpyDeviceToHost, c->st));
   CU(cudaStreamSynchronize(c->st));
@@ -519,13 +810,27 @@ int iga2l_iterate(iga2l_ctx *c, const double *b, double *x, int iters, double *r
   if (int rc = stage_in(c, b, c->hb, c->N, &sb)) return rc;
   if (int rc = stage_in(c, x, c->hx, c->N, &sx)) return rc;
   double *xd = const_cast<double *>(sx.ptr);
-  if (res_hist) {
-    if (iters + 1 > c->hist_cap) return fail(IGA2L_EPARAM, "res_hist supports at most 4095 iterations per call");
-    CU(cudaMemsetAsync(c->hist_count, 0, sizeof(int), c->st));
-    L_apply(c, xd, sb.ptr, c->r, c->partial, 1);
-    launch_sum_partials(c->partial, c->npartial, c->norm, c->hist, c->hist_count, c->hist_cap, c->st);
+  if (res_hist && iters + 1 > c->hist_cap) return fail(IGA2L_EPARAM, "res_hist supports at most 4095 iterations per call");
+  if (c->nranks > 1) {   // slab decomposition
+    if (int rc = S_scatter(c, sb.ptr, xd)) return rc;
+    if (res_hist) {
+      CU(cudaMemsetAsync(c->hist_count, 0, sizeof(int), c->st));
+      if (int rc = S_norm(c, true)) return rc;
+    }
+    for (int k = 0; k < iters; ++k) {
+      c->launch_counter = 0;
+      if (int rc = S_iteration(c, res_hist != nullptr)) return rc;
+      if (!res_hist) c->launches_per_iter = c->launch_counter;
+    }
+    if (int rc = S_gather(c, xd)) return rc;
+  } else {
+    if (res_hist) {
+      CU(cudaMemsetAsync(c->hist_count, 0, sizeof(int), c->st));
+      L_apply(c, xd, sb.ptr, c->r, c->partial, 1);
+      launch_sum_partials(c->partial, c->npartial, c->norm, c->hist, c->hist_count, c->hist_cap, c->st);
+    }
+    if (int rc = run_iterations(c, sb.ptr, xd, iters, res_hist != nullptr)) return rc;
   }
-  if (int rc = run_iterations(c, sb.ptr, xd, iters, res_hist != nullptr)) return rc;
   CU(cudaGetLastError());
   if (res_hist) {
     CU(cudaMemcpyAsync(res_hist, c->hist, (iters + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->st));
@@ -545,9 +850,15 @@ int iga2l_solve(iga2l_ctx *c, const double *b, double *x, double rtol, int maxit
   if (int rc = stage_in(c, b, c->hb, c->N, &sb)) return rc;
   if (int rc = stage_in(c, x, c->hx, c->N, &sx)) return rc;
   double *xd = const_cast<double *>(sx.ptr);
+  const bool slab = c->nranks > 1;
   CU(cudaMemsetAsync(c->hist_count, 0, sizeof(int), c->st));
-  L_apply(c, xd, sb.ptr, c->r, c->partial, 1);
-  launch_sum_partials(c->partial, c->npartial, c->norm, nullptr, nullptr, 0, c->st);
+  if (slab) {
+    if (int rc = S_scatter(c, sb.ptr, xd)) return rc;
+    if (int rc = S_norm(c, false)) return rc;
+  } else {
+    L_apply(c, xd, sb.ptr, c->r, c->partial, 1);
+    launch_sum_partials(c->partial, c->npartial, c->norm, nullptr, nullptr, 0, c->st);
+  }
   CU(cudaMemcpyAsync(c->pinned, c->norm, sizeof(double), cudaMemcpyDeviceToHost, c->st));
   CU(cudaStreamSynchronize(c->st));
   const double r0 = std::sqrt(c->pinned[0]);
@@ -555,7 +866,11 @@ int iga2l_solve(iga2l_ctx *c, const double *b, double *x, double rtol, int maxit
   double rk = r0;
   int it = 0;
   while (it < maxit && rk > rtol * r0) {    // stop at ||r_k|| <= rtol ||r_0||
-    if (int rc = run_iterations(c, sb.ptr, xd, 1, true)) return rc;
+    if (slab) {
+      if (int rc = S_iteration(c, true)) return rc;
+    } else if (int rc = run_iterations(c, sb.ptr, xd, 1, true)) {
+      return rc;
+    }
     CU(cudaMemcpyAsync(c->pinned, c->norm, sizeof(double), cudaMemcpyDeviceToHost, c->st));
     CU(cudaStreamSynchronize(c->st));
     rk = std::sqrt(c->pinned[0]);
@@ -564,6 +879,8 @@ int iga2l_solve(iga2l_ctx *c, const double *b, double *x, double rtol, int maxit
   }
   if (iters_out) *iters_out = it;
   if (relres_out) *relres_out = (r0 > 0) ? rk / r0 : 0.0;
+  if (slab)
+    if (int rc = S_gather(c, xd)) return rc;
   if (int rc = stage_out(c, x, sx, c->N)) return rc;
   if (rk > rtol * r0) return fail(IGA2L_NOTCONV, "maxit reached before rtol");
   return IGA2L_OK;
@@ -571,6 +888,7 @@ int iga2l_solve(iga2l_ctx *c, const double *b, double *x, double rtol, int maxit
 
 int iga2l_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
   if (int rc = check_ctx(c)) return rc;
+  if (c->nranks > 1) return fail(IGA2L_EPARAM, "phase entry points are single-domain only (nranks == 1)");
   if (c0 < 0 || c1 < c0 || c1 > c->colours) return fail(IGA2L_EPARAM, "colour range must satisfy 0 <= begin <= end <= D^d");
   if (int rc = ensure_staging(c)) return rc;
   Staged sb, sx;
@@ -583,6 +901,7 @@ int iga2l_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
 
 int iga2l_defect_restrict(iga2l_ctx *c, const double *b, const double *x, double *dq) {
   if (int rc = check_ctx(c)) return rc;
+  if (c->nranks > 1) return fail(IGA2L_EPARAM, "phase entry points are single-domain only (nranks == 1)");
   if (int rc = ensure_staging(c)) return rc;
   Staged sb, sx;
   if (int rc = stage_in(c, b, c->hb, c->N, &sb)) return rc;
@@ -598,6 +917,7 @@ int iga2l_defect_restrict(iga2l_ctx *c, const double *b, const double *x, double
 
 int iga2l_coarse_solve(iga2l_ctx *c, const double *dq, double *e) {
   if (int rc = check_ctx(c)) return rc;
+  if (c->nranks > 1) return fail(IGA2L_EPARAM, "phase entry points are single-domain only (nranks == 1)");
   if (int rc = ensure_staging(c)) return rc;
   if (!dq || !e) return fail(IGA2L_EPARAM, "NULL vector");
   Level &L0 = c->lev[0];
@@ -613,6 +933,7 @@ int iga2l_coarse_solve(iga2l_ctx *c, const double *dq, double *e) {
 
 int iga2l_prolong_add(iga2l_ctx *c, const double *e, double *x) {
   if (int rc = check_ctx(c)) return rc;
+  if (c->nranks > 1) return fail(IGA2L_EPARAM, "phase entry points are single-domain only (nranks == 1)");
   if (int rc = ensure_staging(c)) return rc;
   Staged se, sx;
   if (int rc = stage_in(c, e, c->hcx, c->lev[0].N, &se)) return rc;
@@ -620,6 +941,32 @@ int iga2l_prolong_add(iga2l_ctx *c, const double *e, double *x) {
   L_tensor(c, c->dim, c->RT.b, se.ptr, const_cast<double *>(sx.ptr), c->t1, c->t2, 1);
   CU(cudaGetLastError());
   return stage_out(c, x, sx, c->N);
+}
+
+int iga2l_nccl_unique_id(void *out128) {
+  if (!out128) return fail(IGA2L_EPARAM, "out128 is NULL");
+  NcclApi &nc = nccl();
+  if (!nc.ok) return fail(IGA2L_ENCCL, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  ncclResult_t r = nc.getUniqueId(&id);
+  if (r != ncclSuccess) return fail(IGA2L_ENCCL, std::string("ncclGetUniqueId: ") + nc.errStr(r));
+  std::memcpy(out128, &id, sizeof(id));
+  return IGA2L_OK;
+}
+
+int iga2l_host_slab_plan(int dim, int p, int block, int64_t m, int nranks, int rank, int64_t *out8) {
+  if (dim < 2 || dim > 3 || p < 1 || p > 8 || block < 1 || m < 1 || nranks < 1 || rank < 0 || rank >= nranks || !out8)
+    return fail(IGA2L_EPARAM, "host_slab_plan arguments");
+  const int64_t n1 = m + p - 2;
+  const int H = block - 1 + p, w = (block - 1) / 2;
+  int z0, z1, za, zb;
+  slab_bounds(n1, nranks, rank, H, &z0, &z1, &za, &zb);
+  out8[0] = z0; out8[1] = z1; out8[2] = za; out8[3] = zb;
+  out8[4] = std::max<int64_t>(0, z0 - w);        // block centres handled: [out8[4], out8[5])
+  out8[5] = std::min<int64_t>(n1, z1 + w);
+  out8[6] = H;
+  out8[7] = (z1 - z0 >= H) ? 1 : 0;              // feasible
+  return IGA2L_OK;
 }
 
 int iga2l_host_band_tables(int p, int64_t m, double *K, double *M) {

@@ -37,18 +37,18 @@ template <int TX, int TY>
 __global__ void __launch_bounds__(256) k_apply2d(int p, int n1, const double *__restrict__ K,
                                                  const double *__restrict__ M, const double *__restrict__ x,
                                                  const double *__restrict__ b, double *__restrict__ y,
-                                                 double *__restrict__ partial, int mode) {
+                                                 double *__restrict__ partial, int mode, int zoff, int zlo, int zhi) {
   extern __shared__ double sm[];
   const int W = 2 * p + 1, WX = TX + 2 * p, WY = TY + 2 * p;
   double *X = sm;              // [WY][WX]
   double *Tk = X + WX * WY;    // [WY][TX]
   double *Tm = Tk + WY * TX;   // [WY][TX]
   __shared__ double red[32];
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int x0 = blockIdx.x * TX, y0 = zlo + blockIdx.y * TY;
   for (int i = threadIdx.x; i < WX * WY; i += blockDim.x) {
     const int wy = i / WX, wx = i - wy * WX;
     const int gx = x0 - p + wx, gy = y0 - p + wy;
-    X[i] = (gx >= 0 && gx < n1 && gy >= 0 && gy < n1) ? x[(int64_t)gy * n1 + gx] : 0.0;
+    X[i] = (gx >= 0 && gx < n1 && gy >= 0 && gy < n1) ? x[(int64_t)(gy - zoff) * n1 + gx] : 0.0;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < WY * TX; i += blockDim.x) {   // pass along x: K_x X, M_x X
@@ -68,14 +68,14 @@ __global__ void __launch_bounds__(256) k_apply2d(int p, int n1, const double *__
   double sq = 0.0;
   for (int i = threadIdx.x; i < TY * TX; i += blockDim.x) {   // pass along y: M_y Tk + K_y Tm
     const int ly = i / TX, lx = i - ly * TX, gx = x0 + lx, gy = y0 + ly;
-    if (gx >= n1 || gy >= n1) continue;
+    if (gx >= n1 || gy >= zhi) continue;
     const double *kr = K + (int64_t)gy * W, *mr = M + (int64_t)gy * W;
     double acc = 0.0;
     for (int u = 0; u < W; ++u) {
       acc = fma(mr[u], Tk[(ly + u) * TX + lx], acc);
       acc = fma(kr[u], Tm[(ly + u) * TX + lx], acc);
     }
-    const int64_t g = (int64_t)gy * n1 + gx;
+    const int64_t g = (int64_t)(gy - zoff) * n1 + gx;
     const double out = mode ? b[g] - acc : acc;
     y[g] = out;
     sq = fma(out, out, sq);
@@ -91,7 +91,7 @@ template <int TX, int TY, int TZ>
 __global__ void __launch_bounds__(256) k_apply3d(int p, int n1, const double *__restrict__ K,
                                                  const double *__restrict__ M, const double *__restrict__ x,
                                                  const double *__restrict__ b, double *__restrict__ y,
-                                                 double *__restrict__ partial, int mode) {
+                                                 double *__restrict__ partial, int mode, int zoff, int zlo, int zhi) {
   extern __shared__ double sm[];
   const int W = 2 * p + 1, WX = TX + 2 * p, WY = TY + 2 * p, WZ = TZ + 2 * p;
   double *X = sm;                       // [WZ][WY][WX]
@@ -101,12 +101,12 @@ __global__ void __launch_bounds__(256) k_apply3d(int p, int n1, const double *__
   double *Pe = Pc + TX * TY * WZ;
   __shared__ double red[32];
   const int nbx = (n1 + TX - 1) / TX;
-  const int x0 = (blockIdx.x % nbx) * TX, y0 = (blockIdx.x / nbx) * TY, z0 = blockIdx.y * TZ;
+  const int x0 = (blockIdx.x % nbx) * TX, y0 = (blockIdx.x / nbx) * TY, z0 = zlo + blockIdx.y * TZ;
   for (int i = threadIdx.x; i < WX * WY * WZ; i += blockDim.x) {
     const int wx = i % WX, wy = (i / WX) % WY, wz = i / (WX * WY);
     const int gx = x0 - p + wx, gy = y0 - p + wy, gz = z0 - p + wz;
     X[i] = (gx >= 0 && gx < n1 && gy >= 0 && gy < n1 && gz >= 0 && gz < n1)
-               ? x[((int64_t)gz * n1 + gy) * n1 + gx] : 0.0;
+               ? x[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx] : 0.0;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < TX * WY * WZ; i += blockDim.x) {
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(256) k_apply3d(int p, int n1, const double *__
   for (int i = threadIdx.x; i < TX * TY * TZ; i += blockDim.x) {
     const int lx = i % TX, ly = (i / TX) % TY, lz = i / (TX * TY);
     const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
-    if (gx >= n1 || gy >= n1 || gz >= n1) continue;
+    if (gx >= n1 || gy >= n1 || gz >= zhi) continue;
     const double *kr = K + (int64_t)gz * W, *mr = M + (int64_t)gz * W;
     double acc = 0.0;
     for (int v = 0; v < W; ++v) {
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(256) k_apply3d(int p, int n1, const double *__
       acc = fma(mr[v], Pc[j], acc);
       acc = fma(kr[v], Pe[j], acc);
     }
-    const int64_t g = ((int64_t)gz * n1 + gy) * n1 + gx;
+    const int64_t g = ((int64_t)(gz - zoff) * n1 + gy) * n1 + gx;
     const double out = mode ? b[g] - acc : acc;
     y[g] = out;
     sq = fma(out, out, sq);
@@ -190,8 +190,11 @@ __global__ void __launch_bounds__(128) k_schwarz(int p, int s, int n1, const dou
                                                  const double *__restrict__ M, const double *__restrict__ Vt,
                                                  const double *__restrict__ lamt, const double *__restrict__ b,
                                                  double *__restrict__ x, int c0, int c1, int c2, int D, int nb0,
-                                                 int nb1) {
+                                                 int nb1, int zoff) {
   extern __shared__ double sm[];
+  // memory index of global point (gx, gy, gz); the last axis is stored from plane zoff on
+#define SIDX(gx, gy, gz) ((DIM == 3) ? (((int64_t)((gz) - zoff) * n1 + (gy)) * n1 + (gx)) \
+                                    : ((int64_t)((gy) - zoff) * n1 + (gx)))
   const int w = (s - 1) / 2, Wn = s + 2 * p, W = 2 * p + 1;
   const int bid = blockIdx.x;
   const int j0 = bid % nb0, j1 = (bid / nb0) % nb1, j2 = bid / (nb0 * nb1);
@@ -228,7 +231,7 @@ __global__ void __launch_bounds__(128) k_schwarz(int p, int s, int n1, const dou
     const int gx = ox + wx, gy = oy + wy, gz = oz + wz;
     bool ok = gx >= 0 && gx < n1 && gy >= 0 && gy < n1;
     if (DIM == 3) ok = ok && gz >= 0 && gz < n1;
-    X[i] = ok ? x[((int64_t)gz * n1 + gy) * n1 + gx] : 0.0;
+    X[i] = ok ? x[SIDX(gx, gy, gz)] : 0.0;
   }
   __syncthreads();
   // pass x over (lx in block) x (rest of window)
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(128) k_schwarz(int p, int s, int n1, const dou
           acc = fma(mr[u], Pa[(ly + u) * s + lx], acc);
           acc = fma(kr[u], Pb[(ly + u) * s + lx], acc);
         }
-        r = b[(int64_t)gy * n1 + gx] - acc;
+        r = b[SIDX(gx, gy, 0)] - acc;
       }
       R[i] = r;
     }
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(128) k_schwarz(int p, int s, int n1, const dou
           acc = fma(mr[v], Pc[j], acc);
           acc = fma(kr[v], Pe[j], acc);
         }
-        r = b[((int64_t)gz * n1 + gy) * n1 + gx] - acc;
+        r = b[SIDX(gx, gy, gz)] - acc;
       }
       R[i] = r;
     }
@@ -329,27 +332,32 @@ __global__ void __launch_bounds__(128) k_schwarz(int p, int s, int n1, const dou
     const int gx = bx + lx, gy = by + ly, gz = bz + lz;
     bool ok = gx >= 0 && gx < n1 && gy >= 0 && gy < n1;
     if (DIM == 3) ok = ok && gz >= 0 && gz < n1;
-    if (ok) x[((int64_t)gz * n1 + gy) * n1 + gx] += R[i];
+    if (ok) x[SIDX(gx, gy, gz)] += R[i];
   }
+#undef SIDX
 }
 
 // =============================== band transform along one axis ===========================
+// Columns valid in [clo, chi), stored from column coff on (nin stored columns per outer slice);
+// output rows r in [rlo, rhi), stored from row rlo on (rhi - rlo rows per outer slice).
 __global__ void k_band_axis(const double *__restrict__ in, double *__restrict__ out, int64_t outer, int nin,
                             int64_t inner, int rows, int W, const int *__restrict__ lo,
-                            const double *__restrict__ c, int acc) {
-  const int64_t total = outer * rows * inner;
+                            const double *__restrict__ c, int acc, int clo, int chi, int coff, int rlo, int rhi) {
+  const int nr = rhi - rlo;
+  const int64_t total = outer * nr * inner;
+  (void)rows;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = idx % inner;
-    const int r = int((idx / inner) % rows);
-    const int64_t o = idx / (inner * rows);
+    const int r = rlo + int((idx / inner) % nr);
+    const int64_t o = idx / (inner * nr);
     const int l0 = lo[r];
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll
     for (int k = 0; k < 16; ++k) {            // all gathers independent (W <= 16 checked at setup)
       const int col = l0 + k;
-      const bool ok = k < W && col >= 0 && col < nin;
-      const double v = ok ? c[(int64_t)r * W + k] * in[(o * nin + col) * inner + i] : 0.0;
+      const bool ok = k < W && col >= clo && col < chi;
+      const double v = ok ? c[(int64_t)r * W + k] * in[(o * nin + (col - coff)) * inner + i] : 0.0;
       if (k & 1) s1 += v; else s0 += v;
     }
     const double s = s0 + s1;
@@ -486,6 +494,14 @@ void ensure_smem(F *kernel, size_t bytes) {
 
 }  // namespace
 
+// first centre >= lo with residue c (mod D) and the number of such centres below hi
+void centre_range(int c, int D, int lo, int hi, int *first, int *count) {
+  int f = c;
+  if (f < lo) f += ((lo - f + D - 1) / D) * D;
+  *first = f;
+  *count = (f < hi) ? (hi - 1 - f) / D + 1 : 0;
+}
+
 int apply_num_partials(int dim, int p, int64_t n1) {
   (void)p;
   if (dim == 2) return int(((n1 + A2X - 1) / A2X) * ((n1 + A2Y - 1) / A2Y));
@@ -493,43 +509,56 @@ int apply_num_partials(int dim, int p, int64_t n1) {
 }
 
 void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, const double *x, const double *b,
-                  double *y, double *partial, int mode, cudaStream_t st, int *nparts) {
+                  double *y, double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv) {
+  if (sv.zhi < 0) sv = SlabView{0, 0, int(n1)};
+  const int nz = sv.zhi - sv.zlo;
   const size_t sm = apply_smem(dim, p);
+  if (nz <= 0) return;
   if (dim == 2) {
-    dim3 grid((unsigned)((n1 + A2X - 1) / A2X), (unsigned)((n1 + A2Y - 1) / A2Y));
+    dim3 grid((unsigned)((n1 + A2X - 1) / A2X), (unsigned)((nz + A2Y - 1) / A2Y));
     ensure_smem(k_apply2d<A2X, A2Y>, sm);
-    k_apply2d<A2X, A2Y><<<grid, 256, sm, st>>>(p, int(n1), K, M, x, b, y, partial, mode);
+    k_apply2d<A2X, A2Y><<<grid, 256, sm, st>>>(p, int(n1), K, M, x, b, y, partial, mode, sv.zoff, sv.zlo, sv.zhi);
     if (nparts) *nparts = int(grid.x * grid.y);
   } else {
     const unsigned nbx = unsigned((n1 + A3X - 1) / A3X), nby = unsigned((n1 + A3Y - 1) / A3Y);
-    dim3 grid(nbx * nby, (unsigned)((n1 + A3Z - 1) / A3Z));
+    dim3 grid(nbx * nby, (unsigned)((nz + A3Z - 1) / A3Z));
     ensure_smem(k_apply3d<A3X, A3Y, A3Z>, sm);
-    k_apply3d<A3X, A3Y, A3Z><<<grid, 256, sm, st>>>(p, int(n1), K, M, x, b, y, partial, mode);
+    k_apply3d<A3X, A3Y, A3Z><<<grid, 256, sm, st>>>(p, int(n1), K, M, x, b, y, partial, mode, sv.zoff, sv.zlo, sv.zhi);
     if (nparts) *nparts = int(grid.x * grid.y);
   }
 }
 
 void launch_schwarz_colour(int dim, int p, int s, int64_t n1, const double *K, const double *M, const double *V,
-                           const double *lam, const double *b, double *x, int colour, int D, cudaStream_t st) {
+                           const double *lam, const double *b, double *x, int colour, int D, cudaStream_t st,
+                           SlabView sv) {
+  if (sv.zhi < 0) sv = SlabView{0, 0, int(n1)};
   const int c0 = colour % D, c1 = (colour / D) % D, c2 = (dim == 3) ? colour / (D * D) : 0;
-  if (c0 >= n1 || c1 >= n1 || c2 >= n1) return;
-  const int nb0 = int((n1 - c0 + D - 1) / D), nb1 = int((n1 - c1 + D - 1) / D);
-  const int nb2 = (dim == 3) ? int((n1 - c2 + D - 1) / D) : 1;
+  int fl, nl;   // last axis: first centre and count inside the slab's centre range
+  centre_range(dim == 3 ? c2 : c1, D, sv.zlo, sv.zhi, &fl, &nl);
+  if (c0 >= n1 || nl == 0) return;
+  if (dim == 3 && c1 >= n1) return;
+  const int nb0 = int((n1 - c0 + D - 1) / D);
+  const int nb1 = (dim == 3) ? int((n1 - c1 + D - 1) / D) : nl;
+  const int nb2 = (dim == 3) ? nl : 1;
   const size_t sm = schwarz_smem(dim, p, s);
   const unsigned nblk = unsigned(nb0) * unsigned(nb1) * unsigned(nb2);
   if (dim == 2) {
     ensure_smem(k_schwarz<2>, sm);
-    k_schwarz<2><<<nblk, 128, sm, st>>>(p, s, int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1);
+    k_schwarz<2><<<nblk, 128, sm, st>>>(p, s, int(n1), K, M, V, lam, b, x, c0, fl, 0, D, nb0, nb1, sv.zoff);
   } else {
     ensure_smem(k_schwarz<3>, sm);
-    k_schwarz<3><<<nblk, 128, sm, st>>>(p, s, int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1);
+    k_schwarz<3><<<nblk, 128, sm, st>>>(p, s, int(n1), K, M, V, lam, b, x, c0, c1, fl, D, nb0, nb1, sv.zoff);
   }
 }
 
 void launch_band_axis(const double *in, double *out, int64_t outer, int nin, int64_t inner, const Band1D &B,
-                      int accumulate, cudaStream_t st) {
-  const int64_t total = outer * B.rows * inner;
-  k_band_axis<<<grid_for(total, 256), 256, 0, st>>>(in, out, outer, nin, inner, B.rows, B.W, B.lo, B.c, accumulate);
+                      int accumulate, cudaStream_t st, int clo, int chi, int coff, int rlo, int rhi) {
+  if (chi < 0) { clo = 0; chi = nin; coff = 0; }
+  if (rhi < 0) { rlo = 0; rhi = B.rows; }
+  const int64_t total = outer * (rhi - rlo) * inner;
+  if (total <= 0) return;
+  k_band_axis<<<grid_for(total, 256), 256, 0, st>>>(in, out, outer, nin, inner, B.rows, B.W, B.lo, B.c, accumulate,
+                                                   clo, chi, coff, rlo, rhi);
 }
 
 void launch_q_gs_colour(int dim, int q, int n, const double *K, const double *M, const double *b, double *x,
@@ -580,24 +609,32 @@ void launch_tensor_rhs(int dim, int64_t n1, const double *g, double scale, doubl
 namespace iga2l {
 namespace {
 
+// barrier for the G warps of one Schwarz block (named barrier 1 + group; __syncwarp if G == 1)
+template <int G>
+__device__ __forceinline__ void group_sync(int group) {
+  if (G == 1) __syncwarp();
+  else asm volatile("bar.sync %0, %1;" ::"r"(group + 1), "r"(32 * G) : "memory");
+}
+
 // One warp per Schwarz block; WPB blocks (warps) per CTA; only __syncwarp inside (blocks of one
 // colour are independent).  Same arithmetic as k_schwarz<2>, compile-time sizes.  Everything the
 // block needs (x window, b_B, the 1D band rows of its rows/columns, its FD tables) is fetched in
 // ONE round of independent loads into shared memory; then four dependent phases:
 //   pass x (K_x X, M_x X), pass y (r_B = b_B - (A x)_B), Z = (Vx^T R Vy) ./ (λx + λy),
 //   δ = Vx Z Vy^T and x_B += δ.   FMA chains are split over two accumulators.
-template <int P, int S, int WPB>
-__global__ void __launch_bounds__(WPB * 32) k_schwarz2d_w(int n1, const double *__restrict__ K,
+template <int P, int S, int WPB, int G>
+__global__ void __launch_bounds__(WPB * G * 32) k_schwarz2d_w(int n1, const double *__restrict__ K,
                                                          const double *__restrict__ M, const double *__restrict__ Vt,
                                                          const double *__restrict__ lamt,
                                                          const double *__restrict__ b, double *__restrict__ x,
-                                                         int c0, int c1, int D, int nb0, int nblk) {
+                                                         int c0, int c1, int D, int nb0, int nblk, int zoff) {
   constexpr int W = 2 * P + 1, Wn = S + 2 * P, w = (S - 1) / 2, S2 = S * S;
   constexpr int PER = Wn * Wn + 2 * S * Wn + 3 * S2 + 4 * S * W + 2 * S2 + 2 * S;
   extern __shared__ double sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int GT = 32 * G;                            // threads per Schwarz block (G warps)
+  const int warp = threadIdx.x / GT, lane = threadIdx.x % GT;
   const int bid = blockIdx.x * WPB + warp;
-  if (bid >= nblk) return;
+  if (bid >= nblk) return;                              // whole group exits together
   double *X = sm + warp * PER, *Pa = X + Wn * Wn, *Pb = Pa + S * Wn, *R = Pb + S * Wn, *Q = R + S2;
   double *Bb = Q + S2;                                   // b_B
   double *Kx = Bb + S2, *Mx = Kx + S * W, *Ky = Mx + S * W, *My = Ky + S * W;   // band rows
@@ -610,7 +647,7 @@ __global__ void __launch_bounds__(WPB * 32) k_schwarz2d_w(int n1, const double *
   // depend on the previous colour (band rows, FD tables, b_B) is loaded before griddepcontrol.wait.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #pragma unroll
-  for (int i = lane; i < S * W; i += 32) {
+  for (int i = lane; i < S * W; i += GT) {
     const int l = i / W, t = i - l * W;
     const int gx = bx + l, gy = by + l;
     const bool okx = unsigned(gx) < un, oky = unsigned(gy) < un;
@@ -620,9 +657,9 @@ __global__ void __launch_bounds__(WPB * 32) k_schwarz2d_w(int n1, const double *
     My[i] = oky ? M[(int64_t)gy * W + t] : 0.0;
   }
 #pragma unroll
-  for (int i = lane; i < S2; i += 32) {
+  for (int i = lane; i < S2; i += GT) {
     const int ly = i / S, lx = i - ly * S, gx = bx + lx, gy = by + ly;
-    Bb[i] = (unsigned(gx) < un && unsigned(gy) < un) ? b[(int64_t)gy * n1 + gx] : 0.0;
+    Bb[i] = (unsigned(gx) < un && unsigned(gy) < un) ? b[(int64_t)(gy - zoff) * n1 + gx] : 0.0;
     Vx[i] = Vt[(int64_t)cx * S2 + i];
     Vy[i] = Vt[(int64_t)cy * S2 + i];
   }
@@ -632,14 +669,14 @@ __global__ void __launch_bounds__(WPB * 32) k_schwarz2d_w(int n1, const double *
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");   // previous colour complete and visible
 #pragma unroll
-  for (int i = lane; i < Wn * Wn; i += 32) {
+  for (int i = lane; i < Wn * Wn; i += GT) {
     const int wy = i / Wn, wx = i - wy * Wn;
     const int gx = ox + wx, gy = oy + wy;
-    X[i] = (unsigned(gx) < un && unsigned(gy) < un) ? x[(int64_t)gy * n1 + gx] : 0.0;
+    X[i] = (unsigned(gx) < un && unsigned(gy) < un) ? x[(int64_t)(gy - zoff) * n1 + gx] : 0.0;
   }
-  __syncwarp();
+  group_sync<G>(warp);
 #pragma unroll
-  for (int i = lane; i < S * Wn; i += 32) {          // pass x: K_x X, M_x X on the block columns
+  for (int i = lane; i < S * Wn; i += GT) {          // pass x: K_x X, M_x X on the block columns
     const int wy = i / S, lx = i - wy * S;
     const double *kr = Kx + lx * W, *mr = Mx + lx * W, *xr = X + wy * Wn + lx;
     double sa0 = 0.0, sb0 = 0.0, sa1 = 0.0, sb1 = 0.0;
@@ -655,9 +692,9 @@ __global__ void __launch_bounds__(WPB * 32) k_schwarz2d_w(int n1, const double *
     Pa[i] = sa0 + sa1;
     Pb[i] = sb0 + sb1;
   }
-  __syncwarp();
+  group_sync<G>(warp);
 #pragma unroll
-  for (int i = lane; i < S2; i += 32) {              // pass y, block residual r_B = b_B - (A x)_B
+  for (int i = lane; i < S2; i += GT) {              // pass y, block residual r_B = b_B - (A x)_B
     const int ly = i / S, lx = i - ly * S;
     const double *kr = Ky + ly * W, *mr = My + ly * W;
     double a0 = 0.0, a1 = 0.0;
@@ -668,9 +705,9 @@ __global__ void __launch_bounds__(WPB * 32) k_schwarz2d_w(int n1, const double *
     }
     R[i] = Bb[i] - (a0 + a1);                        // rows/cols outside the grid: band rows are 0
   }
-  __syncwarp();
+  group_sync<G>(warp);
 #pragma unroll
-  for (int i = lane; i < S2; i += 32) {              // Z[k][j] = Σ_{ly,lx} Vx[lx][j] R[ly][lx] Vy[ly][k] / (λx_j + λy_k)
+  for (int i = lane; i < S2; i += GT) {              // Z[k][j] = Σ_{ly,lx} Vx[lx][j] R[ly][lx] Vy[ly][k] / (λx_j + λy_k)
     const int k = i / S, j = i - k * S;
     double z0 = 0.0, z1 = 0.0;
 #pragma unroll
@@ -682,9 +719,9 @@ __global__ void __launch_bounds__(WPB * 32) k_schwarz2d_w(int n1, const double *
     }
     Q[i] = (z0 + z1) / (Lx[j] + Ly[k]);
   }
-  __syncwarp();
+  group_sync<G>(warp);
 #pragma unroll
-  for (int i = lane; i < S2; i += 32) {              // δ[ly][lx] = Σ_{k,j} Vy[ly][k] Vx[lx][j] Z[k][j];  x_B += δ
+  for (int i = lane; i < S2; i += GT) {              // δ[ly][lx] = Σ_{k,j} Vy[ly][k] Vx[lx][j] Z[k][j];  x_B += δ
     const int ly = i / S, lx = i - ly * S, gx = bx + lx, gy = by + ly;
     double d0 = 0.0, d1 = 0.0;
 #pragma unroll
@@ -694,23 +731,23 @@ __global__ void __launch_bounds__(WPB * 32) k_schwarz2d_w(int n1, const double *
       for (int j = 0; j < S; ++j) t = fma(Vx[lx * S + j], Q[k * S + j], t);
       if (k & 1) d1 = fma(Vy[ly * S + k], t, d1); else d0 = fma(Vy[ly * S + k], t, d0);
     }
-    if (unsigned(gx) < un && unsigned(gy) < un) x[(int64_t)gy * n1 + gx] = X[(ly + P) * Wn + lx + P] + (d0 + d1);
+    if (unsigned(gx) < un && unsigned(gy) < un) x[(int64_t)(gy - zoff) * n1 + gx] = X[(ly + P) * Wn + lx + P] + (d0 + d1);
   }
 }
 
 int g_use_pdl = 0;   // programmatic dependent launch between colour kernels (measured slower: off)
 
-template <int P, int S, int WPB>
+template <int P, int S, int WPB, int G>
 bool try_schwarz2d(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
-                   const double *b, double *x, int c0, int c1, int D, int nb0, int nblk, cudaStream_t st) {
+                   const double *b, double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st) {
   if (p != P || s != S) return false;
   constexpr int Wn = S + 2 * P;
   constexpr int W = 2 * P + 1;
   constexpr size_t sm = sizeof(double) * WPB * (Wn * Wn + 2 * S * Wn + 5 * S * S + 4 * S * W + 2 * S);
-  ensure_smem(k_schwarz2d_w<P, S, WPB>, sm);
+  ensure_smem(k_schwarz2d_w<P, S, WPB, G>, sm);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((nblk + WPB - 1) / WPB);
-  cfg.blockDim = dim3(WPB * 32);
+  cfg.blockDim = dim3(WPB * G * 32);
   cfg.dynamicSmemBytes = sm;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -718,21 +755,23 @@ bool try_schwarz2d(int p, int s, int64_t n1, const double *K, const double *M, c
   at[0].val.programmaticStreamSerializationAllowed = g_use_pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_schwarz2d_w<P, S, WPB>, int(n1), K, M, V, lam, b, x, c0, c1, D, nb0, nblk);
+  cudaLaunchKernelEx(&cfg, k_schwarz2d_w<P, S, WPB, G>, int(n1), K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff);
   return true;
 }
 
 // 2D tensor transfer, direct: out[ry][rx] (+)= Σ_{ky,kx} c[ry][ky] c[rx][kx] in[lo[ry]+ky][lo[rx]+kx].
 // The band loops are unrolled to a compile-time bound so that all W^2 gathers of an output are
 // independent loads (one L2 round trip instead of W^2 dependent ones).
+// Input rows (last axis) are valid in [iylo, iyhi) and stored from row iyoff on; columns in [0, nin).
 template <int WMAX>
-__device__ __forceinline__ double tensor2d_point(const double *__restrict__ in, int nin, int W, const int *__restrict__ lo,
-                                                 const double *__restrict__ c, int ry, int rx) {
+__device__ __forceinline__ double tensor2d_point(const double *__restrict__ in, int nin, int iylo, int iyhi, int iyoff,
+                                                 int W, const int *__restrict__ lo, const double *__restrict__ c,
+                                                 int ry, int rx) {
   const int ly = lo[ry], lx = lo[rx];
   double cy[WMAX], cx[WMAX];
 #pragma unroll
   for (int k = 0; k < WMAX; ++k) {
-    const bool oky = k < W && unsigned(ly + k) < unsigned(nin), okx = k < W && unsigned(lx + k) < unsigned(nin);
+    const bool oky = k < W && ly + k >= iylo && ly + k < iyhi, okx = k < W && unsigned(lx + k) < unsigned(nin);
     cy[k] = oky ? c[(int64_t)ry * W + k] : 0.0;
     cx[k] = okx ? c[(int64_t)rx * W + k] : 0.0;
   }
@@ -743,7 +782,7 @@ __device__ __forceinline__ double tensor2d_point(const double *__restrict__ in, 
 #pragma unroll
     for (int kx = 0; kx < WMAX; ++kx) {
       const bool ok = cy[ky] != 0.0 && cx[kx] != 0.0;
-      const double v = ok ? in[(int64_t)(ly + ky) * nin + (lx + kx)] : 0.0;
+      const double v = ok ? in[(int64_t)(ly + ky - iyoff) * nin + (lx + kx)] : 0.0;
       t = fma(cx[kx], v, t);
     }
     if (ky & 1) s1 = fma(cy[ky], t, s1); else s0 = fma(cy[ky], t, s0);
@@ -751,15 +790,18 @@ __device__ __forceinline__ double tensor2d_point(const double *__restrict__ in, 
   return s0 + s1;
 }
 
+// Output rows ry in [rylo, ryhi) are stored from row ryoff on (all rows.x columns).
 template <int WMAX>
 __global__ void k_tensor2d(const double *__restrict__ in, double *__restrict__ out, int nin, int rows, int W,
-                           const int *__restrict__ lo, const double *__restrict__ c, int acc) {
-  const int64_t total = (int64_t)rows * rows;
+                           const int *__restrict__ lo, const double *__restrict__ c, int acc, int iylo, int iyhi,
+                           int iyoff, int rylo, int ryhi, int ryoff) {
+  const int64_t total = (int64_t)(ryhi - rylo) * rows;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int ry = int(idx / rows), rx = int(idx - (int64_t)ry * rows);
-    const double s = tensor2d_point<WMAX>(in, nin, W, lo, c, ry, rx);
-    out[idx] = acc ? out[idx] + s : s;
+    const int ry = rylo + int(idx / rows), rx = int(idx % rows);
+    const double s = tensor2d_point<WMAX>(in, nin, iylo, iyhi, iyoff, W, lo, c, ry, rx);
+    const int64_t o = (int64_t)(ry - ryoff) * rows + rx;
+    out[o] = acc ? out[o] + s : s;
   }
 }
 
@@ -858,8 +900,8 @@ __device__ __forceinline__ void team_tensor2d(const Team tm, const Band1D B, con
   const int64_t total = (int64_t)B.rows * B.rows;
   for (int64_t idx = tm.tid; idx < total; idx += tm.nthr) {
     const int ry = int(idx / B.rows), rx = int(idx - (int64_t)ry * B.rows);
-    const double s = B.W <= 4 ? tensor2d_point<4>(in, B.cols, B.W, B.lo, B.c, ry, rx)
-                              : tensor2d_point<8>(in, B.cols, B.W, B.lo, B.c, ry, rx);
+    const double s = B.W <= 4 ? tensor2d_point<4>(in, B.cols, 0, B.cols, 0, B.W, B.lo, B.c, ry, rx)
+                              : tensor2d_point<8>(in, B.cols, 0, B.cols, 0, B.W, B.lo, B.c, ry, rx);
     out[idx] = acc ? out[idx] + s : s;
   }
 }
@@ -970,30 +1012,40 @@ __global__ void __launch_bounds__(512) k_vcycle_cluster(const QLevelDev *__restr
 }  // namespace
 
 bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M, const double *V,
-                                const double *lam, const double *b, double *x, int colour, int D, cudaStream_t st) {
+                                const double *lam, const double *b, double *x, int colour, int D, cudaStream_t st,
+                                SlabView sv) {
   if (dim != 2) return false;
+  if (sv.zhi < 0) sv = SlabView{0, 0, int(n1)};
   const int c0 = colour % D, c1 = (colour / D) % D;
-  if (c0 >= n1 || c1 >= n1) return true;   // empty colour
-  const int nb0 = int((n1 - c0 + D - 1) / D), nb1 = int((n1 - c1 + D - 1) / D), nblk = nb0 * nb1;
-  return try_schwarz2d<1, 3, 8>(p, s, n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, st) ||
-         try_schwarz2d<2, 3, 8>(p, s, n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, st) ||
-         try_schwarz2d<3, 3, 8>(p, s, n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, st) ||
-         try_schwarz2d<4, 3, 8>(p, s, n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, st) ||
-         try_schwarz2d<5, 5, 4>(p, s, n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, st) ||
-         try_schwarz2d<6, 5, 4>(p, s, n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, st) ||
-         try_schwarz2d<7, 7, 4>(p, s, n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, st) ||
-         try_schwarz2d<8, 7, 4>(p, s, n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, st);
+  int f1, nb1;
+  centre_range(c1, D, sv.zlo, sv.zhi, &f1, &nb1);
+  if (c0 >= n1 || nb1 == 0) return true;   // empty colour
+  const int nb0 = int((n1 - c0 + D - 1) / D), nblk = nb0 * nb1;
+  const int z = sv.zoff;
+  // <P, S, blocks per CTA, warps per block>
+  return try_schwarz2d<1, 3, 8, 1>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
+         try_schwarz2d<2, 3, 8, 1>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
+         try_schwarz2d<3, 3, 8, 1>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
+         try_schwarz2d<4, 3, 4, 2>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
+         try_schwarz2d<5, 5, 2, 4>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
+         try_schwarz2d<6, 5, 2, 4>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
+         try_schwarz2d<7, 7, 2, 4>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
+         try_schwarz2d<8, 7, 2, 4>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st);
 }
 
-void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumulate, cudaStream_t st) {
-  const int64_t total = (int64_t)B.rows * B.rows;
+void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumulate, cudaStream_t st,
+                     int iylo, int iyhi, int iyoff, int rylo, int ryhi, int ryoff) {
+  if (iyhi < 0) { iylo = 0; iyhi = B.cols; iyoff = 0; }
+  if (ryhi < 0) { rylo = 0; ryhi = B.rows; ryoff = 0; }
+  const int64_t total = (int64_t)(ryhi - rylo) * B.rows;
+  if (total <= 0) return;
   const int g = grid_for(total, 128);
   if (B.W <= 4)
-    k_tensor2d<4><<<g, 128, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate);
+    k_tensor2d<4><<<g, 128, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate, iylo, iyhi, iyoff, rylo, ryhi, ryoff);
   else if (B.W <= 8)
-    k_tensor2d<8><<<g, 128, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate);
+    k_tensor2d<8><<<g, 128, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate, iylo, iyhi, iyoff, rylo, ryhi, ryoff);
   else
-    k_tensor2d<16><<<g, 128, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate);
+    k_tensor2d<16><<<g, 128, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate, iylo, iyhi, iyoff, rylo, ryhi, ryoff);
 }
 
 static int g_vc_cluster[4] = {0, 0, 0, 0};
@@ -1051,4 +1103,17 @@ void launch_vcycle_cta(int dim, const QLevelDev *levs_dev, int l0, int nlev, int
   cudaLaunchKernelEx(&cfg, kern, levs_dev, l0, nlev);
 }
 
+}  // namespace iga2l
+
+namespace iga2l {
+namespace {
+__global__ void k_axpy(double *__restrict__ y, const double *__restrict__ x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] += x[i];
+}
+}  // namespace
+
+void launch_axpy(double *y, const double *x, int64_t n, cudaStream_t st) {
+  k_axpy<<<grid_for(n, 256), 256, 0, st>>>(y, x, n);
+}
 }  // namespace iga2l

@@ -17,24 +17,36 @@ struct Band1D {          // banded 1D transfer: row r uses columns lo[r] .. lo[r
   const double *c;
 };
 
+// Window of the LAST axis (y in 2D, z in 3D) of a vector held by a context: local plane 0 is the
+// global plane zoff; kernels compute/output the global planes [zlo, zhi).  {0, 0, -1} = whole grid.
+struct SlabView {
+  int zoff, zlo, zhi;
+};
+constexpr SlabView kFull{0, 0, -1};
+void centre_range(int c, int D, int lo, int hi, int *first, int *count);
+
 // ---- fine operator: apply / residual -------------------------------------------------------
 // mode 0: y = A x;  mode 1: y = b - A x.  If partial != nullptr, partial[cta] = Σ y^2 over the tile.
 void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, const double *x,
-                  const double *b, double *y, double *partial, int mode, cudaStream_t st, int *nparts);
+                  const double *b, double *y, double *partial, int mode, cudaStream_t st, int *nparts,
+                  SlabView sv = kFull);
 int apply_num_partials(int dim, int p, int64_t n1);
 
 // ---- multicolour Schwarz: one colour ---------------------------------------------------------
 // Blocks centred at c = col + D*j (per axis) are solved in parallel (A-decoupled, reading A4):
 // r_B = b_B - (A x)_B; δ = A_B^{-1} r_B by fast diagonalisation with per-centre 1D tables V, lam;
 // x_B += δ.
+// (slab: blocks with last-axis centre in [sv.zlo, sv.zhi); x, b stored from plane sv.zoff)
 void launch_schwarz_colour(int dim, int p, int s, int64_t n1, const double *K, const double *M,
                            const double *V, const double *lam, const double *b, double *x,
-                           int colour, int D, cudaStream_t st);
+                           int colour, int D, cudaStream_t st, SlabView sv = kFull);
 
 // ---- tensor-product band transform along one axis ------------------------------------------
 // in: [outer][nin][inner]  ->  out: [outer][B.rows][inner],  out (+)= Σ_k B.c[r,k] in[.., lo[r]+k, ..]
+// (optional: only input columns in [clo, chi) stored from coff; only output rows [rlo, rhi))
 void launch_band_axis(const double *in, double *out, int64_t outer, int nin, int64_t inner,
-                      const Band1D &B, int accumulate, cudaStream_t st);
+                      const Band1D &B, int accumulate, cudaStream_t st, int clo = 0, int chi = -1,
+                      int coff = 0, int rlo = 0, int rhi = -1);
 
 // ---- q-level (V-cycle) kernels, direct (2q+1)^d stencil --------------------------------------
 void launch_q_gs_colour(int dim, int q, int n, const double *K, const double *M, const double *b,
@@ -54,9 +66,11 @@ void launch_sum_partials(const double *partial, int n, double *out, double *hist
 // Warp-per-block 2D Schwarz colour kernel for the paper's (p, s) pairs; false = not specialised.
 bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M,
                                 const double *V, const double *lam, const double *b, double *x, int colour,
-                                int D, cudaStream_t st);
+                                int D, cudaStream_t st, SlabView sv = kFull);
 // 2D tensor transfer out (+)= (B ⊗ B) in in one launch (in: B.cols^2, out: B.rows^2).
-void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumulate, cudaStream_t st);
+// (optional: input rows valid in [iylo, iyhi) stored from iyoff; output rows [rylo, ryhi) stored from ryoff)
+void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumulate, cudaStream_t st,
+                     int iylo = 0, int iyhi = -1, int iyoff = 0, int rylo = 0, int ryhi = -1, int ryoff = 0);
 
 // One q-level of the V-cycle hierarchy, as seen by the single-CTA tail kernel (device array).
 struct QLevelDev {
@@ -72,6 +86,9 @@ struct QLevelDev {
 // outside stream capture (it probes the largest schedulable cluster).
 int vcycle_cluster_size(int dim);
 void launch_vcycle_cta(int dim, const QLevelDev *levs_dev, int l0, int nlev, int q, cudaStream_t st);
+
+// y += x (fixed-order sums of the slab partial coarse vectors in local multi-slab mode)
+void launch_axpy(double *y, const double *x, int64_t n, cudaStream_t st);
 
 // b[idx] = scale * ∏_a g[i_a]
 void launch_tensor_rhs(int dim, int64_t n1, const double *g, double scale, double *b, cudaStream_t st);

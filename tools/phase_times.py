@@ -31,18 +31,31 @@ for n in names:
     inf = ctx.info()
 
     def t(fn, r=reps):
+        """Average device time of fn's launches, replayed from a CUDA graph (no host launch cost)."""
         fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            fn()
+        g.replay()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
         for _ in range(r):
-            fn()
+            g.replay()
         e1.record(st)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / r * 1e3   # us
 
     r = {"N": ctx.N, "colours": inf.colours, "launches_per_iter": inf.launches_per_iter}
-    r["iter_us"] = t(lambda: ctx.iterate(b, x, 1))
+    ctx.iterate(b, x, 1)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    ctx.iterate(b, x, reps)
+    e1.record(st)
+    torch.cuda.synchronize()
+    r["iter_us"] = e0.elapsed_time(e1) / reps * 1e3
     r["sweep_us"] = t(lambda: ctx.sweep(b, x))
     r["defect_restrict_us"] = t(lambda: ctx.defect_restrict(b, x, dq))
     r["coarse_us"] = t(lambda: ctx.coarse_solve(dq, e))
