@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -79,6 +80,8 @@ struct iga2l_ctx {
   int next_graph = 0;
   QLevelDev *levdev = nullptr;   // device copy of the level table (single-CTA V-cycle tail)
   int l_cta = -1;                // first level handled by the single-CTA tail kernel
+  int l_sm = -1;                 // first level handled by the shared-memory tail kernel (preferred)
+  VcLayout vcl{};
   int launch_counter = 0;
   int launches_per_iter = 0;
   std::vector<void *> allocs;
@@ -169,6 +172,11 @@ void L_tensor(iga2l_ctx *c, int dim, const Band1D &B, const double *in, double *
 
 void L_vcycle(iga2l_ctx *c, size_t l) {
   Level &L = c->lev[l];
+  if (int(l) == c->l_sm && c->levdev) {    // tail levels resident in shared memory (one cluster)
+    launch_vcycle_smem(c->dim, c->q, c->vcl, c->st);
+    c->launch_counter++;
+    return;
+  }
   if (int(l) == c->l_cta && c->levdev) {   // small tail levels: the whole rest of the cycle in one CTA
     launch_vcycle_cta(c->dim, c->levdev, int(l), int(c->lev.size()), c->q, c->st);
     c->launch_counter++;
@@ -634,7 +642,28 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
       tab[l] = QLevelDev{L.n, L.N, L.K, L.M, L.x, L.b, L.r, L.t1, L.t2, L.P.b, L.PT.b, L.inv};
       if (c->l_cta < 0 && L.N <= kCtaTailMax && c->lev.size() > 1) c->l_cta = int(l);
     }
-    if (c->l_cta >= 0 && (rc = upload(c, &c->levdev, tab))) return bail(rc);
+    // shared-memory tail (one cluster): the first (largest) level from which the rest of the cycle
+    // fits, preferring the widest cluster; IGA2L_VC_SMEM=0 disables it, IGA2L_VC_FORCE_CS=<cs>
+    // forces level 0 on a cluster of cs CTAs (test knob)
+    const char *vc_env = std::getenv("IGA2L_VC_SMEM");
+    const char *force = std::getenv("IGA2L_VC_FORCE_CS");
+    const bool want_sm = !(vc_env && vc_env[0] == '0') && c->lev.size() > 1;
+    const size_t cap = 227 * 1024;
+    for (int l0 = 0; want_sm && c->l_sm < 0 && l0 + 1 < int(c->lev.size()); ++l0) {
+      VcLayout vl;
+      if (force && std::atoi(force) >= 1) {
+        if (vcycle_smem_layout(dim, q, tab.data(), int(tab.size()), 0, std::atoi(force), cap, &vl) &&
+            vcycle_smem_probe(dim, q, vl)) { c->l_sm = 0; c->vcl = vl; }
+        break;
+      }
+      for (int cs : {16, 8, 4, 2, 1})
+        if (vcycle_smem_layout(dim, q, tab.data(), int(tab.size()), l0, cs, cap, &vl) && vcycle_smem_probe(dim, q, vl)) {
+          c->l_sm = l0;
+          c->vcl = vl;
+          break;
+        }
+    }
+    if ((c->l_cta >= 0 || c->l_sm >= 0) && (rc = upload(c, &c->levdev, tab))) return bail(rc);
     if (c->l_cta >= 0) vcycle_cluster_size(dim);   // probe outside any stream capture
   }
   c->npartial = apply_num_partials(dim, p, n1);

@@ -87,6 +87,42 @@ struct QLevelDev {
 int vcycle_cluster_size(int dim);
 void launch_vcycle_cta(int dim, const QLevelDev *levs_dev, int l0, int nlev, int q, cudaStream_t st);
 
+// Shared-memory V-cycle tail (levels [l0, nlev)), one thread-block cluster of cs CTAs:
+//  * levels [l0, l0 + nsp) are SPREAD over the CTAs by rows of the last axis (CTA r owns rows
+//    [z0[l][r], z0[l][r+1]) and keeps H halo rows each side, refreshed by the writing thread with
+//    DSMEM stores to the neighbour); phases are separated by cluster barriers;
+//  * levels [l0 + nsp, nlev) live in CTA 0's shared memory (phases: __syncthreads).
+// Offsets are in doubles (ints for the transfer column starts, in the int area after the doubles).
+constexpr int kVcMaxLev = 12, kVcMaxCS = 16, kVcMaxCopy = 64;
+struct VcCopy {
+  const void *src;
+  int dst, count, is_int, pad;
+};
+struct VcLayout {
+  const double *gb0;                   // level l0 right-hand side (global, written by the caller)
+  double *gx0;                         // level l0 solution (global, read by the caller)
+  const double *ginv;                  // coarsest dense inverse (global)
+  int l0, nlev, nsp, cs, dim3, H;
+  int n[kVcMaxLev], WP[kVcMaxLev], WPT[kVcMaxLev];
+  int x[kVcMaxLev], b[kVcMaxLev], r[kVcMaxLev];
+  int K[kVcMaxLev], M[kVcMaxLev], Pc[kVcMaxLev], PTc[kVcMaxLev], Plo[kVcMaxLev], PTlo[kVcMaxLev];
+  short z0[kVcMaxLev][kVcMaxCS + 1];   // spread levels: row partition
+  short rc0[kVcMaxCS + 1];             // restriction into the first CTA-0 level: coarse rows of CTA r
+  short pc0[kVcMaxCS];                 // prolongation from it: coarse rows [pc0[r], pc0[r] + pcn) pulled
+  int pcn, pbuf, cbuf, inv_sm, xend;   // pull buffers, staged coarsest inverse (-1: global), x area end
+  int ncopy, copy_start[kVcMaxCopy + 1];
+  VcCopy copy[kVcMaxCopy];
+  int ndouble, nint;
+};
+// Build the layout for tail levels [l0, nlev) on a cluster of cs CTAs (cs = 1: CTA-0 levels only).
+// tab: HOST copy of the level table (device pointers inside).  False if it does not fit / partition
+// constraints fail.
+bool vcycle_smem_layout(int dim, int q, const QLevelDev *tab, int nlev, int l0, int cs, size_t max_bytes,
+                        VcLayout *out);
+size_t vcycle_smem_bytes(const VcLayout &L);
+bool vcycle_smem_probe(int dim, int q, const VcLayout &L);   // call outside stream capture
+void launch_vcycle_smem(int dim, int q, const VcLayout &L, cudaStream_t st);
+
 // y += x (fixed-order sums of the slab partial coarse vectors in local multi-slab mode)
 void launch_axpy(double *y, const double *x, int64_t n, cudaStream_t st);
 

@@ -242,3 +242,37 @@ def test_full_size_sampled(name):
     hist = np.zeros(3)
     ctx.iterate(bg, xg, iters=2, res_hist=hist)
     assert hist[2] < 0.9 * hist[1] < 0.9 * hist[0]
+
+
+# ---- V-cycle tail in shared memory: the level spread over a cluster (DSMEM) and the CTA-local
+# levels, forced at small sizes (IGA2L_VC_FORCE_CS) and at full BASELINE sizes (chosen by setup) ----
+VC_SMALL = [c for c in PAR if c[6] == "vcycle"]
+
+
+@pytest.mark.parametrize("cs", [2, 4, 16])
+@pytest.mark.parametrize("cfg", VC_SMALL, ids=[c[0] for c in VC_SMALL])
+def test_vcycle_smem_spread_level(cfg, cs, monkeypatch):
+    name, d, p, q, m, s, coarse, hf = cfg
+    monkeypatch.setenv("IGA2L_VC_FORCE_CS", str(cs))
+    ctx = make_ctx(d, p, q, m, s, coarse, hf)
+    ora = oracle_for(*cfg)
+    dq = random_rhs(ctx.Nc, seed=3)
+    e = torch.empty(ctx.Nc, dtype=torch.float64, device=DEV)
+    ctx.coarse_solve(cu(dq), e)
+    close(host(e), ora._csolve(dq), 1e-11)
+
+
+@pytest.mark.parametrize("q,m,d", [(1, 128, 2), (1, 64, 3), (2, 512, 2)], ids=["C2", "C4", "C3"])
+def test_vcycle_full_size(q, m, d):
+    from oracle.multigrid import QHierarchy
+    H = QHierarchy(q, m, d)
+    n = H.levels[0]["n"]
+    # a fine context whose aggressive second level is exactly this q-level (m_fine = 2 m)
+    p = {(1, 2): 3, (1, 3): 3, (2, 2): 8}[(q, d)]
+    s = 3 if p <= 4 else 7
+    ctx = make_ctx(d, p, q, 2 * m, s, "vcycle", 2)
+    assert ctx.Nc == n ** d
+    dq = random_rhs(ctx.Nc, seed=5)
+    e = torch.empty(ctx.Nc, dtype=torch.float64, device=DEV)
+    ctx.coarse_solve(cu(dq), e)
+    close(host(e), H.vcycle(dq), 1e-11)

@@ -7,7 +7,7 @@ namespace iga2l { void vcycle_trace_enable(unsigned long long *dev_buf); }
 int main(int argc, char **argv) {
   int p = argc > 1 ? atoi(argv[1]) : 3;
   iga2l_ctx *c = nullptr;
-  if (iga2l_setup(2, p, 1, 256, p <= 4 ? 3 : 5, p <= 4 ? 2 : 4, &c)) { printf("setup: %s\n", iga2l_last_error()); return 1; }
+  if (iga2l_setup(argc > 2 ? atoi(argv[2]) : 2, p, argc > 3 ? atoi(argv[3]) : 1, argc > 4 ? atoi(argv[4]) : 256, p <= 4 ? 3 : (p <= 6 ? 5 : 7), p <= 4 ? 2 : (p <= 6 ? 4 : 6), &c)) { printf("setup: %s\n", iga2l_last_error()); return 1; }
   iga2l_info inf; iga2l_get_info(c, &inf);
   double *dq, *e; cudaMalloc(&dq, inf.Nc * 8); cudaMalloc(&e, inf.Nc * 8); cudaMemset(dq, 0, inf.Nc * 8);
   unsigned long long *tb; cudaMalloc(&tb, 1024 * 8);
