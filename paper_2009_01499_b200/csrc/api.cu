@@ -81,6 +81,8 @@ struct iga2l_ctx {
   QLevelDev *levdev = nullptr;   // device copy of the level table (single-CTA V-cycle tail)
   int l_cta = -1;                // first level handled by the single-CTA tail kernel
   int l_sm = -1;                 // first level handled by the shared-memory tail kernel (preferred)
+  int persist_tiles = 0;         // > 0: full sweeps run as one persistent launch with this many tiles
+  unsigned *sweep_ctl = nullptr, *sweep_done = nullptr;
   VcLayout vcl{};
   int launch_counter = 0;
   int launches_per_iter = 0;
@@ -206,6 +208,12 @@ void L_vcycle(iga2l_ctx *c, size_t l) {
 }
 
 void L_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
+  if (c0 == 0 && c1 == c->colours && c->persist_tiles > 0) {   // whole sweep: one persistent launch
+    sweep2d_persist(c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, c->sweep_ctl, c->sweep_done,
+                    c->persist_tiles, c->st, true);
+    c->launch_counter++;
+    return;
+  }
   for (int col = c0; col < c1; ++col) {
     if (!launch_schwarz_colour_fast(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st))
       launch_schwarz_colour(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st);
@@ -665,6 +673,20 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
     }
     if ((c->l_cta >= 0 || c->l_sm >= 0) && (rc = upload(c, &c->levdev, tab))) return bail(rc);
     if (c->l_cta >= 0) vcycle_cluster_size(dim);   // probe outside any stream capture
+  }
+  if (dim == 2 && c->nranks == 1) {   // persistent sweep: opt-in (IGA2L_SWEEP_PERSIST=1); measured slower
+    const char *pe = std::getenv("IGA2L_SWEEP_PERSIST");   // than per-colour graph launches
+    if (pe && pe[0] == '1') {
+      const int nt = sweep2d_persist(p, block, n1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                     nullptr, 1 << 20, nullptr, false);
+      if (nt > 0) {
+        if ((rc = dalloc(c, &c->sweep_ctl, 2)) || (rc = dalloc(c, &c->sweep_done, 32 * size_t(nt)))) return bail(rc);
+        if (cudaMemset(c->sweep_ctl, 0, 2 * sizeof(unsigned)) != cudaSuccess ||
+            cudaMemset(c->sweep_done, 0, 32 * size_t(nt) * sizeof(unsigned)) != cudaSuccess)
+          return bail(fail(IGA2L_ECUDA, "cudaMemset (sweep counters)"));
+        c->persist_tiles = nt;
+      }
+    }
   }
   c->npartial = apply_num_partials(dim, p, n1);
   if (c->nranks > 1) {   // slab buffers (padded with H halo planes) and the communicator

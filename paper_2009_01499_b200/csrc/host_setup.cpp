@@ -104,6 +104,28 @@ void band_tables(int p, int64_t m, std::vector<double> &K, std::vector<double> &
       K[i * W + t + p] = Kf[(i + 1) * W + t + p];
       M[i * W + t + p] = Mf[(i + 1) * W + t + p];
     }
+  // Interior rows: every basis function they couple is a uniform (translated) B-spline, so the rows
+  // are mathematically identical (cardinal B-spline values, SURVEY §8(c) pins); the quadrature
+  // above reproduces them only up to rounding.  Make them bitwise identical (one representative
+  // row) so that kernels may hold them in registers (Toeplitz) and every interior block has the same
+  // local matrix.  Changes entries by a few ulp.
+  int64_t lo, hi;
+  toeplitz_rows(p, m, &lo, &hi);
+  if (lo <= hi) {
+    const int64_t ref = (lo + hi) / 2;
+    for (int64_t i = lo; i <= hi; ++i)
+      for (int t = 0; t < W; ++t) {
+        K[i * W + t] = K[ref * W + t];
+        M[i * W + t] = M[ref * W + t];
+      }
+  }
+}
+
+void toeplitz_rows(int p, int64_t m, int64_t *lo, int64_t *hi) {
+  // constrained row i = full function f = i + 1; f and its neighbours f-p..f+p are uniform B-splines
+  // (support inside [ξ_{p+1}, ξ_{m+p+1}] with simple knots) iff 2p <= f <= m - 1 - p.
+  *lo = 2 * int64_t(p) - 1;
+  *hi = m - 2 - int64_t(p);
 }
 
 std::vector<double> load_1d_sine(int p, int64_t m) {

@@ -31,6 +31,8 @@ void basis_on_span(const std::vector<double> &U, int p, int k, double x, double 
 // Constrained 1D band tables (P:83 in 1D): K[i*(2p+1) + t+p] = ∫ N'_{i+2} N'_{i+2+t},
 // M[...] = ∫ N_{i+2} N_{i+2+t}, i in [0, n1), zero where i+t is outside [0, n1).
 void band_tables(int p, int64_t m, std::vector<double> &K, std::vector<double> &M);
+// constrained rows [lo, hi] whose band rows are translation invariant (bitwise equal after band_tables)
+void toeplitz_rows(int p, int64_t m, int64_t *lo, int64_t *hi);
 
 // g_i = ∫ sin(π x) N_{i+2}(x) dx, p+3 Gauss points per span (reading A17); n1 values.
 std::vector<double> load_1d_sine(int p, int64_t m);

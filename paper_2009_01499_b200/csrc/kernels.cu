@@ -32,6 +32,13 @@ __device__ double block_sum(double v, double *scratch) {
   return r;
 }
 
+// 8-byte asynchronous global->shared copy (LDGSTS); ok == false writes 0.0 (zero fill, no read)
+__device__ __forceinline__ void cp_async8(double *dst, const double *src, bool ok) {
+  const unsigned d = unsigned(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // ============================ fine operator: apply / residual ============================
 // 2D tile TX x TY outputs; window (TX+2p) x (TY+2p) staged in shared memory.
 template <int TX, int TY>
@@ -46,11 +53,13 @@ __global__ void __launch_bounds__(256) k_apply2d(int p, int n1, const double *__
   double *Tm = Tk + WY * TX;   // [WY][TX]
   __shared__ double red[32];
   const int x0 = blockIdx.x * TX, y0 = zlo + blockIdx.y * TY;
-  for (int i = threadIdx.x; i < WX * WY; i += blockDim.x) {
+  for (int i = threadIdx.x; i < WX * WY; i += blockDim.x) {   // asynchronous staging (LDGSTS)
     const int wy = i / WX, wx = i - wy * WX;
     const int gx = x0 - p + wx, gy = y0 - p + wy;
-    X[i] = (gx >= 0 && gx < n1 && gy >= 0 && gy < n1) ? x[(int64_t)(gy - zoff) * n1 + gx] : 0.0;
+    const bool ok = gx >= 0 && gx < n1 && gy >= 0 && gy < n1;
+    cp_async8(X + i, x + (ok ? (int64_t)(gy - zoff) * n1 + gx : 0), ok);
   }
+  cp_async_wait_all();
   __syncthreads();
   for (int i = threadIdx.x; i < WY * TX; i += blockDim.x) {   // pass along x: K_x X, M_x X
     const int wy = i / TX, lx = i - wy * TX, gx = x0 + lx;
@@ -103,12 +112,13 @@ __global__ void __launch_bounds__(256) k_apply3d(int p, int n1, const double *__
   __shared__ double red[32];
   const int nbx = (n1 + TX - 1) / TX;
   const int x0 = (blockIdx.x % nbx) * TX, y0 = (blockIdx.x / nbx) * TY, z0 = zlo + blockIdx.y * TZ;
-  for (int i = threadIdx.x; i < WX * WY * WZ; i += blockDim.x) {
+  for (int i = threadIdx.x; i < WX * WY * WZ; i += blockDim.x) {   // asynchronous staging (LDGSTS)
     const int wx = i % WX, wy = (i / WX) % WY, wz = i / (WX * WY);
     const int gx = x0 - p + wx, gy = y0 - p + wy, gz = z0 - p + wz;
-    X[i] = (gx >= 0 && gx < n1 && gy >= 0 && gy < n1 && gz >= 0 && gz < n1)
-               ? x[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx] : 0.0;
+    const bool ok = gx >= 0 && gx < n1 && gy >= 0 && gy < n1 && gz >= 0 && gz < n1;
+    cp_async8(X + i, x + (ok ? ((int64_t)(gz - zoff) * n1 + gy) * n1 + gx : 0), ok);
   }
+  cp_async_wait_all();
   __syncthreads();
   for (int i = threadIdx.x; i < TX * WY * WZ; i += blockDim.x) {
     const int lx = i % TX, wyz = i / TX, gx = x0 + lx;
@@ -611,129 +621,183 @@ namespace iga2l {
 namespace {
 
 // barrier for the G warps of one Schwarz block (named barrier 1 + group; __syncwarp if G == 1)
+// (barrier ids are compile-time constants for groups 0..3 so that ptxas reserves only the ids used)
 template <int G>
 __device__ __forceinline__ void group_sync(int group) {
-  if (G == 1) __syncwarp();
-  else asm volatile("bar.sync %0, %1;" ::"r"(group + 1), "r"(32 * G) : "memory");
+  if (G == 1) {
+    __syncwarp();
+    return;
+  }
+  switch (group) {
+    case 0: asm volatile("bar.sync 1, %0;" ::"n"(32 * G) : "memory"); break;
+    case 1: asm volatile("bar.sync 2, %0;" ::"n"(32 * G) : "memory"); break;
+    case 2: asm volatile("bar.sync 3, %0;" ::"n"(32 * G) : "memory"); break;
+    case 3: asm volatile("bar.sync 4, %0;" ::"n"(32 * G) : "memory"); break;
+    default: asm volatile("bar.sync %0, %1;" ::"r"(group + 1), "n"(32 * G) : "memory"); break;
+  }
 }
 
-// One warp per Schwarz block; WPB blocks (warps) per CTA; only __syncwarp inside (blocks of one
-// colour are independent).  Same arithmetic as k_schwarz<2>, compile-time sizes.  Everything the
-// block needs (x window, b_B, the 1D band rows of its rows/columns, its FD tables) is fetched in
-// ONE round of independent loads into shared memory; then four dependent phases:
-//   pass x (K_x X, M_x X), pass y (r_B = b_B - (A x)_B), Z = (Vx^T R Vy) ./ (λx + λy),
-//   δ = Vx Z Vy^T and x_B += δ.   FMA chains are split over two accumulators.
+// One 2D Schwarz block solve by a group of G warps (GT = 32 G threads), compile-time p, s.
+// Per-group shared memory (PER doubles): x window, two pass buffers, r_B, Z, b_B, the block's 1D band
+// rows and FD tables.  Phases: load_const (band rows, FD tables, b_B: independent of the sweep state),
+// load_x (the (s+2p)^2 window of x), compute (pass x: K_x X, M_x X; pass y: r_B = b_B - (A x)_B;
+// Z = (Vx^T R Vy) ./ (λx + λy); δ = Vx Z Vy^T; x_B += δ).  FMA chains split over two accumulators.
+template <int P, int S, int G>
+struct Blk2 {
+  static constexpr int W = 2 * P + 1, Wn = S + 2 * P, w = (S - 1) / 2, S2 = S * S, GT = 32 * G;
+  static constexpr int PER = Wn * Wn + 2 * S * Wn + 3 * S2 + 4 * S * W + 2 * S2 + 2 * S;
+
+  __device__ static __forceinline__ void load_const(double *X, int lane, int n1, int cx, int cy,
+                                                    const double *__restrict__ K, const double *__restrict__ M,
+                                                    const double *__restrict__ Vt, const double *__restrict__ lamt,
+                                                    const double *__restrict__ b, int zoff) {
+    double *Pa = X + Wn * Wn, *Pb = Pa + S * Wn, *R = Pb + S * Wn, *Q = R + S2, *Bb = Q + S2;
+    double *Kx = Bb + S2, *Mx = Kx + S * W, *Ky = Mx + S * W, *My = Ky + S * W;
+    double *Vx = My + S * W, *Vy = Vx + S2, *Lx = Vy + S2, *Ly = Lx + S;
+    const int bx = cx - w, by = cy - w;
+    const unsigned un = unsigned(n1);
+    for (int i = lane; i < S * W; i += GT) {
+      const int l = i / W, t = i - l * W;
+      const int gx = bx + l, gy = by + l;
+      const bool okx = unsigned(gx) < un, oky = unsigned(gy) < un;
+      cp_async8(Kx + i, K + (okx ? (int64_t)gx * W + t : 0), okx);
+      cp_async8(Mx + i, M + (okx ? (int64_t)gx * W + t : 0), okx);
+      cp_async8(Ky + i, K + (oky ? (int64_t)gy * W + t : 0), oky);
+      cp_async8(My + i, M + (oky ? (int64_t)gy * W + t : 0), oky);
+    }
+    for (int i = lane; i < S2; i += GT) {
+      const int ly = i / S, lx = i - ly * S, gx = bx + lx, gy = by + ly;
+      const bool ok = unsigned(gx) < un && unsigned(gy) < un;
+      cp_async8(Bb + i, b + (ok ? (int64_t)(gy - zoff) * n1 + gx : 0), ok);
+      cp_async8(Vx + i, Vt + (int64_t)cx * S2 + i, true);
+      cp_async8(Vy + i, Vt + (int64_t)cy * S2 + i, true);
+    }
+    if (lane < S) {
+      cp_async8(Lx + lane, lamt + (int64_t)cx * S + lane, true);
+      cp_async8(Ly + lane, lamt + (int64_t)cy * S + lane, true);
+    }
+  }
+
+  // CG: read x through L2 only (other SMs update it inside the same kernel)
+  template <bool CG>
+  __device__ static __forceinline__ void load_x(double *X, int lane, int n1, int cx, int cy,
+                                                const double *x, int zoff) {
+    const int ox = cx - w - P, oy = cy - w - P;
+    const unsigned un = unsigned(n1);
+    if (CG) {   // registers, L2 only (ld.global.cg); all loads issued before the stores
+      constexpr int IT = (Wn * Wn + GT - 1) / GT;
+      double v[IT];
+#pragma unroll
+      for (int k = 0; k < IT; ++k) {
+        const int i = lane + k * GT, wy = i / Wn, wx = i - wy * Wn;
+        const int gx = ox + wx, gy = oy + wy;
+        v[k] = (i < Wn * Wn && unsigned(gx) < un && unsigned(gy) < un) ? __ldcg(x + (int64_t)(gy - zoff) * n1 + gx) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < IT; ++k)
+        if (lane + k * GT < Wn * Wn) X[lane + k * GT] = v[k];
+    } else {
+      for (int i = lane; i < Wn * Wn; i += GT) {
+        const int wy = i / Wn, wx = i - wy * Wn;
+        const int gx = ox + wx, gy = oy + wy;
+        const bool ok = unsigned(gx) < un && unsigned(gy) < un;
+        cp_async8(X + i, x + (ok ? (int64_t)(gy - zoff) * n1 + gx : 0), ok);
+      }
+    }
+    cp_async_wait_all();   // this thread's copies (const and x) landed; compute() syncs the group
+  }
+
+  __device__ static __forceinline__ void compute(double *X, int lane, int group, int n1, int cx, int cy, double *x,
+                                                 int zoff) {
+    double *Pa = X + Wn * Wn, *Pb = Pa + S * Wn, *R = Pb + S * Wn, *Q = R + S2, *Bb = Q + S2;
+    double *Kx = Bb + S2, *Mx = Kx + S * W, *Ky = Mx + S * W, *My = Ky + S * W;
+    double *Vx = My + S * W, *Vy = Vx + S2, *Lx = Vy + S2, *Ly = Lx + S;
+    const int bx = cx - w, by = cy - w;
+    const unsigned un = unsigned(n1);
+    group_sync<G>(group);
+#pragma unroll
+    for (int i = lane; i < S * Wn; i += GT) {          // pass x: K_x X, M_x X on the block columns
+      const int wy = i / S, lx = i - wy * S;
+      const double *kr = Kx + lx * W, *mr = Mx + lx * W, *xr = X + wy * Wn + lx;
+      double sa0 = 0.0, sb0 = 0.0, sa1 = 0.0, sb1 = 0.0;
+#pragma unroll
+      for (int t = 0; t + 1 < W; t += 2) {
+        sa0 = fma(kr[t], xr[t], sa0);
+        sb0 = fma(mr[t], xr[t], sb0);
+        sa1 = fma(kr[t + 1], xr[t + 1], sa1);
+        sb1 = fma(mr[t + 1], xr[t + 1], sb1);
+      }
+      sa0 = fma(kr[W - 1], xr[W - 1], sa0);            // W = 2P+1 is odd
+      sb0 = fma(mr[W - 1], xr[W - 1], sb0);
+      Pa[i] = sa0 + sa1;
+      Pb[i] = sb0 + sb1;
+    }
+    group_sync<G>(group);
+#pragma unroll
+    for (int i = lane; i < S2; i += GT) {              // pass y, block residual r_B = b_B - (A x)_B
+      const int ly = i / S, lx = i - ly * S;
+      const double *kr = Ky + ly * W, *mr = My + ly * W;
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int u = 0; u < W; ++u) {
+        a0 = fma(mr[u], Pa[(ly + u) * S + lx], a0);
+        a1 = fma(kr[u], Pb[(ly + u) * S + lx], a1);
+      }
+      R[i] = Bb[i] - (a0 + a1);                        // rows/cols outside the grid: band rows are 0
+    }
+    group_sync<G>(group);
+#pragma unroll
+    for (int i = lane; i < S2; i += GT) {              // Z[k][j] = Σ_{ly,lx} Vx[lx][j] R[ly][lx] Vy[ly][k] / (λx_j + λy_k)
+      const int k = i / S, j = i - k * S;
+      double z0 = 0.0, z1 = 0.0;
+#pragma unroll
+      for (int ly = 0; ly < S; ++ly) {
+        double t = 0.0;
+#pragma unroll
+        for (int lx = 0; lx < S; ++lx) t = fma(Vx[lx * S + j], R[ly * S + lx], t);
+        if (ly & 1) z1 = fma(Vy[ly * S + k], t, z1); else z0 = fma(Vy[ly * S + k], t, z0);
+      }
+      Q[i] = (z0 + z1) / (Lx[j] + Ly[k]);
+    }
+    group_sync<G>(group);
+#pragma unroll
+    for (int i = lane; i < S2; i += GT) {              // δ[ly][lx] = Σ_{k,j} Vy[ly][k] Vx[lx][j] Z[k][j];  x_B += δ
+      const int ly = i / S, lx = i - ly * S, gx = bx + lx, gy = by + ly;
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        double t = 0.0;
+#pragma unroll
+        for (int j = 0; j < S; ++j) t = fma(Vx[lx * S + j], Q[k * S + j], t);
+        if (k & 1) d1 = fma(Vy[ly * S + k], t, d1); else d0 = fma(Vy[ly * S + k], t, d0);
+      }
+      if (unsigned(gx) < un && unsigned(gy) < un) x[(int64_t)(gy - zoff) * n1 + gx] = X[(ly + P) * Wn + lx + P] + (d0 + d1);
+    }
+  }
+};
+
+// One colour: WPB Schwarz blocks (groups of G warps) per CTA; only group barriers inside.
 template <int P, int S, int WPB, int G>
 __global__ void __launch_bounds__(WPB * G * 32) k_schwarz2d_w(int n1, const double *__restrict__ K,
                                                          const double *__restrict__ M, const double *__restrict__ Vt,
                                                          const double *__restrict__ lamt,
                                                          const double *__restrict__ b, double *__restrict__ x,
                                                          int c0, int c1, int D, int nb0, int nblk, int zoff) {
-  constexpr int W = 2 * P + 1, Wn = S + 2 * P, w = (S - 1) / 2, S2 = S * S;
-  constexpr int PER = Wn * Wn + 2 * S * Wn + 3 * S2 + 4 * S * W + 2 * S2 + 2 * S;
+  using B = Blk2<P, S, G>;
   extern __shared__ double sm[];
-  constexpr int GT = 32 * G;                            // threads per Schwarz block (G warps)
-  const int warp = threadIdx.x / GT, lane = threadIdx.x % GT;
+  const int warp = threadIdx.x / B::GT, lane = threadIdx.x % B::GT;
   const int bid = blockIdx.x * WPB + warp;
   if (bid >= nblk) return;                              // whole group exits together
-  double *X = sm + warp * PER, *Pa = X + Wn * Wn, *Pb = Pa + S * Wn, *R = Pb + S * Wn, *Q = R + S2;
-  double *Bb = Q + S2;                                   // b_B
-  double *Kx = Bb + S2, *Mx = Kx + S * W, *Ky = Mx + S * W, *My = Ky + S * W;   // band rows
-  double *Vx = My + S * W, *Vy = Vx + S2, *Lx = Vy + S2, *Ly = Lx + S;
+  double *X = sm + warp * B::PER;
   const int j1 = bid / nb0, j0 = bid - j1 * nb0;
   const int cx = c0 + D * j0, cy = c1 + D * j1;
-  const int ox = cx - w - P, oy = cy - w - P, bx = cx - w, by = cy - w;
-  const unsigned un = unsigned(n1);
   // Programmatic dependent launch: let the next colour's grid start now; everything that does not
-  // depend on the previous colour (band rows, FD tables, b_B) is loaded before griddepcontrol.wait.
+  // depend on the previous colour is loaded before griddepcontrol.wait.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#pragma unroll
-  for (int i = lane; i < S * W; i += GT) {
-    const int l = i / W, t = i - l * W;
-    const int gx = bx + l, gy = by + l;
-    const bool okx = unsigned(gx) < un, oky = unsigned(gy) < un;
-    Kx[i] = okx ? K[(int64_t)gx * W + t] : 0.0;
-    Mx[i] = okx ? M[(int64_t)gx * W + t] : 0.0;
-    Ky[i] = oky ? K[(int64_t)gy * W + t] : 0.0;
-    My[i] = oky ? M[(int64_t)gy * W + t] : 0.0;
-  }
-#pragma unroll
-  for (int i = lane; i < S2; i += GT) {
-    const int ly = i / S, lx = i - ly * S, gx = bx + lx, gy = by + ly;
-    Bb[i] = (unsigned(gx) < un && unsigned(gy) < un) ? b[(int64_t)(gy - zoff) * n1 + gx] : 0.0;
-    Vx[i] = Vt[(int64_t)cx * S2 + i];
-    Vy[i] = Vt[(int64_t)cy * S2 + i];
-  }
-  if (lane < S) {
-    Lx[lane] = lamt[(int64_t)cx * S + lane];
-    Ly[lane] = lamt[(int64_t)cy * S + lane];
-  }
+  B::load_const(X, lane, n1, cx, cy, K, M, Vt, lamt, b, zoff);
   asm volatile("griddepcontrol.wait;" ::: "memory");   // previous colour complete and visible
-#pragma unroll
-  for (int i = lane; i < Wn * Wn; i += GT) {
-    const int wy = i / Wn, wx = i - wy * Wn;
-    const int gx = ox + wx, gy = oy + wy;
-    X[i] = (unsigned(gx) < un && unsigned(gy) < un) ? x[(int64_t)(gy - zoff) * n1 + gx] : 0.0;
-  }
-  group_sync<G>(warp);
-#pragma unroll
-  for (int i = lane; i < S * Wn; i += GT) {          // pass x: K_x X, M_x X on the block columns
-    const int wy = i / S, lx = i - wy * S;
-    const double *kr = Kx + lx * W, *mr = Mx + lx * W, *xr = X + wy * Wn + lx;
-    double sa0 = 0.0, sb0 = 0.0, sa1 = 0.0, sb1 = 0.0;
-#pragma unroll
-    for (int t = 0; t + 1 < W; t += 2) {
-      sa0 = fma(kr[t], xr[t], sa0);
-      sb0 = fma(mr[t], xr[t], sb0);
-      sa1 = fma(kr[t + 1], xr[t + 1], sa1);
-      sb1 = fma(mr[t + 1], xr[t + 1], sb1);
-    }
-    sa0 = fma(kr[W - 1], xr[W - 1], sa0);            // W = 2P+1 is odd
-    sb0 = fma(mr[W - 1], xr[W - 1], sb0);
-    Pa[i] = sa0 + sa1;
-    Pb[i] = sb0 + sb1;
-  }
-  group_sync<G>(warp);
-#pragma unroll
-  for (int i = lane; i < S2; i += GT) {              // pass y, block residual r_B = b_B - (A x)_B
-    const int ly = i / S, lx = i - ly * S;
-    const double *kr = Ky + ly * W, *mr = My + ly * W;
-    double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-    for (int u = 0; u < W; ++u) {
-      a0 = fma(mr[u], Pa[(ly + u) * S + lx], a0);
-      a1 = fma(kr[u], Pb[(ly + u) * S + lx], a1);
-    }
-    R[i] = Bb[i] - (a0 + a1);                        // rows/cols outside the grid: band rows are 0
-  }
-  group_sync<G>(warp);
-#pragma unroll
-  for (int i = lane; i < S2; i += GT) {              // Z[k][j] = Σ_{ly,lx} Vx[lx][j] R[ly][lx] Vy[ly][k] / (λx_j + λy_k)
-    const int k = i / S, j = i - k * S;
-    double z0 = 0.0, z1 = 0.0;
-#pragma unroll
-    for (int ly = 0; ly < S; ++ly) {
-      double t = 0.0;
-#pragma unroll
-      for (int lx = 0; lx < S; ++lx) t = fma(Vx[lx * S + j], R[ly * S + lx], t);
-      if (ly & 1) z1 = fma(Vy[ly * S + k], t, z1); else z0 = fma(Vy[ly * S + k], t, z0);
-    }
-    Q[i] = (z0 + z1) / (Lx[j] + Ly[k]);
-  }
-  group_sync<G>(warp);
-#pragma unroll
-  for (int i = lane; i < S2; i += GT) {              // δ[ly][lx] = Σ_{k,j} Vy[ly][k] Vx[lx][j] Z[k][j];  x_B += δ
-    const int ly = i / S, lx = i - ly * S, gx = bx + lx, gy = by + ly;
-    double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-    for (int k = 0; k < S; ++k) {
-      double t = 0.0;
-#pragma unroll
-      for (int j = 0; j < S; ++j) t = fma(Vx[lx * S + j], Q[k * S + j], t);
-      if (k & 1) d1 = fma(Vy[ly * S + k], t, d1); else d0 = fma(Vy[ly * S + k], t, d0);
-    }
-    if (unsigned(gx) < un && unsigned(gy) < un) x[(int64_t)(gy - zoff) * n1 + gx] = X[(ly + P) * Wn + lx + P] + (d0 + d1);
-  }
+  B::template load_x<false>(X, lane, n1, cx, cy, x, zoff);
+  B::compute(X, lane, warp, n1, cx, cy, x, zoff);
 }
 
 int g_use_pdl = 0;   // programmatic dependent launch between colour kernels (measured slower: off)
@@ -742,9 +806,7 @@ template <int P, int S, int WPB, int G>
 bool try_schwarz2d(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
                    const double *b, double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st) {
   if (p != P || s != S) return false;
-  constexpr int Wn = S + 2 * P;
-  constexpr int W = 2 * P + 1;
-  constexpr size_t sm = sizeof(double) * WPB * (Wn * Wn + 2 * S * Wn + 5 * S * S + 4 * S * W + 2 * S);
+  constexpr size_t sm = sizeof(double) * WPB * Blk2<P, S, G>::PER;
   ensure_smem(k_schwarz2d_w<P, S, WPB, G>, sm);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((nblk + WPB - 1) / WPB);
@@ -758,6 +820,121 @@ bool try_schwarz2d(int p, int s, int64_t n1, const double *K, const double *M, c
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, k_schwarz2d_w<P, S, WPB, G>, int(n1), K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff);
   return true;
+}
+
+// ---------------- persistent 2D sweep: all D^2 colours in ONE launch -------------------------
+// CTA t owns tile t of block centres (D*AX x D*AY, aligned to D, so each colour has the same AX*AY
+// block positions in every tile) for the whole sweep; groups of G warps solve its blocks of the
+// current colour.  Colour c of tile T may start once T and its 8 neighbour tiles have finished colour
+// c-1 (per-tile progress counters done[], release/acquire at GPU scope): only blocks within
+// 2w + p < D of each other interact, so this reproduces the colour-major multiplicative sweep exactly
+// (reading A4).  The grid is launched cooperatively (all tiles co-resident, so the waits cannot
+// deadlock).  done[] counts colours monotonically across launches: the launch's base is ctl[0], and
+// the last CTA to finish advances it by D^2.
+constexpr int kFlagStride = 32;   // one progress counter per 128-byte line
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int P, int S, int AX, int AY, int NB, int G>
+__global__ void __launch_bounds__(NB * G * 32) k_sweep2d_persist(int n1, const double *__restrict__ K,
+                                                                 const double *__restrict__ M,
+                                                                 const double *__restrict__ Vt,
+                                                                 const double *__restrict__ lamt,
+                                                                 const double *__restrict__ b, double *x, int ntx,
+                                                                 int nty, unsigned *ctl, unsigned *done) {
+  using B = Blk2<P, S, G>;
+  constexpr int D = S + P, TX = D * AX, TY = D * AY, NC = D * D, NBLK = AX * AY;
+  extern __shared__ double sm[];
+  __shared__ unsigned s_base;
+  const int group = threadIdx.x / B::GT, lane = threadIdx.x % B::GT;
+  double *X = sm + group * B::PER;
+  const int T = blockIdx.x, tx = T % ntx, ty = T / ntx;
+  if (threadIdx.x == 0) s_base = *reinterpret_cast<volatile unsigned *>(ctl);
+  __syncthreads();
+  const unsigned base = s_base;
+  for (int c = 0; c < NC; ++c) {
+    auto centre = [&](int blk, int *cx, int *cy) {
+      *cx = tx * TX + (c % D) + D * (blk % AX);
+      *cy = ty * TY + (c / D) + D * (blk / AX);
+      return *cx < n1 && *cy < n1;
+    };
+    int cx, cy;
+    if (group < NBLK && centre(group, &cx, &cy))       // first block's constants overlap the wait
+      B::load_const(X, lane, n1, cx, cy, K, M, Vt, lamt, b, 0);
+    if (c > 0 && threadIdx.x < 9) {                    // wait: this tile and its neighbours done with c-1
+      const int ux = tx + int(threadIdx.x % 3) - 1, uy = ty + int(threadIdx.x / 3) - 1;
+      if (ux >= 0 && ux < ntx && uy >= 0 && uy < nty) {
+        const volatile unsigned *f = done + kFlagStride * (uy * ntx + ux);
+        while (int(*f - (base + unsigned(c))) < 0) {
+        }
+        __threadfence();                               // acquire side of the flag handshake
+      }
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int blk = group; blk < NBLK; blk += NB) {     // this group's blocks of colour c in the tile
+      if (!centre(blk, &cx, &cy)) continue;
+      if (blk != group) B::load_const(X, lane, n1, cx, cy, K, M, Vt, lamt, b, 0);
+      B::template load_x<true>(X, lane, n1, cx, cy, x, 0);
+      B::compute(X, lane, group, n1, cx, cy, x, 0);
+      group_sync<G>(group);                            // the group's smem is reused by its next block
+    }
+    __syncthreads();                                   // every warp's x stores precede ...
+    if (threadIdx.x == 0) {                            // ... the release by thread 0 (grid-sync pattern)
+      __threadfence();
+      *reinterpret_cast<volatile unsigned *>(done + kFlagStride * T) = base + unsigned(c) + 1u;
+    }
+  }
+  if (threadIdx.x == 0) {                              // last CTA out advances the base
+    __threadfence();
+    if (atomicAdd(ctl + 1, 1u) == gridDim.x - 1) {
+      ctl[1] = 0;
+      __threadfence();
+      atomicAdd(ctl, unsigned(NC));
+    }
+  }
+}
+
+template <int P, int S, int AX, int AY, int NB, int G>
+int try_sweep2d_persist(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
+                        const double *b, double *x, unsigned *ctl, unsigned *done, int max_tiles, cudaStream_t st,
+                        bool launch) {
+  if (p != P || s != S) return -1;
+  constexpr int D = S + P;
+  const int ntx = int((n1 + D * AX - 1) / (D * AX)), nty = int((n1 + D * AY - 1) / (D * AY));
+  const int ntiles = ntx * nty;
+  constexpr size_t sm = sizeof(double) * NB * Blk2<P, S, G>::PER;
+  auto kern = k_sweep2d_persist<P, S, AX, AY, NB, G>;
+  if (!launch) {   // feasibility: every tile co-resident
+    ensure_smem(kern, sm);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NB * G * 32, sm) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    return (ntiles <= per_sm * nsm && ntiles <= max_tiles) ? ntiles : 0;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ntiles);
+  cfg.blockDim = dim3(NB * G * 32);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, int(n1), K, M, V, lam, b, x, ntx, nty, ctl, done);
+  return ntiles;
 }
 
 // 2D tensor transfer, direct: out[ry][rx] (+)= Σ_{ky,kx} c[ry][ky] c[rx][kx] in[lo[ry]+ky][lo[rx]+kx].
@@ -1010,13 +1187,315 @@ __global__ void __launch_bounds__(512) k_vcycle_cluster(const QLevelDev *__restr
   }
 }
 
+// ---------------- 3D Schwarz colour kernel, compile-time (p, s): one CTA per block ------------
+// Same arithmetic as k_schwarz<3> (sum-factorised block residual over the (s+2p)^3 window, then
+// fast diagonalisation), register-blocked: every pass maps one thread to a PENCIL (a line of the
+// window along the contracted axis), loads it once into registers and produces all s outputs of that
+// line.  A pass along an axis whose s block rows are all translation-invariant rows (tlo..thi, made
+// bitwise equal at setup) keeps the 2(2p+1) band coefficients in registers; otherwise they are read
+// per row from shared memory.
+template <int S, int W, int Wn, bool TOE>
+__device__ __forceinline__ void band_pencil(const double *in, int stride, const double *ck, const double *cm,
+                                            double (&oa)[S], double (&ob)[S]) {
+  double v[Wn];
+#pragma unroll
+  for (int k = 0; k < Wn; ++k) v[k] = in[k * stride];
+#pragma unroll
+  for (int l = 0; l < S; ++l) {
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < W; ++t) {
+      const double kc = TOE ? ck[t] : ck[l * W + t], mc = TOE ? cm[t] : cm[l * W + t];
+      if (t & 1) { a1 = fma(kc, v[l + t], a1); b1 = fma(mc, v[l + t], b1); }
+      else { a0 = fma(kc, v[l + t], a0); b0 = fma(mc, v[l + t], b0); }
+    }
+    oa[l] = a0 + a1;
+    ob[l] = b0 + b1;
+  }
+}
+
+// pass y: from pencils pa, pb (stride) -> c = My pa + Ky pb, e = My pb
+template <int S, int W, int Wn, bool TOE>
+__device__ __forceinline__ void band_pencil2(const double *pa_, const double *pb_, int stride, const double *ck,
+                                             const double *cm, double (&oc)[S], double (&oe)[S]) {
+  double pa[Wn], pb[Wn];
+#pragma unroll
+  for (int k = 0; k < Wn; ++k) { pa[k] = pa_[k * stride]; pb[k] = pb_[k * stride]; }
+#pragma unroll
+  for (int l = 0; l < S; ++l) {
+    double c0 = 0.0, c1 = 0.0, e0 = 0.0;
+#pragma unroll
+    for (int t = 0; t < W; ++t) {
+      const double kc = TOE ? ck[t] : ck[l * W + t], mc = TOE ? cm[t] : cm[l * W + t];
+      c0 = fma(mc, pa[l + t], c0);
+      c1 = fma(kc, pb[l + t], c1);
+      e0 = fma(mc, pb[l + t], e0);
+    }
+    oc[l] = c0 + c1;
+    oe[l] = e0;
+  }
+}
+
+template <int P, int S>
+struct Blk3 {
+  static constexpr int W = 2 * P + 1, Wn = S + 2 * P, w = (S - 1) / 2, S2 = S * S, S3 = S2 * S, Wn2 = Wn * Wn;
+  static constexpr int PER = Wn2 * Wn + 2 * Wn2 * S + 2 * Wn * S2 + 3 * S3 + 6 * S * W + 3 * S2 + 3 * S;
+};
+
+// NBK blocks per CTA (block g = blockIdx.x * NBK + k of the colour's nb0 x nb1 x nb2 grid); every phase
+// runs over (block, pencil) pairs so that the short phases still occupy the CTA.
+template <int P, int S, int NBK, int NT, bool ROW>
+__global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__restrict__ K, const double *__restrict__ M,
+                                                    const double *__restrict__ Vt, const double *__restrict__ lamt,
+                                                    const double *__restrict__ b, double *__restrict__ x, int c0, int c1,
+                                                    int c2, int D, int nb0, int nb1, int nblk, int zoff, int tlo,
+                                                    int thi) {
+  using B = Blk3<P, S>;
+  constexpr int W = B::W, Wn = B::Wn, w = B::w, S2 = B::S2, S3 = B::S3, Wn2 = B::Wn2, PER = B::PER;
+  extern __shared__ double sm[];
+  const int tid = threadIdx.x;
+  const unsigned un = unsigned(n1);
+  // per-block regions: X [z][y][x] window, Pa/Pb [wz][wy][lx], Pc/Pe [wz][ly][lx], R, Q, Bb,
+  // Tk/Tm [axis][row][t], Vs [axis][l][j], Ls [axis][j]
+  auto X = [&](int k) { return sm + k * PER; };
+  auto Pa = [&](int k) { return sm + k * PER + Wn2 * Wn; };
+  auto Pb = [&](int k) { return sm + k * PER + Wn2 * Wn + Wn2 * S; };
+  auto Pc = [&](int k) { return sm + k * PER + Wn2 * Wn + 2 * Wn2 * S; };
+  auto Pe = [&](int k) { return sm + k * PER + Wn2 * Wn + 2 * Wn2 * S + Wn * S2; };
+  auto R = [&](int k) { return sm + k * PER + Wn2 * Wn + 2 * Wn2 * S + 2 * Wn * S2; };
+  auto Q = [&](int k) { return R(k) + S3; };
+  auto Bb = [&](int k) { return R(k) + 2 * S3; };
+  auto Tk = [&](int k) { return R(k) + 3 * S3; };
+  auto Tm = [&](int k) { return R(k) + 3 * S3 + 3 * S * W; };
+  auto Vs = [&](int k) { return R(k) + 3 * S3 + 6 * S * W; };
+  auto Ls = [&](int k) { return R(k) + 3 * S3 + 6 * S * W + 3 * S2; };
+  __shared__ int sC[NBK][3];
+  __shared__ bool sT[NBK][3];
+  if (NBK > 1 && tid < NBK) {                               // block centres, Toeplitz flags per axis
+    const int g = blockIdx.x * NBK + tid;
+    const int cc[3] = {c0 + D * (g % nb0), c1 + D * ((g / nb0) % nb1), c2 + D * (g / (nb0 * nb1))};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      sC[tid][a] = cc[a];
+      sT[tid][a] = (cc[a] - w >= tlo) && (cc[a] + w <= thi);
+    }
+  }
+  __syncthreads();
+  int cc1[3];                                               // NBK == 1: the centre in registers
+  bool tt1[3];
+  if (NBK == 1) {
+    const int g = blockIdx.x;
+    cc1[0] = c0 + D * (g % nb0);
+    cc1[1] = c1 + D * ((g / nb0) % nb1);
+    cc1[2] = c2 + D * (g / (nb0 * nb1));
+#pragma unroll
+    for (int a = 0; a < 3; ++a) tt1[a] = (cc1[a] - w >= tlo) && (cc1[a] + w <= thi);
+  }
+  auto centre = [&](int k, int a) { return NBK == 1 ? cc1[a] : sC[k][a]; };
+  const int nk = min(NBK, nblk - int(blockIdx.x) * NBK);   // blocks of this CTA
+  // ---- loads: band rows, FD tables, b_B, x windows: all asynchronous (LDGSTS), one wait ----
+  for (int i = tid; i < nk * 3 * S * W; i += NT) {
+    const int k = NBK == 1 ? 0 : i / (3 * S * W), r = NBK == 1 ? i : i % (3 * S * W);
+    const int a = r / (S * W), l = (r / W) % S, t = r % W;
+    const int g = centre(k, a) - w + l;
+    const bool ok = unsigned(g) < un;
+    cp_async8(Tk(k) + r, K + (ok ? (int64_t)g * W + t : 0), ok);
+    cp_async8(Tm(k) + r, M + (ok ? (int64_t)g * W + t : 0), ok);
+  }
+  for (int i = tid; i < nk * 3 * S2; i += NT) {
+    const int k = NBK == 1 ? 0 : i / (3 * S2), r = NBK == 1 ? i : i % (3 * S2);
+    cp_async8(Vs(k) + r, Vt + (int64_t)centre(k, r / S2) * S2 + r % S2, true);
+  }
+  for (int i = tid; i < nk * 3 * S; i += NT) {
+    const int k = NBK == 1 ? 0 : i / (3 * S), r = NBK == 1 ? i : i % (3 * S);
+    cp_async8(Ls(k) + r, lamt + (int64_t)centre(k, r / S) * S + r % S, true);
+  }
+  for (int i = tid; i < nk * S3; i += NT) {
+    const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3;
+    const int gx = centre(k, 0) - w + r % S, gy = centre(k, 1) - w + (r / S) % S, gz = centre(k, 2) - w + r / S2;
+    const bool ok = unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un;
+    cp_async8(Bb(k) + r, b + (ok ? ((int64_t)(gz - zoff) * n1 + gy) * n1 + gx : 0), ok);
+  }
+  if (!ROW) {                                       // x windows, element by element
+    for (int i = tid; i < nk * Wn2 * Wn; i += NT) {
+      const int k = NBK == 1 ? 0 : i / (Wn2 * Wn), r = NBK == 1 ? i : i % (Wn2 * Wn);
+      const int gx = centre(k, 0) - w - P + r % Wn, gy = centre(k, 1) - w - P + (r / Wn) % Wn,
+                gz = centre(k, 2) - w - P + r / Wn2;
+      const bool ok = unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un;
+      cp_async8(X(k) + r, x + (ok ? ((int64_t)(gz - zoff) * n1 + gy) * n1 + gx : 0), ok);
+    }
+  } else {                                          // x windows: one window row per 16 lanes
+    const int lane16 = tid & 15;
+    for (int row = tid >> 4; row < nk * Wn2; row += NT / 16) {
+      const int k = NBK == 1 ? 0 : row / Wn2, rr = row - k * Wn2, wz = rr / Wn, wy = rr - wz * Wn;
+      const int ox = centre(k, 0) - w - P, gy = centre(k, 1) - w - P + wy, gz = centre(k, 2) - w - P + wz;
+      const bool okyz = unsigned(gy) < un && unsigned(gz) < un;
+      const double *src = x + (okyz ? ((int64_t)(gz - zoff) * n1 + gy) * n1 : 0);
+      double *dst = X(k) + rr * Wn;
+#pragma unroll
+      for (int wx = lane16; wx < Wn; wx += 16) {
+        const int gx = ox + wx;
+        const bool ok = okyz && unsigned(gx) < un;
+        cp_async8(dst + wx, ok ? src + gx : x, ok);
+      }
+    }
+  }
+  cp_async_wait_all();
+  auto toe = [&](int k, int a) { return NBK == 1 ? tt1[a] : sT[k][a]; };
+  __syncthreads();
+  // ---- pass x: pencils (wy, wz) along x -> Pa = Kx X, Pb = Mx X ----
+  for (int i = tid; i < nk * Wn2; i += NT) {
+    const int k = NBK == 1 ? 0 : i / Wn2, pi = NBK == 1 ? i : i % Wn2;
+    double oa[S], ob[S];
+    if (toe(k, 0)) band_pencil<S, W, Wn, true>(X(k) + pi * Wn, 1, Tk(k), Tm(k), oa, ob);
+    else band_pencil<S, W, Wn, false>(X(k) + pi * Wn, 1, Tk(k), Tm(k), oa, ob);
+#pragma unroll
+    for (int l = 0; l < S; ++l) { Pa(k)[pi * S + l] = oa[l]; Pb(k)[pi * S + l] = ob[l]; }
+  }
+  __syncthreads();
+  // ---- pass y: pencils (wz, lx) along y -> Pc = My Pa + Ky Pb, Pe = My Pb ----
+  for (int i = tid; i < nk * Wn * S; i += NT) {
+    const int k = NBK == 1 ? 0 : i / (Wn * S), pi = NBK == 1 ? i : i % (Wn * S);
+    const int wz = pi / S, lx = pi % S;
+    double oc[S], oe[S];
+    const double *pa = Pa(k) + wz * Wn * S + lx, *pb = Pb(k) + wz * Wn * S + lx;
+    if (toe(k, 1)) band_pencil2<S, W, Wn, true>(pa, pb, S, Tk(k) + S * W, Tm(k) + S * W, oc, oe);
+    else band_pencil2<S, W, Wn, false>(pa, pb, S, Tk(k) + S * W, Tm(k) + S * W, oc, oe);
+#pragma unroll
+    for (int l = 0; l < S; ++l) { Pc(k)[(wz * S + l) * S + lx] = oc[l]; Pe(k)[(wz * S + l) * S + lx] = oe[l]; }
+  }
+  __syncthreads();
+  // ---- pass z: pencils (ly, lx) along z -> r_B = b_B - (Mz Pc + Kz Pe) ----
+  for (int i = tid; i < nk * S2; i += NT) {
+    const int k = NBK == 1 ? 0 : i / S2, pi = NBK == 1 ? i : i % S2;
+    double oc[S], oe[S];
+    if (toe(k, 2)) band_pencil2<S, W, Wn, true>(Pc(k) + pi, Pe(k) + pi, S2, Tk(k) + 2 * S * W, Tm(k) + 2 * S * W, oc, oe);
+    else band_pencil2<S, W, Wn, false>(Pc(k) + pi, Pe(k) + pi, S2, Tk(k) + 2 * S * W, Tm(k) + 2 * S * W, oc, oe);
+#pragma unroll
+    for (int l = 0; l < S; ++l) R(k)[l * S2 + pi] = Bb(k)[l * S2 + pi] - oc[l];
+  }
+  __syncthreads();
+  // ---- δ = (⊗V) Λ^{-1} (⊗V)^T r ----
+  for (int i = tid; i < nk * S3; i += NT) {         // along x (transposed)
+    const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3, j = r % S, rest = r - j;
+    const double *Vx = Vs(k);
+    double a0 = 0.0;
+#pragma unroll
+    for (int l = 0; l < S; ++l) a0 = fma(Vx[l * S + j], R(k)[rest + l], a0);
+    Q(k)[r] = a0;
+  }
+  __syncthreads();
+  for (int i = tid; i < nk * S3; i += NT) {         // along y (transposed)
+    const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3, j = r % S, kk = (r / S) % S, lz = r / S2;
+    const double *Vy = Vs(k) + S2;
+    double a0 = 0.0;
+#pragma unroll
+    for (int l = 0; l < S; ++l) a0 = fma(Vy[l * S + kk], Q(k)[(lz * S + l) * S + j], a0);
+    R(k)[r] = a0;
+  }
+  __syncthreads();
+  for (int i = tid; i < nk * S3; i += NT) {         // along z (transposed), then / (λx + λy + λz)
+    const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3, j = r % S, kk = (r / S) % S, l3 = r / S2;
+    const double *Vz = Vs(k) + 2 * S2, *L = Ls(k);
+    double a0 = 0.0;
+#pragma unroll
+    for (int l = 0; l < S; ++l) a0 = fma(Vz[l * S + l3], R(k)[(l * S + kk) * S + j], a0);
+    Q(k)[r] = a0 / (L[j] + L[S + kk] + L[2 * S + l3]);
+  }
+  __syncthreads();
+  for (int i = tid; i < nk * S3; i += NT) {         // along z
+    const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3, j = r % S, kk = (r / S) % S, lz = r / S2;
+    const double *Vz = Vs(k) + 2 * S2;
+    double a0 = 0.0;
+#pragma unroll
+    for (int l = 0; l < S; ++l) a0 = fma(Vz[lz * S + l], Q(k)[(l * S + kk) * S + j], a0);
+    R(k)[r] = a0;
+  }
+  __syncthreads();
+  for (int i = tid; i < nk * S3; i += NT) {         // along y
+    const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3, j = r % S, ly = (r / S) % S, lz = r / S2;
+    const double *Vy = Vs(k) + S2;
+    double a0 = 0.0;
+#pragma unroll
+    for (int l = 0; l < S; ++l) a0 = fma(Vy[ly * S + l], R(k)[(lz * S + l) * S + j], a0);
+    Q(k)[r] = a0;
+  }
+  __syncthreads();
+  for (int i = tid; i < nk * S3; i += NT) {         // along x, and x_B += δ
+    const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3, lx = r % S, ly = (r / S) % S, lz = r / S2, rest = r - lx;
+    const double *Vx = Vs(k);
+    double a0 = 0.0;
+#pragma unroll
+    for (int l = 0; l < S; ++l) a0 = fma(Vx[lx * S + l], Q(k)[rest + l], a0);
+    const int gx = centre(k, 0) - w + lx, gy = centre(k, 1) - w + ly, gz = centre(k, 2) - w + lz;
+    if (unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un)
+      x[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx] = X(k)[((lz + P) * Wn + ly + P) * Wn + lx + P] + a0;
+  }
+}
+
+// Launch variants per (p, s): <blocks per CTA, threads, row-wise window staging>.  The default is
+// variant 0; IGA2L_S3D_VARIANT=<i> selects another (A/B timing on one box, tools/variants.py).
+int g_s3d_variant = -1;
+int s3d_variant() {
+  if (g_s3d_variant < 0) {
+    const char *e = std::getenv("IGA2L_S3D_VARIANT");
+    g_s3d_variant = e ? std::atoi(e) : 0;
+  }
+  return g_s3d_variant;
+}
+
+template <int P, int S, int NBK, int NT, bool ROW>
+void launch3d(int64_t n1, const double *K, const double *M, const double *V, const double *lam, const double *b,
+              double *x, int c0, int c1, int c2, int D, int nb0, int nb1, int nb2, int zoff, int tlo, int thi,
+              cudaStream_t st) {
+  constexpr size_t sm = sizeof(double) * NBK * Blk3<P, S>::PER;
+  ensure_smem(k_schwarz3d_t<P, S, NBK, NT, ROW>, sm);
+  const int nblk = nb0 * nb1 * nb2;
+  k_schwarz3d_t<P, S, NBK, NT, ROW><<<(nblk + NBK - 1) / NBK, NT, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, c2,
+                                                                            D, nb0, nb1, nblk, zoff, tlo, thi);
+}
+
+template <int P, int S>
+bool try_schwarz3d(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
+                   const double *b, double *x, int c0, int c1, int c2, int D, int nb0, int nb1, int nb2, int zoff,
+                   int tlo, int thi, cudaStream_t st) {
+  if (p != P || s != S) return false;
+  constexpr int NT1 = ((Blk3<P, S>::Wn2 + 31) / 32) * 32 > 512 ? 512 : ((Blk3<P, S>::Wn2 + 31) / 32) * 32;
+  switch (s3d_variant()) {
+    case 1: launch3d<P, S, 1, NT1, true>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, zoff, tlo, thi, st); break;
+    case 2: launch3d<P, S, 2, (2 * NT1 > 512 ? 512 : 2 * NT1), false>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, zoff, tlo, thi, st); break;
+    case 3: launch3d<P, S, 1, (NT1 >= 128 ? NT1 / 2 : NT1), false>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, zoff, tlo, thi, st); break;
+    default:   // measured best (tools/variants.py): s >= 5 -> half the pass-x pencil count of threads
+      launch3d<P, S, 1, (S >= 5 && NT1 >= 128 ? NT1 / 2 : NT1), false>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1,
+                                                                      nb2, zoff, tlo, thi, st);
+      break;
+  }
+  return true;
+}
+
 }  // namespace
 
 bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M, const double *V,
                                 const double *lam, const double *b, double *x, int colour, int D, cudaStream_t st,
                                 SlabView sv) {
-  if (dim != 2) return false;
   if (sv.zhi < 0) sv = SlabView{0, 0, int(n1)};
+  if (dim == 3) {
+    const int c0 = colour % D, c1 = (colour / D) % D, c2 = colour / (D * D);
+    int f2, nb2;
+    centre_range(c2, D, sv.zlo, sv.zhi, &f2, &nb2);
+    if (c0 >= n1 || c1 >= n1 || nb2 == 0) return true;   // empty colour
+    const int nb0 = int((n1 - c0 + D - 1) / D), nb1 = int((n1 - c1 + D - 1) / D);
+    const int m = int(n1) - p + 2;
+    const int tlo = 2 * p - 1, thi = m - 2 - p;            // translation-invariant rows (toeplitz_rows)
+    const int z = sv.zoff;
+    return try_schwarz3d<1, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st) ||
+           try_schwarz3d<2, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st) ||
+           try_schwarz3d<3, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st) ||
+           try_schwarz3d<4, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st) ||
+           try_schwarz3d<5, 5>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st) ||
+           try_schwarz3d<6, 5>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st);
+  }
+  if (dim != 2) return false;
   const int c0 = colour % D, c1 = (colour / D) % D;
   int f1, nb1;
   centre_range(c1, D, sv.zlo, sv.zhi, &f1, &nb1);
@@ -1032,6 +1511,29 @@ bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double 
          try_schwarz2d<6, 5, 2, 4>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
          try_schwarz2d<7, 7, 2, 4>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
          try_schwarz2d<8, 7, 2, 4>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st);
+}
+
+// Persistent sweep dispatcher (2D).  launch = false: number of tiles (= CTAs, = progress counters)
+// the kernel would use, 0 if it cannot keep all of them co-resident, -1 if (p, s) is not specialised.
+int sweep2d_persist(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
+                    const double *b, double *x, unsigned *ctl, unsigned *done, int max_tiles, cudaStream_t st,
+                    bool launch) {
+  int r;
+  // <P, S, tile blocks AX x AY, groups per CTA, warps per group>
+#define IGA2L_TRY(P_, S_, AX_, AY_, NB_, G_)                                                                    \
+  if ((r = try_sweep2d_persist<P_, S_, AX_, AY_, NB_, G_>(p, s, n1, K, M, V, lam, b, x, ctl, done, max_tiles, st, \
+                                                          launch)) >= 0)                                         \
+    return r;
+  IGA2L_TRY(1, 3, 2, 2, 4, 1)
+  IGA2L_TRY(2, 3, 2, 2, 4, 1)
+  IGA2L_TRY(3, 3, 2, 2, 4, 1)
+  IGA2L_TRY(4, 3, 2, 2, 4, 2)
+  IGA2L_TRY(5, 5, 2, 2, 4, 4)
+  IGA2L_TRY(6, 5, 2, 2, 4, 4)
+  IGA2L_TRY(7, 7, 4, 4, 4, 4)
+  IGA2L_TRY(8, 7, 4, 4, 4, 4)
+#undef IGA2L_TRY
+  return -1;
 }
 
 void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumulate, cudaStream_t st,

@@ -67,6 +67,12 @@ void launch_sum_partials(const double *partial, int n, double *out, double *hist
 bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M,
                                 const double *V, const double *lam, const double *b, double *x, int colour,
                                 int D, cudaStream_t st, SlabView sv = kFull);
+// Persistent 2D sweep (all D^2 colours in one cooperative launch, per-tile progress counters).
+// ctl: 2 unsigned (zeroed once), done: one unsigned per tile (zeroed once).  launch = false returns the
+// tile count (0: cannot be co-resident or more than max_tiles; -1: (p, s) not specialised).
+int sweep2d_persist(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
+                    const double *b, double *x, unsigned *ctl, unsigned *done, int max_tiles, cudaStream_t st,
+                    bool launch);
 // 2D tensor transfer out (+)= (B ⊗ B) in in one launch (in: B.cols^2, out: B.rows^2).
 // (optional: input rows valid in [iylo, iyhi) stored from iyoff; output rows [rylo, ryhi) stored from ryoff)
 void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumulate, cudaStream_t st,

@@ -276,3 +276,25 @@ def test_vcycle_full_size(q, m, d):
     e = torch.empty(ctx.Nc, dtype=torch.float64, device=DEV)
     ctx.coarse_solve(cu(dq), e)
     close(host(e), H.vcycle(dq), 1e-11)
+
+
+# ---- persistent sweep (one cooperative launch per sweep, per-tile progress counters) against the
+# per-colour launches: same block arithmetic, so bitwise equal; repeated launches advance the counters ----
+PERSIST = [(1, 3, 48), (2, 3, 48), (3, 3, 48), (4, 3, 48), (5, 5, 48), (6, 5, 48), (7, 7, 96), (8, 7, 96)]
+
+
+@pytest.mark.parametrize("p,s,m", PERSIST, ids=[f"p{c[0]}" for c in PERSIST])
+def test_persistent_sweep_bitwise(p, s, m, monkeypatch):
+    monkeypatch.setenv("IGA2L_SWEEP_PERSIST", "1")
+    ctx = make_ctx(2, p, 1, m, s, "vcycle", 2)
+    monkeypatch.setenv("IGA2L_SWEEP_PERSIST", "0")
+    ref = make_ctx(2, p, 1, m, s, "vcycle", 2)
+    b, x0 = cu(random_rhs(ctx.N)), cu(initial_guess(ctx.N))
+    x1, x2 = x0.clone(), x0.clone()
+    for _ in range(3):
+        ctx.sweep(b, x1)
+        ref.sweep(b, x2)
+    assert torch.equal(x1, x2)
+    ctx.iterate(b, x1, iters=4)
+    ref.iterate(b, x2, iters=4)
+    assert torch.equal(x1, x2)

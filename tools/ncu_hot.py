@@ -1,0 +1,36 @@
+"""Top stall lines of an ncu report's source page: ncu_hot.py report.ncu-rep [n] [kernel-regex]."""
+import csv
+import io
+import subprocess
+import sys
+
+rep = sys.argv[1]
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+cmd = ["ncu", "-i", rep, "--page", "source", "--csv"]
+if len(sys.argv) > 3:
+    cmd += ["--kernel-name", "regex:" + sys.argv[3]]
+out = subprocess.run(cmd, capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+blocks, cur = [], None
+for r in rows:
+    if r and r[0] == "Kernel Name":
+        cur = {"name": r[1], "rows": []}
+        blocks.append(cur)
+    elif cur is not None:
+        cur["rows"].append(r)
+if not blocks:
+    blocks = [{"name": "?", "rows": rows}]
+for b in blocks:
+    hdr = b["rows"][0]
+    data = [r for r in b["rows"][1:] if len(r) == len(hdr)]
+    i_s, i_src, i_ex = hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Source"), hdr.index("Instructions Executed")
+
+    def f(v):
+        try:
+            return float(v)
+        except ValueError:
+            return 0.0
+    tot = sum(f(r[i_s]) for r in data)
+    print(b["name"][:90], "| samples", tot, "| sass", len(data), "| executed", sum(f(r[i_ex]) for r in data))
+    for r in sorted(data, key=lambda r: -f(r[i_s]))[:n]:
+        print(f"  {f(r[i_s]):7.0f} {100*f(r[i_s])/max(tot,1):5.1f}% {r[i_ex]:>9} {r[i_src][:70]}")
