@@ -2,6 +2,7 @@
 #include "kernels.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <vector>
 
@@ -173,7 +174,164 @@ __global__ void __launch_bounds__(256) k_apply3d(int p, int n1, const double *__
   }
 }
 
+template <typename F>
+void ensure_smem(F *kernel, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+}
+
+// 2D apply, compile-time p, register-blocked (v2).  Tile AT x AT outputs; the (AT+2p)^2 window of x
+// is staged by cp.async; pass x: each task = one window row, RX consecutive outputs (loads RX+2p
+// values, 2(2p+1)RX FMAs); pass y: each task = one column, RY consecutive outputs.  Axes whose tile
+// rows are translation-invariant (A27) keep the 2(2p+1) band coefficients in registers.
+constexpr int ARY = 4;
+template <int P, int AT>
+struct Apl2 {
+  static constexpr int ARX = P >= 6 ? 4 : 8;
+  static constexpr int W = 2 * P + 1, WN = AT + 2 * P;
+  static constexpr int SM = WN * WN + 2 * WN * AT + 4 * AT * W;   // doubles
+};
+
+template <int P, int AT, bool TOE>
+__device__ __forceinline__ void apl_row(const double *xr, const double *ck, const double *cm, double *ok_, double *om_) {
+  constexpr int W = 2 * P + 1, ARX = Apl2<P, AT>::ARX;
+  double v[ARX + 2 * P];
+#pragma unroll
+  for (int k = 0; k < ARX + 2 * P; ++k) v[k] = xr[k];
+#pragma unroll
+  for (int i = 0; i < ARX; ++i) {
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < W; ++t) {
+      const double kc = TOE ? ck[t] : ck[i * W + t], mc = TOE ? cm[t] : cm[i * W + t];
+      if (t & 1) { a1 = fma(kc, v[i + t], a1); b1 = fma(mc, v[i + t], b1); }
+      else { a0 = fma(kc, v[i + t], a0); b0 = fma(mc, v[i + t], b0); }
+    }
+    ok_[i] = a0 + a1;
+    om_[i] = b0 + b1;
+  }
+}
+
+template <int P, int AT, bool TOE>
+__device__ __forceinline__ void apl_col(const double *tk, const double *tm, const double *ck, const double *cm,
+                                        double *out) {
+  constexpr int W = 2 * P + 1;
+  double a[ARY + 2 * P], c[ARY + 2 * P];
+#pragma unroll
+  for (int k = 0; k < ARY + 2 * P; ++k) { a[k] = tk[k * AT]; c[k] = tm[k * AT]; }
+#pragma unroll
+  for (int i = 0; i < ARY; ++i) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+      const double kc = TOE ? ck[u] : ck[i * W + u], mc = TOE ? cm[u] : cm[i * W + u];
+      s0 = fma(mc, a[i + u], s0);      // M_y (K_x X)
+      s1 = fma(kc, c[i + u], s1);      // K_y (M_x X)
+    }
+    out[i] = s0 + s1;
+  }
+}
+
+template <int P, int AT>
+__global__ void __launch_bounds__(AT * AT / ARY, 2) k_apply2d_t(int n1, const double *__restrict__ K, const double *__restrict__ M,
+                                                   const double *__restrict__ x, const double *__restrict__ b,
+                                                   double *__restrict__ y, double *__restrict__ partial, int mode,
+                                                   int zoff, int zlo, int zhi, int tlo, int thi) {
+  using A = Apl2<P, AT>;
+  constexpr int NT = AT * AT / ARY;
+  constexpr int W = A::W, WN = A::WN, ARX = A::ARX;
+  extern __shared__ double sm[];
+  double *X = sm;                    // [WN][WN]
+  double *Tk = X + WN * WN;          // [WN][AT]  K_x X
+  double *Tm = Tk + WN * AT;         // [WN][AT]  M_x X
+  double *Kx = Tm + WN * AT, *Mx = Kx + AT * W, *Ky = Mx + AT * W, *My = Ky + AT * W;
+  __shared__ double red[32];
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * AT, y0 = zlo + blockIdx.y * AT;
+  const unsigned un = unsigned(n1);
+  for (int i = tid; i < WN * WN; i += NT) {
+    const int wy = i / WN, wx = i - wy * WN;
+    const int gx = x0 - P + wx, gy = y0 - P + wy;
+    const bool ok = unsigned(gx) < un && unsigned(gy) < un;
+    cp_async8(X + i, x + (ok ? (int64_t)(gy - zoff) * n1 + gx : 0), ok);
+  }
+  for (int i = tid; i < AT * W; i += NT) {
+    const int l = i / W, t = i - l * W;
+    const int gx = x0 + l, gy = y0 + l;
+    const bool okx = unsigned(gx) < un, oky = gy < zhi && unsigned(gy) < un;
+    cp_async8(Kx + i, K + (okx ? (int64_t)gx * W + t : 0), okx);
+    cp_async8(Mx + i, M + (okx ? (int64_t)gx * W + t : 0), okx);
+    cp_async8(Ky + i, K + (oky ? (int64_t)gy * W + t : 0), oky);
+    cp_async8(My + i, M + (oky ? (int64_t)gy * W + t : 0), oky);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const bool tx = x0 >= tlo && x0 + AT - 1 <= thi, ty = y0 >= tlo && y0 + AT - 1 <= thi;
+  // pass x: rows wy of the window, segments of ARX outputs
+  for (int task = tid; task < WN * (AT / ARX); task += NT) {
+    const int wy = task / (AT / ARX), sg = task - wy * (AT / ARX);
+    double ok_[ARX], om_[ARX];
+    if (tx) apl_row<P, AT, true>(X + wy * WN + sg * ARX, Kx, Mx, ok_, om_);
+    else apl_row<P, AT, false>(X + wy * WN + sg * ARX, Kx + sg * ARX * W, Mx + sg * ARX * W, ok_, om_);
+#pragma unroll
+    for (int i = 0; i < ARX; ++i) {
+      Tk[wy * AT + sg * ARX + i] = ok_[i];
+      Tm[wy * AT + sg * ARX + i] = om_[i];
+    }
+  }
+  __syncthreads();
+  // pass y: columns lx, segments of ARY outputs; y = A x or b - A x
+  double sq = 0.0;
+  {
+    const int lx = tid % AT, sg = tid / AT;   // NT tasks = AT columns x AT/ARY segments
+    double out[ARY];
+    if (ty) apl_col<P, AT, true>(Tk + sg * ARY * AT + lx, Tm + sg * ARY * AT + lx, Ky, My, out);
+    else apl_col<P, AT, false>(Tk + sg * ARY * AT + lx, Tm + sg * ARY * AT + lx, Ky + sg * ARY * W, My + sg * ARY * W, out);
+    const int gx = x0 + lx;
+#pragma unroll
+    for (int i = 0; i < ARY; ++i) {
+      const int gy = y0 + sg * ARY + i;
+      if (gx < n1 && gy < zhi) {
+        const int64_t g = (int64_t)(gy - zoff) * n1 + gx;
+        const double v = mode ? b[g] - out[i] : out[i];
+        y[g] = v;
+        sq = fma(v, v, sq);
+      }
+    }
+  }
+  if (partial) {
+    const double t = block_sum(sq, red);
+    if (tid == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+template <int P>
+bool try_apply2d(int p, int64_t n1, const double *K, const double *M, const double *x, const double *b, double *y,
+                 double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv) {
+  if (p != P) return false;
+  const int nz = sv.zhi - sv.zlo;
+  const int m = int(n1) - P + 2;
+  auto go = [&](auto kern, int at, size_t sm) {
+    ensure_smem(kern, sm);
+    dim3 grid((unsigned)((n1 + at - 1) / at), (unsigned)((nz + at - 1) / at));
+    kern<<<grid, at * at / ARY, sm, st>>>(int(n1), K, M, x, b, y, partial, mode, sv.zoff, sv.zlo, sv.zhi, 2 * P - 1,
+                                          m - 2 - P);
+    if (nparts) *nparts = int(grid.x * grid.y);
+  };
+  // 32x32 tiles; 16x16 when that would leave fewer than two CTAs per SM
+  if (((n1 + 31) / 32) * ((nz + 31) / 32) >= 296) go(k_apply2d_t<P, 32>, 32, sizeof(double) * Apl2<P, 32>::SM);
+  else go(k_apply2d_t<P, 16>, 16, sizeof(double) * Apl2<P, 16>::SM);
+  return true;
+}
+
 constexpr int A2X = 32, A2Y = 8, A3X = 8, A3Y = 8, A3Z = 4;
+static const bool g_transfer_v2 = [] {
+  const char *e = std::getenv("IGA2L_TRANSFER_V2");
+  return !(e && e[0] == '0');
+}();
+static const bool g_apply_v2 = [] {
+  const char *e = std::getenv("IGA2L_APPLY_V2");
+  return !(e && e[0] == '0');
+}();
 
 // =============================== Schwarz colour kernel ====================================
 // contract one axis of a [s]^DIM array (first index fastest) with an s x s matrix V[l*s + j]:
@@ -498,10 +656,6 @@ size_t schwarz_smem(int dim, int p, int s) {
   return sizeof(double) * (nX + 2 * nP + 2 * nC + 3 * sd + 3 * s2 + 3 * s);
 }
 
-template <typename F>
-void ensure_smem(F *kernel, size_t bytes) {
-  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-}
 
 }  // namespace
 
@@ -515,7 +669,10 @@ void centre_range(int c, int D, int lo, int hi, int *first, int *count) {
 
 int apply_num_partials(int dim, int p, int64_t n1) {
   (void)p;
-  if (dim == 2) return int(((n1 + A2X - 1) / A2X) * ((n1 + A2Y - 1) / A2Y));
+  if (dim == 2) {   // the most tiles any 2D apply variant launches
+    const int64_t v1 = ((n1 + A2X - 1) / A2X) * ((n1 + A2Y - 1) / A2Y), v2 = ((n1 + 15) / 16) * ((n1 + 15) / 16);
+    return int(std::max(v1, v2));
+  }
   return int(((n1 + A3X - 1) / A3X) * ((n1 + A3Y - 1) / A3Y) * ((n1 + A3Z - 1) / A3Z));
 }
 
@@ -525,6 +682,16 @@ void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, 
   const int nz = sv.zhi - sv.zlo;
   const size_t sm = apply_smem(dim, p);
   if (nz <= 0) return;
+  if (dim == 2 && g_apply_v2 &&
+      (try_apply2d<1>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
+       try_apply2d<2>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
+       try_apply2d<3>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
+       try_apply2d<4>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
+       try_apply2d<5>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
+       try_apply2d<6>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
+       try_apply2d<7>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
+       try_apply2d<8>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv)))
+    return;
   if (dim == 2) {
     dim3 grid((unsigned)((n1 + A2X - 1) / A2X), (unsigned)((nz + A2Y - 1) / A2Y));
     ensure_smem(k_apply2d<A2X, A2Y>, sm);
@@ -1473,6 +1640,70 @@ bool try_schwarz3d(int p, int s, int64_t n1, const double *K, const double *M, c
   return true;
 }
 
+// ---------------- separable 2D tensor transfer (v2): out (+)= (B ⊗ B) in, two passes ----------
+// CTA = TO x TO outputs.  Pass 1 (x): T[iy][rx] = Σ_k c[rx][k] in[iy][lo[rx]+k] for the input rows the
+// tile needs; pass 2 (y): out[ry][rx] = Σ_k c[ry][k] T[lo[ry]+k][rx].  2W FMAs per output (plus the
+// input-row halo of pass 1) instead of W^2 gathers.  Input rows valid in [iylo, iyhi) stored from
+// iyoff; output rows [rylo, ryhi) stored from ryoff (slab views).
+constexpr int TO = 32;
+__global__ void __launch_bounds__(256) k_transfer2d_sep(const double *__restrict__ in, double *__restrict__ out, int nin,
+                                                        int rows, int W, const int *__restrict__ lo,
+                                                        const double *__restrict__ c, int acc, int iylo, int iyhi,
+                                                        int iyoff, int rylo, int ryhi, int ryoff, int LI) {
+  extern __shared__ double sm[];
+  const int rx0 = blockIdx.x * TO, ry0 = rylo + blockIdx.y * TO;
+  const int nrx = min(TO, rows - rx0), nry = min(TO, ryhi - ry0);
+  if (nrx <= 0 || nry <= 0) return;
+  const int ix0 = lo[rx0], iy0 = lo[ry0];                 // first input column / row of the tile
+  double *X = sm;                                           // [LI][LI] input window
+  double *T = X + LI * LI;                                  // [LI][TO]
+  double *cx = T + LI * TO, *cy = cx + TO * W;              // coefficient rows of the tile
+  int *lx = reinterpret_cast<int *>(cy + TO * W), *ly = lx + TO;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < LI * LI; i += 256) {
+    const int wy = i / LI, wx = i - wy * LI, gx = ix0 + wx, gy = iy0 + wy;
+    const bool ok = unsigned(gx) < unsigned(nin) && gy >= iylo && gy < iyhi;
+    cp_async8(X + i, in + (ok ? (int64_t)(gy - iyoff) * nin + gx : 0), ok);
+  }
+  for (int i = tid; i < TO * W; i += 256) {
+    const int r = i / W;
+    const bool okx = r < nrx, oky = r < nry;
+    cp_async8(cx + i, c + (okx ? (int64_t)(rx0 + r) * W + i % W : 0), okx);
+    cp_async8(cy + i, c + (oky ? (int64_t)(ry0 + r) * W + i % W : 0), oky);
+  }
+  if (tid < TO) {
+    lx[tid] = tid < nrx ? lo[rx0 + tid] - ix0 : 0;
+    ly[tid] = tid < nry ? lo[ry0 + tid] - iy0 : 0;
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  // pass 1: rows of the window that pass 2 reads: [0, ly[nry-1] + W)
+  const int nrow = min(LI, ly[nry - 1] + W);
+  for (int i = tid; i < nrow * TO; i += 256) {
+    const int wy = i / TO, r = i - wy * TO;
+    double s0 = 0.0, s1 = 0.0;
+    if (r < nrx) {
+      const double *xr = X + wy * LI + lx[r], *cr = cx + r * W;
+      for (int k = 0; k < W; ++k) {
+        if (k & 1) s1 = fma(cr[k], xr[k], s1); else s0 = fma(cr[k], xr[k], s0);
+      }
+    }
+    T[i] = s0 + s1;
+  }
+  __syncthreads();
+  for (int i = tid; i < TO * TO; i += 256) {
+    const int ry = i / TO, r = i - ry * TO;
+    if (ry >= nry || r >= nrx) continue;
+    const double *tc = T + ly[ry] * TO + r, *cr = cy + ry * W;
+    double s0 = 0.0, s1 = 0.0;
+    for (int k = 0; k < W; ++k) {
+      if (k & 1) s1 = fma(cr[k], tc[k * TO], s1); else s0 = fma(cr[k], tc[k * TO], s0);
+    }
+    const int64_t o = (int64_t)(ry0 + ry - ryoff) * rows + rx0 + r;
+    out[o] = acc ? out[o] + (s0 + s1) : (s0 + s1);
+  }
+}
+
 }  // namespace
 
 bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M, const double *V,
@@ -1542,6 +1773,17 @@ void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumul
   if (ryhi < 0) { rylo = 0; ryhi = B.rows; ryoff = 0; }
   const int64_t total = (int64_t)(ryhi - rylo) * B.rows;
   if (total <= 0) return;
+  if (g_transfer_v2 && B.lo_max_span > 0 && total >= 200000) {   // separable two-pass (large grids; measured)
+    const int LI = B.lo_max_span + B.W;
+    const size_t sm = sizeof(double) * (size_t(LI) * LI + size_t(LI) * TO + 2 * TO * B.W) + 2 * TO * sizeof(int);
+    if (sm <= 200 * 1024) {
+      ensure_smem(k_transfer2d_sep, sm);
+      dim3 grid((unsigned)((B.rows + TO - 1) / TO), (unsigned)((ryhi - rylo + TO - 1) / TO));
+      k_transfer2d_sep<<<grid, 256, sm, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate, iylo, iyhi, iyoff,
+                                              rylo, ryhi, ryoff, LI);
+      return;
+    }
+  }
   const int g = grid_for(total, 128);
   if (B.W <= 4)
     k_tensor2d<4><<<g, 128, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate, iylo, iyhi, iyoff, rylo, ryhi, ryoff);

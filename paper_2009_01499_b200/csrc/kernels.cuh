@@ -15,6 +15,7 @@ struct Band1D {          // banded 1D transfer: row r uses columns lo[r] .. lo[r
   int rows, cols, W;
   const int *lo;
   const double *c;
+  int lo_max_span;       // max over 32-row tiles of lo[last] - lo[first] (0: unknown)
 };
 
 // Window of the LAST axis (y in 2D, z in 3D) of a vector held by a context: local plane 0 is the

@@ -57,6 +57,9 @@ for n in names:
     torch.cuda.synchronize()
     r["iter_us"] = e0.elapsed_time(e1) / reps * 1e3
     r["sweep_us"] = t(lambda: ctx.sweep(b, x))
+    yv = torch.empty_like(x)
+    r["apply_us"] = t(lambda: ctx.apply(x, yv))
+    r["apply_GBps"] = 24.0 * ctx.N / (r["apply_us"] * 1e-6) / 1e9   # x, b read + r written
     r["defect_restrict_us"] = t(lambda: ctx.defect_restrict(b, x, dq))
     r["coarse_us"] = t(lambda: ctx.coarse_solve(dq, e))
     r["prolong_us"] = t(lambda: ctx.prolong_add(e, x))

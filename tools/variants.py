@@ -17,6 +17,8 @@ for rnd in range(2):
             name, js = line.split(" ", 1)
             d = json.loads(js)
             print(f"round {rnd} {var}={v} {name}: sweep/colour {d['sweep_us_per_colour']:.2f} us, "
-                  f"{d['sweep_tflops']:.2f} TFLOP/s, iter {d['iter_us']:.1f} us", flush=True)
+                  f"{d['sweep_tflops']:.2f} TFLOP/s, apply {d['apply_us']:.1f} us ({d['apply_GBps']:.0f} GB/s), "
+                  f"defect+R {d['defect_restrict_us']:.1f}, prolong {d['prolong_us']:.1f}, coarse {d['coarse_us']:.1f}, "
+                  f"iter {d['iter_us']:.1f} us", flush=True)
         if out.returncode:
             print(out.stderr[-2000:])
