@@ -62,6 +62,7 @@ struct iga2l_ctx {
   bool own_stream = false;
   double *K1 = nullptr, *M1 = nullptr, *V = nullptr, *lam = nullptr, *g1 = nullptr;
   DevBand R, RT;
+  ToeP toe{};                    // interior 1D data (A27) for the kernels' constant-bank path
   std::vector<Level> lev;
   double *r = nullptr, *t1 = nullptr, *t2 = nullptr;   // fine scratch, N each
   double *partial = nullptr, *norm = nullptr, *hist = nullptr;
@@ -220,7 +221,8 @@ void L_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
     return;
   }
   for (int col = c0; col < c1; ++col) {
-    if (!launch_schwarz_colour_fast(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st))
+    if (!launch_schwarz_colour_fast(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st,
+                                    kFull, &c->toe))
       launch_schwarz_colour(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st);
     c->launch_counter++;
   }
@@ -421,7 +423,7 @@ int S_iteration(iga2l_ctx *c, bool with_norm) {
       for (auto &S : c->slabs) {
         const SlabView sv{S.za, std::max(0, S.z0 - c->w), std::min(n1, S.z1 + c->w)};
         if (!launch_schwarz_colour_fast(d, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, S.bp, S.xp, col, c->D,
-                                        c->st, sv))
+                                        c->st, sv, &c->toe))
           launch_schwarz_colour(d, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, S.bp, S.xp, col, c->D, c->st, sv);
         c->launch_counter++;
       }
@@ -608,6 +610,18 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
   std::vector<double> K, M, V, lam;
   band_tables(p, n, K, M);
   if (!fd_tables(p, block, n1, K, M, V, lam)) return bail(fail(IGA2L_ENUMERIC, "Schwarz block matrix not SPD"));
+  {  // interior (translation-invariant) band row and FD tables, passed to kernels by value (A27)
+    int64_t tlo, thi;
+    toeplitz_rows(p, n, &tlo, &thi);
+    const int W = 2 * p + 1, w = (block - 1) / 2;
+    if (thi - tlo >= 2 * w && W <= kToeMaxW && block <= kToeMaxS) {
+      const int64_t r = (tlo + thi) / 2;
+      for (int t = 0; t < W; ++t) { c->toe.k[t] = K[r * W + t]; c->toe.m[t] = M[r * W + t]; }
+      for (int i = 0; i < block * block; ++i) c->toe.v[i] = V[r * block * block + i];
+      for (int i = 0; i < block; ++i) c->toe.lam[i] = lam[r * block + i];
+      c->toe.valid = 1;
+    }
+  }
   if ((rc = upload(c, &c->K1, K)) || (rc = upload(c, &c->M1, M)) || (rc = upload(c, &c->V, V)) ||
       (rc = upload(c, &c->lam, lam)) || (rc = upload(c, &c->g1, load_1d_sine(p, n))))
     return bail(rc);

@@ -967,7 +967,11 @@ __global__ void __launch_bounds__(WPB * G * 32) k_schwarz2d_w(int n1, const doub
   B::compute(X, lane, warp, n1, cx, cy, x, zoff);
 }
 
-int g_use_pdl = 0;   // programmatic dependent launch between colour kernels (measured slower: off)
+// programmatic dependent launch between colour kernels (IGA2L_PDL=1; off by default)
+int g_use_pdl = [] {
+  const char *e = std::getenv("IGA2L_PDL");
+  return (e && e[0] == '1') ? 1 : 0;
+}();
 
 template <int P, int S, int WPB, int G>
 bool try_schwarz2d(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
@@ -1704,11 +1708,447 @@ __global__ void __launch_bounds__(256) k_transfer2d_sep(const double *__restrict
   }
 }
 
+// ---------------- 2D Schwarz colour kernel, register-blocked (v3): NBK blocks per CTA ------------
+// Same arithmetic as Blk2 (pass x, pass y, fast diagonalisation), organised for FP64 throughput:
+// pass x: one task per window ROW (Wn loads, 2 s (2p+1) FMAs, coefficients in registers on Toeplitz
+// axes, A27); pass y: one task per (column, half of the block rows); FD as four s x s contractions
+// with one task per row/column.  All phases run over the CTA's (block, task) pairs.
+template <int P, int S>
+struct Blk2R {
+  static constexpr int W = 2 * P + 1, Wn = S + 2 * P, w = (S - 1) / 2, S2 = S * S;
+  static constexpr int PER = Wn * Wn + 2 * Wn * S + 3 * S2 + 4 * S * W + 2 * S2 + 2 * S;
+  static constexpr int HY = (S + 1) / 2;   // rows per pass-y task (two tasks per column)
+};
+
+template <int P, int S, int NBK, int NT>
+__global__ void __launch_bounds__(NT) k_schwarz2d_r(int n1, const double *__restrict__ K, const double *__restrict__ M,
+                                                    const double *__restrict__ Vt, const double *__restrict__ lamt,
+                                                    const double *__restrict__ b, double *__restrict__ x, int c0, int c1,
+                                                    int D, int nb0, int nblk, int zoff, int tlo, int thi,
+                                                    const ToeP tp) {
+  using B = Blk2R<P, S>;
+  constexpr int W = B::W, Wn = B::Wn, w = B::w, S2 = B::S2, PER = B::PER, HY = B::HY;
+  extern __shared__ double sm[];
+  __shared__ int sC[NBK][2];
+  __shared__ bool sT[NBK][2];
+  const int tid = threadIdx.x;
+  const unsigned un = unsigned(n1);
+  const int nk = min(NBK, nblk - int(blockIdx.x) * NBK);
+  if (tid < NBK) {
+    const int g = blockIdx.x * NBK + tid, j1 = g / nb0, j0 = g - j1 * nb0;
+    const int cx = c0 + D * j0, cy = c1 + D * j1;
+    sC[tid][0] = cx; sC[tid][1] = cy;
+    sT[tid][0] = tp.valid && cx - w >= tlo && cx + w <= thi;   // interior axis: tables in tp
+    sT[tid][1] = tp.valid && cy - w >= tlo && cy + w <= thi;
+  }
+  __syncthreads();
+  // per-block regions
+  auto X = [&](int k) { return sm + k * PER; };                       // [wy][wx]
+  auto Pa = [&](int k) { return X(k) + Wn * Wn; };                    // [wy][lx]
+  auto Pb = [&](int k) { return Pa(k) + Wn * S; };
+  auto R = [&](int k) { return Pb(k) + Wn * S; };                     // [ly][lx]
+  auto Q = [&](int k) { return R(k) + S2; };
+  auto Bb = [&](int k) { return Q(k) + S2; };
+  auto Kx = [&](int k) { return Bb(k) + S2; };                        // [l][t]   (boundary axes only)
+  auto Mx = [&](int k) { return Kx(k) + S * W; };
+  auto Ky = [&](int k) { return Mx(k) + S * W; };
+  auto My = [&](int k) { return Ky(k) + S * W; };
+  auto Vx = [&](int k) { return My(k) + S * W; };                     // [l][j]
+  auto Vy = [&](int k) { return Vx(k) + S2; };
+  auto Lx = [&](int k) { return Vy(k) + S2; };
+  auto Ly = [&](int k) { return Lx(k) + S; };
+  // ---- loads (cp.async): x windows row by row, b_B, and the tables of boundary axes only ----
+  for (int row = tid >> 4; row < nk * Wn; row += NT >> 4) {
+    const int k = row / Wn, wy = row - k * Wn;
+    const int gy = sC[k][1] - w - P + wy, ox = sC[k][0] - w - P;
+    const bool oky = unsigned(gy) < un;
+    const double *src = x + (oky ? (int64_t)(gy - zoff) * n1 : 0);
+    double *dst = X(k) + wy * Wn;
+#pragma unroll
+    for (int wx = tid & 15; wx < Wn; wx += 16) {
+      const int gx = ox + wx;
+      const bool ok = oky && unsigned(gx) < un;
+      cp_async8(dst + wx, ok ? src + gx : x, ok);
+    }
+  }
+  for (int i = tid; i < nk * S2; i += NT) {
+    const int k = i / S2, r = i - k * S2, ly = r / S, lx = r - ly * S;
+    const int gx = sC[k][0] - w + lx, gy = sC[k][1] - w + ly;
+    const bool ok = unsigned(gx) < un && unsigned(gy) < un;
+    cp_async8(Bb(k) + r, b + (ok ? (int64_t)(gy - zoff) * n1 + gx : 0), ok);
+  }
+  for (int i = tid; i < nk * 2 * (S * W + S2 + S); i += NT) {
+    const int k = i / (2 * (S * W + S2 + S)), r = i - k * (2 * (S * W + S2 + S));
+    const int a = r / (S * W + S2 + S), e = r - a * (S * W + S2 + S);
+    if (sT[k][a]) continue;
+    const int c = sC[k][a];
+    if (e < S * W) {
+      const int l = e / W, t = e - l * W, g = c - w + l;
+      const bool ok = unsigned(g) < un;
+      cp_async8((a ? Ky(k) : Kx(k)) + e, K + (ok ? (int64_t)g * W + t : 0), ok);
+      cp_async8((a ? My(k) : Mx(k)) + e, M + (ok ? (int64_t)g * W + t : 0), ok);
+    } else if (e < S * W + S2) {
+      cp_async8((a ? Vy(k) : Vx(k)) + (e - S * W), Vt + (int64_t)c * S2 + (e - S * W), true);
+    } else {
+      cp_async8((a ? Ly(k) : Lx(k)) + (e - S * W - S2), lamt + (int64_t)c * S + (e - S * W - S2), true);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  // ---- pass x: task = (block, window row wy) -> Pa[wy][lx] = Σ_t K_x v, Pb = Σ_t M_x v ----
+  for (int i = tid; i < nk * Wn; i += NT) {
+    const int k = i / Wn, wy = i - k * Wn;
+    double v[Wn];
+#pragma unroll
+    for (int q = 0; q < Wn; ++q) v[q] = X(k)[wy * Wn + q];
+    const bool toe = sT[k][0];
+    const double *ck = Kx(k), *cm = Mx(k);
+#pragma unroll
+    for (int l = 0; l < S; ++l) {
+      double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+      for (int t = 0; t < W; ++t) {
+        const double kc = toe ? tp.k[t] : ck[l * W + t], mc = toe ? tp.m[t] : cm[l * W + t];
+        if (t & 1) { a1 = fma(kc, v[l + t], a1); b1 = fma(mc, v[l + t], b1); }
+        else { a0 = fma(kc, v[l + t], a0); b0 = fma(mc, v[l + t], b0); }
+      }
+      Pa(k)[wy * S + l] = a0 + a1;
+      Pb(k)[wy * S + l] = b0 + b1;
+    }
+  }
+  __syncthreads();
+  // ---- pass y: task = (block, column lx, half h) -> R[ly][lx] = b - Σ_u (M_y Pa + K_y Pb) ----
+  for (int i = tid; i < nk * S * 2; i += NT) {
+    const int k = i / (2 * S), r = i - k * (2 * S), lx = r >> 1, h = r & 1;
+    const int ly0 = h * HY, nly = h ? S - HY : HY;
+    const double *pa = Pa(k) + lx, *pb = Pb(k) + lx;
+    double a[HY + 2 * P], c[HY + 2 * P];
+#pragma unroll
+    for (int u = 0; u < HY + 2 * P; ++u) {
+      const bool ok = ly0 + u < Wn;
+      a[u] = ok ? pa[(ly0 + u) * S] : 0.0;
+      c[u] = ok ? pb[(ly0 + u) * S] : 0.0;
+    }
+    const bool toe = sT[k][1];
+    const double *ky = Ky(k), *my = My(k);
+#pragma unroll
+    for (int l = 0; l < HY; ++l) {
+      if (l >= nly) break;
+      const int ly = ly0 + l;
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int u = 0; u < W; ++u) {
+        const double mc = toe ? tp.m[u] : my[ly * W + u], kc = toe ? tp.k[u] : ky[ly * W + u];
+        s0 = fma(mc, a[l + u], s0);
+        s1 = fma(kc, c[l + u], s1);
+      }
+      R(k)[ly * S + lx] = Bb(k)[ly * S + lx] - (s0 + s1);
+    }
+  }
+  __syncthreads();
+  // ---- FD: Q[ly][j] = Σ_lx R[ly][lx] Vx[lx][j] ----
+  for (int i = tid; i < nk * S; i += NT) {
+    const int k = i / S, ly = i - k * S;
+    double rr[S];
+#pragma unroll
+    for (int l = 0; l < S; ++l) rr[l] = R(k)[ly * S + l];
+    const bool toe = sT[k][0];
+    const double *vx = Vx(k);
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      double a0 = 0.0;
+#pragma unroll
+      for (int l = 0; l < S; ++l) a0 = fma(toe ? tp.v[l * S + j] : vx[l * S + j], rr[l], a0);
+      Q(k)[ly * S + j] = a0;
+    }
+  }
+  __syncthreads();
+  // Z[kk][j] = Σ_ly Vy[ly][kk] Q[ly][j] / (λx_j + λy_kk)   (stored in R as [kk][j])
+  for (int i = tid; i < nk * S; i += NT) {
+    const int k = i / S, j = i - k * S;
+    double qq[S];
+#pragma unroll
+    for (int l = 0; l < S; ++l) qq[l] = Q(k)[l * S + j];
+    const bool tx = sT[k][0], ty = sT[k][1];
+    const double *vy = Vy(k), *ly_ = Ly(k);
+    double lxj = Lx(k)[j];
+    if (tx) {
+#pragma unroll
+      for (int l = 0; l < S; ++l) if (l == j) lxj = tp.lam[l];
+    }
+#pragma unroll
+    for (int kk = 0; kk < S; ++kk) {
+      double a0 = 0.0;
+#pragma unroll
+      for (int l = 0; l < S; ++l) a0 = fma(ty ? tp.v[l * S + kk] : vy[l * S + kk], qq[l], a0);
+      R(k)[kk * S + j] = a0 / (lxj + (ty ? tp.lam[kk] : ly_[kk]));
+    }
+  }
+  __syncthreads();
+  // U[kk][lx] = Σ_j Vx[lx][j] Z[kk][j]   (into Q)
+  for (int i = tid; i < nk * S; i += NT) {
+    const int k = i / S, kk = i - k * S;
+    double zz[S];
+#pragma unroll
+    for (int l = 0; l < S; ++l) zz[l] = R(k)[kk * S + l];
+    const bool toe = sT[k][0];
+    const double *vx = Vx(k);
+#pragma unroll
+    for (int lx = 0; lx < S; ++lx) {
+      double a0 = 0.0;
+#pragma unroll
+      for (int j = 0; j < S; ++j) a0 = fma(toe ? tp.v[lx * S + j] : vx[lx * S + j], zz[j], a0);
+      Q(k)[kk * S + lx] = a0;
+    }
+  }
+  __syncthreads();
+  // δ[ly][lx] = Σ_kk Vy[ly][kk] U[kk][lx];  x_B += δ
+  for (int i = tid; i < nk * S; i += NT) {
+    const int k = i / S, lx = i - k * S;
+    double uu[S];
+#pragma unroll
+    for (int l = 0; l < S; ++l) uu[l] = Q(k)[l * S + lx];
+    const bool toe = sT[k][1];
+    const double *vy = Vy(k);
+    const int gx = sC[k][0] - w + lx;
+#pragma unroll
+    for (int ly = 0; ly < S; ++ly) {
+      double a0 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < S; ++kk) a0 = fma(toe ? tp.v[ly * S + kk] : vy[ly * S + kk], uu[kk], a0);
+      const int gy = sC[k][1] - w + ly;
+      if (unsigned(gx) < un && unsigned(gy) < un)
+        x[(int64_t)(gy - zoff) * n1 + gx] = X(k)[(ly + P) * Wn + lx + P] + a0;
+    }
+  }
+}
+
+template <int P, int S, int NBK, int NT>
+void launch2d_r(int64_t n1, const double *K, const double *M, const double *V, const double *lam, const double *b,
+                double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st, const ToeP &tp) {
+  constexpr size_t sm = sizeof(double) * NBK * Blk2R<P, S>::PER;
+  ensure_smem(k_schwarz2d_r<P, S, NBK, NT>, sm);
+  const int m = int(n1) - P + 2;
+  k_schwarz2d_r<P, S, NBK, NT><<<(nblk + NBK - 1) / NBK, NT, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, D, nb0,
+                                                                       nblk, zoff, 2 * P - 1, m - 2 - P, tp);
+}
+
+int s2d_variant() {   // IGA2L_S2D_VARIANT: 0/9 = DMMA kernel, 1-4 = register-blocked variants, 10 = warp-group (Blk2)
+  const char *e = std::getenv("IGA2L_S2D_VARIANT");   // read per launch (host side, cheap): tests switch it
+  return e ? std::atoi(e) : 0;
+}
+
+template <int P, int S>
+bool try_schwarz2d_r(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
+                     const double *b, double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st,
+                     int variant, const ToeP *tpp) {
+  if (p != P || s != S) return false;
+  constexpr int Wn = S + 2 * P;
+  ToeP tp{};
+  if (tpp) tp = *tpp;
+  switch (variant) {
+    case 1: launch2d_r<P, S, 8, ((8 * Wn + 31) / 32) * 32>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st, tp); break;
+    case 2: launch2d_r<P, S, 4, ((4 * Wn + 31) / 32) * 32>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st, tp); break;
+    case 3: launch2d_r<P, S, 16, (((16 * Wn + 31) / 32) * 32 > 512 ? 512 : ((16 * Wn + 31) / 32) * 32)>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st, tp); break;
+    default: launch2d_r<P, S, 2, ((2 * Wn + 31) / 32) * 32>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st, tp); break;
+  }
+  return true;
+}
+
+// ---------------- 2D Schwarz colour kernel on the FP64 tensor pipe (DMMA), one warp per block -------
+// mma.sync.m8n8k4.f64 (A 8x4 row-major, B 4x8 column-major, C 8x8): per lane a = A[l/4][l%4],
+// b = B[l%4][l/4], c[i] = C[l/4][2(l%4)+i].  The block solve is five small GEMMs:
+//   pass x  Pab[wy][j] = Σ_c X[wy][c] Bx[c][j],  Bx[c][lx] = K(bx+lx, c-lx), Bx[c][S+lx] = M(..)
+//   pass y  R[ly][lx] = b_B - Σ_r Ay[ly][r] Pab'[r][lx],  Ay = [M_y band | K_y band], Pab' = [Pa; Pb]
+//   FD      T = R Vx,  Z = (Vy^T T) ./ (λx_j + λy_k),  U = Z Vx^T,  δ = Vy U
+// Band and FD operands are read through L1 (__ldg) straight into fragments; C fragments feed the next
+// GEMM through warp shuffles.  Zero padding everywhere outside the s x s block / window.
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+// element (row, col) of an 8x8 C fragment held by the warp (c0, c1 of every lane)
+__device__ __forceinline__ double c_elem(double c0, double c1, int row, int col) {
+  const int src = (row << 2) | (col >> 1);
+  const double v0 = __shfl_sync(0xffffffffu, c0, src), v1 = __shfl_sync(0xffffffffu, c1, src);
+  return (col & 1) ? v1 : v0;
+}
+
+template <int P, int S>
+struct Mma2 {
+  static constexpr int W = 2 * P + 1, Wn = S + 2 * P, w = (S - 1) / 2;
+  static constexpr int MT = (Wn + 7) / 8;            // pass-x m-tiles (window rows)
+  static constexpr int KT = (Wn + 3) / 4;            // pass-x k-steps (window cols)
+  static constexpr int NTX = (2 * S + 7) / 8;        // pass-x n-tiles (K and M columns)
+  static constexpr int WN4 = KT * 4;                 // padded window width
+  static constexpr int LDX = WN4 + 1;                // smem row stride of the window (odd: fewer conflicts)
+  static constexpr int LDP = NTX * 8 + 1;            // smem row stride of Pab
+  static constexpr int KY = (2 * WN4) / 4;           // pass-y k-steps
+  static constexpr int KF = (S + 3) / 4;             // FD k-steps
+  static constexpr int PER = MT * 8 * LDX + MT * 8 * LDP + S * S;   // doubles per warp
+};
+
+template <int P, int S, int WPC>
+__global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma(int n1, const double *__restrict__ K,
+                                                            const double *__restrict__ M,
+                                                            const double *__restrict__ Vt,
+                                                            const double *__restrict__ lamt,
+                                                            const double *__restrict__ b, double *__restrict__ x,
+                                                            int c0, int c1, int D, int nb0, int nblk, int zoff) {
+  using G = Mma2<P, S>;
+  constexpr int W = G::W, Wn = G::Wn, w = G::w, MT = G::MT, KT = G::KT, NTX = G::NTX, WN4 = G::WN4, LDX = G::LDX,
+                LDP = G::LDP, KY = G::KY, KF = G::KF;
+  extern __shared__ double sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bid = blockIdx.x * WPC + warp;
+  if (bid >= nblk) return;                                   // whole warp exits together
+  double *X = sm + warp * G::PER, *Pab = X + MT * 8 * LDX, *Bb = Pab + MT * 8 * LDP;
+  const int j1 = bid / nb0, j0 = bid - j1 * nb0;
+  const int cx = c0 + D * j0, cy = c1 + D * j1;
+  const int bx = cx - w, by = cy - w, ox = bx - P, oy = by - P;
+  const unsigned un = unsigned(n1);
+  const int r4 = lane >> 2, q4 = lane & 3;
+  // ---- stage the zero-padded window (MT*8 x WN4) and b_B asynchronously ----
+  for (int row = 0; row < MT * 8; ++row) {
+    const int gy = oy + row;
+    const bool oky = row < Wn && unsigned(gy) < un;
+    const double *src = x + (oky ? (int64_t)(gy - zoff) * n1 : 0);
+#pragma unroll
+    for (int cc = lane; cc < WN4; cc += 32) {
+      const int gx = ox + cc;
+      const bool ok = oky && cc < Wn && unsigned(gx) < un;
+      cp_async8(X + row * LDX + cc, ok ? src + gx : x, ok);
+    }
+  }
+  for (int i = lane; i < S * S; i += 32) {
+    const int ly = i / S, lx = i - ly * S, gx = bx + lx, gy = by + ly;
+    const bool ok = unsigned(gx) < un && unsigned(gy) < un;
+    cp_async8(Bb + i, b + (ok ? (int64_t)(gy - zoff) * n1 + gx : 0), ok);
+  }
+  // ---- operand fragments from the 1D tables (independent of the window; overlap the copies) ----
+  double bxf[KT][NTX];                                       // pass x B: Bx[4kt+q4][8nt+r4]
+#pragma unroll
+  for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+    for (int nt = 0; nt < NTX; ++nt) {
+      const int c = 4 * kt + q4, j = 8 * nt + r4;
+      const int lx = j < S ? j : j - S, t = c - lx;
+      const int g = bx + lx;
+      const bool ok = j < 2 * S && t >= 0 && t < W && unsigned(g) < un;
+      bxf[kt][nt] = ok ? __ldg((j < S ? K : M) + (int64_t)g * W + t) : 0.0;
+    }
+  double ayf[KY];                                            // pass y A: Ay[r4][4kt+q4]
+#pragma unroll
+  for (int kt = 0; kt < KY; ++kt) {
+    const int r = 4 * kt + q4, ly = r4;
+    const bool second = r >= WN4;
+    const int rr = second ? r - WN4 : r, t = rr - ly, g = by + ly;
+    const bool ok = ly < S && t >= 0 && t < W && unsigned(g) < un;
+    ayf[kt] = ok ? __ldg((second ? K : M) + (int64_t)g * W + t) : 0.0;
+  }
+  double vxb[KF], vyta[KF], vxtb[KF], vya[KF];               // FD operands (Vx as B, Vy^T as A, Vx^T as B, Vy as A)
+  const double *Vx = Vt + (int64_t)cx * S * S, *Vy = Vt + (int64_t)cy * S * S;
+#pragma unroll
+  for (int kt = 0; kt < KF; ++kt) {
+    const int kk = 4 * kt + q4;
+    const bool okk = kk < S, okr = r4 < S;
+    vxb[kt] = (okk && okr) ? __ldg(Vx + kk * S + r4) : 0.0;   // B[kk][r4] = Vx[kk][r4]
+    vyta[kt] = (okk && okr) ? __ldg(Vy + kk * S + r4) : 0.0;  // A[r4][kk] = Vy[kk][r4]
+    vxtb[kt] = (okk && okr) ? __ldg(Vx + r4 * S + kk) : 0.0;  // B[kk][r4] = Vx[r4][kk]
+    vya[kt] = (okk && okr) ? __ldg(Vy + r4 * S + kk) : 0.0;   // A[r4][kk] = Vy[r4][kk]
+  }
+  double rden[2];                                            // 1 / (λx_j + λy_k) at this lane's C elements
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int kk = r4, j = 2 * q4 + i;
+    rden[i] = (kk < S && j < S) ? 1.0 / (__ldg(lamt + (int64_t)cx * S + j) + __ldg(lamt + (int64_t)cy * S + kk)) : 0.0;
+  }
+  cp_async_wait_all();
+  __syncwarp();
+  // ---- pass x ----
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    double acc[NTX][2];
+#pragma unroll
+    for (int nt = 0; nt < NTX; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+      const double a = X[(8 * mt + r4) * LDX + 4 * kt + q4];
+#pragma unroll
+      for (int nt = 0; nt < NTX; ++nt) dmma(acc[nt][0], acc[nt][1], a, bxf[kt][nt]);
+    }
+#pragma unroll
+    for (int nt = 0; nt < NTX; ++nt) {
+      Pab[(8 * mt + r4) * LDP + 8 * nt + 2 * q4] = acc[nt][0];
+      Pab[(8 * mt + r4) * LDP + 8 * nt + 2 * q4 + 1] = acc[nt][1];
+    }
+  }
+  __syncwarp();
+  // ---- pass y: R = b_B - Ay [Pa; Pb] ----
+  double r0 = 0.0, r1 = 0.0, s0 = 0.0, s1 = 0.0;      // two independent accumulation chains
+#pragma unroll
+  for (int kt = 0; kt < KY; ++kt) {
+    const int r = 4 * kt + q4, lx = r4;
+    const bool second = r >= WN4;
+    const int rr = second ? r - WN4 : r;
+    const double bv = (lx < S && rr < Wn) ? Pab[rr * LDP + (second ? S : 0) + lx] : 0.0;
+    if (kt & 1) dmma(s0, s1, ayf[kt], bv);
+    else dmma(r0, r1, ayf[kt], bv);
+  }
+  r0 += s0;
+  r1 += s1;
+  {
+    const int ly = r4, lx0 = 2 * q4;
+    r0 = (ly < S && lx0 < S) ? Bb[ly * S + lx0] - r0 : 0.0;
+    r1 = (ly < S && lx0 + 1 < S) ? Bb[ly * S + lx0 + 1] - r1 : 0.0;
+  }
+  // ---- FD: T = R Vx ----
+  double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+  for (int kt = 0; kt < KF; ++kt) dmma(t0, t1, c_elem(r0, r1, r4, 4 * kt + q4), vxb[kt]);
+  // Z = Vy^T T ./ den
+  double z0 = 0.0, z1 = 0.0;
+#pragma unroll
+  for (int kt = 0; kt < KF; ++kt) dmma(z0, z1, vyta[kt], c_elem(t0, t1, 4 * kt + q4, r4));
+  z0 *= rden[0];
+  z1 *= rden[1];
+  // U = Z Vx^T
+  double u0 = 0.0, u1 = 0.0;
+#pragma unroll
+  for (int kt = 0; kt < KF; ++kt) dmma(u0, u1, c_elem(z0, z1, r4, 4 * kt + q4), vxtb[kt]);
+  // δ = Vy U
+  double e0 = 0.0, e1 = 0.0;
+#pragma unroll
+  for (int kt = 0; kt < KF; ++kt) dmma(e0, e1, vya[kt], c_elem(u0, u1, 4 * kt + q4, r4));
+  // ---- x_B += δ ----
+  {
+    const int ly = r4, gy = by + ly;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int lx = 2 * q4 + i, gx = bx + lx;
+      if (ly < S && lx < S && unsigned(gx) < un && unsigned(gy) < un)
+        x[(int64_t)(gy - zoff) * n1 + gx] = X[(ly + P) * LDX + lx + P] + (i ? e1 : e0);
+    }
+  }
+}
+
+template <int P, int S>
+bool try_schwarz2d_mma(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
+                       const double *b, double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st) {
+  if (p != P || s != S) return false;
+  constexpr int WPC = 4;
+  constexpr size_t sm = sizeof(double) * WPC * Mma2<P, S>::PER;
+  ensure_smem(k_schwarz2d_mma<P, S, WPC>, sm);
+  k_schwarz2d_mma<P, S, WPC><<<(nblk + WPC - 1) / WPC, WPC * 32, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, D,
+                                                                           nb0, nblk, zoff);
+  return true;
+}
+
 }  // namespace
 
 bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M, const double *V,
                                 const double *lam, const double *b, double *x, int colour, int D, cudaStream_t st,
-                                SlabView sv) {
+                                SlabView sv, const ToeP *tp) {
   if (sv.zhi < 0) sv = SlabView{0, 0, int(n1)};
   if (dim == 3) {
     const int c0 = colour % D, c1 = (colour / D) % D, c2 = colour / (D * D);
@@ -1733,6 +2173,26 @@ bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double 
   if (c0 >= n1 || nb1 == 0) return true;   // empty colour
   const int nb0 = int((n1 - c0 + D - 1) / D), nblk = nb0 * nb1;
   const int z = sv.zoff;
+  if (s2d_variant() == 0 || s2d_variant() == 9)   // default: FP64 tensor-pipe kernel
+    if (try_schwarz2d_mma<1, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
+        try_schwarz2d_mma<2, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
+        try_schwarz2d_mma<3, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
+        try_schwarz2d_mma<4, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
+        try_schwarz2d_mma<5, 5>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
+        try_schwarz2d_mma<6, 5>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
+        try_schwarz2d_mma<7, 7>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
+        try_schwarz2d_mma<8, 7>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st))
+      return true;
+  if (const int v = s2d_variant(); v >= 1 && v <= 4)
+    if (try_schwarz2d_r<1, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, v, tp) ||
+        try_schwarz2d_r<2, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, v, tp) ||
+        try_schwarz2d_r<3, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, v, tp) ||
+        try_schwarz2d_r<4, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, v, tp) ||
+        try_schwarz2d_r<5, 5>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, v, tp) ||
+        try_schwarz2d_r<6, 5>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, v, tp) ||
+        try_schwarz2d_r<7, 7>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, v, tp) ||
+        try_schwarz2d_r<8, 7>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, v, tp))
+      return true;
   // <P, S, blocks per CTA, warps per block>
   return try_schwarz2d<1, 3, 8, 1>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
          try_schwarz2d<2, 3, 8, 1>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||

@@ -33,6 +33,15 @@ void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, 
                   SlabView sv = kFull);
 int apply_num_partials(int dim, int p, int64_t n1);
 
+// Interior (translation-invariant) 1D data of the fine level (reading A27), passed BY VALUE as a
+// kernel parameter: with compile-time indices the FMAs read it as constant-bank operands.
+constexpr int kToeMaxW = 17, kToeMaxS = 7;
+struct ToeP {
+  double k[kToeMaxW], m[kToeMaxW];           // interior band row of K and M (t = 0 .. 2p)
+  double v[kToeMaxS * kToeMaxS], lam[kToeMaxS];   // FD tables of an interior block (V[l][j], λ_j)
+  int valid;                                 // 0: no interior rows (small grids)
+};
+
 // ---- multicolour Schwarz: one colour ---------------------------------------------------------
 // Blocks centred at c = col + D*j (per axis) are solved in parallel (A-decoupled, reading A4):
 // r_B = b_B - (A x)_B; δ = A_B^{-1} r_B by fast diagonalisation with per-centre 1D tables V, lam;
@@ -67,7 +76,7 @@ void launch_sum_partials(const double *partial, int n, double *out, double *hist
 // Warp-per-block 2D Schwarz colour kernel for the paper's (p, s) pairs; false = not specialised.
 bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M,
                                 const double *V, const double *lam, const double *b, double *x, int colour,
-                                int D, cudaStream_t st, SlabView sv = kFull);
+                                int D, cudaStream_t st, SlabView sv = kFull, const ToeP *tp = nullptr);
 // Persistent 2D sweep (all D^2 colours in one cooperative launch, per-tile progress counters).
 // ctl: 2 unsigned (zeroed once), done: one unsigned per tile (zeroed once).  launch = false returns the
 // tile count (0: cannot be co-resident or more than max_tiles; -1: (p, s) not specialised).

@@ -285,6 +285,9 @@ PERSIST = [(1, 3, 48), (2, 3, 48), (3, 3, 48), (4, 3, 48), (5, 5, 48), (6, 5, 48
 
 @pytest.mark.parametrize("p,s,m", PERSIST, ids=[f"p{c[0]}" for c in PERSIST])
 def test_persistent_sweep_bitwise(p, s, m, monkeypatch):
+    # the persistent kernel runs the warp-group block solve (Blk2): compare with the per-colour launches
+    # of the same block solve (IGA2L_S2D_VARIANT=10), bitwise
+    monkeypatch.setenv("IGA2L_S2D_VARIANT", "10")
     monkeypatch.setenv("IGA2L_SWEEP_PERSIST", "1")
     ctx = make_ctx(2, p, 1, m, s, "vcycle", 2)
     monkeypatch.setenv("IGA2L_SWEEP_PERSIST", "0")
@@ -298,3 +301,17 @@ def test_persistent_sweep_bitwise(p, s, m, monkeypatch):
     ctx.iterate(b, x1, iters=4)
     ref.iterate(b, x2, iters=4)
     assert torch.equal(x1, x2)
+
+
+# ---- every 2D block-solve variant (DMMA default, register-blocked, warp-group) against the oracle ----
+@pytest.mark.parametrize("variant", ["1", "2", "10"])
+@pytest.mark.parametrize("cfg", [c for c in PAR if c[1] == 2], ids=[c[0] for c in PAR if c[1] == 2])
+def test_sweep_variants_match_oracle(cfg, variant, monkeypatch):
+    name, d, p, q, m, s, coarse, hf = cfg
+    monkeypatch.setenv("IGA2L_S2D_VARIANT", variant)
+    ctx = make_ctx(d, p, q, m, s, coarse, hf)
+    ora = oracle_for(*cfg)
+    b, x0 = random_rhs(ctx.N), initial_guess(ctx.N)
+    xg = cu(x0)
+    ctx.sweep(cu(b), xg)
+    close(host(xg), ora.smoother.sweep(x0.copy(), b), 1e-11)
