@@ -83,6 +83,7 @@ struct iga2l_ctx {
   int l_cta = -1;                // first level handled by the single-CTA tail kernel
   int l_sm = -1;                 // first level handled by the shared-memory tail kernel (preferred)
   int persist_tiles = 0;         // > 0: full sweeps run as one persistent launch with this many tiles
+  int tb_kc = 0;                 // temporal blocking (colours per launch) chosen at setup; 0 = per-colour
   unsigned *sweep_ctl = nullptr, *sweep_done = nullptr;
   VcLayout vcl{};
   int launch_counter = 0;
@@ -219,6 +220,18 @@ void L_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
                     c->persist_tiles, c->st, true);
     c->launch_counter++;
     return;
+  }
+  const char *tbe = std::getenv("IGA2L_TB");   // temporal blocking: colours per launch (0 = off)
+  const int kc = tbe ? std::atoi(tbe) : c->tb_kc;
+  if (c->dim == 2 && kc >= 2) {
+    bool ok = true;
+    for (int col = c0; col < c1 && ok; col += kc) {
+      ok = launch_schwarz2d_tb(c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, std::min(kc, c1 - col), kc,
+                               c->st);
+      if (ok) c->launch_counter++;
+      else if (col != c0) return;   // (cannot happen: the same (p, s) either specialises or not)
+    }
+    if (ok) return;
   }
   for (int col = c0; col < c1; ++col) {
     if (!launch_schwarz_colour_fast(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st,

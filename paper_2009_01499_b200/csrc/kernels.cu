@@ -1988,83 +1988,95 @@ struct Mma2 {
   static constexpr int PER = MT * 8 * LDX + MT * 8 * LDP + S * S;   // doubles per warp
 };
 
-template <int P, int S, int WPC>
-__global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma(int n1, const double *__restrict__ K,
-                                                            const double *__restrict__ M,
-                                                            const double *__restrict__ Vt,
-                                                            const double *__restrict__ lamt,
-                                                            const double *__restrict__ b, double *__restrict__ x,
-                                                            int c0, int c1, int D, int nb0, int nblk, int zoff) {
+// Operand fragments of one block solve (per lane), split by axis so that translation-invariant axes
+// (A27) can reuse a warp's cached copy: x-axis: pass-x band B operand, Vx (as B and as B^T), λx;
+// y-axis: pass-y band A operand, Vy (as A^T and as A), λy.
+template <int P, int S>
+struct FragX {
+  double bxf[Mma2<P, S>::KT][Mma2<P, S>::NTX], vxb[Mma2<P, S>::KF], vxtb[Mma2<P, S>::KF], lam[2];
+};
+template <int P, int S>
+struct FragY {
+  double ayf[Mma2<P, S>::KY], vyta[Mma2<P, S>::KF], vya[Mma2<P, S>::KF], lam;
+};
+
+template <int P, int S>
+__device__ __forceinline__ void build_fragx(FragX<P, S> &f, int n1, int cx, const double *__restrict__ K,
+                                            const double *__restrict__ M, const double *__restrict__ Vt,
+                                            const double *__restrict__ lamt) {
   using G = Mma2<P, S>;
-  constexpr int W = G::W, Wn = G::Wn, w = G::w, MT = G::MT, KT = G::KT, NTX = G::NTX, WN4 = G::WN4, LDX = G::LDX,
-                LDP = G::LDP, KY = G::KY, KF = G::KF;
-  extern __shared__ double sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bid = blockIdx.x * WPC + warp;
-  if (bid >= nblk) return;                                   // whole warp exits together
-  double *X = sm + warp * G::PER, *Pab = X + MT * 8 * LDX, *Bb = Pab + MT * 8 * LDP;
-  const int j1 = bid / nb0, j0 = bid - j1 * nb0;
-  const int cx = c0 + D * j0, cy = c1 + D * j1;
-  const int bx = cx - w, by = cy - w, ox = bx - P, oy = by - P;
+  constexpr int W = G::W, w = G::w, KT = G::KT, NTX = G::NTX, KF = G::KF;
+  const int lane = threadIdx.x & 31, r4 = lane >> 2, q4 = lane & 3, bx = cx - w;
   const unsigned un = unsigned(n1);
-  const int r4 = lane >> 2, q4 = lane & 3;
-  // ---- stage the zero-padded window (MT*8 x WN4) and b_B asynchronously ----
-  for (int row = 0; row < MT * 8; ++row) {
-    const int gy = oy + row;
-    const bool oky = row < Wn && unsigned(gy) < un;
-    const double *src = x + (oky ? (int64_t)(gy - zoff) * n1 : 0);
-#pragma unroll
-    for (int cc = lane; cc < WN4; cc += 32) {
-      const int gx = ox + cc;
-      const bool ok = oky && cc < Wn && unsigned(gx) < un;
-      cp_async8(X + row * LDX + cc, ok ? src + gx : x, ok);
-    }
-  }
-  for (int i = lane; i < S * S; i += 32) {
-    const int ly = i / S, lx = i - ly * S, gx = bx + lx, gy = by + ly;
-    const bool ok = unsigned(gx) < un && unsigned(gy) < un;
-    cp_async8(Bb + i, b + (ok ? (int64_t)(gy - zoff) * n1 + gx : 0), ok);
-  }
-  // ---- operand fragments from the 1D tables (independent of the window; overlap the copies) ----
-  double bxf[KT][NTX];                                       // pass x B: Bx[4kt+q4][8nt+r4]
 #pragma unroll
   for (int kt = 0; kt < KT; ++kt)
 #pragma unroll
     for (int nt = 0; nt < NTX; ++nt) {
       const int c = 4 * kt + q4, j = 8 * nt + r4;
-      const int lx = j < S ? j : j - S, t = c - lx;
-      const int g = bx + lx;
+      const int lx = j < S ? j : j - S, t = c - lx, g = bx + lx;
       const bool ok = j < 2 * S && t >= 0 && t < W && unsigned(g) < un;
-      bxf[kt][nt] = ok ? __ldg((j < S ? K : M) + (int64_t)g * W + t) : 0.0;
+      f.bxf[kt][nt] = ok ? __ldg((j < S ? K : M) + (int64_t)g * W + t) : 0.0;
     }
-  double ayf[KY];                                            // pass y A: Ay[r4][4kt+q4]
+  const double *Vx = Vt + (int64_t)cx * S * S;
+#pragma unroll
+  for (int kt = 0; kt < KF; ++kt) {
+    const int kk = 4 * kt + q4;
+    const bool ok = kk < S && r4 < S;
+    f.vxb[kt] = ok ? __ldg(Vx + kk * S + r4) : 0.0;
+    f.vxtb[kt] = ok ? __ldg(Vx + r4 * S + kk) : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) f.lam[i] = (2 * q4 + i < S) ? __ldg(lamt + (int64_t)cx * S + 2 * q4 + i) : 1.0;
+}
+
+template <int P, int S>
+__device__ __forceinline__ void build_fragy(FragY<P, S> &f, int n1, int cy, const double *__restrict__ K,
+                                            const double *__restrict__ M, const double *__restrict__ Vt,
+                                            const double *__restrict__ lamt) {
+  using G = Mma2<P, S>;
+  constexpr int W = G::W, w = G::w, KY = G::KY, KF = G::KF, WN4 = G::WN4;
+  const int lane = threadIdx.x & 31, r4 = lane >> 2, q4 = lane & 3, by = cy - w;
+  const unsigned un = unsigned(n1);
 #pragma unroll
   for (int kt = 0; kt < KY; ++kt) {
     const int r = 4 * kt + q4, ly = r4;
     const bool second = r >= WN4;
     const int rr = second ? r - WN4 : r, t = rr - ly, g = by + ly;
     const bool ok = ly < S && t >= 0 && t < W && unsigned(g) < un;
-    ayf[kt] = ok ? __ldg((second ? K : M) + (int64_t)g * W + t) : 0.0;
+    f.ayf[kt] = ok ? __ldg((second ? K : M) + (int64_t)g * W + t) : 0.0;
   }
-  double vxb[KF], vyta[KF], vxtb[KF], vya[KF];               // FD operands (Vx as B, Vy^T as A, Vx^T as B, Vy as A)
-  const double *Vx = Vt + (int64_t)cx * S * S, *Vy = Vt + (int64_t)cy * S * S;
+  const double *Vy = Vt + (int64_t)cy * S * S;
 #pragma unroll
   for (int kt = 0; kt < KF; ++kt) {
     const int kk = 4 * kt + q4;
-    const bool okk = kk < S, okr = r4 < S;
-    vxb[kt] = (okk && okr) ? __ldg(Vx + kk * S + r4) : 0.0;   // B[kk][r4] = Vx[kk][r4]
-    vyta[kt] = (okk && okr) ? __ldg(Vy + kk * S + r4) : 0.0;  // A[r4][kk] = Vy[kk][r4]
-    vxtb[kt] = (okk && okr) ? __ldg(Vx + r4 * S + kk) : 0.0;  // B[kk][r4] = Vx[r4][kk]
-    vya[kt] = (okk && okr) ? __ldg(Vy + r4 * S + kk) : 0.0;   // A[r4][kk] = Vy[r4][kk]
+    const bool ok = kk < S && r4 < S;
+    f.vyta[kt] = ok ? __ldg(Vy + kk * S + r4) : 0.0;
+    f.vya[kt] = ok ? __ldg(Vy + r4 * S + kk) : 0.0;
   }
-  double rden[2];                                            // 1 / (λx_j + λy_k) at this lane's C elements
+  f.lam = r4 < S ? __ldg(lamt + (int64_t)cy * S + r4) : 1.0;
+}
+
+// One block solve by one warp.  Xw: the block's (s+2p)^2 window inside a zero-padded array with row
+// stride ldx (rows/cols beyond the window up to the fragment padding must be finite); Pab: per-warp
+// scratch (MT*8 x LDP); writes x_B = Xw-centre + δ through out(ly, lx, value) for in-domain cells.
+template <int P, int S, class OUT>
+__device__ __forceinline__ void mma_block_f(const double *Xw, int ldx, double *Pab, int n1, int cx, int cy,
+                                            const FragX<P, S> &fx, const FragY<P, S> &fy,
+                                            const double *__restrict__ b, int zoff, OUT out) {
+  using G = Mma2<P, S>;
+  constexpr int Wn = G::Wn, w = G::w, MT = G::MT, KT = G::KT, NTX = G::NTX, WN4 = G::WN4, LDP = G::LDP,
+                KY = G::KY, KF = G::KF;
+  const int lane = threadIdx.x & 31, r4 = lane >> 2, q4 = lane & 3;
+  const int bx = cx - w, by = cy - w;
+  const unsigned un = unsigned(n1);
+  double rden[2], bb[2];                                     // 1/(λx_j + λy_k) and b_B at this lane's C elements
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    const int kk = r4, j = 2 * q4 + i;
-    rden[i] = (kk < S && j < S) ? 1.0 / (__ldg(lamt + (int64_t)cx * S + j) + __ldg(lamt + (int64_t)cy * S + kk)) : 0.0;
+    const int j = 2 * q4 + i;
+    rden[i] = (r4 < S && j < S) ? 1.0 / (fx.lam[i] + fy.lam) : 0.0;
+    const int gx = bx + j, gy = by + r4;
+    bb[i] = (r4 < S && j < S && unsigned(gx) < un && unsigned(gy) < un) ? __ldg(b + (int64_t)(gy - zoff) * n1 + gx) : 0.0;
   }
-  cp_async_wait_all();
-  __syncwarp();
   // ---- pass x ----
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
@@ -2073,9 +2085,9 @@ __global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma(int n1, const double
     for (int nt = 0; nt < NTX; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
 #pragma unroll
     for (int kt = 0; kt < KT; ++kt) {
-      const double a = X[(8 * mt + r4) * LDX + 4 * kt + q4];
+      const double a = Xw[(8 * mt + r4) * ldx + 4 * kt + q4];
 #pragma unroll
-      for (int nt = 0; nt < NTX; ++nt) dmma(acc[nt][0], acc[nt][1], a, bxf[kt][nt]);
+      for (int nt = 0; nt < NTX; ++nt) dmma(acc[nt][0], acc[nt][1], a, fx.bxf[kt][nt]);
     }
 #pragma unroll
     for (int nt = 0; nt < NTX; ++nt) {
@@ -2092,43 +2104,151 @@ __global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma(int n1, const double
     const bool second = r >= WN4;
     const int rr = second ? r - WN4 : r;
     const double bv = (lx < S && rr < Wn) ? Pab[rr * LDP + (second ? S : 0) + lx] : 0.0;
-    if (kt & 1) dmma(s0, s1, ayf[kt], bv);
-    else dmma(r0, r1, ayf[kt], bv);
+    if (kt & 1) dmma(s0, s1, fy.ayf[kt], bv);
+    else dmma(r0, r1, fy.ayf[kt], bv);
   }
-  r0 += s0;
-  r1 += s1;
-  {
-    const int ly = r4, lx0 = 2 * q4;
-    r0 = (ly < S && lx0 < S) ? Bb[ly * S + lx0] - r0 : 0.0;
-    r1 = (ly < S && lx0 + 1 < S) ? Bb[ly * S + lx0 + 1] - r1 : 0.0;
-  }
-  // ---- FD: T = R Vx ----
+  r0 = (r4 < S && 2 * q4 < S) ? bb[0] - (r0 + s0) : 0.0;
+  r1 = (r4 < S && 2 * q4 + 1 < S) ? bb[1] - (r1 + s1) : 0.0;
+  // ---- FD: T = R Vx;  Z = Vy^T T ./ den;  U = Z Vx^T;  δ = Vy U ----
   double t0 = 0.0, t1 = 0.0;
 #pragma unroll
-  for (int kt = 0; kt < KF; ++kt) dmma(t0, t1, c_elem(r0, r1, r4, 4 * kt + q4), vxb[kt]);
-  // Z = Vy^T T ./ den
+  for (int kt = 0; kt < KF; ++kt) dmma(t0, t1, c_elem(r0, r1, r4, 4 * kt + q4), fx.vxb[kt]);
   double z0 = 0.0, z1 = 0.0;
 #pragma unroll
-  for (int kt = 0; kt < KF; ++kt) dmma(z0, z1, vyta[kt], c_elem(t0, t1, 4 * kt + q4, r4));
+  for (int kt = 0; kt < KF; ++kt) dmma(z0, z1, fy.vyta[kt], c_elem(t0, t1, 4 * kt + q4, r4));
   z0 *= rden[0];
   z1 *= rden[1];
-  // U = Z Vx^T
   double u0 = 0.0, u1 = 0.0;
 #pragma unroll
-  for (int kt = 0; kt < KF; ++kt) dmma(u0, u1, c_elem(z0, z1, r4, 4 * kt + q4), vxtb[kt]);
-  // δ = Vy U
+  for (int kt = 0; kt < KF; ++kt) dmma(u0, u1, c_elem(z0, z1, r4, 4 * kt + q4), fx.vxtb[kt]);
   double e0 = 0.0, e1 = 0.0;
 #pragma unroll
-  for (int kt = 0; kt < KF; ++kt) dmma(e0, e1, vya[kt], c_elem(u0, u1, 4 * kt + q4, r4));
+  for (int kt = 0; kt < KF; ++kt) dmma(e0, e1, fy.vya[kt], c_elem(u0, u1, 4 * kt + q4, r4));
   // ---- x_B += δ ----
-  {
-    const int ly = r4, gy = by + ly;
+  const int ly = r4, gy = by + ly;
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int lx = 2 * q4 + i, gx = bx + lx;
-      if (ly < S && lx < S && unsigned(gx) < un && unsigned(gy) < un)
-        x[(int64_t)(gy - zoff) * n1 + gx] = X[(ly + P) * LDX + lx + P] + (i ? e1 : e0);
+  for (int i = 0; i < 2; ++i) {
+    const int lx = 2 * q4 + i, gx = bx + lx;
+    if (ly < S && lx < S && unsigned(gx) < un && unsigned(gy) < un)
+      out(ly, lx, Xw[(ly + P) * ldx + lx + P] + (i ? e1 : e0));
+  }
+}
+
+template <int P, int S, class OUT>
+__device__ __forceinline__ void mma_block(const double *Xw, int ldx, double *Pab, int n1, int cx, int cy,
+                                          const double *__restrict__ K, const double *__restrict__ M,
+                                          const double *__restrict__ Vt, const double *__restrict__ lamt,
+                                          const double *__restrict__ b, int zoff, OUT out) {
+  FragX<P, S> fx;
+  FragY<P, S> fy;
+  build_fragx<P, S>(fx, n1, cx, K, M, Vt, lamt);
+  build_fragy<P, S>(fy, n1, cy, K, M, Vt, lamt);
+  mma_block_f<P, S>(Xw, ldx, Pab, n1, cx, cy, fx, fy, b, zoff, out);
+}
+
+template <int P, int S, int WPC>
+__global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma(int n1, const double *__restrict__ K,
+                                                            const double *__restrict__ M,
+                                                            const double *__restrict__ Vt,
+                                                            const double *__restrict__ lamt,
+                                                            const double *__restrict__ b, double *__restrict__ x,
+                                                            int c0, int c1, int D, int nb0, int nblk, int zoff) {
+  using G = Mma2<P, S>;
+  constexpr int Wn = G::Wn, w = G::w, MT = G::MT, WN4 = G::WN4, LDX = G::LDX, LDP = G::LDP;
+  extern __shared__ double sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bid = blockIdx.x * WPC + warp;
+  if (bid >= nblk) return;                                   // whole warp exits together
+  double *X = sm + warp * G::PER, *Pab = X + MT * 8 * LDX;
+  const int j1 = bid / nb0, j0 = bid - j1 * nb0;
+  const int cx = c0 + D * j0, cy = c1 + D * j1;
+  const int bx = cx - w, by = cy - w, ox = bx - P, oy = by - P;
+  const unsigned un = unsigned(n1);
+  for (int row = 0; row < MT * 8; ++row) {                   // zero-padded window, asynchronously
+    const int gy = oy + row;
+    const bool oky = row < Wn && unsigned(gy) < un;
+    const double *src = x + (oky ? (int64_t)(gy - zoff) * n1 : 0);
+#pragma unroll
+    for (int cc = lane; cc < WN4; cc += 32) {
+      const int gx = ox + cc;
+      const bool ok = oky && cc < Wn && unsigned(gx) < un;
+      cp_async8(X + row * LDX + cc, ok ? src + gx : x, ok);
     }
+  }
+  cp_async_wait_all();
+  __syncwarp();
+  mma_block<P, S>(X, LDX, Pab, n1, cx, cy, K, M, Vt, lamt, b, zoff, [&](int ly, int lx, double v) {
+    x[(int64_t)(by + ly - zoff) * n1 + bx + lx] = v;
+  });
+}
+
+// ---------------- temporal blocking: KC consecutive colours per launch (latency-bound sizes) ------
+// CTA = core tile [X0, X0+T)^2 (T = 2D).  It loads x on core ± KC r (r = 2w + p, the reach of one
+// block update on the next colour's residual) into shared memory, solves colour c+j's blocks with
+// centres in core ± (w + (KC-1-j) r) from that copy (outer ones redundantly with the neighbours,
+// same arithmetic), and writes back its core only.  Equals KC per-colour launches (reading A4).
+template <int P, int S>
+struct Tb2 {
+  using G = Mma2<P, S>;
+  static constexpr int D = S + P, T = 2 * D, r = S - 1 + P, w = (S - 1) / 2;
+  static constexpr int PADX = (G::MT * 8 - G::Wn) > (G::WN4 - G::Wn) ? (G::MT * 8 - G::Wn) : (G::WN4 - G::Wn);
+  __host__ __device__ static constexpr int side(int kc) { return T + 2 * kc * r + PADX; }
+};
+
+template <int P, int S, int KC, int WPC>
+__global__ void __launch_bounds__(WPC * 32) k_schwarz2d_tb(int n1, const double *__restrict__ K,
+                                                           const double *__restrict__ M,
+                                                           const double *__restrict__ Vt,
+                                                           const double *__restrict__ lamt,
+                                                           const double *__restrict__ b, double *__restrict__ x,
+                                                           int col0, int ncol, int ntx, int tlo, int thi, int cref) {
+  using G = Mma2<P, S>;
+  using TB = Tb2<P, S>;
+  constexpr int D = TB::D, T = TB::T, r = TB::r, w = TB::w, L = TB::side(KC), LDR = L + 1, LDP = G::LDP;
+  extern __shared__ double sm[];
+  const int warp = threadIdx.x >> 5;
+  double *Rg = sm, *Pab = sm + L * LDR + warp * (G::MT * 8 * LDP);
+  const int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;
+  const int X0 = tx * T, Y0 = ty * T, H = ncol * r;
+  const int rx0 = X0 - H, ry0 = Y0 - H;                      // region origin (global)
+  const unsigned un = unsigned(n1);
+  for (int i = threadIdx.x; i < L * L; i += WPC * 32) {      // region (zero outside the domain / region)
+    const int ry = i / L, rx = i - ry * L, gx = rx0 + rx, gy = ry0 + ry;
+    const bool ok = rx < T + 2 * H && ry < T + 2 * H && unsigned(gx) < un && unsigned(gy) < un;
+    cp_async8(Rg + ry * LDR + rx, x + (ok ? (int64_t)gy * n1 + gx : 0), ok);
+  }
+  FragX<P, S> fxi;                                           // interior fragments (A27), built once per warp
+  FragY<P, S> fyi;
+  if (cref >= 0) {
+    build_fragx<P, S>(fxi, n1, cref, K, M, Vt, lamt);
+    build_fragy<P, S>(fyi, n1, cref, K, M, Vt, lamt);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  for (int j = 0; j < ncol; ++j) {
+    const int c = col0 + j, cc0 = c % D, cc1 = c / D;
+    const int rho = w + (ncol - 1 - j) * r;
+    // centres with residue (cc0, cc1) in [X0 - rho, X0 + T + rho) x [Y0 - rho, Y0 + T + rho), inside the domain
+    auto first = [&](int res, int lo) { int f = res; if (f < lo) f += ((lo - f + D - 1) / D) * D; return f; };
+    const int lox = max(0, X0 - rho), hix = min(n1, X0 + T + rho), loy = max(0, Y0 - rho), hiy = min(n1, Y0 + T + rho);
+    const int fx = first(cc0, lox), fy = first(cc1, loy);
+    const int nx = fx < hix ? (hix - 1 - fx) / D + 1 : 0, ny = fy < hiy ? (hiy - 1 - fy) / D + 1 : 0;
+    for (int blk = warp; blk < nx * ny; blk += WPC) {
+      const int cx = fx + D * (blk % nx), cy = fy + D * (blk / nx);
+      const int ox = cx - w - P - rx0, oy = cy - w - P - ry0;  // window origin in the region
+      double *Xw = Rg + oy * LDR + ox;
+      auto put = [&](int ly, int lx, double v) { Xw[(ly + P) * LDR + lx + P] = v; };
+      if (cref >= 0 && cx - w >= tlo && cx + w <= thi && cy - w >= tlo && cy + w <= thi)
+        mma_block_f<P, S>(Xw, LDR, Pab, n1, cx, cy, fxi, fyi, b, 0, put);
+      else
+        mma_block<P, S>(Xw, LDR, Pab, n1, cx, cy, K, M, Vt, lamt, b, 0, put);
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < T * T; i += WPC * 32) {      // write back the core
+    const int cy = i / T, cx = i - cy * T, gx = X0 + cx, gy = Y0 + cy;
+    if (gx < n1 && gy < n1) x[(int64_t)gy * n1 + gx] = Rg[(cy + H) * LDR + cx + H];
   }
 }
 
@@ -2141,6 +2261,22 @@ bool try_schwarz2d_mma(int p, int s, int64_t n1, const double *K, const double *
   ensure_smem(k_schwarz2d_mma<P, S, WPC>, sm);
   k_schwarz2d_mma<P, S, WPC><<<(nblk + WPC - 1) / WPC, WPC * 32, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, D,
                                                                            nb0, nblk, zoff);
+  return true;
+}
+
+template <int P, int S, int KC>
+bool try_schwarz2d_tb(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
+                      const double *b, double *x, int col0, int ncol, cudaStream_t st) {
+  if (p != P || s != S) return false;
+  using TB = Tb2<P, S>;
+  constexpr int WPC = 8, L = TB::side(KC);
+  constexpr size_t sm = sizeof(double) * (size_t(L) * (L + 1) + WPC * Mma2<P, S>::MT * 8 * Mma2<P, S>::LDP);
+  ensure_smem(k_schwarz2d_tb<P, S, KC, WPC>, sm);
+  const int ntx = int((n1 + TB::T - 1) / TB::T);
+  const int m = int(n1) - P + 2, tlo = 2 * P - 1, thi = m - 2 - P, w = (S - 1) / 2;
+  const int cref = (thi - tlo >= 2 * w) ? (tlo + thi) / 2 : -1;   // an interior centre (A27)
+  k_schwarz2d_tb<P, S, KC, WPC><<<ntx * ntx, WPC * 32, sm, st>>>(int(n1), K, M, V, lam, b, x, col0, ncol, ntx, tlo,
+                                                                 thi, cref);
   return true;
 }
 
@@ -2225,6 +2361,16 @@ int sweep2d_persist(int p, int s, int64_t n1, const double *K, const double *M, 
   IGA2L_TRY(8, 7, 4, 4, 4, 4)
 #undef IGA2L_TRY
   return -1;
+}
+
+bool launch_schwarz2d_tb(int p, int s, int64_t n1, const double *K, const double *M, const double *V,
+                         const double *lam, const double *b, double *x, int col0, int ncol, int kc, cudaStream_t st) {
+#define IGA2L_TB(P_, S_)                                                                                      \
+  if (kc == 2 && try_schwarz2d_tb<P_, S_, 2>(p, s, n1, K, M, V, lam, b, x, col0, ncol, st)) return true;    \
+  if (kc == 3 && try_schwarz2d_tb<P_, S_, 3>(p, s, n1, K, M, V, lam, b, x, col0, ncol, st)) return true;
+  IGA2L_TB(1, 3) IGA2L_TB(2, 3) IGA2L_TB(3, 3) IGA2L_TB(4, 3) IGA2L_TB(5, 5) IGA2L_TB(6, 5)
+#undef IGA2L_TB
+  return false;
 }
 
 void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumulate, cudaStream_t st,

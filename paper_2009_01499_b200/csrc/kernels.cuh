@@ -77,6 +77,11 @@ void launch_sum_partials(const double *partial, int n, double *out, double *hist
 bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M,
                                 const double *V, const double *lam, const double *b, double *x, int colour,
                                 int D, cudaStream_t st, SlabView sv = kFull, const ToeP *tp = nullptr);
+// Temporal blocking (2D, single domain): colours [col0, col0 + ncol), ncol <= kc in {2, 3}, in ONE
+// launch (each CTA solves its core's blocks and the halo blocks they depend on from a shared-memory
+// copy of x).  False if (p, s, kc) is not specialised.
+bool launch_schwarz2d_tb(int p, int s, int64_t n1, const double *K, const double *M, const double *V,
+                         const double *lam, const double *b, double *x, int col0, int ncol, int kc, cudaStream_t st);
 // Persistent 2D sweep (all D^2 colours in one cooperative launch, per-tile progress counters).
 // ctl: 2 unsigned (zeroed once), done: one unsigned per tile (zeroed once).  launch = false returns the
 // tile count (0: cannot be co-resident or more than max_tiles; -1: (p, s) not specialised).

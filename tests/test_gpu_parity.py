@@ -315,3 +315,28 @@ def test_sweep_variants_match_oracle(cfg, variant, monkeypatch):
     xg = cu(x0)
     ctx.sweep(cu(b), xg)
     close(host(xg), ora.smoother.sweep(x0.copy(), b), 1e-11)
+
+
+# ---- temporal blocking (several colours per launch, halo blocks recomputed per CTA): the same block
+# arithmetic as the per-colour DMMA launches, so bitwise equal; and against the oracle ----
+TB_CASES = [(1, 3, 48), (2, 3, 64), (3, 3, 96), (4, 3, 64), (5, 5, 96), (6, 5, 48)]
+
+
+@pytest.mark.parametrize("kc", ["2", "3"])
+@pytest.mark.parametrize("p,s,m", TB_CASES, ids=[f"p{c[0]}" for c in TB_CASES])
+def test_temporal_blocking_bitwise(p, s, m, kc, monkeypatch):
+    monkeypatch.setenv("IGA2L_TB", "0")
+    ref = make_ctx(2, p, 1, m, s, "vcycle", 2)
+    monkeypatch.setenv("IGA2L_TB", kc)
+    ctx = make_ctx(2, p, 1, m, s, "vcycle", 2)
+    b, x0 = cu(random_rhs(ctx.N)), cu(initial_guess(ctx.N))
+    x1, x2 = x0.clone(), x0.clone()
+    ctx.sweep(b, x1)
+    monkeypatch.setenv("IGA2L_TB", "0")
+    ref.sweep(b, x2)
+    assert torch.equal(x1, x2)
+    monkeypatch.setenv("IGA2L_TB", kc)
+    ctx.sweep(b, x1, 1, 6)                 # a partial range (odd start, ragged chunk)
+    monkeypatch.setenv("IGA2L_TB", "0")
+    ref.sweep(b, x2, 1, 6)
+    assert torch.equal(x1, x2)
