@@ -30,6 +30,9 @@ UNIT = "DOF*it/s"
 WORKLOAD = "C2: 2D Poisson, p in {3,4,5}, 256x256 elements, q=1 V(1,1) at H=2h, fp64"
 PS = (3, 4, 5)
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # SMs x FP64 FMA/clk/SM x 2 x max SM clock
+# FP64 tensor pipe (DMMA, mma.sync m8n8k4 f64): measured 37.09 TFLOP/s by tools/microbench.cu on this
+# pool's B200 (profiles/microbench_r01.txt); MEASURED_PEAKS.json has no FP64 entry
+DMMA_PEAK_TFLOPS = 37.09
 
 
 def env_rank():
@@ -271,10 +274,11 @@ def main():
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                "kernel": "k_schwarz (one launch per colour)",
-                "note": "FP64 FMA pipe; peak derived 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md); "
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / DMMA_PEAK_TFLOPS, "traffic": traffic,
+                "kernel": "k_schwarz2d_mma (FP64 DMMA block solves, one launch per colour)",
+                "peak_source": "measured FP64 DMMA peak, tools/microbench.cu (profiles/microbench_r01.txt)",
+                "note": "C2 is latency bound (36/49/100 dependent colours of ~1.3k blocks); "
                         f"achieved = SURVEY 8(d) sweep flops / CUDA-event sweep time over {sw_launches} launches"}
 
     # convergence factor (b = 0, 20 iterations, last 10 ratios) and iterations to 1e-8
