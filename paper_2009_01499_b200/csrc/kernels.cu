@@ -323,6 +323,170 @@ bool try_apply2d(int p, int64_t n1, const double *K, const double *M, const doub
   return true;
 }
 
+// 3D apply, z-streaming (v2).  CTA = (x, y) tile of TX x TY outputs and a chunk [zlo, zhi) of
+// output planes.  For every input plane gi in [zlo - p, zhi + p): stage its (TY+2p) x (TX+2p) window
+// (cp.async, double-buffered), pass x (K_x, M_x) into shared memory, pass y into a RING of 2p+1
+// planes holding c = M_y K_x X + K_y M_x X and e = M_y M_x X; output plane go = gi - p is then
+// complete: y = [b -] Σ_v (M_z(go, v) c[go-p+v] + K_z(go, v) e[go-p+v]).  Sum-factorised,
+// 2(2p+1)(TY+2p)/TY + 3(2p+1) + 2(2p+1) FMAs per output; each x value is read once per CTA.
+constexpr int A3TX = 32, A3TY = 16, A3NT = 256;
+template <int P>
+struct Apl3 {
+  static constexpr int W = 2 * P + 1, WX = A3TX + 2 * P, WY = A3TY + 2 * P, NR = 2 * P + 1;
+  static constexpr int SM = 2 * WY * WX + 2 * WY * A3TX + 2 * NR * A3TY * A3TX;   // doubles
+};
+
+template <int P>
+__global__ void __launch_bounds__(A3NT) k_apply3d_s(int n1, const double *__restrict__ K, const double *__restrict__ M,
+                                                    const double *__restrict__ x, const double *__restrict__ b,
+                                                    double *__restrict__ y, double *__restrict__ partial, int mode,
+                                                    int zoff, int zlo0, int zhi0, int zchunk, int tlo, int thi) {
+  using A = Apl3<P>;
+  constexpr int W = A::W, WX = A::WX, WY = A::WY, NR = A::NR, TX = A3TX, TY = A3TY, NT = A3NT;
+  extern __shared__ double sm[];
+  double *Xb = sm;                          // [2][WY][WX]
+  double *Pa = Xb + 2 * WY * WX;            // [WY][TX]  K_x X
+  double *Pb = Pa + WY * TX;                // [WY][TX]  M_x X
+  double *Rc = Pb + WY * TX;                // [NR][TY][TX]
+  double *Re = Rc + NR * TY * TX;
+  __shared__ double red[32];
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int zlo = zlo0 + blockIdx.z * zchunk, zhi = min(zhi0, zlo + zchunk);
+  const unsigned un = unsigned(n1);
+  const bool tx = x0 >= tlo && x0 + TX - 1 <= thi, ty = y0 >= tlo && y0 + TY - 1 <= thi;
+  // this thread's band coefficients for pass x rows (lx) and pass y rows (ly): rows of the tile are
+  // fixed, so load them once (registers) -- Toeplitz tiles use one row for all
+  auto stage = [&](int gi, int buf) {       // window of input plane gi into buffer buf (zero outside)
+    double *dst = Xb + buf * WY * WX;
+    const bool okz = unsigned(gi) < un;
+    for (int i = tid; i < WY * WX; i += NT) {
+      const int wy = i / WX, wx = i - wy * WX, gx = x0 - P + wx, gyy = y0 - P + wy;
+      const bool ok = okz && unsigned(gx) < un && unsigned(gyy) < un;
+      cp_async8(dst + i, x + (ok ? ((int64_t)(gi - zoff) * n1 + gyy) * n1 + gx : 0), ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double sq = 0.0;
+  const int gs = zlo - P, ge = zhi + P;
+  if (zlo >= zhi) return;
+  stage(gs, 0);
+  for (int gi = gs; gi < ge; ++gi) {
+    const int buf = (gi - gs) & 1;
+    if (gi + 1 < ge) {
+      stage(gi + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const int slot = ((gi % NR) + NR) % NR;
+    const bool okz = unsigned(gi) < un;
+    if (okz) {
+      const double *X = Xb + buf * WY * WX;
+      // pass x: tasks = (window row wy, 4 consecutive lx)
+      for (int task = tid; task < WY * (TX / 4); task += NT) {
+        const int wy = task / (TX / 4), lx0 = (task - wy * (TX / 4)) * 4;
+        double v[4 + 2 * P];
+#pragma unroll
+        for (int k = 0; k < 4 + 2 * P; ++k) v[k] = X[wy * WX + lx0 + k];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int gx = x0 + lx0 + i;
+          const bool okx = unsigned(gx) < un;
+          const int row = tx ? tlo : (okx ? gx : 0);
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+          for (int t = 0; t < W; ++t) {
+            const double kc = __ldg(K + (int64_t)row * W + t), mc = __ldg(M + (int64_t)row * W + t);
+            a0 = fma(kc, v[i + t], a0);
+            a1 = fma(mc, v[i + t], a1);
+          }
+          Pa[wy * TX + lx0 + i] = okx ? a0 : 0.0;
+          Pb[wy * TX + lx0 + i] = okx ? a1 : 0.0;
+        }
+      }
+    }
+    __syncthreads();
+    // pass y: each thread owns TX*TY/NT (= 2) output columns (lx, ly)
+#pragma unroll
+    for (int o = 0; o < TX * TY / NT; ++o) {
+      const int pt = tid + o * NT, ly = pt / TX, lx = pt - ly * TX;
+      double c = 0.0, e = 0.0;
+      if (okz) {
+        const int gyy = y0 + ly;
+        const bool oky = unsigned(gyy) < un;
+        const int row = ty ? tlo : (oky ? gyy : 0);
+        double c1 = 0.0;
+#pragma unroll
+        for (int u = 0; u < W; ++u) {
+          const double kc = __ldg(K + (int64_t)row * W + u), mc = __ldg(M + (int64_t)row * W + u);
+          const double pa = Pa[(ly + u) * TX + lx], pb = Pb[(ly + u) * TX + lx];
+          c = fma(mc, pa, c);
+          c1 = fma(kc, pb, c1);
+          e = fma(mc, pb, e);
+        }
+        c = oky ? c + c1 : 0.0;
+        e = oky ? e : 0.0;
+      }
+      Rc[(slot * TY + ly) * TX + lx] = c;
+      Re[(slot * TY + ly) * TX + lx] = e;
+    }
+    __syncthreads();
+    // output plane go = gi - P complete
+    const int go = gi - P;
+    if (go >= zlo && go < zhi) {
+      const bool tz = go >= tlo && go <= thi;
+      const int row = tz ? tlo : go;
+#pragma unroll
+      for (int o = 0; o < TX * TY / NT; ++o) {
+        const int pt = tid + o * NT, ly = pt / TX, lx = pt - ly * TX;
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int v = 0; v < W; ++v) {
+          const int sl = ((go - P + v) % NR + NR) % NR;
+          s0 = fma(__ldg(M + (int64_t)row * W + v), Rc[(sl * TY + ly) * TX + lx], s0);
+          s1 = fma(__ldg(K + (int64_t)row * W + v), Re[(sl * TY + ly) * TX + lx], s1);
+        }
+        const int gx = x0 + lx, gyy = y0 + ly;
+        if (gx < n1 && gyy < n1) {
+          const int64_t g = ((int64_t)(go - zoff) * n1 + gyy) * n1 + gx;
+          const double val = mode ? b[g] - (s0 + s1) : (s0 + s1);
+          y[g] = val;
+          sq = fma(val, val, sq);
+        }
+      }
+    }
+  }
+  if (partial) {
+    const double t = block_sum(sq, red);
+    if (tid == 0) partial[(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+int apply3d_zchunks(int64_t n1, int nz) {   // z chunks: about two CTAs per SM, chunks >= 8 planes
+  const int64_t tiles = ((n1 + A3TX - 1) / A3TX) * ((n1 + A3TY - 1) / A3TY);
+  int ch = int(std::max<int64_t>(1, (296 + tiles - 1) / tiles));
+  ch = std::min(ch, std::max(1, nz / 8));
+  return ch;
+}
+
+template <int P>
+bool try_apply3d(int p, int64_t n1, const double *K, const double *M, const double *x, const double *b, double *y,
+                 double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv) {
+  if (p != P) return false;
+  const int nz = sv.zhi - sv.zlo;
+  const int ch = apply3d_zchunks(n1, nz), zchunk = (nz + ch - 1) / ch;
+  const int m = int(n1) - P + 2;
+  constexpr size_t sm = sizeof(double) * Apl3<P>::SM;
+  ensure_smem(k_apply3d_s<P>, sm);
+  dim3 grid((unsigned)((n1 + A3TX - 1) / A3TX), (unsigned)((n1 + A3TY - 1) / A3TY), (unsigned)ch);
+  k_apply3d_s<P><<<grid, A3NT, sm, st>>>(int(n1), K, M, x, b, y, partial, mode, sv.zoff, sv.zlo, sv.zhi, zchunk,
+                                         2 * P - 1, m - 2 - P);
+  if (nparts) *nparts = int(grid.x * grid.y * grid.z);
+  return true;
+}
+
 constexpr int A2X = 32, A2Y = 8, A3X = 8, A3Y = 8, A3Z = 4;
 static const bool g_transfer_v2 = [] {
   const char *e = std::getenv("IGA2L_TRANSFER_V2");
@@ -673,7 +837,9 @@ int apply_num_partials(int dim, int p, int64_t n1) {
     const int64_t v1 = ((n1 + A2X - 1) / A2X) * ((n1 + A2Y - 1) / A2Y), v2 = ((n1 + 15) / 16) * ((n1 + 15) / 16);
     return int(std::max(v1, v2));
   }
-  return int(((n1 + A3X - 1) / A3X) * ((n1 + A3Y - 1) / A3Y) * ((n1 + A3Z - 1) / A3Z));
+  const int64_t v1 = ((n1 + A3X - 1) / A3X) * ((n1 + A3Y - 1) / A3Y) * ((n1 + A3Z - 1) / A3Z);
+  const int64_t v2 = ((n1 + A3TX - 1) / A3TX) * ((n1 + A3TY - 1) / A3TY) * apply3d_zchunks(n1, int(n1));
+  return int(std::max(v1, v2));
 }
 
 void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, const double *x, const double *b,
@@ -691,6 +857,14 @@ void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, 
        try_apply2d<6>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
        try_apply2d<7>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
        try_apply2d<8>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv)))
+    return;
+  if (dim == 3 && g_apply_v2 &&
+      (try_apply3d<1>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
+       try_apply3d<2>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
+       try_apply3d<3>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
+       try_apply3d<4>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
+       try_apply3d<5>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
+       try_apply3d<6>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv)))
     return;
   if (dim == 2) {
     dim3 grid((unsigned)((n1 + A2X - 1) / A2X), (unsigned)((nz + A2Y - 1) / A2Y));
