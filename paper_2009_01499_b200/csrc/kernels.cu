@@ -2328,7 +2328,7 @@ __global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma(int n1, const double
                                                             const double *__restrict__ b, double *__restrict__ x,
                                                             int c0, int c1, int D, int nb0, int nblk, int zoff) {
   using G = Mma2<P, S>;
-  constexpr int Wn = G::Wn, w = G::w, MT = G::MT, WN4 = G::WN4, LDX = G::LDX, LDP = G::LDP;
+  constexpr int Wn = G::Wn, w = G::w, MT = G::MT, WN4 = G::WN4, LDX = G::LDX;
   extern __shared__ double sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bid = blockIdx.x * WPC + warp;
@@ -2454,6 +2454,233 @@ bool try_schwarz2d_tb(int p, int s, int64_t n1, const double *K, const double *M
   return true;
 }
 
+// ---------------- 3D Schwarz colour kernel on the FP64 tensor pipe (DMMA): one CTA (NW warps) per block ----
+// pass x : Pab[pencil][j]   = X[pencil][c] · Bx[c][j]               (pencil = (wz, wy); j: K part, M part)
+// pass y : PcPe[m][(wz,lx)] = [[M_y, K_y], [0, M_y]][m][r] · [Pa; Pb][r][(wz,lx)]
+// pass z : R[lz][(ly,lx)]   = b_B - [M_z | K_z][lz][r] · [Pc; Pe][r][(ly,lx)]
+// FD     : six S^2 x S x S contractions (x, y, z forward, / (λx+λy+λz), z, y, x back) through shared memory.
+template <int P, int S>
+struct Mma3 {
+  static constexpr int W = 2 * P + 1, Wn = S + 2 * P, w = (S - 1) / 2, S2 = S * S, S3 = S2 * S;
+  static constexpr int WN4 = ((Wn + 3) / 4) * 4, KT = WN4 / 4;          // window x (pass-x K)
+  static constexpr int MX = (Wn * Wn + 7) / 8;                           // pencils (pass-x M tiles)
+  static constexpr int NTX = (2 * S + 7) / 8;                            // pass-x N tiles
+  static constexpr int LDX = WN4 + 1, LDP = NTX * 8 + 1;
+  static constexpr int MTY = (2 * S + 7) / 8, KY = 2 * WN4 / 4, NTY = (Wn * S + 7) / 8, LDQ = NTY * 8 + 1;
+  static constexpr int KZ = 2 * WN4 / 4, NTZ = (S2 + 7) / 8;
+  static constexpr int MF = (S2 + 7) / 8, KF = (S + 3) / 4;
+  static constexpr int OX = 0, OP = MX * 8 * LDX, OQ = OP + MX * 8 * LDP, OR = OQ + MTY * 8 * LDQ;
+  static constexpr int OT = OR + S3, OB = OT + S3, SM = OB + S3;        // doubles
+};
+
+// One FD contraction of a 3D s^3 array (index [z][y][x], x fastest) on DMMA; STEP selects the axis and
+// direction: 0/1/2 = x/y/z forward (Vᵀ; step 2 also divides by λx_j + λy_k + λz_m), 3/4/5 = z/y/x back.
+template <int S, int KF, int MF, int NW, int STEP>
+__device__ __forceinline__ void fd3_step(const double *in, double *out, const double (&bf)[KF], const double *lx_,
+                                         const double *ly_, const double *lz_) {
+  constexpr int S2 = S * S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, r4 = lane >> 2, q4 = lane & 3;
+  auto addr = [](int i, int l) -> int {   // element (row i, contracted index l); i = pair of the other two
+    if (STEP == 0 || STEP == 5) return i * S + l;                              // rows (z,y), axis x
+    if (STEP == 1 || STEP == 4) return ((i / S) * S + l) * S + i % S;          // rows (z,x), axis y
+    return l * S2 + i;                                                          // rows (y,x), axis z
+  };
+  for (int mt = warp; mt < MF; mt += NW) {
+    double d0 = 0.0, d1 = 0.0;
+    const int i = 8 * mt + r4;
+#pragma unroll
+    for (int kt = 0; kt < KF; ++kt) {
+      const int l = 4 * kt + q4;
+      const double a = (i < S2 && l < S) ? in[addr(i, l)] : 0.0;
+      dmma(d0, d1, a, bf[kt]);
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int j = 2 * q4 + e;
+      if (i < S2 && j < S) {
+        double v = e ? d1 : d0;
+        if (STEP == 2) v /= (__ldg(lx_ + i % S) + __ldg(ly_ + i / S) + __ldg(lz_ + j));
+        out[addr(i, j)] = v;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <int P, int S, int NW>
+__global__ void __launch_bounds__(NW * 32) k_schwarz3d_mma(int n1, const double *__restrict__ K,
+                                                           const double *__restrict__ M,
+                                                           const double *__restrict__ Vt,
+                                                           const double *__restrict__ lamt,
+                                                           const double *__restrict__ b, double *__restrict__ x,
+                                                           int c0, int c1, int c2, int D, int nb0, int nb1, int zoff) {
+  using G = Mma3<P, S>;
+  constexpr int W = G::W, Wn = G::Wn, w = G::w, S2 = G::S2, S3 = G::S3, WN4 = G::WN4, KT = G::KT, MX = G::MX,
+                NTX = G::NTX, LDX = G::LDX, LDP = G::LDP, MTY = G::MTY, KY = G::KY, NTY = G::NTY, LDQ = G::LDQ,
+                KZ = G::KZ, NTZ = G::NTZ, MF = G::MF, KF = G::KF;
+  extern __shared__ double sm[];
+  double *X = sm + G::OX, *Pab = sm + G::OP, *Q = sm + G::OQ, *R = sm + G::OR, *T = sm + G::OT, *Bb = sm + G::OB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, r4 = lane >> 2, q4 = lane & 3;
+  const int g = blockIdx.x;
+  const int cx = c0 + D * (g % nb0), cy = c1 + D * ((g / nb0) % nb1), cz = c2 + D * (g / (nb0 * nb1));
+  const int bx = cx - w, by = cy - w, bz = cz - w;
+  const unsigned un = unsigned(n1);
+  // ---- stage: window pencils [(wz, wy)][wx] (zero padded), b_B ----
+  for (int row = warp; row < MX * 8; row += NW) {
+    const int wz = row / Wn, wy = row - wz * Wn, gy = by - P + wy, gz = bz - P + wz;
+    const bool okyz = row < Wn * Wn && unsigned(gy) < un && unsigned(gz) < un;
+    const double *src = x + (okyz ? ((int64_t)(gz - zoff) * n1 + gy) * n1 : 0);
+#pragma unroll
+    for (int c = lane; c < WN4; c += 32) {
+      const int gx = bx - P + c;
+      const bool ok = okyz && c < Wn && unsigned(gx) < un;
+      cp_async8(X + row * LDX + c, ok ? src + gx : x, ok);
+    }
+  }
+  for (int i = threadIdx.x; i < S3; i += NW * 32) {
+    const int gx = bx + i % S, gy = by + (i / S) % S, gz = bz + i / S2;
+    const bool ok = unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un;
+    cp_async8(Bb + i, b + (ok ? ((int64_t)(gz - zoff) * n1 + gy) * n1 + gx : 0), ok);
+  }
+  // ---- operand fragments (independent of x; overlap the copies) ----
+  auto band = [&](const double *T_, int row0, int l, int t) {   // T_(row0 + l, t), 0 outside
+    const int gr = row0 + l;
+    return (t >= 0 && t < W && unsigned(gr) < un) ? __ldg(T_ + (int64_t)gr * W + t) : 0.0;
+  };
+  double bxf[KT][NTX];
+#pragma unroll
+  for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+    for (int nt = 0; nt < NTX; ++nt) {
+      const int c = 4 * kt + q4, j = 8 * nt + r4;
+      bxf[kt][nt] = j < S ? band(K, bx, j, c - j) : (j < 2 * S ? band(M, bx, j - S, c - (j - S)) : 0.0);
+    }
+  double ayf[MTY][KY];
+#pragma unroll
+  for (int mt = 0; mt < MTY; ++mt)
+#pragma unroll
+    for (int kt = 0; kt < KY; ++kt) {
+      const int m = 8 * mt + r4, r = 4 * kt + q4;
+      const bool second = r >= WN4;
+      const int rr = second ? r - WN4 : r;
+      double v = 0.0;
+      if (m < S) v = second ? band(K, by, m, rr - m) : band(M, by, m, rr - m);
+      else if (m < 2 * S) v = second ? band(M, by, m - S, rr - (m - S)) : 0.0;
+      ayf[mt][kt] = v;
+    }
+  double azf[KZ];
+#pragma unroll
+  for (int kt = 0; kt < KZ; ++kt) {
+    const int r = 4 * kt + q4;
+    const bool second = r >= WN4;
+    const int rr = second ? r - WN4 : r;
+    azf[kt] = r4 < S ? (second ? band(K, bz, r4, rr - r4) : band(M, bz, r4, rr - r4)) : 0.0;
+  }
+  const double *Vx = Vt + (int64_t)cx * S2, *Vy = Vt + (int64_t)cy * S2, *Vz = Vt + (int64_t)cz * S2;
+  double vf[6][KF];   // FD B operands: B[l][j], l = 4kt+q4, j = r4
+#pragma unroll
+  for (int kt = 0; kt < KF; ++kt) {
+    const int l = 4 * kt + q4, j = r4;
+    const bool ok = l < S && j < S;
+    vf[0][kt] = ok ? __ldg(Vx + l * S + j) : 0.0;   // x forward:  Vx[l][j]
+    vf[1][kt] = ok ? __ldg(Vy + l * S + j) : 0.0;   // y forward:  Vy[l][k]
+    vf[2][kt] = ok ? __ldg(Vz + l * S + j) : 0.0;   // z forward:  Vz[l][m]
+    vf[3][kt] = ok ? __ldg(Vz + j * S + l) : 0.0;   // z back:     Vz[z][m]  (B[m][z])
+    vf[4][kt] = ok ? __ldg(Vy + j * S + l) : 0.0;   // y back:     Vy[y][k]  (B[k][y])
+    vf[5][kt] = ok ? __ldg(Vx + j * S + l) : 0.0;   // x back:     Vx[x][j]  (B[j][x])
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  // ---- pass x ----
+  for (int mt = warp; mt < MX; mt += NW) {
+    double acc[NTX][2];
+#pragma unroll
+    for (int nt = 0; nt < NTX; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+      const double a = X[(8 * mt + r4) * LDX + 4 * kt + q4];
+#pragma unroll
+      for (int nt = 0; nt < NTX; ++nt) dmma(acc[nt][0], acc[nt][1], a, bxf[kt][nt]);
+    }
+#pragma unroll
+    for (int nt = 0; nt < NTX; ++nt) {
+      Pab[(8 * mt + r4) * LDP + 8 * nt + 2 * q4] = acc[nt][0];
+      Pab[(8 * mt + r4) * LDP + 8 * nt + 2 * q4 + 1] = acc[nt][1];
+    }
+  }
+  __syncthreads();
+  // ---- pass y: columns (wz, lx) ----
+  for (int nt = warp; nt < NTY; nt += NW) {
+    double acc[MTY][2];
+#pragma unroll
+    for (int mt = 0; mt < MTY; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+    const int col = 8 * nt + r4, wz = col / S, lx = col - wz * S;
+    const bool okc = col < Wn * S;
+#pragma unroll
+    for (int kt = 0; kt < KY; ++kt) {
+      const int r = 4 * kt + q4;
+      const bool second = r >= WN4;
+      const int rr = second ? r - WN4 : r;
+      const double bv = (okc && rr < Wn) ? Pab[(wz * Wn + rr) * LDP + (second ? S : 0) + lx] : 0.0;
+#pragma unroll
+      for (int mt = 0; mt < MTY; ++mt) dmma(acc[mt][0], acc[mt][1], ayf[mt][kt], bv);
+    }
+#pragma unroll
+    for (int mt = 0; mt < MTY; ++mt) {
+      Q[(8 * mt + r4) * LDQ + 8 * nt + 2 * q4] = acc[mt][0];
+      Q[(8 * mt + r4) * LDQ + 8 * nt + 2 * q4 + 1] = acc[mt][1];
+    }
+  }
+  __syncthreads();
+  // ---- pass z: columns (ly, lx); R = b_B - [M_z | K_z] [Pc; Pe] ----
+  for (int nt = warp; nt < NTZ; nt += NW) {
+    double a0 = 0.0, a1 = 0.0;
+    const int col = 8 * nt + r4, ly = col / S, lx = col - ly * S;
+    const bool okc = col < S2;
+#pragma unroll
+    for (int kt = 0; kt < KZ; ++kt) {
+      const int r = 4 * kt + q4;
+      const bool second = r >= WN4;
+      const int rr = second ? r - WN4 : r;
+      const double bv = (okc && rr < Wn) ? Q[((second ? S : 0) + ly) * LDQ + rr * S + lx] : 0.0;
+      dmma(a0, a1, azf[kt], bv);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int cc = 8 * nt + 2 * q4 + i;
+      if (r4 < S && cc < S2) R[r4 * S2 + cc] = Bb[r4 * S2 + cc] - (i ? a1 : a0);
+    }
+  }
+  __syncthreads();
+  // ---- FD: six contractions out[C(i,j)] = Σ_l in[A(i,l)] B[l][j] (rows i in [0, S^2)) ----
+  const double *lx_ = lamt + (int64_t)cx * S, *ly_ = lamt + (int64_t)cy * S, *lz_ = lamt + (int64_t)cz * S;
+  fd3_step<S, KF, MF, NW, 0>(R, T, vf[0], lx_, ly_, lz_);   // x forward: rows (z,y)
+  fd3_step<S, KF, MF, NW, 1>(T, R, vf[1], lx_, ly_, lz_);   // y forward: rows (z,x)
+  fd3_step<S, KF, MF, NW, 2>(R, T, vf[2], lx_, ly_, lz_);   // z forward, / (λx + λy + λz): rows (k,j)
+  fd3_step<S, KF, MF, NW, 3>(T, R, vf[3], lx_, ly_, lz_);   // z back: rows (k,j)
+  fd3_step<S, KF, MF, NW, 4>(R, T, vf[4], lx_, ly_, lz_);   // y back: rows (z,j)
+  fd3_step<S, KF, MF, NW, 5>(T, R, vf[5], lx_, ly_, lz_);   // x back: rows (z,y)
+  // ---- x_B += δ ----
+  for (int i = threadIdx.x; i < S3; i += NW * 32) {
+    const int lx = i % S, ly = (i / S) % S, lz = i / S2;
+    const int gx = bx + lx, gy = by + ly, gz = bz + lz;
+    if (unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un)
+      x[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx] = X[((lz + P) * Wn + ly + P) * LDX + lx + P] + R[i];
+  }
+}
+
+template <int P, int S, int NW>
+bool try_schwarz3d_mma(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
+                       const double *b, double *x, int c0, int c1, int c2, int D, int nb0, int nb1, int nb2, int zoff,
+                       cudaStream_t st) {
+  if (p != P || s != S) return false;
+  constexpr size_t sm = sizeof(double) * Mma3<P, S>::SM;
+  ensure_smem(k_schwarz3d_mma<P, S, NW>, sm);
+  k_schwarz3d_mma<P, S, NW><<<unsigned(nb0) * unsigned(nb1) * unsigned(nb2), NW * 32, sm, st>>>(
+      int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, zoff);
+  return true;
+}
+
 }  // namespace
 
 bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M, const double *V,
@@ -2469,6 +2696,15 @@ bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double 
     const int m = int(n1) - p + 2;
     const int tlo = 2 * p - 1, thi = m - 2 - p;            // translation-invariant rows (toeplitz_rows)
     const int z = sv.zoff;
+    const char *v3 = std::getenv("IGA2L_S3D_MMA");    // 3D block solves on DMMA: opt-in (measured 2x slower
+    if ((v3 && v3[0] == '1') &&                        // than the DFMA pencil kernel)
+        (try_schwarz3d_mma<1, 3, 4>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, st) ||
+         try_schwarz3d_mma<2, 3, 4>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, st) ||
+         try_schwarz3d_mma<3, 3, 4>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, st) ||
+         try_schwarz3d_mma<4, 3, 4>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, st) ||
+         try_schwarz3d_mma<5, 5, 8>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, st) ||
+         try_schwarz3d_mma<6, 5, 8>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, st)))
+      return true;
     return try_schwarz3d<1, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st) ||
            try_schwarz3d<2, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st) ||
            try_schwarz3d<3, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st) ||

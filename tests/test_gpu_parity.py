@@ -340,3 +340,16 @@ def test_temporal_blocking_bitwise(p, s, m, kc, monkeypatch):
     monkeypatch.setenv("IGA2L_TB", "0")
     ref.sweep(b, x2, 1, 6)
     assert torch.equal(x1, x2)
+
+
+# ---- 3D block-solve variants (opt-in DMMA kernel, DFMA default) against the oracle ----
+@pytest.mark.parametrize("cfg", [c for c in PAR if c[1] == 3], ids=[c[0] for c in PAR if c[1] == 3])
+def test_sweep3d_dmma_matches_oracle(cfg, monkeypatch):
+    name, d, p, q, m, s, coarse, hf = cfg
+    monkeypatch.setenv("IGA2L_S3D_MMA", "1")
+    ctx = make_ctx(d, p, q, m, s, coarse, hf)
+    ora = oracle_for(*cfg)
+    b, x0 = random_rhs(ctx.N), initial_guess(ctx.N)
+    xg = cu(x0)
+    ctx.sweep(cu(b), xg)
+    close(host(xg), ora.smoother.sweep(x0.copy(), b), 1e-11)
