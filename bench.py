@@ -82,9 +82,24 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def make_ctx(pkg, torch, p, stream):
-    s = 3 if p <= 4 else 5
-    return pkg.Context(2, p, 1, 256, s, coarse_mode=pkg.COARSE_VCYCLE, coarse_h_factor=2, stream=stream)
+# --config: the BASELINE.json configuration timed (default C2, the one the metric is quoted on; the
+# others are the parity configs, measured with the same protocol for DESIGN.md's tables)
+CONFIG_PROBLEMS = {"C1": ["C1"], "C2": ["C2p3", "C2p4", "C2p5"], "C3": ["C3"], "C4": ["C4"], "C5": ["C5"]}
+CONFIG_TEXT = {
+    "C1": "C1: 2D Poisson, p=2, 16x16 elements, q=1 exact coarse at h, fp64",
+    "C2": WORKLOAD,
+    "C3": "C3: 2D Poisson, p=8, 1024x1024 elements, q=2 V(1,1) at H=2h, fp64",
+    "C4": "C4: 3D Poisson, p=3, 128^3 elements, q=1 V(1,1) at H=2h, fp64",
+    "C5": "C5: 3D Poisson, p=5, 256^3 elements, q=2 V(1,1) at H=2h, fp64",
+}
+
+
+def make_ctx(pkg, name, stream):
+    from synthetic_inputs import CONFIGS
+    c = CONFIGS[name]
+    return pkg.Context(c["d"], c["p"], c["q"], c["m"], c["s"],
+                       coarse_mode=pkg.COARSE_EXACT if c["coarse"] == "exact" else pkg.COARSE_VCYCLE,
+                       coarse_h_factor=c["h_factor"], stream=stream)
 
 
 def cpu_baseline_sample(p=3, colours_timed=2):
@@ -151,6 +166,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIG_PROBLEMS))
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -174,10 +190,12 @@ def main():
     # the three problems of the workload are independent: each context runs on its own stream and a
     # step forks them from the main stream and joins them back (events), so their latency-bound
     # kernels overlap on the GPU
-    side = [torch.cuda.Stream(dev) for _ in PS]
+    probs = CONFIG_PROBLEMS[args.config]
+    PSn = [int(__import__("synthetic_inputs").CONFIGS[n]["p"]) for n in probs]
+    side = [torch.cuda.Stream(dev) for _ in probs]
     ctxs, bs, xs, Ns = [], [], [], []
-    for p, s_ in zip(PS, side):
-        c = make_ctx(pkg, torch, p, s_.cuda_stream)
+    for name, s_ in zip(probs, side):
+        c = make_ctx(pkg, name, s_.cuda_stream)
         b = torch.empty(c.N, dtype=torch.float64, device=dev)
         x = torch.tensor(initial_guess(c.N), device=dev)
         torch.cuda.synchronize()
@@ -188,7 +206,7 @@ def main():
     torch.cuda.synchronize()
     info = [c.info() for c in ctxs]
     fork = torch.cuda.Event()
-    joins = [torch.cuda.Event() for _ in PS]
+    joins = [torch.cuda.Event() for _ in probs]
 
     def on_side(i, fn):
         """Run fn() (library calls on side stream i) ordered after / before the main stream."""
@@ -236,7 +254,7 @@ def main():
 
     # per-p iteration rate (same protocol, each problem alone)
     per_p = {}
-    for i, (p, c, b, x) in enumerate(zip(PS, ctxs, bs, xs)):
+    for i, (p, c, b, x) in enumerate(zip(PSn, ctxs, bs, xs)):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = max(args.steps, 5)
         ms = 0.0
@@ -274,16 +292,25 @@ def main():
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / DMMA_PEAK_TFLOPS, "traffic": traffic,
-                "kernel": "k_schwarz2d_mma (FP64 DMMA block solves, one launch per colour)",
-                "peak_source": "measured FP64 DMMA peak, tools/microbench.cu (profiles/microbench_r01.txt)",
-                "note": "C2 is latency bound (36/49/100 dependent colours of ~1.3k blocks); "
-                        f"achieved = SURVEY 8(d) sweep flops / CUDA-event sweep time over {sw_launches} launches"}
+    dim = ctxs[0].dim
+    if dim == 2:
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": achieved / DMMA_PEAK_TFLOPS, "traffic": traffic,
+                    "kernel": "k_schwarz2d_mma (FP64 DMMA block solves, one launch per colour)",
+                    "peak_source": "measured FP64 DMMA peak, tools/microbench.cu (profiles/microbench_r01.txt)",
+                    "note": ("C2 is latency bound (36/49/100 dependent colours of ~0.7-1.8k blocks); " if args.config == "C2"
+                             else "") +
+                            f"achieved = SURVEY 8(d) sweep flops / CUDA-event sweep time over {sw_launches} launches"}
+    else:
+        roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                    "kernel": "k_schwarz3d_t (FP64 FMA pencil block solves, one launch per colour)",
+                    "peak_source": "derived 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md)",
+                    "note": f"achieved = SURVEY 8(d) sweep flops / CUDA-event sweep time over {sw_launches} launches"}
 
     # convergence factor (b = 0, 20 iterations, last 10 ratios) and iterations to 1e-8
     conv = {}
-    for p, c, b in zip(PS, ctxs, bs):
+    for p, c, b in zip(PSn, ctxs, bs):
         z = torch.zeros(c.N, dtype=torch.float64, device=dev)
         x = torch.tensor(initial_guess(c.N), device=dev)
         torch.cuda.synchronize()
@@ -322,16 +349,17 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "global_batch": world * 3, "dofs": Ns,
+            "config": {"workload": CONFIG_TEXT[args.config], "global_batch": world * len(probs), "dofs": Ns,
                        "l2": "flushed before every timed step (256 MiB write)",
                        "parallelism": "replicas" if world > 1 else "single-gpu",
                        "graph": "one CUDA graph per iteration and problem",
-                       "concurrency": "the 3 independent problems (p=3,4,5) of a step run on 3 streams"},
+                       "concurrency": ("the 3 independent problems (p=3,4,5) of a step run on 3 streams"
+                                       if len(probs) > 1 else "one problem")},
             "per_p": per_p, "conv": conv, "roofline": roofline,
             "clocks": clk.summary(), "gpu_launches": launches,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "wall_s_timed": t_wall}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == "C2":
         v, t, desc = cpu_baseline_sample()
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
                                 "host_cores_available": len(os.sched_getaffinity(0))}
