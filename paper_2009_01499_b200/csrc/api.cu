@@ -50,6 +50,7 @@ struct Level {
   double *x = nullptr, *b = nullptr, *r = nullptr, *t1 = nullptr, *t2 = nullptr;
   DevBand P, PT;      // to the next coarser level: P (n x n_c), PT (n_c x n)
   double *inv = nullptr;               // dense inverse at the coarsest level
+  double *fdV = nullptr, *fdLam = nullptr;   // exact solve by Kronecker fast diagonalisation (large levels)
 };
 
 }  // namespace
@@ -189,6 +190,10 @@ void L_vcycle(iga2l_ctx *c, size_t l) {
   if (int(l) == c->l_cta && c->levdev) {   // small tail levels: the whole rest of the cycle in one CTA
     launch_vcycle_cta(c->dim, c->levdev, int(l), int(c->lev.size()), c->q, c->st);
     c->launch_counter++;
+    return;
+  }
+  if (L.fdV) {   // exact: (⊗V)(Σλ)^{-1}(⊗V)^T on the tensor pipe
+    c->launch_counter += launch_coarse_fd(c->dim, L.n, L.fdV, L.fdLam, L.b, L.x, L.t1, L.t2, c->st);
     return;
   }
   if (L.inv) {
@@ -660,8 +665,18 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
         (rc = dalloc(c, &L.t2, L.N)))
       return bail(rc);
     const bool direct = (o.coarse_mode == IGA2L_COARSE_EXACT) || ml <= o.vcycle_coarsest_m;
+    const char *fde = std::getenv("IGA2L_COARSE_FD");   // force / forbid the FD exact solve (tests)
+    const bool use_fd = direct && o.coarse_mode == IGA2L_COARSE_EXACT &&
+                        (fde ? fde[0] == '1' : L.N > 4096) && L.n <= 2048;
+    if (use_fd) {   // exact second level at any size: Kronecker fast diagonalisation (host eigensolve)
+      std::vector<double> V, lam;
+      if (!coarse_fd_tables(q, ml, V, lam)) return bail(fail(IGA2L_ENUMERIC, "coarse matrix not SPD"));
+      if ((rc = upload(c, &L.fdV, V)) || (rc = upload(c, &L.fdLam, lam))) return bail(rc);
+      c->lev.push_back(L);
+      break;
+    }
     if (direct) {
-      if (L.N > 4096) return bail(fail(IGA2L_EPARAM, "exact second level limited to 4096 unknowns in this build"));
+      if (L.N > 4096) return bail(fail(IGA2L_EPARAM, "exact second level: dense inverse limited to 4096 unknowns, FD to n <= 2048 per axis"));
       std::vector<double> inv;
       if (!dense_kron_inverse(dim, q, L.n, Kq, Mq, inv)) return bail(fail(IGA2L_ENUMERIC, "coarse matrix not SPD"));
       if ((rc = upload(c, &L.inv, inv))) return bail(rc);

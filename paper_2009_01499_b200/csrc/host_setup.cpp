@@ -424,4 +424,136 @@ bool dense_kron_inverse(int dim, int q, int n, const std::vector<double> &K, con
   return true;
 }
 
+
+// ---- symmetric eigen-decomposition for larger n (coarse-level fast diagonalisation) ----------
+// Householder tridiagonalisation, then implicit symmetric QR steps with the Wilkinson shift and
+// Givens rotations accumulated into Q (Golub & Van Loan, Matrix Computations, Alg. 8.3.1 / 8.3.2).
+// A: n x n symmetric, row-major (destroyed).  On return A = Q diag(lam) Q^T, Q row-major.
+static void sym_eigen(std::vector<double> &A, int n, std::vector<double> &Q, std::vector<double> &lam) {
+  auto a = [&](int i, int j) -> double & { return A[(size_t)i * n + j]; };
+  std::vector<double> vs((size_t)n * n, 0.0), betas(n, 0.0), v(n), pv(n), wv(n);
+  for (int k = 0; k + 2 < n; ++k) {                  // Householder: zero A[k+2:, k]
+    double sig = 0.0;
+    for (int i = k + 2; i < n; ++i) sig += a(i, k) * a(i, k);
+    const double x0 = a(k + 1, k);
+    if (sig == 0.0) { betas[k] = 0.0; continue; }
+    const double mu = std::sqrt(x0 * x0 + sig);
+    const double v0 = x0 <= 0.0 ? x0 - mu : -sig / (x0 + mu);
+    const double beta = 2.0 * v0 * v0 / (sig + v0 * v0);
+    for (int i = k + 1; i < n; ++i) v[i] = (i == k + 1) ? 1.0 : a(i, k) / v0;
+    betas[k] = beta;
+    for (int i = k + 1; i < n; ++i) vs[(size_t)k * n + i] = v[i];
+    for (int i = k + 1; i < n; ++i) {                // p = beta A v (trailing block)
+      double t = 0.0;
+      for (int j = k + 1; j < n; ++j) t += a(i, j) * v[j];
+      pv[i] = beta * t;
+    }
+    double pvv = 0.0;
+    for (int i = k + 1; i < n; ++i) pvv += pv[i] * v[i];
+    for (int i = k + 1; i < n; ++i) wv[i] = pv[i] - 0.5 * beta * pvv * v[i];
+    for (int i = k + 1; i < n; ++i)
+      for (int j = k + 1; j < n; ++j) a(i, j) -= v[i] * wv[j] + wv[i] * v[j];
+    a(k + 1, k) = a(k, k + 1) = mu;                    // P x = ||x|| e_1 (GVL house)
+    for (int i = k + 2; i < n; ++i) a(i, k) = a(k, i) = 0.0;
+  }
+  std::vector<double> d(n), e(n, 0.0);
+  for (int i = 0; i < n; ++i) d[i] = a(i, i);
+  for (int i = 0; i + 1 < n; ++i) e[i] = a(i + 1, i);
+  Q.assign((size_t)n * n, 0.0);                        // Q = H_0 H_1 ... H_{n-3}
+  for (int i = 0; i < n; ++i) Q[(size_t)i * n + i] = 1.0;
+  for (int k = n - 3; k >= 0; --k) {
+    if (betas[k] == 0.0) continue;
+    const double *vk = &vs[(size_t)k * n];
+    for (int j = k + 1; j < n; ++j) {
+      double t = 0.0;
+      for (int i = k + 1; i < n; ++i) t += vk[i] * Q[(size_t)i * n + j];
+      t *= betas[k];
+      for (int i = k + 1; i < n; ++i) Q[(size_t)i * n + j] -= t * vk[i];
+    }
+  }
+  // implicit symmetric QR on (d, e); rotations applied to the columns of Q
+  int hi = n - 1;
+  int guard = 0;
+  while (hi > 0 && guard < 100 * n) {
+    ++guard;
+    for (int i = 0; i < hi; ++i)
+      if (std::fabs(e[i]) <= 1e-16 * (std::fabs(d[i]) + std::fabs(d[i + 1]))) e[i] = 0.0;
+    if (e[hi - 1] == 0.0) { --hi; continue; }
+    int lo = hi - 1;
+    while (lo > 0 && e[lo - 1] != 0.0) --lo;
+    const double dd = 0.5 * (d[hi - 1] - d[hi]), eh = e[hi - 1];
+    const double mu = d[hi] - eh * eh / (dd + (dd >= 0 ? 1.0 : -1.0) * std::sqrt(dd * dd + eh * eh));
+    double x = d[lo] - mu, z = e[lo];
+    for (int k = lo; k < hi; ++k) {
+      double c, s_;
+      if (z == 0.0) { c = 1.0; s_ = 0.0; }
+      else if (std::fabs(z) > std::fabs(x)) { const double t = -x / z; s_ = 1.0 / std::sqrt(1.0 + t * t); c = s_ * t; }
+      else { const double t = -z / x; c = 1.0 / std::sqrt(1.0 + t * t); s_ = c * t; }
+      // rotation G = [c s; -s c] on rows/cols k, k+1 of T
+      if (k > lo) e[k - 1] = c * e[k - 1] - s_ * z;
+      const double dk = d[k], dk1 = d[k + 1], ek = e[k];
+      d[k] = c * c * dk - 2.0 * c * s_ * ek + s_ * s_ * dk1;
+      d[k + 1] = s_ * s_ * dk + 2.0 * c * s_ * ek + c * c * dk1;
+      e[k] = c * s_ * (dk - dk1) + (c * c - s_ * s_) * ek;
+      if (k + 1 < hi) { x = e[k]; z = -s_ * e[k + 1]; e[k + 1] = c * e[k + 1]; }
+      for (int i = 0; i < n; ++i) {
+        const double qk = Q[(size_t)i * n + k], qk1 = Q[(size_t)i * n + k + 1];
+        Q[(size_t)i * n + k] = c * qk - s_ * qk1;
+        Q[(size_t)i * n + k + 1] = s_ * qk + c * qk1;
+      }
+    }
+  }
+  lam = d;
+}
+
+bool coarse_fd_tables(int q, int64_t m, std::vector<double> &V, std::vector<double> &lam) {
+  // generalized problem K V = M V Λ with V^T M V = I for the constrained degree-q tables on m spans:
+  // M = L L^T, C = L^{-1} K L^{-T} = Q Λ Q^T, V = L^{-T} Q  (then A_q^{-1} = (⊗V)(Σ_a λ)^{-1}(⊗V)^T)
+  std::vector<double> Kb, Mb;
+  band_tables(q, m, Kb, Mb);
+  const int n = int(m + q - 2), W = 2 * q + 1;
+  if (n < 1) return false;
+  std::vector<double> Kd((size_t)n * n, 0.0), L((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int t = 0; t < W; ++t) {
+      const int j = i + t - q;
+      if (j < 0 || j >= n) continue;
+      Kd[(size_t)i * n + j] = Kb[(size_t)i * W + t];
+      L[(size_t)i * n + j] = Mb[(size_t)i * W + t];
+    }
+  if (!cholesky(L, n)) return false;
+  // C = L^{-1} K L^{-T}: X = L^{-1} K (forward substitution per column), C = L^{-1} X^T
+  auto fwd = [&](std::vector<double> &B) {            // B <- L^{-1} B (all columns)
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) {
+        double sacc = B[(size_t)i * n + j];
+        for (int k = std::max(0, i - q); k < i; ++k) sacc -= L[(size_t)i * n + k] * B[(size_t)k * n + j];
+        B[(size_t)i * n + j] = sacc / L[(size_t)i * n + i];
+      }
+  };
+  fwd(Kd);                                             // L^{-1} K
+  std::vector<double> C((size_t)n * n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) C[(size_t)i * n + j] = Kd[(size_t)j * n + i];   // (L^{-1} K)^T = K L^{-T}
+  fwd(C);                                              // L^{-1} K L^{-T}
+  for (int i = 0; i < n; ++i)                          // symmetrise
+    for (int j = i + 1; j < n; ++j) {
+      const double av = 0.5 * (C[(size_t)i * n + j] + C[(size_t)j * n + i]);
+      C[(size_t)i * n + j] = C[(size_t)j * n + i] = av;
+    }
+  std::vector<double> Q;
+  sym_eigen(C, n, Q, lam);
+  for (double l : lam)
+    if (!(l > 0.0)) return false;
+  // V = L^{-T} Q: back substitution with L^T (upper, bandwidth q)
+  V = Q;
+  for (int j = 0; j < n; ++j)
+    for (int i = n - 1; i >= 0; --i) {
+      double sacc = V[(size_t)i * n + j];
+      for (int k = i + 1; k <= std::min(n - 1, i + q); ++k) sacc -= L[(size_t)k * n + i] * V[(size_t)k * n + j];
+      V[(size_t)i * n + j] = sacc / L[(size_t)i * n + i];
+    }
+  return true;
+}
+
 }  // namespace iga2l

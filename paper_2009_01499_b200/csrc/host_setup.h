@@ -55,6 +55,10 @@ BandOp multiply(const BandOp &A, const BandOp &B);  // A (r x k) * B (k x c), ba
 bool fd_tables(int p, int s, int64_t n1, const std::vector<double> &K, const std::vector<double> &M,
                std::vector<double> &V, std::vector<double> &lam);
 
+// Fast diagonalisation of the degree-q level on m spans (exact coarse solve at any size, SURVEY
+// §8(f) row 1): K V = M V Λ, V^T M V = I; V row-major n x n (row = 1D index, column = eigen index).
+bool coarse_fd_tables(int q, int64_t m, std::vector<double> &V, std::vector<double> &lam);
+
 // Dense inverse of the d-dim operator Σ_a ⊗ (K on axis a, M elsewhere) from band tables of
 // degree q (bandwidth 2q+1) on n points per axis.  Returns false if not SPD.  Row-major N x N.
 bool dense_kron_inverse(int dim, int q, int n, const std::vector<double> &K, const std::vector<double> &M,

@@ -144,6 +144,15 @@ size_t vcycle_smem_bytes(const VcLayout &L);
 bool vcycle_smem_probe(int dim, int q, const VcLayout &L);   // call outside stream capture
 void launch_vcycle_smem(int dim, int q, const VcLayout &L, cudaStream_t st);
 
+// Strided batched FP64 GEMM on the tensor pipe: C[b](m,n) = Σ_k A[b](m,k) B[b](k,n).
+void launch_dgemm(const double *A, const double *B, double *C, int M, int N, int K, int batch, int64_t sAb,
+                  int64_t sAm, int64_t sAk, int64_t sBb, int64_t sBk, int64_t sBn, int64_t sCb, int64_t sCm,
+                  int64_t sCn, cudaStream_t st);
+// Exact second-level solve by Kronecker fast diagonalisation: e = (⊗V)(Σ_a λ)^{-1}(⊗V)^T d
+// (V: n x n row-major, K V = M V Λ, V^T M V = I).  t1, t2: n^dim scratch.  Returns the launch count.
+int launch_coarse_fd(int dim, int n, const double *V, const double *lam, const double *d, double *e, double *t1,
+                     double *t2, cudaStream_t st);
+
 // y += x (fixed-order sums of the slab partial coarse vectors in local multi-slab mode)
 void launch_axpy(double *y, const double *x, int64_t n, cudaStream_t st);
 

@@ -353,3 +353,41 @@ def test_sweep3d_dmma_matches_oracle(cfg, monkeypatch):
     xg = cu(x0)
     ctx.sweep(cu(b), xg)
     close(host(xg), ora.smoother.sweep(x0.copy(), b), 1e-11)
+
+
+# ---- exact second level at scale by Kronecker fast diagonalisation ----
+EXACT_FD = [("2d_p3_exact_h", 2, 3, 1, 48, 3, "exact", 1), ("2d_p5_exact_2h", 2, 5, 1, 64, 5, "exact", 2),
+            ("2d_p8_q2_exact_2h", 2, 8, 2, 40, 7, "exact", 2), ("3d_p3_exact_2h", 3, 3, 1, 16, 3, "exact", 2),
+            ("3d_p5_q2_exact_h", 3, 5, 2, 10, 5, "exact", 1)]
+
+
+@pytest.mark.parametrize("cfg", EXACT_FD, ids=[c[0] for c in EXACT_FD])
+def test_exact_coarse_fd(cfg, monkeypatch):
+    name, d, p, q, m, s, coarse, hf = cfg
+    monkeypatch.setenv("IGA2L_COARSE_FD", "1")
+    ctx = make_ctx(d, p, q, m, s, coarse, hf)
+    ora = oracle_for(*cfg)
+    dq = random_rhs(ctx.Nc, seed=4)
+    e = torch.empty(ctx.Nc, dtype=torch.float64, device=DEV)
+    ctx.coarse_solve(cu(dq), e)
+    close(host(e), ora._csolve(dq), 1e-10)
+    # the whole iteration with the exact second level
+    b, x0 = random_rhs(ctx.N), initial_guess(ctx.N)
+    xg = cu(x0)
+    ctx.iterate(cu(b), xg, iters=3)
+    xo = x0.copy()
+    for _ in range(3):
+        ora.iterate(xo, b)
+    assert np.linalg.norm(host(xg) - xo) <= 1e-10 * np.linalg.norm(xo)
+
+
+def test_exact_coarse_fd_large():
+    # C2-shaped problem with the exact second level at H = 2h (127^2 unknowns > the dense limit)
+    ctx = make_ctx(2, 3, 1, 256, 3, "exact", 2)
+    from oracle.assembly import stiffness
+    A = stiffness(1, 128, 2).tocsc()
+    import scipy.sparse.linalg as spla
+    dq = random_rhs(ctx.Nc, seed=6)
+    e = torch.empty(ctx.Nc, dtype=torch.float64, device=DEV)
+    ctx.coarse_solve(cu(dq), e)
+    close(host(e), spla.spsolve(A, dq), 1e-10)
