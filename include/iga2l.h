@@ -164,6 +164,12 @@ int iga2l_host_slab_plan(int dim, int p, int block, int64_t m, int nranks, int r
  * (n1c x n1) host matrix (h_factor 1: D^{-1} M_c; 2: P_mesh^T D^{-1} M_c). */
 int iga2l_host_restriction_1d(int p, int q, int64_t m, int h_factor, double *R);
 
+/* Host-only helper: the exact second-level solve's 1D generalised eigen-decomposition for degree q on
+ * m spans (n = m+q-2): K V = M V diag(lam), V^T M V = I.  V: host n*n doubles, row-major (row = 1D
+ * index, column = eigen index); lam: host n doubles.  Then A_q^{-1} = (⊗V) (Σ_a lam)^{-1} (⊗V)^T
+ * (SURVEY §8(f) row 1).  ENUMERIC if M or K is not SPD. */
+int iga2l_host_coarse_fd(int q, int64_t m, double *V, double *lam);
+
 int iga2l_destroy(iga2l_ctx *ctx);
 const char *iga2l_last_error(void);
 const char *iga2l_version(void);

@@ -66,6 +66,7 @@ def lib():
         "iga2l_prolong_add": (i, [vp, vp, vp]),
         "iga2l_get_info": (i, [vp, P(Info)]),
         "iga2l_host_band_tables": (i, [i, i64, vp, vp]),
+        "iga2l_host_coarse_fd": (i, [i, i64, vp, vp]),
         "iga2l_host_restriction_1d": (i, [i, i, i64, i, vp]),
         "iga2l_host_slab_plan": (i, [i, i, i, i64, i, i, vp]),
         "iga2l_nccl_unique_id": (i, [vp]),
@@ -115,6 +116,16 @@ def host_band_tables(p, m):
     M = np.zeros_like(K)
     _check(lib().iga2l_host_band_tables(p, m, _ptr(K), _ptr(M)))
     return K.reshape(n1, 2 * p + 1), M.reshape(n1, 2 * p + 1)
+
+
+def host_coarse_fd(q, m):
+    """1D generalised eigen-decomposition of the degree-q level (host-only): V (n x n), lam (n)."""
+    import numpy as np
+    n = m + q - 2
+    V = np.zeros(n * n)
+    lam = np.zeros(n)
+    _check(lib().iga2l_host_coarse_fd(q, m, _ptr(V), _ptr(lam)))
+    return V.reshape(n, n), lam
 
 
 def host_slab_plan(dim, p, block, m, nranks, rank):

@@ -1067,6 +1067,16 @@ int iga2l_host_slab_plan(int dim, int p, int block, int64_t m, int nranks, int r
   return IGA2L_OK;
 }
 
+int iga2l_host_coarse_fd(int q, int64_t m, double *V, double *lam) {
+  if (q < 1 || q > 8 || m < 1 || m + q - 2 < 1 || m + q - 2 > 4096 || !V || !lam)
+    return fail(IGA2L_EPARAM, "host_coarse_fd arguments");
+  std::vector<double> v, l;
+  if (!coarse_fd_tables(q, m, v, l)) return fail(IGA2L_ENUMERIC, "coarse matrix not SPD");
+  std::memcpy(V, v.data(), v.size() * sizeof(double));
+  std::memcpy(lam, l.data(), l.size() * sizeof(double));
+  return IGA2L_OK;
+}
+
 int iga2l_host_band_tables(int p, int64_t m, double *K, double *M) {
   if (p < 0 || p > 8 || m < 1 || m + p - 2 < 1 || !K || !M) return fail(IGA2L_EPARAM, "host_band_tables arguments");
   std::vector<double> k, mm;

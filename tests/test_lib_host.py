@@ -71,3 +71,25 @@ def test_setup_errors_without_gpu_or_bad_params():
         assert rc == pkg.ECUDA and b"no CUDA device" in L.iga2l_last_error()
         with pytest.raises(pkg.IgaError):
             pkg.Context(2, 2, 1, 16, 3)
+
+
+@pytest.mark.parametrize("q,m", [(1, 8), (1, 64), (2, 16), (2, 130)])
+def test_host_coarse_fd_diagonalises_the_oracle_matrices(q, m):
+    """The exact second-level solve's eigen-decomposition against the oracle's own
+    1D matrices: V^T M V = I, V^T K V = diag(lam), and the Kronecker inverse equals a sparse solve."""
+    import numpy as np
+    import scipy.sparse.linalg as spla
+    from oracle.assembly import matrices_1d, stiffness
+    V, lam = pkg.host_coarse_fd(q, m)
+    K, M = matrices_1d(q, m)
+    K, M = K.toarray() if hasattr(K, "toarray") else K, M.toarray() if hasattr(M, "toarray") else M
+    n = V.shape[0]
+    assert np.abs(V.T @ M @ V - np.eye(n)).max() <= 1e-12
+    assert np.abs(V.T @ K @ V - np.diag(lam)).max() <= 1e-11 * lam.max()
+    # 2D: A^{-1} d = V [(V^T D V) / (lam_j + lam_k)] V^T  (D[y][x])
+    d = np.random.default_rng(3).uniform(-1, 1, n * n)
+    D = d.reshape(n, n)
+    E = V @ ((V.T @ D @ V) / (lam[:, None] + lam[None, :])) @ V.T
+    A = stiffness(q, m, 2).tocsc()
+    ref = spla.spsolve(A, d)
+    assert np.abs(E.ravel() - ref).max() <= 1e-11 * np.abs(ref).max()
