@@ -102,59 +102,70 @@ def make_ctx(pkg, name, stream):
                        coarse_h_factor=c["h_factor"], stream=stream)
 
 
+class OracleSample:
+    """The oracle, as it stands, on a bounded sample of the workload: full-size C2 (p=3) built once
+    (assembly and the factorisations of the timed blocks are setup, not timed); one sample = the first
+    `colours_timed` of the D^2 Schwarz colours, timed and scaled to the whole sweep, plus the complete
+    defect / restriction / V(1,1) / prolongation."""
+
+    def __init__(self, p=3, colours_timed=2):
+        os.environ.setdefault("OMP_NUM_THREADS", "1")
+        from oracle.schwarz import colour_of
+        from oracle.twolevel import TwoLevel
+        from oracle.assembly import load_sine
+        from synthetic_inputs import initial_guess
+        t0 = time.perf_counter()
+        self.p, self.ct = p, colours_timed
+        self.tl = TwoLevel(2, p, 1, 256, s=3, coarse="vcycle", h_factor=2, order="multicolour")
+        self.D = self.tl.s + p
+        self.b = load_sine(p, 256, 2)
+        self.x = initial_guess(self.tl.N)
+        self.sel = [c for c in self.tl.smoother.seq if colour_of(c, self.D) < colours_timed]
+        for c in self.sel:
+            self.tl.smoother._factor(c)
+        self.setup_s = time.perf_counter() - t0
+
+    def sample(self):
+        """Returns (DOF*it/s, seconds of timed CPU work)."""
+        tl, x, b = self.tl, self.x, self.b
+        t0 = time.perf_counter()
+        tl.smoother.sweep(x, b, self.sel)
+        t_sw = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        dq = tl.R @ (b - tl.A @ x)
+        e = tl._csolve(dq)
+        x += tl.RT @ e
+        t_rest = time.perf_counter() - t0
+        t_iter = t_sw * (self.D * self.D) / self.ct + t_rest
+        return tl.N / t_iter, t_iter
+
+    def describe(self):
+        return (f"oracle (NumPy/SciPy, 1 thread) on full-size C2 p={self.p}: {self.ct}/{self.D * self.D} Schwarz "
+                f"colours timed and scaled x{self.D * self.D / self.ct:.0f}, plus full defect+restriction+V(1,1)+"
+                f"prolongation; setup ({self.setup_s:.1f} s: assembly, block factorisations) excluded")
+
+
 def cpu_baseline_sample(p=3, colours_timed=2):
-    """The oracle, as it stands, on a bounded sample of the workload: full-size C2 (p=3), the
-    first `colours_timed` of the D^2 Schwarz colours timed and scaled to the whole sweep, plus the
-    complete defect / restriction / V(1,1) / prolongation; setup (assembly, factorisations of the
-    timed blocks) excluded.  Returns (DOF*it/s, seconds of CPU work, description)."""
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    from oracle.schwarz import colour_of
-    from oracle.twolevel import TwoLevel
-    from oracle.assembly import load_sine
-    from synthetic_inputs import initial_guess
-    t_all = time.perf_counter()
-    tl = TwoLevel(2, p, 1, 256, s=3, coarse="vcycle", h_factor=2, order="multicolour")
-    D = tl.s + p
-    b = load_sine(p, 256, 2)
-    x = initial_guess(tl.N)
-    sel = [c for c in tl.smoother.seq if colour_of(c, D) < colours_timed]
-    for c in sel:                                   # factorisations = setup (not timed)
-        tl.smoother._factor(c)
-    t0 = time.perf_counter()
-    tl.smoother.sweep(x, b, sel)
-    t_sw = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    dq = tl.R @ (b - tl.A @ x)
-    e = tl._csolve(dq)
-    x += tl.RT @ e
-    t_rest = time.perf_counter() - t0
-    t_iter = t_sw * (D * D) / colours_timed + t_rest
-    desc = (f"oracle (NumPy/SciPy, 1 thread) on full-size C2 p={p}: {colours_timed}/{D*D} Schwarz colours timed "
-            f"and scaled x{D*D/colours_timed:.0f}, plus full defect+restriction+V(1,1)+prolongation; "
-            f"setup excluded; {time.perf_counter() - t_all:.1f} s wall incl. setup")
-    return tl.N / t_iter, t_iter, desc
+    o = OracleSample(p, colours_timed)
+    v, t = o.sample()
+    return v, t, o.describe()
 
 
 def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    vals = []
-    for _ in range(args.warmup if args.warmup < 1 else 0):
-        pass
-    t_cpu = 0.0
-    desc = ""
-    for k in range(max(args.steps, 1)):
-        v, t, desc = cpu_baseline_sample()
-        vals.append(v)
-        t_cpu += t
+    o = OracleSample()
+    for _ in range(args.warmup):
+        o.sample()
+    vals = [o.sample()[0] for _ in range(max(args.steps, 1))]
     value = float(np.median(vals))
-    ms = float(1e3 * 66049 / value)
+    ms = float(1e3 * o.tl.N / value)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD + " (reference arm: oracle, p=3 sample)"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+            "config": {"workload": WORKLOAD + " (reference arm: the CPU oracle, p=3 sample per step)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": o.describe()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
