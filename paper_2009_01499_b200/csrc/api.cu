@@ -156,7 +156,7 @@ bool is_device_ptr(const void *p) {
 
 // ---- launch helpers (count our kernel launches) ----
 void L_apply(iga2l_ctx *c, const double *x, const double *b, double *y, double *partial, int mode) {
-  launch_apply(c->dim, c->p, c->n1, c->K1, c->M1, x, b, y, partial, mode, c->st, nullptr);
+  launch_apply(c->dim, c->p, c->n1, c->K1, c->M1, x, b, y, partial, mode, c->st, nullptr, kFull, &c->toe);
   c->launch_counter++;
 }
 
@@ -412,7 +412,8 @@ SlabView sv_owned(const iga2l_ctx::Slab &s) { return SlabView{s.za, s.z0, s.z1};
 int S_norm(iga2l_ctx *c, bool push_hist) {
   for (size_t r = 0; r < c->slabs.size(); ++r) {
     auto &S = c->slabs[r];
-    launch_apply(c->dim, c->p, c->n1, c->K1, c->M1, S.xp, S.bp, S.rp, S.partial, 1, c->st, &S.npart, sv_owned(S));
+    launch_apply(c->dim, c->p, c->n1, c->K1, c->M1, S.xp, S.bp, S.rp, S.partial, 1, c->st, &S.npart, sv_owned(S),
+                 &c->toe);
     launch_sum_partials(S.partial, S.npart, c->normparts + r, nullptr, nullptr, 0, c->st);
     c->launch_counter += 2;
   }
@@ -451,7 +452,7 @@ int S_iteration(iga2l_ctx *c, bool with_norm) {
   const Band1D &R = c->R.b;
   const int nc = R.rows;
   for (auto &S : c->slabs) {                           // d_p = b - A x on owned planes; partial d_q
-    launch_apply(d, c->p, c->n1, c->K1, c->M1, S.xp, S.bp, S.rp, nullptr, 1, c->st, nullptr, sv_owned(S));
+    launch_apply(d, c->p, c->n1, c->K1, c->M1, S.xp, S.bp, S.rp, nullptr, 1, c->st, nullptr, sv_owned(S), &c->toe);
     c->launch_counter++;
     if (d == 2) {
       launch_tensor2d(S.rp, S.cpart, R, 0, c->st, S.z0, S.z1, S.za, 0, nc, 0);
@@ -865,7 +866,8 @@ int iga2l_apply(iga2l_ctx *c, const double *x, double *y) {
   if (c->nranks > 1) {
     if (int rc = S_scatter(c, nullptr, sx.ptr)) return rc;
     for (auto &S : c->slabs) {
-      launch_apply(c->dim, c->p, c->n1, c->K1, c->M1, S.xp, nullptr, S.rp, nullptr, 0, c->st, nullptr, sv_owned(S));
+      launch_apply(c->dim, c->p, c->n1, c->K1, c->M1, S.xp, nullptr, S.rp, nullptr, 0, c->st, nullptr, sv_owned(S),
+                   &c->toe);
       double *dst = const_cast<double *>(sy.ptr) + (c->rank < 0 ? size_t(S.z0) * c->plane : 0);
       CU(cudaMemcpyAsync(dst, S.rp + size_t(S.z0 - S.za) * c->plane, size_t(S.z1 - S.z0) * c->plane * 8,
                          cudaMemcpyDeviceToDevice, c->st));

@@ -464,6 +464,149 @@ __global__ void __launch_bounds__(A3NT) k_apply3d_s(int n1, const double *__rest
   }
 }
 
+// 3D apply v3: z-streaming with the z pass in REGISTERS.  Each thread owns two output columns
+// (lx, ly0), (lx, ly0+1); input plane gi's pass-y values c = M_y K_x X + K_y M_x X, e = M_y M_x X are
+// added into a register ring of 2p+1 partial outputs (plane loop unrolled by 2p+1, so ring slots are
+// compile-time); output plane gi - p is complete after plane gi.  Interior band rows (A27) come from
+// the kernel parameter tp (constant-bank operands); boundary rows through L1.
+template <int P>
+__device__ __forceinline__ void apl3_coef(const ToeP &tp, bool toe, const double *__restrict__ K,
+                                          const double *__restrict__ M, int row, int t, double &kc, double &mc) {
+  if (toe) { kc = tp.k[t]; mc = tp.m[t]; }
+  else { kc = __ldg(K + (int64_t)row * (2 * P + 1) + t); mc = __ldg(M + (int64_t)row * (2 * P + 1) + t); }
+}
+
+template <int P>
+__global__ void __launch_bounds__(A3NT) k_apply3d_r(int n1, const double *__restrict__ K, const double *__restrict__ M,
+                                                    const double *__restrict__ x, const double *__restrict__ b,
+                                                    double *__restrict__ y, double *__restrict__ partial, int mode,
+                                                    int zoff, int zlo0, int zhi0, int zchunk, int tlo, int thi,
+                                                    const ToeP tp) {
+  constexpr int W = 2 * P + 1, TX = A3TX, TY = A3TY, NT = A3NT, WX = TX + 2 * P, WY = TY + 2 * P, NR = W;
+  constexpr int SEG = 8;                    // pass-x outputs per task
+  extern __shared__ double sm[];
+  double *Xb = sm;                          // [2][WY][WX]
+  double *Pa = Xb + 2 * WY * WX;            // [WY][TX]  K_x X
+  double *Pb = Pa + WY * TX;                // [WY][TX]  M_x X
+  __shared__ double red[32];
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int zlo = zlo0 + blockIdx.z * zchunk, zhi = min(zhi0, zlo + zchunk);
+  if (zlo >= zhi) return;
+  const unsigned un = unsigned(n1);
+  const bool tv = tp.valid != 0;
+  const bool tx = tv && x0 >= tlo && x0 + TX - 1 <= thi, ty = tv && y0 >= tlo && y0 + TY - 1 <= thi;
+  const int lx = tid % TX, ly0 = 2 * (tid / TX);              // this thread's two output columns
+  auto stage = [&](int gi, int buf) {
+    double *dst = Xb + buf * WY * WX;
+    const bool okz = unsigned(gi) < un;
+    for (int i = tid; i < WY * WX; i += NT) {
+      const int wy = i / WX, wx = i - wy * WX, gx = x0 - P + wx, gyy = y0 - P + wy;
+      const bool ok = okz && unsigned(gx) < un && unsigned(gyy) < un;
+      cp_async8(dst + i, x + (ok ? ((int64_t)(gi - zoff) * n1 + gyy) * n1 + gx : 0), ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[NR][2];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) acc[r][0] = acc[r][1] = 0.0;
+  double sq = 0.0;
+  const int gs = zlo - P, ge = zhi + P;
+  stage(gs, 0);
+  for (int g0 = gs; g0 < ge; g0 += NR) {
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      const int gi = g0 + k;
+      if (gi >= ge) break;
+      const int buf = (gi - gs) & 1;
+      if (gi + 1 < ge) {
+        stage(gi + 1, buf ^ 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncthreads();
+      const bool okz = unsigned(gi) < un;
+      if (okz) {                                              // pass x: (row, SEG consecutive outputs)
+        const double *X = Xb + buf * WY * WX;
+        for (int task = tid; task < WY * (TX / SEG); task += NT) {
+          const int wy = task / (TX / SEG), l0 = (task - wy * (TX / SEG)) * SEG;
+          double v[SEG + 2 * P];
+#pragma unroll
+          for (int q = 0; q < SEG + 2 * P; ++q) v[q] = X[wy * WX + l0 + q];
+#pragma unroll
+          for (int i = 0; i < SEG; ++i) {
+            const int gx = x0 + l0 + i;
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int t = 0; t < W; ++t) {
+              double kc, mc;
+              apl3_coef<P>(tp, tx, K, M, min(gx, n1 - 1), t, kc, mc);
+              a0 = fma(kc, v[i + t], a0);
+              a1 = fma(mc, v[i + t], a1);
+            }
+            Pa[wy * TX + l0 + i] = gx < n1 ? a0 : 0.0;
+            Pb[wy * TX + l0 + i] = gx < n1 ? a1 : 0.0;
+          }
+        }
+      }
+      __syncthreads();
+      // pass y for the two columns, then scatter into the register ring (output go = gi + P - t)
+      double c[2] = {0.0, 0.0}, e[2] = {0.0, 0.0};
+      if (okz) {
+        double pa[2 + 2 * P], pb[2 + 2 * P];
+#pragma unroll
+        for (int u = 0; u < 2 + 2 * P; ++u) { pa[u] = Pa[(ly0 + u) * TX + lx]; pb[u] = Pb[(ly0 + u) * TX + lx]; }
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          const int gyy = y0 + ly0 + o;
+          double c1 = 0.0;
+#pragma unroll
+          for (int u = 0; u < W; ++u) {
+            double kc, mc;
+            apl3_coef<P>(tp, ty, K, M, min(gyy, n1 - 1), u, kc, mc);
+            c[o] = fma(mc, pa[o + u], c[o]);
+            c1 = fma(kc, pb[o + u], c1);
+            e[o] = fma(mc, pb[o + u], e[o]);
+          }
+          c[o] = gyy < n1 ? c[o] + c1 : 0.0;
+          e[o] = gyy < n1 ? e[o] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < W; ++t) {                           // output go = gi + P - t gets tap t
+        const int go = gi + P - t;
+        if (go < zlo || go >= zhi) continue;
+        const bool tz = tv && go >= tlo && go <= thi;
+        double kc, mc;
+        apl3_coef<P>(tp, tz, K, M, go, t, kc, mc);
+        const int slot = (k + P - t + 2 * NR) % NR;            // compile-time after unrolling
+#pragma unroll
+        for (int o = 0; o < 2; ++o) acc[slot][o] = fma(mc, c[o], fma(kc, e[o], acc[slot][o]));
+      }
+      const int go = gi - P;                                   // complete now
+      if (go >= zlo && go < zhi) {
+        const int slot = (k + P + 1) % NR;
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          const int gx = x0 + lx, gyy = y0 + ly0 + o;
+          if (gx < n1 && gyy < n1) {
+            const int64_t gg = ((int64_t)(go - zoff) * n1 + gyy) * n1 + gx;
+            const double val = mode ? b[gg] - acc[slot][o] : acc[slot][o];
+            y[gg] = val;
+            sq = fma(val, val, sq);
+          }
+          acc[slot][o] = 0.0;
+        }
+      }
+    }
+  }
+  if (partial) {
+    const double t = block_sum(sq, red);
+    if (tid == 0) partial[(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+  }
+}
+
 int apply3d_zchunks(int64_t n1, int nz) {   // z chunks: about two CTAs per SM, chunks >= 8 planes
   const int64_t tiles = ((n1 + A3TX - 1) / A3TX) * ((n1 + A3TY - 1) / A3TY);
   int ch = int(std::max<int64_t>(1, (296 + tiles - 1) / tiles));
@@ -473,14 +616,26 @@ int apply3d_zchunks(int64_t n1, int nz) {   // z chunks: about two CTAs per SM, 
 
 template <int P>
 bool try_apply3d(int p, int64_t n1, const double *K, const double *M, const double *x, const double *b, double *y,
-                 double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv) {
+                 double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv, const ToeP *tpp) {
   if (p != P) return false;
   const int nz = sv.zhi - sv.zlo;
   const int ch = apply3d_zchunks(n1, nz), zchunk = (nz + ch - 1) / ch;
   const int m = int(n1) - P + 2;
+  dim3 grid((unsigned)((n1 + A3TX - 1) / A3TX), (unsigned)((n1 + A3TY - 1) / A3TY), (unsigned)ch);
+  const char *ev = std::getenv("IGA2L_APPLY3D");   // 2 (default): shared-memory ring; 3: register z ring
+  if (ev && ev[0] == '3') {                        // (measured slower: C5 2.07 vs 1.33 ms)
+    ToeP tp{};
+    if (tpp) tp = *tpp;
+    constexpr int WX = A3TX + 2 * P, WY = A3TY + 2 * P;
+    constexpr size_t sm = sizeof(double) * (2 * WY * WX + 2 * WY * A3TX);
+    ensure_smem(k_apply3d_r<P>, sm);
+    k_apply3d_r<P><<<grid, A3NT, sm, st>>>(int(n1), K, M, x, b, y, partial, mode, sv.zoff, sv.zlo, sv.zhi, zchunk,
+                                           2 * P - 1, m - 2 - P, tp);
+    if (nparts) *nparts = int(grid.x * grid.y * grid.z);
+    return true;
+  }
   constexpr size_t sm = sizeof(double) * Apl3<P>::SM;
   ensure_smem(k_apply3d_s<P>, sm);
-  dim3 grid((unsigned)((n1 + A3TX - 1) / A3TX), (unsigned)((n1 + A3TY - 1) / A3TY), (unsigned)ch);
   k_apply3d_s<P><<<grid, A3NT, sm, st>>>(int(n1), K, M, x, b, y, partial, mode, sv.zoff, sv.zlo, sv.zhi, zchunk,
                                          2 * P - 1, m - 2 - P);
   if (nparts) *nparts = int(grid.x * grid.y * grid.z);
@@ -843,7 +998,7 @@ int apply_num_partials(int dim, int p, int64_t n1) {
 }
 
 void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, const double *x, const double *b,
-                  double *y, double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv) {
+                  double *y, double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv, const ToeP *tp) {
   if (sv.zhi < 0) sv = SlabView{0, 0, int(n1)};
   const int nz = sv.zhi - sv.zlo;
   const size_t sm = apply_smem(dim, p);
@@ -859,12 +1014,12 @@ void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, 
        try_apply2d<8>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv)))
     return;
   if (dim == 3 && g_apply_v2 &&
-      (try_apply3d<1>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
-       try_apply3d<2>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
-       try_apply3d<3>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
-       try_apply3d<4>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
-       try_apply3d<5>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
-       try_apply3d<6>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv)))
+      (try_apply3d<1>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
+       try_apply3d<2>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
+       try_apply3d<3>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
+       try_apply3d<4>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
+       try_apply3d<5>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
+       try_apply3d<6>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp)))
     return;
   if (dim == 2) {
     dim3 grid((unsigned)((n1 + A2X - 1) / A2X), (unsigned)((nz + A2Y - 1) / A2Y));
@@ -1177,15 +1332,6 @@ bool try_schwarz2d(int p, int s, int64_t n1, const double *K, const double *M, c
 // deadlock).  done[] counts colours monotonically across launches: the launch's base is ctl[0], and
 // the last CTA to finish advances it by D^2.
 constexpr int kFlagStride = 32;   // one progress counter per 128-byte line
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 template <int P, int S, int AX, int AY, int NB, int G>
 __global__ void __launch_bounds__(NB * G * 32) k_sweep2d_persist(int n1, const double *__restrict__ K,
                                                                  const double *__restrict__ M,

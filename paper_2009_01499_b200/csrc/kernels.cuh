@@ -26,13 +26,6 @@ struct SlabView {
 constexpr SlabView kFull{0, 0, -1};
 void centre_range(int c, int D, int lo, int hi, int *first, int *count);
 
-// ---- fine operator: apply / residual -------------------------------------------------------
-// mode 0: y = A x;  mode 1: y = b - A x.  If partial != nullptr, partial[cta] = Σ y^2 over the tile.
-void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, const double *x,
-                  const double *b, double *y, double *partial, int mode, cudaStream_t st, int *nparts,
-                  SlabView sv = kFull);
-int apply_num_partials(int dim, int p, int64_t n1);
-
 // Interior (translation-invariant) 1D data of the fine level (reading A27), passed BY VALUE as a
 // kernel parameter: with compile-time indices the FMAs read it as constant-bank operands.
 constexpr int kToeMaxW = 17, kToeMaxS = 7;
@@ -41,6 +34,13 @@ struct ToeP {
   double v[kToeMaxS * kToeMaxS], lam[kToeMaxS];   // FD tables of an interior block (V[l][j], λ_j)
   int valid;                                 // 0: no interior rows (small grids)
 };
+
+// ---- fine operator: apply / residual -------------------------------------------------------
+// mode 0: y = A x;  mode 1: y = b - A x.  If partial != nullptr, partial[cta] = Σ y^2 over the tile.
+void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, const double *x,
+                  const double *b, double *y, double *partial, int mode, cudaStream_t st, int *nparts,
+                  SlabView sv = kFull, const ToeP *tp = nullptr);
+int apply_num_partials(int dim, int p, int64_t n1);
 
 // ---- multicolour Schwarz: one colour ---------------------------------------------------------
 // Blocks centred at c = col + D*j (per axis) are solved in parallel (A-decoupled, reading A4):
