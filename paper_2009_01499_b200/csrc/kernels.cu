@@ -2572,15 +2572,25 @@ __global__ void __launch_bounds__(WPC * 32) k_schwarz2d_tb(int n1, const double 
   }
 }
 
-template <int P, int S>
-bool try_schwarz2d_mma(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
-                       const double *b, double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st) {
-  if (p != P || s != S) return false;
-  constexpr int WPC = 4;
+template <int P, int S, int WPC>
+void launch2d_mma(int64_t n1, const double *K, const double *M, const double *V, const double *lam, const double *b,
+                  double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st) {
   constexpr size_t sm = sizeof(double) * WPC * Mma2<P, S>::PER;
   ensure_smem(k_schwarz2d_mma<P, S, WPC>, sm);
   k_schwarz2d_mma<P, S, WPC><<<(nblk + WPC - 1) / WPC, WPC * 32, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, D,
                                                                            nb0, nblk, zoff);
+}
+
+template <int P, int S>
+bool try_schwarz2d_mma(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
+                       const double *b, double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st) {
+  if (p != P || s != S) return false;
+  const char *e = std::getenv("IGA2L_MMA_WPC");   // warps (blocks) per CTA; measured best (variants_wpc_r01):
+  const int wpc = e ? std::atoi(e) : (S >= 5 ? 1 : 4);   // 1 for s >= 5 (C2 p5, C3), 4 for s = 3
+  if (wpc == 1) launch2d_mma<P, S, 1>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st);
+  else if (wpc == 2) launch2d_mma<P, S, 2>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st);
+  else if (wpc == 8) launch2d_mma<P, S, 8>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st);
+  else launch2d_mma<P, S, 4>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st);
   return true;
 }
 
