@@ -192,7 +192,8 @@ struct Apl2 {
 };
 
 template <int P, int AT, bool TOE>
-__device__ __forceinline__ void apl_row(const double *xr, const double *ck, const double *cm, double *ok_, double *om_) {
+__device__ __forceinline__ void apl_row(const double *xr, const double *ck, const double *cm, double *ok_, double *om_,
+                                        const ToeP &tp) {
   constexpr int W = 2 * P + 1, ARX = Apl2<P, AT>::ARX;
   double v[ARX + 2 * P];
 #pragma unroll
@@ -202,7 +203,7 @@ __device__ __forceinline__ void apl_row(const double *xr, const double *ck, cons
     double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
 #pragma unroll
     for (int t = 0; t < W; ++t) {
-      const double kc = TOE ? ck[t] : ck[i * W + t], mc = TOE ? cm[t] : cm[i * W + t];
+      const double kc = TOE ? tp.k[t] : ck[i * W + t], mc = TOE ? tp.m[t] : cm[i * W + t];
       if (t & 1) { a1 = fma(kc, v[i + t], a1); b1 = fma(mc, v[i + t], b1); }
       else { a0 = fma(kc, v[i + t], a0); b0 = fma(mc, v[i + t], b0); }
     }
@@ -213,7 +214,7 @@ __device__ __forceinline__ void apl_row(const double *xr, const double *ck, cons
 
 template <int P, int AT, bool TOE>
 __device__ __forceinline__ void apl_col(const double *tk, const double *tm, const double *ck, const double *cm,
-                                        double *out) {
+                                        double *out, const ToeP &tp) {
   constexpr int W = 2 * P + 1;
   double a[ARY + 2 * P], c[ARY + 2 * P];
 #pragma unroll
@@ -223,7 +224,7 @@ __device__ __forceinline__ void apl_col(const double *tk, const double *tm, cons
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll
     for (int u = 0; u < W; ++u) {
-      const double kc = TOE ? ck[u] : ck[i * W + u], mc = TOE ? cm[u] : cm[i * W + u];
+      const double kc = TOE ? tp.k[u] : ck[i * W + u], mc = TOE ? tp.m[u] : cm[i * W + u];
       s0 = fma(mc, a[i + u], s0);      // M_y (K_x X)
       s1 = fma(kc, c[i + u], s1);      // K_y (M_x X)
     }
@@ -235,7 +236,7 @@ template <int P, int AT>
 __global__ void __launch_bounds__(AT * AT / ARY, 2) k_apply2d_t(int n1, const double *__restrict__ K, const double *__restrict__ M,
                                                    const double *__restrict__ x, const double *__restrict__ b,
                                                    double *__restrict__ y, double *__restrict__ partial, int mode,
-                                                   int zoff, int zlo, int zhi, int tlo, int thi) {
+                                                   int zoff, int zlo, int zhi, int tlo, int thi, const ToeP tp) {
   using A = Apl2<P, AT>;
   constexpr int NT = AT * AT / ARY;
   constexpr int W = A::W, WN = A::WN, ARX = A::ARX;
@@ -254,24 +255,28 @@ __global__ void __launch_bounds__(AT * AT / ARY, 2) k_apply2d_t(int n1, const do
     const bool ok = unsigned(gx) < un && unsigned(gy) < un;
     cp_async8(X + i, x + (ok ? (int64_t)(gy - zoff) * n1 + gx : 0), ok);
   }
-  for (int i = tid; i < AT * W; i += NT) {
+  const bool tx = tp.valid && x0 >= tlo && x0 + AT - 1 <= thi, ty = tp.valid && y0 >= tlo && y0 + AT - 1 <= thi;
+  for (int i = tid; i < AT * W; i += NT) {   // band rows of boundary tiles only (interior: tp, A27)
     const int l = i / W, t = i - l * W;
     const int gx = x0 + l, gy = y0 + l;
     const bool okx = unsigned(gx) < un, oky = gy < zhi && unsigned(gy) < un;
-    cp_async8(Kx + i, K + (okx ? (int64_t)gx * W + t : 0), okx);
-    cp_async8(Mx + i, M + (okx ? (int64_t)gx * W + t : 0), okx);
-    cp_async8(Ky + i, K + (oky ? (int64_t)gy * W + t : 0), oky);
-    cp_async8(My + i, M + (oky ? (int64_t)gy * W + t : 0), oky);
+    if (!tx) {
+      cp_async8(Kx + i, K + (okx ? (int64_t)gx * W + t : 0), okx);
+      cp_async8(Mx + i, M + (okx ? (int64_t)gx * W + t : 0), okx);
+    }
+    if (!ty) {
+      cp_async8(Ky + i, K + (oky ? (int64_t)gy * W + t : 0), oky);
+      cp_async8(My + i, M + (oky ? (int64_t)gy * W + t : 0), oky);
+    }
   }
   cp_async_wait_all();
   __syncthreads();
-  const bool tx = x0 >= tlo && x0 + AT - 1 <= thi, ty = y0 >= tlo && y0 + AT - 1 <= thi;
   // pass x: rows wy of the window, segments of ARX outputs
   for (int task = tid; task < WN * (AT / ARX); task += NT) {
     const int wy = task / (AT / ARX), sg = task - wy * (AT / ARX);
     double ok_[ARX], om_[ARX];
-    if (tx) apl_row<P, AT, true>(X + wy * WN + sg * ARX, Kx, Mx, ok_, om_);
-    else apl_row<P, AT, false>(X + wy * WN + sg * ARX, Kx + sg * ARX * W, Mx + sg * ARX * W, ok_, om_);
+    if (tx) apl_row<P, AT, true>(X + wy * WN + sg * ARX, Kx, Mx, ok_, om_, tp);
+    else apl_row<P, AT, false>(X + wy * WN + sg * ARX, Kx + sg * ARX * W, Mx + sg * ARX * W, ok_, om_, tp);
 #pragma unroll
     for (int i = 0; i < ARX; ++i) {
       Tk[wy * AT + sg * ARX + i] = ok_[i];
@@ -284,8 +289,8 @@ __global__ void __launch_bounds__(AT * AT / ARY, 2) k_apply2d_t(int n1, const do
   {
     const int lx = tid % AT, sg = tid / AT;   // NT tasks = AT columns x AT/ARY segments
     double out[ARY];
-    if (ty) apl_col<P, AT, true>(Tk + sg * ARY * AT + lx, Tm + sg * ARY * AT + lx, Ky, My, out);
-    else apl_col<P, AT, false>(Tk + sg * ARY * AT + lx, Tm + sg * ARY * AT + lx, Ky + sg * ARY * W, My + sg * ARY * W, out);
+    if (ty) apl_col<P, AT, true>(Tk + sg * ARY * AT + lx, Tm + sg * ARY * AT + lx, Ky, My, out, tp);
+    else apl_col<P, AT, false>(Tk + sg * ARY * AT + lx, Tm + sg * ARY * AT + lx, Ky + sg * ARY * W, My + sg * ARY * W, out, tp);
     const int gx = x0 + lx;
 #pragma unroll
     for (int i = 0; i < ARY; ++i) {
@@ -306,15 +311,17 @@ __global__ void __launch_bounds__(AT * AT / ARY, 2) k_apply2d_t(int n1, const do
 
 template <int P>
 bool try_apply2d(int p, int64_t n1, const double *K, const double *M, const double *x, const double *b, double *y,
-                 double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv) {
+                 double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv, const ToeP *tpp) {
   if (p != P) return false;
+  ToeP tp{};
+  if (tpp) tp = *tpp;
   const int nz = sv.zhi - sv.zlo;
   const int m = int(n1) - P + 2;
   auto go = [&](auto kern, int at, size_t sm) {
     ensure_smem(kern, sm);
     dim3 grid((unsigned)((n1 + at - 1) / at), (unsigned)((nz + at - 1) / at));
     kern<<<grid, at * at / ARY, sm, st>>>(int(n1), K, M, x, b, y, partial, mode, sv.zoff, sv.zlo, sv.zhi, 2 * P - 1,
-                                          m - 2 - P);
+                                          m - 2 - P, tp);
     if (nparts) *nparts = int(grid.x * grid.y);
   };
   // 32x32 tiles; 16x16 when that would leave fewer than two CTAs per SM
@@ -1004,14 +1011,14 @@ void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, 
   const size_t sm = apply_smem(dim, p);
   if (nz <= 0) return;
   if (dim == 2 && g_apply_v2 &&
-      (try_apply2d<1>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
-       try_apply2d<2>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
-       try_apply2d<3>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
-       try_apply2d<4>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
-       try_apply2d<5>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
-       try_apply2d<6>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
-       try_apply2d<7>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv) ||
-       try_apply2d<8>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv)))
+      (try_apply2d<1>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
+       try_apply2d<2>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
+       try_apply2d<3>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
+       try_apply2d<4>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
+       try_apply2d<5>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
+       try_apply2d<6>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
+       try_apply2d<7>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
+       try_apply2d<8>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp)))
     return;
   if (dim == 3 && g_apply_v2 &&
       (try_apply3d<1>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
