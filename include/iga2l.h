@@ -50,7 +50,8 @@ typedef enum {
 } iga2l_status;
 
 typedef enum {
-  IGA2L_COARSE_EXACT = 0,  /* A_q e = d_q solved exactly (dense Cholesky inverse; Nc <= 4096)  */
+  IGA2L_COARSE_EXACT = 0,  /* A_q e = d_q solved exactly: dense inverse (Nc <= 4096) or, above,  */
+                           /* Kronecker fast diagonalisation (⊗V)(Σλ)^{-1}(⊗V)^T, n <= 2048/axis */
   IGA2L_COARSE_VCYCLE = 1  /* one V(1,1) h-multigrid cycle, zero initial guess     */
 } iga2l_coarse_mode;
 

@@ -2579,6 +2579,77 @@ __global__ void __launch_bounds__(WPC * 32) k_schwarz2d_tb(int n1, const double 
   }
 }
 
+// Several blocks per warp (BPW consecutive blocks of the colour): interior fragments (A27) built once
+// per warp, the next block's window prefetched by cp.async into the second buffer while this one is
+// solved.  Same arithmetic as k_schwarz2d_mma (bitwise equal).
+template <int P, int S, int WPC, int BPW>
+__global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma_m(int n1, const double *__restrict__ K,
+                                                              const double *__restrict__ M,
+                                                              const double *__restrict__ Vt,
+                                                              const double *__restrict__ lamt,
+                                                              const double *__restrict__ b, double *__restrict__ x,
+                                                              int c0, int c1, int D, int nb0, int nblk, int zoff,
+                                                              int tlo, int thi, int cref) {
+  using G = Mma2<P, S>;
+  constexpr int Wn = G::Wn, w = G::w, MT = G::MT, WN4 = G::WN4, LDX = G::LDX, LDP = G::LDP;
+  constexpr int XSZ = MT * 8 * LDX;
+  extern __shared__ double sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b0 = (blockIdx.x * WPC + warp) * BPW;
+  if (b0 >= nblk) return;
+  double *Xs = sm + warp * (2 * XSZ + MT * 8 * LDP), *Pab = Xs + 2 * XSZ;
+  const unsigned un = unsigned(n1);
+  auto centre = [&](int bid, int *cx, int *cy) {
+    const int j1 = bid / nb0, j0 = bid - j1 * nb0;
+    *cx = c0 + D * j0;
+    *cy = c1 + D * j1;
+  };
+  auto stage = [&](int bid, double *X) {
+    int cx, cy;
+    centre(bid, &cx, &cy);
+    const int ox = cx - w - P, oy = cy - w - P;
+    for (int row = 0; row < MT * 8; ++row) {
+      const int gy = oy + row;
+      const bool oky = row < Wn && unsigned(gy) < un;
+      const double *src = x + (oky ? (int64_t)(gy - zoff) * n1 : 0);
+#pragma unroll
+      for (int cc = lane; cc < WN4; cc += 32) {
+        const int gx = ox + cc;
+        const bool ok = oky && cc < Wn && unsigned(gx) < un;
+        cp_async8(X + row * LDX + cc, ok ? src + gx : x, ok);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  FragX<P, S> fxi;
+  FragY<P, S> fyi;
+  if (cref >= 0) {
+    build_fragx<P, S>(fxi, n1, cref, K, M, Vt, lamt);
+    build_fragy<P, S>(fyi, n1, cref, K, M, Vt, lamt);
+  }
+  const int nb = min(BPW, nblk - b0);
+  stage(b0, Xs);
+  for (int j = 0; j < nb; ++j) {
+    double *X = Xs + (j & 1) * XSZ;
+    if (j + 1 < nb) {
+      stage(b0 + j + 1, Xs + ((j + 1) & 1) * XSZ);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncwarp();
+    int cx, cy;
+    centre(b0 + j, &cx, &cy);
+    const int bx = cx - w, by = cy - w;
+    auto put = [&](int ly, int lx, double v) { x[(int64_t)(by + ly - zoff) * n1 + bx + lx] = v; };
+    if (cref >= 0 && cx - w >= tlo && cx + w <= thi && cy - w >= tlo && cy + w <= thi)
+      mma_block_f<P, S>(X, LDX, Pab, n1, cx, cy, fxi, fyi, b, zoff, put);
+    else
+      mma_block<P, S>(X, LDX, Pab, n1, cx, cy, K, M, Vt, lamt, b, zoff, put);
+    __syncwarp();
+  }
+}
+
 template <int P, int S, int WPC>
 void launch2d_mma(int64_t n1, const double *K, const double *M, const double *V, const double *lam, const double *b,
                   double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st) {
@@ -2592,6 +2663,24 @@ template <int P, int S>
 bool try_schwarz2d_mma(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
                        const double *b, double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st) {
   if (p != P || s != S) return false;
+  const char *eb = std::getenv("IGA2L_MMA_BPW");   // blocks per warp (> 1: prefetching multi-block warps)
+  const int bpw = eb ? std::atoi(eb) : 1;
+  if (bpw > 1) {
+    const int m = int(n1) - P + 2, tlo = 2 * P - 1, thi = m - 2 - P, w = (S - 1) / 2;
+    const int cref = (thi - tlo >= 2 * w) ? (tlo + thi) / 2 : -1;
+    constexpr int WPCm = 4;
+    constexpr size_t sm = sizeof(double) * WPCm * (2 * Mma2<P, S>::MT * 8 * Mma2<P, S>::LDX + Mma2<P, S>::MT * 8 * Mma2<P, S>::LDP);
+    auto go = [&](auto kern, int B) {
+      ensure_smem(kern, sm);
+      const int nw = (nblk + B - 1) / B;
+      kern<<<(nw + WPCm - 1) / WPCm, WPCm * 32, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, tlo,
+                                                          thi, cref);
+    };
+    if (bpw == 2) go(k_schwarz2d_mma_m<P, S, WPCm, 2>, 2);
+    else if (bpw == 4) go(k_schwarz2d_mma_m<P, S, WPCm, 4>, 4);
+    else go(k_schwarz2d_mma_m<P, S, WPCm, 8>, 8);
+    return true;
+  }
   const char *e = std::getenv("IGA2L_MMA_WPC");   // warps (blocks) per CTA; measured best (variants_wpc_r01):
   const int wpc = e ? std::atoi(e) : (S >= 5 ? 1 : 4);   // 1 for s >= 5 (C2 p5, C3), 4 for s = 3
   if (wpc == 1) launch2d_mma<P, S, 1>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st);

@@ -391,3 +391,18 @@ def test_exact_coarse_fd_large():
     e = torch.empty(ctx.Nc, dtype=torch.float64, device=DEV)
     ctx.coarse_solve(cu(dq), e)
     close(host(e), spla.spsolve(A, dq), 1e-10)
+
+
+@pytest.mark.parametrize("bpw", ["2", "4", "8"])
+@pytest.mark.parametrize("p,s,m", [(3, 3, 96), (5, 5, 96), (8, 7, 96)], ids=["p3", "p5", "p8"])
+def test_multiblock_warps_bitwise(p, s, m, bpw, monkeypatch):
+    """Several blocks per warp with prefetch (IGA2L_MMA_BPW) == one block per warp, bitwise."""
+    monkeypatch.setenv("IGA2L_MMA_BPW", "1")
+    ref = make_ctx(2, p, 1, m, s, "vcycle", 2)
+    ctx = make_ctx(2, p, 1, m, s, "vcycle", 2)
+    b, x0 = cu(random_rhs(ctx.N)), cu(initial_guess(ctx.N))
+    x1, x2 = x0.clone(), x0.clone()
+    ref.sweep(b, x1)
+    monkeypatch.setenv("IGA2L_MMA_BPW", bpw)
+    ctx.sweep(b, x2)
+    assert torch.equal(x1, x2)
