@@ -1486,6 +1486,7 @@ __global__ void k_tensor2d(const double *__restrict__ in, double *__restrict__ o
 // acquire at cluster scope; it also invalidates L1, so plain loads see the other SMs' stores).
 // Each CTA stages the current level's 1D band tables K_q, M_q in shared memory.
 __device__ unsigned long long *g_vc_trace = nullptr;   // optional phase timestamps (debug builds)
+__device__ long long g_s2d_trace[8];                     // DMMA colour kernel phase clocks (IGA2L_TRACE builds)
 __device__ int g_vc_trace_n = 0;
 
 struct Team {
@@ -1814,7 +1815,26 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
     const bool ok = unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un;
     cp_async8(Bb(k) + r, b + (ok ? ((int64_t)(gz - zoff) * n1 + gy) * n1 + gx : 0), ok);
   }
-  if (!ROW) {                                       // x windows, element by element
+  if (!ROW && NBK == 1 && Wn2 * Wn <= 1024) {      // x window through registers, in batches of 16 loads
+                                                   // (measured: C4 40.6 -> 36.6 us/colour; C5 slower)
+    constexpr int TOT = Wn2 * Wn, BATCH = 16;      // (8-byte cp.async issue costs ~95 cycles each)
+    const int ox = centre(0, 0) - w - P, oy = centre(0, 1) - w - P, oz = centre(0, 2) - w - P;
+    for (int i0 = 0; i0 < TOT; i0 += NT * BATCH) {
+      double v[BATCH];
+#pragma unroll
+      for (int k = 0; k < BATCH; ++k) {
+        const int r = i0 + tid + k * NT;
+        const int gx = ox + r % Wn, gy = oy + (r / Wn) % Wn, gz = oz + r / Wn2;
+        const bool ok = r < TOT && unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un;
+        v[k] = ok ? x[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < BATCH; ++k) {
+        const int r = i0 + tid + k * NT;
+        if (r < TOT) X(0)[r] = v[k];
+      }
+    }
+  } else if (!ROW) {                               // x windows, element by element
     for (int i = tid; i < nk * Wn2 * Wn; i += NT) {
       const int k = NBK == 1 ? 0 : i / (Wn2 * Wn), r = NBK == 1 ? i : i % (Wn2 * Wn);
       const int gx = centre(k, 0) - w - P + r % Wn, gy = centre(k, 1) - w - P + (r / Wn) % Wn,
@@ -2491,22 +2511,49 @@ __global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma(int n1, const double
   const int cx = c0 + D * j0, cy = c1 + D * j1;
   const int bx = cx - w, by = cy - w, ox = bx - P, oy = by - P;
   const unsigned un = unsigned(n1);
-  for (int row = 0; row < MT * 8; ++row) {                   // zero-padded window, asynchronously
-    const int gy = oy + row;
-    const bool oky = row < Wn && unsigned(gy) < un;
-    const double *src = x + (oky ? (int64_t)(gy - zoff) * n1 : 0);
+#ifdef IGA2L_TRACE
+  const bool tr = (bid == 0 && lane == 0);
+  long long t0 = clock64();
+#endif
+  // zero-padded window through registers: every lane issues all its loads back to back, then stores
+  // (measured: 8-byte cp.async copies cost ~95 issue cycles per window row, 1.2-3k cycles per block)
+  constexpr int WT = MT * 8 * WN4, WI = (WT + 31) / 32;
+  double wv[WI];
 #pragma unroll
-    for (int cc = lane; cc < WN4; cc += 32) {
-      const int gx = ox + cc;
-      const bool ok = oky && cc < Wn && unsigned(gx) < un;
-      cp_async8(X + row * LDX + cc, ok ? src + gx : x, ok);
-    }
+  for (int k = 0; k < WI; ++k) {
+    const int i = lane + 32 * k, row = i / WN4, cc = i - row * WN4;
+    const int gx = ox + cc, gy = oy + row;
+    const bool ok = i < WT && row < Wn && cc < Wn && unsigned(gx) < un && unsigned(gy) < un;
+    wv[k] = ok ? x[(int64_t)(gy - zoff) * n1 + gx] : 0.0;
   }
-  cp_async_wait_all();
+#ifdef IGA2L_TRACE
+  long long t1 = clock64();
+#endif
+  FragX<P, S> fx;
+  FragY<P, S> fy;
+  build_fragx<P, S>(fx, n1, cx, K, M, Vt, lamt);
+  build_fragy<P, S>(fy, n1, cy, K, M, Vt, lamt);
+#pragma unroll
+  for (int k = 0; k < WI; ++k) {
+    const int i = lane + 32 * k, row = i / WN4, cc = i - row * WN4;
+    if (i < WT) X[row * LDX + cc] = wv[k];
+  }
   __syncwarp();
-  mma_block<P, S>(X, LDX, Pab, n1, cx, cy, K, M, Vt, lamt, b, zoff, [&](int ly, int lx, double v) {
+#ifdef IGA2L_TRACE
+  const double f0 = fx.bxf[0][0] + fy.ayf[0];   // force the fragment loads to complete here
+  long long t2 = clock64() + (f0 == 1.2345e300 ? 1 : 0);
+#endif
+  mma_block_f<P, S>(X, LDX, Pab, n1, cx, cy, fx, fy, b, zoff, [&](int ly, int lx, double v) {
     x[(int64_t)(by + ly - zoff) * n1 + bx + lx] = v;
   });
+#ifdef IGA2L_TRACE
+  long long t3 = clock64();
+  if (tr) {
+    g_s2d_trace[0] = t1 - t0;   // issue of the window copies
+    g_s2d_trace[1] = t2 - t1;   // window + fragment loads landed
+    g_s2d_trace[2] = t3 - t2;   // the DMMA block solve incl. the x store issue
+  }
+#endif
 }
 
 // ---------------- temporal blocking: KC consecutive colours per launch (latency-bound sizes) ------
@@ -3176,6 +3223,8 @@ void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumul
 }
 
 static int g_vc_cluster[4] = {0, 0, 0, 0};
+
+void s2d_trace_read(long long *host8) { cudaMemcpyFromSymbol(host8, g_s2d_trace, 8 * sizeof(long long)); }
 
 void vcycle_trace_enable(unsigned long long *dev_buf) {
   cudaMemcpyToSymbol(g_vc_trace, &dev_buf, sizeof(dev_buf));
