@@ -3304,13 +3304,25 @@ void launch_axpy(double *y, const double *x, int64_t n, cudaStream_t st) {
 namespace iga2l {
 namespace {
 
-// optional phase timestamps (thread 0 of cluster rank 0; tools/vc_trace.cu, -DIGA2L_TRACE)
+// optional phase clocks (thread 0 of cluster rank 0, buffered in shared memory, written at the end;
+// tools/vc_trace.cu, -DIGA2L_TRACE)
+#ifdef IGA2L_TRACE
+__shared__ long long s_vc_clk[128];
+__shared__ int s_vc_n;
+#endif
 __device__ __forceinline__ void vc_mark() {
 #ifdef IGA2L_TRACE
-  if (g_vc_trace && threadIdx.x == 0 && cg::this_cluster().block_rank() == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_vc_trace[g_vc_trace_n++ & 1023] = t;
+  if (threadIdx.x == 0 && cg::this_cluster().block_rank() == 0) {
+    if (s_vc_n < 128) s_vc_clk[s_vc_n] = clock64();
+    ++s_vc_n;
+  }
+#endif
+}
+__device__ __forceinline__ void vc_flush() {
+#ifdef IGA2L_TRACE
+  if (threadIdx.x == 0 && cg::this_cluster().block_rank() == 0 && g_vc_trace) {
+    for (int i = 0; i < s_vc_n && i < 128; ++i) g_vc_trace[i] = (unsigned long long)s_vc_clk[i];
+    g_vc_trace_n = s_vc_n;
   }
 #endif
 }
@@ -3575,8 +3587,25 @@ __device__ __forceinline__ void vc_prolong(const VcLayout &L, const VcLev &v, co
   }
 }
 
-// coarsest level: x = A^{-1} b, rows [r0, r1) by warps; b from bsrc, x to xdst (may be remote)
+// coarsest level: x = A^{-1} b, rows [r0, r1): one thread per row when they fit the CTA (4 partial sums),
+// else by warps; b from bsrc, x to xdst (may be remote)
 __device__ __forceinline__ void vc_dense(const double *inv, int Nc, const double *bsrc, double *xdst, int r0, int r1) {
+  if (r1 - r0 <= int(blockDim.x) && Nc <= 128) {
+    const int row = r0 + int(threadIdx.x);
+    if (row < r1) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int j = 0;
+      for (; j + 3 < Nc; j += 4) {
+        s0 = fma(inv[(int64_t)row * Nc + j], bsrc[j], s0);
+        s1 = fma(inv[(int64_t)row * Nc + j + 1], bsrc[j + 1], s1);
+        s2 = fma(inv[(int64_t)row * Nc + j + 2], bsrc[j + 2], s2);
+        s3 = fma(inv[(int64_t)row * Nc + j + 3], bsrc[j + 3], s3);
+      }
+      for (; j < Nc; ++j) s0 = fma(inv[(int64_t)row * Nc + j], bsrc[j], s0);
+      xdst[row] = (s0 + s1) + (s2 + s3);
+    }
+    return;
+  }
   const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int row = r0 + int(threadIdx.x >> 5); row < r1; row += nw) {
     double s = 0.0;
@@ -3631,37 +3660,35 @@ __global__ void __launch_bounds__(512, 1) k_vcycle_smem(const VcLayout L) {
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int l0 = L.l0, nlev = L.nlev, lf = l0 + L.nsp;   // lf: first CTA-0 level
   const bool spread = L.nsp > 0;
+#ifdef IGA2L_TRACE
+  if (threadIdx.x == 0) s_vc_n = 0;
+  __syncthreads();
+#endif
   vc_mark();
   if (!spread && rank != 0) return;
   // ---- staging: zero x (with halos); tables by a flat copy list (4 independent loads in flight per
   // thread); level l0's right-hand side (own rows) ----
   for (int i = tid; i < L.xend; i += nthr) sm[i] = 0.0;
-  for (int i0 = tid; i0 < L.copy_start[L.ncopy]; i0 += 4 * nthr) {
-    double v[4];
-    int dst[4], isint[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int i = i0 + k * nthr;
-      dst[k] = -1;
-      if (i < L.copy_start[L.ncopy]) {
-        int lo = 0, hi = L.ncopy - 1;                 // last entry e with copy_start[e] <= i
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (L.copy_start[mid] <= i) lo = mid; else hi = mid - 1;
-        }
-        const VcCopy &e = L.copy[lo];
-        const int j = i - L.copy_start[lo];
-        isint[k] = e.is_int;
-        dst[k] = e.dst + j;
-        v[k] = e.is_int ? __hiloint2double(static_cast<const int *>(e.src)[j], 0) : static_cast<const double *>(e.src)[j];
+  {                                                  // tables: one copy-list entry per warp, lanes strided,
+    const int warp = tid >> 5, lane = tid & 31, nw = nthr >> 5;   // asynchronous (LDGSTS)
+    const int ninv = L.inv_sm >= 0 ? 1 : 0;        // the staged coarsest inverse is the last entry: own group
+    for (int e = warp; e < L.ncopy - ninv; e += nw) {
+      const VcCopy &c = L.copy[e];
+      if (c.is_int) {
+        const int *src = static_cast<const int *>(c.src);
+        for (int j = lane; j < c.count; j += 32) si[c.dst + j] = src[j];
+      } else {
+        const double *src = static_cast<const double *>(c.src);
+        for (int j = lane; j < c.count; j += 32) cp_async8(sm + c.dst + j, src + j, true);
       }
     }
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (dst[k] >= 0) {
-        if (isint[k]) si[dst[k]] = __double2hiint(v[k]);
-        else sm[dst[k]] = v[k];
-      }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (ninv) {                                      // needed only at the coarsest solve: overlaps the down-sweep
+      const VcCopy &c = L.copy[L.ncopy - 1];
+      const double *src = static_cast<const double *>(c.src);
+      for (int j = tid; j < c.count; j += nthr) cp_async8(sm + c.dst + j, src + j, true);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
   {
     const VcLev v = vc_level<DIM>(L, l0, rank, sm);
@@ -3680,6 +3707,7 @@ __global__ void __launch_bounds__(512, 1) k_vcycle_smem(const VcLayout L) {
       }
     }
   }
+  asm volatile("cp.async.wait_group 1;" ::: "memory");   // tables landed (the inverse may still be in flight)
   if (spread) cl.sync(); else __syncthreads();
   vc_mark();
   // ---- down-sweep on the spread levels ----
@@ -3706,6 +3734,8 @@ __global__ void __launch_bounds__(512, 1) k_vcycle_smem(const VcLayout L) {
   const int NC = DIM == 3 ? L.n[nlev - 1] * L.n[nlev - 1] * L.n[nlev - 1] : L.n[nlev - 1] * L.n[nlev - 1];
   const double *inv = L.inv_sm >= 0 ? sm + L.inv_sm : L.ginv;
   if (rank == 0) vc_local_down<DIM, Q>(L, lf, sm, si);
+  cp_async_wait_all();                                      // the staged inverse (own copies) ...
+  __syncthreads();                                          // ... visible to the whole CTA
   if (spread && L.cbuf >= 0) {                                   // coarsest by the whole cluster
     cl.sync();
     const double *bc0 = cl.map_shared_rank(sm + L.b[nlev - 1], 0);
@@ -3750,6 +3780,8 @@ __global__ void __launch_bounds__(512, 1) k_vcycle_smem(const VcLayout L) {
     const int tot = (v.zhi - v.zlo) * v.plane;
     for (int i = tid; i < tot; i += nthr) L.gx0[(int64_t)v.zlo * v.plane + i] = v.x[(v.zlo - v.zoff) * v.plane + i];
   }
+  vc_mark();
+  vc_flush();
 }
 
 }  // namespace

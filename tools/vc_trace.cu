@@ -16,8 +16,8 @@ int main(int argc, char **argv) {
   iga2l_coarse_solve(c, dq, e); cudaDeviceSynchronize();
   std::vector<unsigned long long> h(1024); cudaMemcpy(h.data(), tb, 1024 * 8, cudaMemcpyDeviceToHost);
   int n = 0; while (n < 1023 && h[n + 1] > h[n]) ++n;
-  printf("phases %d total %.2f us\n", n, (h[n] - h[0]) * 1e-3);
-  for (int i = 1; i <= n; ++i) printf("%d:%.2f ", i, (h[i] - h[i - 1]) * 1e-3);
+  printf("phases %d total %llu cycles (%.2f us at 1.965 GHz)\n", n, h[n] - h[0], (h[n] - h[0]) / 1965.0);
+  for (int i = 1; i <= n; ++i) printf("%d:%llu ", i, h[i] - h[i - 1]);
   printf("\n");
   return 0;
 }
