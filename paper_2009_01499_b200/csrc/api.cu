@@ -64,6 +64,7 @@ struct iga2l_ctx {
   double *K1 = nullptr, *M1 = nullptr, *V = nullptr, *lam = nullptr, *g1 = nullptr;
   DevBand R, RT;
   ToeP toe{};                    // interior 1D data (A27) for the kernels' constant-bank path
+  double *frags = nullptr;       // interior-block DMMA operand fragments, lane-major (A27)
   std::vector<Level> lev;
   double *r = nullptr, *t1 = nullptr, *t2 = nullptr;   // fine scratch, N each
   double *partial = nullptr, *norm = nullptr, *hist = nullptr;
@@ -240,7 +241,7 @@ void L_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
   }
   for (int col = c0; col < c1; ++col) {
     if (!launch_schwarz_colour_fast(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st,
-                                    kFull, &c->toe))
+                                    kFull, &c->toe, c->frags))
       launch_schwarz_colour(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st);
     c->launch_counter++;
   }
@@ -442,7 +443,7 @@ int S_iteration(iga2l_ctx *c, bool with_norm) {
       for (auto &S : c->slabs) {
         const SlabView sv{S.za, std::max(0, S.z0 - c->w), std::min(n1, S.z1 + c->w)};
         if (!launch_schwarz_colour_fast(d, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, S.bp, S.xp, col, c->D,
-                                        c->st, sv, &c->toe))
+                                        c->st, sv, &c->toe, c->frags))
           launch_schwarz_colour(d, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, S.bp, S.xp, col, c->D, c->st, sv);
         c->launch_counter++;
       }
@@ -734,6 +735,15 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
           return bail(fail(IGA2L_ECUDA, "cudaMemset (sweep counters)"));
         c->persist_tiles = nt;
       }
+    }
+  }
+  if (dim == 2) {   // interior-block fragments for the DMMA colour kernel (IGA2L_MMA_FRAGS=0 disables)
+    const char *fe = std::getenv("IGA2L_MMA_FRAGS");
+    const int nf = export_interior_frags(p, block, n1, c->K1, c->M1, c->V, c->lam, nullptr, nullptr);
+    if (nf > 0 && !(fe && fe[0] == '0')) {
+      if ((rc = dalloc(c, &c->frags, nf))) return bail(rc);
+      export_interior_frags(p, block, n1, c->K1, c->M1, c->V, c->lam, c->frags, nullptr);
+      if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(IGA2L_ECUDA, "fragment export"));
     }
   }
   c->npartial = apply_num_partials(dim, p, n1);

@@ -2409,7 +2409,7 @@ __device__ __forceinline__ void build_fragy(FragY<P, S> &f, int n1, int cy, cons
 template <int P, int S, class OUT>
 __device__ __forceinline__ void mma_block_f(const double *Xw, int ldx, double *Pab, int n1, int cx, int cy,
                                             const FragX<P, S> &fx, const FragY<P, S> &fy,
-                                            const double *__restrict__ b, int zoff, OUT out) {
+                                            const double *__restrict__ b, int zoff, OUT out, bool trace = false) {
   using G = Mma2<P, S>;
   constexpr int Wn = G::Wn, w = G::w, MT = G::MT, KT = G::KT, NTX = G::NTX, WN4 = G::WN4, LDP = G::LDP,
                 KY = G::KY, KF = G::KF;
@@ -2443,6 +2443,9 @@ __device__ __forceinline__ void mma_block_f(const double *Xw, int ldx, double *P
     }
   }
   __syncwarp();
+#ifdef IGA2L_TRACE
+  if (trace) g_s2d_trace[3] = clock64();
+#endif
   // ---- pass y: R = b_B - Ay [Pa; Pb] ----
   double r0 = 0.0, r1 = 0.0, s0 = 0.0, s1 = 0.0;      // two independent accumulation chains
 #pragma unroll
@@ -2456,6 +2459,9 @@ __device__ __forceinline__ void mma_block_f(const double *Xw, int ldx, double *P
   }
   r0 = (r4 < S && 2 * q4 < S) ? bb[0] - (r0 + s0) : 0.0;
   r1 = (r4 < S && 2 * q4 + 1 < S) ? bb[1] - (r1 + s1) : 0.0;
+#ifdef IGA2L_TRACE
+  if (trace) g_s2d_trace[4] = clock64() + (r0 == 1.2345e300 ? 1 : 0);
+#endif
   // ---- FD: T = R Vx;  Z = Vy^T T ./ den;  U = Z Vx^T;  δ = Vy U ----
   double t0 = 0.0, t1 = 0.0;
 #pragma unroll
@@ -2471,6 +2477,9 @@ __device__ __forceinline__ void mma_block_f(const double *Xw, int ldx, double *P
   double e0 = 0.0, e1 = 0.0;
 #pragma unroll
   for (int kt = 0; kt < KF; ++kt) dmma(e0, e1, fy.vya[kt], c_elem(u0, u1, 4 * kt + q4, r4));
+#ifdef IGA2L_TRACE
+  if (trace) g_s2d_trace[5] = clock64() + (e0 == 1.2345e300 ? 1 : 0);
+#endif
   // ---- x_B += δ ----
   const int ly = r4, gy = by + ly;
 #pragma unroll
@@ -2493,13 +2502,45 @@ __device__ __forceinline__ void mma_block(const double *Xw, int ldx, double *Pab
   mma_block_f<P, S>(Xw, ldx, Pab, n1, cx, cy, fx, fy, b, zoff, out);
 }
 
+// Interior fragments (A27) of the per-colour DMMA kernel, lane-major: frag[k * 32 + lane], k over the
+// FragX then FragY fields.  Built once per context by one warp; loaded coalesced by interior blocks.
+template <int P, int S>
+constexpr int frag_count() {
+  return (sizeof(FragX<P, S>) + sizeof(FragY<P, S>)) / sizeof(double);
+}
+template <int P, int S>
+__global__ void k_export_frags(int n1, int cref, const double *__restrict__ K, const double *__restrict__ M,
+                               const double *__restrict__ Vt, const double *__restrict__ lamt, double *out) {
+  FragX<P, S> fx;
+  FragY<P, S> fy;
+  build_fragx<P, S>(fx, n1, cref, K, M, Vt, lamt);
+  build_fragy<P, S>(fy, n1, cref, K, M, Vt, lamt);
+  const double *a = reinterpret_cast<const double *>(&fx), *c = reinterpret_cast<const double *>(&fy);
+  constexpr int NX = sizeof(FragX<P, S>) / sizeof(double), NY = sizeof(FragY<P, S>) / sizeof(double);
+#pragma unroll
+  for (int k = 0; k < NX; ++k) out[k * 32 + threadIdx.x] = a[k];
+#pragma unroll
+  for (int k = 0; k < NY; ++k) out[(NX + k) * 32 + threadIdx.x] = c[k];
+}
+template <int P, int S>
+__device__ __forceinline__ void load_frags(const double *__restrict__ fb, FragX<P, S> &fx, FragY<P, S> &fy) {
+  constexpr int NX = sizeof(FragX<P, S>) / sizeof(double), NY = sizeof(FragY<P, S>) / sizeof(double);
+  const int lane = threadIdx.x & 31;
+  double *a = reinterpret_cast<double *>(&fx), *c = reinterpret_cast<double *>(&fy);
+#pragma unroll
+  for (int k = 0; k < NX; ++k) a[k] = __ldg(fb + k * 32 + lane);
+#pragma unroll
+  for (int k = 0; k < NY; ++k) c[k] = __ldg(fb + (NX + k) * 32 + lane);
+}
+
 template <int P, int S, int WPC>
 __global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma(int n1, const double *__restrict__ K,
                                                             const double *__restrict__ M,
                                                             const double *__restrict__ Vt,
                                                             const double *__restrict__ lamt,
                                                             const double *__restrict__ b, double *__restrict__ x,
-                                                            int c0, int c1, int D, int nb0, int nblk, int zoff) {
+                                                            int c0, int c1, int D, int nb0, int nblk, int zoff,
+                                                            const double *__restrict__ fb, int tlo, int thi) {
   using G = Mma2<P, S>;
   constexpr int Wn = G::Wn, w = G::w, MT = G::MT, WN4 = G::WN4, LDX = G::LDX;
   extern __shared__ double sm[];
@@ -2531,8 +2572,12 @@ __global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma(int n1, const double
 #endif
   FragX<P, S> fx;
   FragY<P, S> fy;
-  build_fragx<P, S>(fx, n1, cx, K, M, Vt, lamt);
-  build_fragy<P, S>(fy, n1, cy, K, M, Vt, lamt);
+  if (fb && cx - w >= tlo && cx + w <= thi && cy - w >= tlo && cy + w <= thi) {
+    load_frags<P, S>(fb, fx, fy);                            // interior block: shared fragments (A27)
+  } else {
+    build_fragx<P, S>(fx, n1, cx, K, M, Vt, lamt);
+    build_fragy<P, S>(fy, n1, cy, K, M, Vt, lamt);
+  }
 #pragma unroll
   for (int k = 0; k < WI; ++k) {
     const int i = lane + 32 * k, row = i / WN4, cc = i - row * WN4;
@@ -2543,15 +2588,24 @@ __global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma(int n1, const double
   const double f0 = fx.bxf[0][0] + fy.ayf[0];   // force the fragment loads to complete here
   long long t2 = clock64() + (f0 == 1.2345e300 ? 1 : 0);
 #endif
+#ifdef IGA2L_TRACE
+  const bool trs = tr;
+#else
+  const bool trs = false;
+#endif
   mma_block_f<P, S>(X, LDX, Pab, n1, cx, cy, fx, fy, b, zoff, [&](int ly, int lx, double v) {
     x[(int64_t)(by + ly - zoff) * n1 + bx + lx] = v;
-  });
+  }, trs);
 #ifdef IGA2L_TRACE
   long long t3 = clock64();
   if (tr) {
-    g_s2d_trace[0] = t1 - t0;   // issue of the window copies
-    g_s2d_trace[1] = t2 - t1;   // window + fragment loads landed
-    g_s2d_trace[2] = t3 - t2;   // the DMMA block solve incl. the x store issue
+    g_s2d_trace[0] = t1 - t0;                  // issue of the window loads
+    g_s2d_trace[1] = t2 - t1;                  // window + fragment loads landed
+    g_s2d_trace[2] = t3 - t2;                  // the DMMA block solve incl. the x store issue
+    g_s2d_trace[6] = g_s2d_trace[3] - t2;      // pass x (+ Pab stores)
+    g_s2d_trace[7] = g_s2d_trace[4] - g_s2d_trace[3];   // pass y
+    g_s2d_trace[3] = g_s2d_trace[5] - g_s2d_trace[4];   // FD chain
+    g_s2d_trace[4] = t3 - g_s2d_trace[5];               // x update
   }
 #endif
 }
@@ -2699,16 +2753,18 @@ __global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma_m(int n1, const doub
 
 template <int P, int S, int WPC>
 void launch2d_mma(int64_t n1, const double *K, const double *M, const double *V, const double *lam, const double *b,
-                  double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st) {
+                  double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st, const double *fb) {
   constexpr size_t sm = sizeof(double) * WPC * Mma2<P, S>::PER;
   ensure_smem(k_schwarz2d_mma<P, S, WPC>, sm);
+  const int m = int(n1) - P + 2;
   k_schwarz2d_mma<P, S, WPC><<<(nblk + WPC - 1) / WPC, WPC * 32, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, D,
-                                                                           nb0, nblk, zoff);
+                                                                           nb0, nblk, zoff, fb, 2 * P - 1, m - 2 - P);
 }
 
 template <int P, int S>
 bool try_schwarz2d_mma(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
-                       const double *b, double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st) {
+                       const double *b, double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st,
+                       const double *fb) {
   if (p != P || s != S) return false;
   const char *eb = std::getenv("IGA2L_MMA_BPW");   // blocks per warp (> 1: prefetching multi-block warps)
   const int bpw = eb ? std::atoi(eb) : 1;
@@ -2730,10 +2786,10 @@ bool try_schwarz2d_mma(int p, int s, int64_t n1, const double *K, const double *
   }
   const char *e = std::getenv("IGA2L_MMA_WPC");   // warps (blocks) per CTA; measured best (variants_wpc_r01):
   const int wpc = e ? std::atoi(e) : (S >= 5 ? 1 : 4);   // 1 for s >= 5 (C2 p5, C3), 4 for s = 3
-  if (wpc == 1) launch2d_mma<P, S, 1>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st);
-  else if (wpc == 2) launch2d_mma<P, S, 2>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st);
-  else if (wpc == 8) launch2d_mma<P, S, 8>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st);
-  else launch2d_mma<P, S, 4>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st);
+  if (wpc == 1) launch2d_mma<P, S, 1>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st, fb);
+  else if (wpc == 2) launch2d_mma<P, S, 2>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st, fb);
+  else if (wpc == 8) launch2d_mma<P, S, 8>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st, fb);
+  else launch2d_mma<P, S, 4>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st, fb);
   return true;
 }
 
@@ -3068,7 +3124,7 @@ __global__ void k_eig_divide(double *__restrict__ T, const double *__restrict__ 
 
 bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M, const double *V,
                                 const double *lam, const double *b, double *x, int colour, int D, cudaStream_t st,
-                                SlabView sv, const ToeP *tp) {
+                                SlabView sv, const ToeP *tp, const double *fb) {
   if (sv.zhi < 0) sv = SlabView{0, 0, int(n1)};
   if (dim == 3) {
     const int c0 = colour % D, c1 = (colour / D) % D, c2 = colour / (D * D);
@@ -3103,14 +3159,14 @@ bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double 
   const int nb0 = int((n1 - c0 + D - 1) / D), nblk = nb0 * nb1;
   const int z = sv.zoff;
   if (s2d_variant() == 0 || s2d_variant() == 9)   // default: FP64 tensor-pipe kernel
-    if (try_schwarz2d_mma<1, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
-        try_schwarz2d_mma<2, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
-        try_schwarz2d_mma<3, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
-        try_schwarz2d_mma<4, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
-        try_schwarz2d_mma<5, 5>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
-        try_schwarz2d_mma<6, 5>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
-        try_schwarz2d_mma<7, 7>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st) ||
-        try_schwarz2d_mma<8, 7>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st))
+    if (try_schwarz2d_mma<1, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb) ||
+        try_schwarz2d_mma<2, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb) ||
+        try_schwarz2d_mma<3, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb) ||
+        try_schwarz2d_mma<4, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb) ||
+        try_schwarz2d_mma<5, 5>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb) ||
+        try_schwarz2d_mma<6, 5>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb) ||
+        try_schwarz2d_mma<7, 7>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb) ||
+        try_schwarz2d_mma<8, 7>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb))
       return true;
   if (const int v = s2d_variant(); v >= 1 && v <= 4)
     if (try_schwarz2d_r<1, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, v, tp) ||
@@ -3194,6 +3250,23 @@ int launch_coarse_fd(int dim, int n, const double *V, const double *lam, const d
   launch_dgemm(V, t2, t1, n, n, n, n, 0, n1, 1, n2, n1, 1, n2, n1, 1, st);             // y back (batch z)
   launch_dgemm(t1, V, e, int(n2), n, n, 1, 0, n1, 1, 0, 1, n1, 0, n1, 1, st);          // x back
   return 7;
+}
+
+int export_interior_frags(int p, int s, int64_t n1, const double *K, const double *M, const double *V,
+                          const double *lam, double *out, cudaStream_t st) {
+  const int m = int(n1) - p + 2, tlo = 2 * p - 1, thi = m - 2 - p, w = (s - 1) / 2;
+  if (thi - tlo < 2 * w) return -1;
+  const int cref = (tlo + thi) / 2;
+#define IGA2L_EXP(P_, S_)                                                                                   \
+  if (p == P_ && s == S_) {                                                                                 \
+    if (!out) return frag_count<P_, S_>() * 32;                                                            \
+    k_export_frags<P_, S_><<<1, 32, 0, st>>>(int(n1), cref, K, M, V, lam, out);                            \
+    return frag_count<P_, S_>() * 32;                                                                      \
+  }
+  IGA2L_EXP(1, 3) IGA2L_EXP(2, 3) IGA2L_EXP(3, 3) IGA2L_EXP(4, 3) IGA2L_EXP(5, 5) IGA2L_EXP(6, 5) IGA2L_EXP(7, 7)
+  IGA2L_EXP(8, 7)
+#undef IGA2L_EXP
+  return -1;
 }
 
 void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumulate, cudaStream_t st,

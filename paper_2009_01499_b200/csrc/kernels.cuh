@@ -76,7 +76,12 @@ void launch_sum_partials(const double *partial, int n, double *out, double *hist
 // Warp-per-block 2D Schwarz colour kernel for the paper's (p, s) pairs; false = not specialised.
 bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M,
                                 const double *V, const double *lam, const double *b, double *x, int colour,
-                                int D, cudaStream_t st, SlabView sv = kFull, const ToeP *tp = nullptr);
+                                int D, cudaStream_t st, SlabView sv = kFull, const ToeP *tp = nullptr,
+                                const double *fb = nullptr);
+// Interior-block operand fragments of the 2D DMMA kernel (lane-major, A27) into out (device); with
+// out == nullptr returns the number of doubles needed; -1 if no interior block or (p, s) not specialised.
+int export_interior_frags(int p, int s, int64_t n1, const double *K, const double *M, const double *V,
+                          const double *lam, double *out, cudaStream_t st);
 // Temporal blocking (2D, single domain): colours [col0, col0 + ncol), ncol <= kc in {2, 3}, in ONE
 // launch (each CTA solves its core's blocks and the halo blocks they depend on from a shared-memory
 // copy of x).  False if (p, s, kc) is not specialised.

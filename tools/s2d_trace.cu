@@ -20,7 +20,9 @@ int main(int argc, char **argv) {
       cudaDeviceSynchronize();
       long long t[8];
       iga2l::s2d_trace_read(t);
-      if (rep == 2) printf("p=%d colour %d: issue %lld  loads %lld  solve %lld cycles\n", p, col, t[0], t[1], t[2]);
+      if (rep == 2)
+        printf("p=%d colour %d: issue %lld  loads %lld  solve %lld (pass x %lld, pass y %lld, FD %lld, update %lld) cycles\n",
+               p, col, t[0], t[1], t[2], t[6], t[7], t[3], t[4]);
     }
   }
   return 0;
