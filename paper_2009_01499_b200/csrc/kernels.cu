@@ -1754,6 +1754,9 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
   extern __shared__ double sm[];
   const int tid = threadIdx.x;
   const unsigned un = unsigned(n1);
+#ifdef IGA2L_TRACE
+  if (blockIdx.x == 0 && tid == 0) g_s2d_trace[0] = clock64();
+#endif
   // per-block regions: X [z][y][x] window, Pa/Pb [wz][wy][lx], Pc/Pe [wz][ly][lx], R, Q, Bb,
   // Tk/Tm [axis][row][t], Vs [axis][l][j], Ls [axis][j]
   auto X = [&](int k) { return sm + k * PER; };
@@ -1792,7 +1795,44 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
   }
   auto centre = [&](int k, int a) { return NBK == 1 ? cc1[a] : sC[k][a]; };
   const int nk = min(NBK, nblk - int(blockIdx.x) * NBK);   // blocks of this CTA
-  // ---- loads: band rows, FD tables, b_B, x windows: all asynchronous (LDGSTS), one wait ----
+  // ---- loads: band rows, FD tables, b_B (through registers when one block per CTA: the 8-byte cp.async
+  // issue cost dominated this phase), x windows ----
+  if (NBK == 1 && !ROW) {
+    constexpr int NTAB = 2 * 3 * S * W + 3 * S2 + 3 * S + S3;   // Tk, Tm, Vs, Ls, Bb
+    constexpr int IT = (NTAB + NT - 1) / NT;
+    double v[IT];
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+      const int i = tid + k * NT;
+      double val = 0.0;
+      if (i < 2 * 3 * S * W) {
+        const int r = i % (3 * S * W), a = r / (S * W), l = (r / W) % S, t = r % W;
+        const int g = centre(0, a) - w + l;
+        if (unsigned(g) < un) val = (i < 3 * S * W ? K : M)[(int64_t)g * W + t];
+      } else if (i < 2 * 3 * S * W + 3 * S2) {
+        const int r = i - 2 * 3 * S * W;
+        val = Vt[(int64_t)centre(0, r / S2) * S2 + r % S2];
+      } else if (i < 2 * 3 * S * W + 3 * S2 + 3 * S) {
+        const int r = i - 2 * 3 * S * W - 3 * S2;
+        val = lamt[(int64_t)centre(0, r / S) * S + r % S];
+      } else if (i < NTAB) {
+        const int r = i - 2 * 3 * S * W - 3 * S2 - 3 * S;
+        const int gx = centre(0, 0) - w + r % S, gy = centre(0, 1) - w + (r / S) % S, gz = centre(0, 2) - w + r / S2;
+        if (unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un)
+          val = b[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx];
+      }
+      v[k] = val;
+    }
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+      const int i = tid + k * NT;
+      if (i < 3 * S * W) Tk(0)[i] = v[k];
+      else if (i < 2 * 3 * S * W) Tm(0)[i - 3 * S * W] = v[k];
+      else if (i < 2 * 3 * S * W + 3 * S2) Vs(0)[i - 2 * 3 * S * W] = v[k];
+      else if (i < 2 * 3 * S * W + 3 * S2 + 3 * S) Ls(0)[i - 2 * 3 * S * W - 3 * S2] = v[k];
+      else if (i < NTAB) Bb(0)[i - 2 * 3 * S * W - 3 * S2 - 3 * S] = v[k];
+    }
+  } else {
   for (int i = tid; i < nk * 3 * S * W; i += NT) {
     const int k = NBK == 1 ? 0 : i / (3 * S * W), r = NBK == 1 ? i : i % (3 * S * W);
     const int a = r / (S * W), l = (r / W) % S, t = r % W;
@@ -1814,6 +1854,7 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
     const int gx = centre(k, 0) - w + r % S, gy = centre(k, 1) - w + (r / S) % S, gz = centre(k, 2) - w + r / S2;
     const bool ok = unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un;
     cp_async8(Bb(k) + r, b + (ok ? ((int64_t)(gz - zoff) * n1 + gy) * n1 + gx : 0), ok);
+  }
   }
   if (!ROW && NBK == 1 && Wn2 * Wn <= 1024) {      // x window through registers, in batches of 16 loads
                                                    // (measured: C4 40.6 -> 36.6 us/colour; C5 slower)
@@ -1861,6 +1902,9 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
   cp_async_wait_all();
   auto toe = [&](int k, int a) { return NBK == 1 ? tt1[a] : sT[k][a]; };
   __syncthreads();
+#ifdef IGA2L_TRACE
+  if (blockIdx.x == 0 && tid == 0) g_s2d_trace[1] = clock64();
+#endif
   // ---- pass x: pencils (wy, wz) along x -> Pa = Kx X, Pb = Mx X ----
   for (int i = tid; i < nk * Wn2; i += NT) {
     const int k = NBK == 1 ? 0 : i / Wn2, pi = NBK == 1 ? i : i % Wn2;
@@ -1871,6 +1915,9 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
     for (int l = 0; l < S; ++l) { Pa(k)[pi * S + l] = oa[l]; Pb(k)[pi * S + l] = ob[l]; }
   }
   __syncthreads();
+#ifdef IGA2L_TRACE
+  if (blockIdx.x == 0 && tid == 0) g_s2d_trace[2] = clock64();
+#endif
   // ---- pass y: pencils (wz, lx) along y -> Pc = My Pa + Ky Pb, Pe = My Pb ----
   for (int i = tid; i < nk * Wn * S; i += NT) {
     const int k = NBK == 1 ? 0 : i / (Wn * S), pi = NBK == 1 ? i : i % (Wn * S);
@@ -1883,6 +1930,9 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
     for (int l = 0; l < S; ++l) { Pc(k)[(wz * S + l) * S + lx] = oc[l]; Pe(k)[(wz * S + l) * S + lx] = oe[l]; }
   }
   __syncthreads();
+#ifdef IGA2L_TRACE
+  if (blockIdx.x == 0 && tid == 0) g_s2d_trace[3] = clock64();
+#endif
   // ---- pass z: pencils (ly, lx) along z -> r_B = b_B - (Mz Pc + Kz Pe) ----
   for (int i = tid; i < nk * S2; i += NT) {
     const int k = NBK == 1 ? 0 : i / S2, pi = NBK == 1 ? i : i % S2;
@@ -1893,7 +1943,44 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
     for (int l = 0; l < S; ++l) R(k)[l * S2 + pi] = Bb(k)[l * S2 + pi] - oc[l];
   }
   __syncthreads();
+#ifdef IGA2L_TRACE
+  if (blockIdx.x == 0 && tid == 0) g_s2d_trace[4] = clock64();
+#endif
   // ---- δ = (⊗V) Λ^{-1} (⊗V)^T r ----
+  if constexpr (S == 3 && NBK == 1) {   // s^3 = 27 values: the whole FD in one warp's registers (shuffles)
+    if (tid < 32) {
+      const int lane = tid, li = lane < 27 ? lane : 0;
+      const int lx = li % 3, ly = (li / 3) % 3, lz = li / 9;
+      const double *Vx = Vs(0), *Vy = Vs(0) + 9, *Vz = Vs(0) + 18, *L = Ls(0);
+      double v = lane < 27 ? R(0)[li] : 0.0;
+      auto src = [&](int ax, int l) { return ax == 0 ? lz * 9 + ly * 3 + l : (ax == 1 ? lz * 9 + l * 3 + lx : l * 9 + ly * 3 + lx); };
+      auto step = [&](int ax, const double *V, bool trans) {   // trans: out[j] = Σ_l V[l][j] in[l]; else V[j][l]
+        const int j = ax == 0 ? lx : (ax == 1 ? ly : lz);
+        double o = 0.0;
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+          const double in = __shfl_sync(0xffffffffu, v, src(ax, l));
+          o = fma(trans ? V[l * 3 + j] : V[j * 3 + l], in, o);
+        }
+        v = o;
+      };
+      step(0, Vx, true);
+      step(1, Vy, true);
+      step(2, Vz, true);
+      v /= (L[lx] + L[3 + ly] + L[6 + lz]);
+      step(2, Vz, false);
+      step(1, Vy, false);
+      step(0, Vx, false);
+      const int gx = centre(0, 0) - w + lx, gy = centre(0, 1) - w + ly, gz = centre(0, 2) - w + lz;
+      if (lane < 27 && unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un)
+        x[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx] = X(0)[((lz + P) * Wn + ly + P) * Wn + lx + P] + v;
+    }
+#ifdef IGA2L_TRACE
+    __syncthreads();
+    if (blockIdx.x == 0 && tid == 0) g_s2d_trace[5] = clock64();
+#endif
+    return;
+  }
   for (int i = tid; i < nk * S3; i += NT) {         // along x (transposed)
     const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3, j = r % S, rest = r - j;
     const double *Vx = Vs(k);
@@ -1949,6 +2036,10 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
     if (unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un)
       x[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx] = X(k)[((lz + P) * Wn + ly + P) * Wn + lx + P] + a0;
   }
+#ifdef IGA2L_TRACE
+  __syncthreads();
+  if (blockIdx.x == 0 && tid == 0) g_s2d_trace[5] = clock64();
+#endif
 }
 
 // Launch variants per (p, s): <blocks per CTA, threads, row-wise window staging>.  The default is
