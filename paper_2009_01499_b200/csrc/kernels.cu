@@ -1738,7 +1738,11 @@ __device__ __forceinline__ void band_pencil2(const double *pa_, const double *pb
 template <int P, int S>
 struct Blk3 {
   static constexpr int W = 2 * P + 1, Wn = S + 2 * P, w = (S - 1) / 2, S2 = S * S, S3 = S2 * S, Wn2 = Wn * Wn;
-  static constexpr int PER = Wn2 * Wn + 2 * Wn2 * S + 2 * Wn * S2 + 3 * S3 + 6 * S * W + 3 * S2 + 3 * S;
+  // per-block layout; Pc/Pe alias the window X (dead after pass x once its s^3 centre values are in Xc)
+  static constexpr int OPa = Wn2 * Wn, OPb = OPa + Wn2 * S, OXc = OPb + Wn2 * S, OR = OXc + S3, OQ = OR + S3,
+                       OBb = OQ + S3, OTk = OBb + S3, OTm = OTk + 3 * S * W, OVs = OTm + 3 * S * W, OLs = OVs + 3 * S2;
+  static constexpr int PER = OLs + 3 * S;
+  static_assert(2 * Wn * S2 <= Wn2 * Wn, "Pc/Pe must fit in the window");
 };
 
 // NBK blocks per CTA (block g = blockIdx.x * NBK + k of the colour's nb0 x nb1 x nb2 grid); every phase
@@ -1760,17 +1764,18 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
   // per-block regions: X [z][y][x] window, Pa/Pb [wz][wy][lx], Pc/Pe [wz][ly][lx], R, Q, Bb,
   // Tk/Tm [axis][row][t], Vs [axis][l][j], Ls [axis][j]
   auto X = [&](int k) { return sm + k * PER; };
-  auto Pa = [&](int k) { return sm + k * PER + Wn2 * Wn; };
-  auto Pb = [&](int k) { return sm + k * PER + Wn2 * Wn + Wn2 * S; };
-  auto Pc = [&](int k) { return sm + k * PER + Wn2 * Wn + 2 * Wn2 * S; };
-  auto Pe = [&](int k) { return sm + k * PER + Wn2 * Wn + 2 * Wn2 * S + Wn * S2; };
-  auto R = [&](int k) { return sm + k * PER + Wn2 * Wn + 2 * Wn2 * S + 2 * Wn * S2; };
-  auto Q = [&](int k) { return R(k) + S3; };
-  auto Bb = [&](int k) { return R(k) + 2 * S3; };
-  auto Tk = [&](int k) { return R(k) + 3 * S3; };
-  auto Tm = [&](int k) { return R(k) + 3 * S3 + 3 * S * W; };
-  auto Vs = [&](int k) { return R(k) + 3 * S3 + 6 * S * W; };
-  auto Ls = [&](int k) { return R(k) + 3 * S3 + 6 * S * W + 3 * S2; };
+  auto Pa = [&](int k) { return sm + k * PER + B::OPa; };
+  auto Pb = [&](int k) { return sm + k * PER + B::OPb; };
+  auto Pc = [&](int k) { return sm + k * PER; };                     // aliases X (see Blk3)
+  auto Pe = [&](int k) { return sm + k * PER + Wn * S2; };
+  auto Xc = [&](int k) { return sm + k * PER + B::OXc; };
+  auto R = [&](int k) { return sm + k * PER + B::OR; };
+  auto Q = [&](int k) { return sm + k * PER + B::OQ; };
+  auto Bb = [&](int k) { return sm + k * PER + B::OBb; };
+  auto Tk = [&](int k) { return sm + k * PER + B::OTk; };
+  auto Tm = [&](int k) { return sm + k * PER + B::OTm; };
+  auto Vs = [&](int k) { return sm + k * PER + B::OVs; };
+  auto Ls = [&](int k) { return sm + k * PER + B::OLs; };
   __shared__ int sC[NBK][3];
   __shared__ bool sT[NBK][3];
   if (NBK > 1 && tid < NBK) {                               // block centres, Toeplitz flags per axis
@@ -1914,6 +1919,11 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
 #pragma unroll
     for (int l = 0; l < S; ++l) { Pa(k)[pi * S + l] = oa[l]; Pb(k)[pi * S + l] = ob[l]; }
   }
+  for (int i = tid; i < nk * S3; i += NT) {        // the block's centre values, before Pc/Pe overwrite X
+    const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3;
+    const int lx = r % S, ly = (r / S) % S, lz = r / S2;
+    Xc(k)[r] = X(k)[((lz + P) * Wn + ly + P) * Wn + lx + P];
+  }
   __syncthreads();
 #ifdef IGA2L_TRACE
   if (blockIdx.x == 0 && tid == 0) g_s2d_trace[2] = clock64();
@@ -1973,7 +1983,7 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
       step(0, Vx, false);
       const int gx = centre(0, 0) - w + lx, gy = centre(0, 1) - w + ly, gz = centre(0, 2) - w + lz;
       if (lane < 27 && unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un)
-        x[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx] = X(0)[((lz + P) * Wn + ly + P) * Wn + lx + P] + v;
+        x[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx] = Xc(0)[(lz * S + ly) * S + lx] + v;
     }
 #ifdef IGA2L_TRACE
     __syncthreads();
@@ -2034,7 +2044,7 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
     for (int l = 0; l < S; ++l) a0 = fma(Vx[lx * S + l], Q(k)[rest + l], a0);
     const int gx = centre(k, 0) - w + lx, gy = centre(k, 1) - w + ly, gz = centre(k, 2) - w + lz;
     if (unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un)
-      x[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx] = X(k)[((lz + P) * Wn + ly + P) * Wn + lx + P] + a0;
+      x[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx] = Xc(k)[r] + a0;
   }
 #ifdef IGA2L_TRACE
   __syncthreads();
