@@ -1747,7 +1747,7 @@ struct Blk3 {
 
 // NBK blocks per CTA (block g = blockIdx.x * NBK + k of the colour's nb0 x nb1 x nb2 grid); every phase
 // runs over (block, pencil) pairs so that the short phases still occupy the CTA.
-template <int P, int S, int NBK, int NT, bool ROW>
+template <int P, int S, int NBK, int NT, bool ROW, bool REGW = false>
 __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__restrict__ K, const double *__restrict__ M,
                                                     const double *__restrict__ Vt, const double *__restrict__ lamt,
                                                     const double *__restrict__ b, double *__restrict__ x, int c0, int c1,
@@ -1861,7 +1861,7 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
     cp_async8(Bb(k) + r, b + (ok ? ((int64_t)(gz - zoff) * n1 + gy) * n1 + gx : 0), ok);
   }
   }
-  if (!ROW && NBK == 1 && Wn2 * Wn <= 1024) {      // x window through registers, in batches of 16 loads
+  if (!ROW && NBK == 1 && (REGW || Wn2 * Wn <= 1024)) {   // x window through registers, batches of 16 loads
                                                    // (measured: C4 40.6 -> 36.6 us/colour; C5 slower)
     constexpr int TOT = Wn2 * Wn, BATCH = 16;      // (8-byte cp.async issue costs ~95 cycles each)
     const int ox = centre(0, 0) - w - P, oy = centre(0, 1) - w - P, oz = centre(0, 2) - w - P;
@@ -2063,15 +2063,15 @@ int s3d_variant() {
   return g_s3d_variant;
 }
 
-template <int P, int S, int NBK, int NT, bool ROW>
+template <int P, int S, int NBK, int NT, bool ROW, bool REGW = false>
 void launch3d(int64_t n1, const double *K, const double *M, const double *V, const double *lam, const double *b,
               double *x, int c0, int c1, int c2, int D, int nb0, int nb1, int nb2, int zoff, int tlo, int thi,
               cudaStream_t st) {
   constexpr size_t sm = sizeof(double) * NBK * Blk3<P, S>::PER;
-  ensure_smem(k_schwarz3d_t<P, S, NBK, NT, ROW>, sm);
+  ensure_smem(k_schwarz3d_t<P, S, NBK, NT, ROW, REGW>, sm);
   const int nblk = nb0 * nb1 * nb2;
-  k_schwarz3d_t<P, S, NBK, NT, ROW><<<(nblk + NBK - 1) / NBK, NT, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, c2,
-                                                                            D, nb0, nb1, nblk, zoff, tlo, thi);
+  k_schwarz3d_t<P, S, NBK, NT, ROW, REGW><<<(nblk + NBK - 1) / NBK, NT, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1,
+                                                                                  c2, D, nb0, nb1, nblk, zoff, tlo, thi);
 }
 
 template <int P, int S>
@@ -2084,6 +2084,8 @@ bool try_schwarz3d(int p, int s, int64_t n1, const double *K, const double *M, c
     case 1: launch3d<P, S, 1, NT1, true>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, zoff, tlo, thi, st); break;
     case 2: launch3d<P, S, 2, (2 * NT1 > 512 ? 512 : 2 * NT1), false>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, zoff, tlo, thi, st); break;
     case 3: launch3d<P, S, 1, (NT1 >= 128 ? NT1 / 2 : NT1), false>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, zoff, tlo, thi, st); break;
+    case 5: launch3d<P, S, 1, (S >= 5 && NT1 >= 128 ? NT1 / 2 : NT1), false, true>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, zoff, tlo, thi, st); break;
+    case 6: launch3d<P, S, 1, NT1, false, true>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, zoff, tlo, thi, st); break;
     default:   // measured best (tools/variants.py): s >= 5 -> half the pass-x pencil count of threads
       launch3d<P, S, 1, (S >= 5 && NT1 >= 128 ? NT1 / 2 : NT1), false>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1,
                                                                       nb2, zoff, tlo, thi, st);
