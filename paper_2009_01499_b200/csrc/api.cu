@@ -130,12 +130,15 @@ int upload(iga2l_ctx *c, T **ptr, const std::vector<T> &v) {
 int upload_band(iga2l_ctx *c, DevBand &d, const BandOp &h) {
   int rc = upload(c, &d.lo, h.lo);
   if (!rc) rc = upload(c, &d.c, h.c);
-  int span = 0;   // tile input span for the separable 2D transfer (32-row tiles)
-  for (int r0 = 0; r0 < h.rows; r0 += 32) {
-    const int r1 = std::min(h.rows, r0 + 32) - 1;
-    span = std::max(span, h.lo[r1] - h.lo[r0]);
-  }
-  d.b = Band1D{h.rows, h.cols, h.W, d.lo, d.c, span};
+  auto span_of = [&](int t) {   // tile input span for the separable 2D transfer (t-row tiles)
+    int sp = 0;
+    for (int r0 = 0; r0 < h.rows; r0 += t) {
+      const int r1 = std::min(h.rows, r0 + t) - 1;
+      sp = std::max(sp, h.lo[r1] - h.lo[r0]);
+    }
+    return sp;
+  };
+  d.b = Band1D{h.rows, h.cols, h.W, d.lo, d.c, span_of(32), span_of(16)};
   return rc;
 }
 

@@ -2099,7 +2099,7 @@ bool try_schwarz3d(int p, int s, int64_t n1, const double *K, const double *M, c
 // tile needs; pass 2 (y): out[ry][rx] = Σ_k c[ry][k] T[lo[ry]+k][rx].  2W FMAs per output (plus the
 // input-row halo of pass 1) instead of W^2 gathers.  Input rows valid in [iylo, iyhi) stored from
 // iyoff; output rows [rylo, ryhi) stored from ryoff (slab views).
-constexpr int TO = 32;
+template <int TO>
 __global__ void __launch_bounds__(256) k_transfer2d_sep(const double *__restrict__ in, double *__restrict__ out, int nin,
                                                         int rows, int W, const int *__restrict__ lo,
                                                         const double *__restrict__ c, int acc, int iylo, int iyhi,
@@ -3378,14 +3378,22 @@ void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumul
   if (ryhi < 0) { rylo = 0; ryhi = B.rows; ryoff = 0; }
   const int64_t total = (int64_t)(ryhi - rylo) * B.rows;
   if (total <= 0) return;
-  if (g_transfer_v2 && B.lo_max_span > 0 && total >= 200000) {   // separable two-pass (large grids; measured)
-    const int LI = B.lo_max_span + B.W;
-    const size_t sm = sizeof(double) * (size_t(LI) * LI + size_t(LI) * TO + 2 * TO * B.W) + 2 * TO * sizeof(int);
-    if (sm <= 200 * 1024) {
-      ensure_smem(k_transfer2d_sep, sm);
+  const char *te = std::getenv("IGA2L_TRANSFER_SMALL");   // 16x16 separable tiles for small grids (default on)
+  const bool small_sep = !(te && te[0] == '0');
+  if (g_transfer_v2 && B.lo_max_span > 0 && (total >= 200000 || small_sep)) {   // separable two-pass
+    auto go = [&](auto kern, int TO, int span) {
+      const int LI = span + B.W;
+      const size_t sm = sizeof(double) * (size_t(LI) * LI + size_t(LI) * TO + 2 * TO * B.W) + 2 * TO * sizeof(int);
+      if (sm > 200 * 1024) return false;
+      ensure_smem(kern, sm);
       dim3 grid((unsigned)((B.rows + TO - 1) / TO), (unsigned)((ryhi - rylo + TO - 1) / TO));
-      k_transfer2d_sep<<<grid, 256, sm, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate, iylo, iyhi, iyoff,
-                                              rylo, ryhi, ryoff, LI);
+      kern<<<grid, 256, sm, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate, iylo, iyhi, iyoff, rylo, ryhi,
+                                  ryoff, LI);
+      return true;
+    };
+    if (total >= 200000) {
+      if (go(k_transfer2d_sep<32>, 32, B.lo_max_span)) return;
+    } else if (B.lo_max_span16 > 0 && go(k_transfer2d_sep<16>, 16, B.lo_max_span16)) {
       return;
     }
   }

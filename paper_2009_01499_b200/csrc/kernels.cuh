@@ -16,6 +16,7 @@ struct Band1D {          // banded 1D transfer: row r uses columns lo[r] .. lo[r
   const int *lo;
   const double *c;
   int lo_max_span;       // max over 32-row tiles of lo[last] - lo[first] (0: unknown)
+  int lo_max_span16;     // the same over 16-row tiles
 };
 
 // Window of the LAST axis (y in 2D, z in 3D) of a vector held by a context: local plane 0 is the
