@@ -1991,6 +1991,7 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
 #endif
     return;
   }
+  if constexpr (!(S == 3 && NBK == 1)) {   // general FD (s >= 5 or several blocks per CTA)
   for (int i = tid; i < nk * S3; i += NT) {         // along x (transposed)
     const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3, j = r % S, rest = r - j;
     const double *Vx = Vs(k);
@@ -2045,6 +2046,7 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
     const int gx = centre(k, 0) - w + lx, gy = centre(k, 1) - w + ly, gz = centre(k, 2) - w + lz;
     if (unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un)
       x[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx] = Xc(k)[r] + a0;
+  }
   }
 #ifdef IGA2L_TRACE
   __syncthreads();
