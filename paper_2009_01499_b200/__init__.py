@@ -59,6 +59,7 @@ def lib():
         "iga2l_apply": (i, [vp, vp, vp]),
         "iga2l_residual_norm": (i, [vp, vp, vp, P(d)]),
         "iga2l_iterate": (i, [vp, vp, vp, i, vp]),
+        "iga2l_iterate_batch": (i, [i, vp, vp, vp, i]),
         "iga2l_solve": (i, [vp, vp, vp, d, i, P(i), P(d)]),
         "iga2l_sweep": (i, [vp, vp, vp, i, i]),
         "iga2l_defect_restrict": (i, [vp, vp, vp, vp]),
@@ -126,6 +127,17 @@ def host_coarse_fd(q, m):
     lam = np.zeros(n)
     _check(lib().iga2l_host_coarse_fd(q, m, _ptr(V), _ptr(lam)))
     return V.reshape(n, n), lam
+
+
+def iterate_batch(ctxs, bs, xs, iters=1):
+    """iga2l_iterate_batch: one batched iteration schedule over independent problems (see the header)."""
+    n = len(ctxs)
+    h = (ctypes.c_void_p * n)(*[c._h.value for c in ctxs])
+    pb = (ctypes.c_void_p * n)(*[_ptr(b).value for b in bs])
+    px = (ctypes.c_void_p * n)(*[_ptr(x).value for x in xs])
+    _check(lib().iga2l_iterate_batch(n, ctypes.cast(h, ctypes.c_void_p), ctypes.cast(pb, ctypes.c_void_p),
+                                     ctypes.cast(px, ctypes.c_void_p), iters))
+    return xs
 
 
 def host_slab_plan(dim, p, block, m, nranks, rank):

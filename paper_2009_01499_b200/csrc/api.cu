@@ -5,6 +5,9 @@
 #include <nccl.h>   // types only; the library is dlopen'ed (the process may already hold torch's copy)
 
 #include <algorithm>
+#include <atomic>
+#include <map>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -86,6 +89,8 @@ struct iga2l_ctx {
   int l_sm = -1;                 // first level handled by the shared-memory tail kernel (preferred)
   int persist_tiles = 0;         // > 0: full sweeps run as one persistent launch with this many tiles
   int tb_kc = 0;                 // temporal blocking (colours per launch) chosen at setup; 0 = per-colour
+  uint64_t gen = 0;              // unique id (batched-graph cache key)
+  cudaStream_t batch_st = nullptr;   // internal stream of iga2l_iterate_batch (fused colour launches)
   unsigned *sweep_ctl = nullptr, *sweep_done = nullptr;
   VcLayout vcl{};
   int launch_counter = 0;
@@ -263,6 +268,19 @@ void L_iteration(iga2l_ctx *c, const double *b, double *x, bool with_norm) {
     c->launch_counter++;
   }
 }
+
+// Algorithm 1 after the sweep (defect, restriction, second level, prolongation) on the context's stream.
+void L_post(iga2l_ctx *c, const double *b, double *x) {
+  L_apply(c, x, b, c->r, nullptr, 1);
+  L_tensor(c, c->dim, c->R.b, c->r, c->lev[0].b, c->t1, c->t2, 0);
+  L_vcycle(c, 0);
+  L_tensor(c, c->dim, c->RT.b, c->lev[0].x, x, c->t1, c->t2, 1);
+}
+
+// batched-iteration graph cache: key = (ctx generations, b, x pointers)
+std::mutex g_batch_mu;
+std::map<std::vector<uintptr_t>, cudaGraphExec_t> g_batch_graphs;
+std::atomic<uint64_t> g_ctx_gen{1};
 
 int check_ctx(const iga2l_ctx *c) {
   if (!c) return fail(IGA2L_EPARAM, "ctx is NULL");
@@ -559,6 +577,20 @@ int iga2l_setup(int dim, int p, int q, int64_t n, int block, int overlap, iga2l_
 
 int iga2l_destroy(iga2l_ctx *c) {
   if (!c) return IGA2L_OK;
+  {
+    std::lock_guard<std::mutex> lk(g_batch_mu);
+    for (auto it = g_batch_graphs.begin(); it != g_batch_graphs.end();) {
+      bool has = false;
+      for (size_t k = 1; k < it->first.size(); k += 3) has = has || it->first[k] == c->gen;
+      if (has) {
+        cudaGraphExecDestroy(it->second);
+        it = g_batch_graphs.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+  if (c->batch_st) cudaStreamDestroy(c->batch_st);
   for (auto &g : c->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (c->comm) nccl().commDestroy(static_cast<ncclComm_t>(c->comm));
@@ -612,6 +644,7 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
   if (N > (int64_t)1 << 31) return fail(IGA2L_EPARAM, "problem too large");
 
   iga2l_ctx *c = new iga2l_ctx();
+  c->gen = g_ctx_gen.fetch_add(1);
   c->dim = dim; c->p = p; c->q = q; c->s = block; c->w = (block - 1) / 2; c->D = block + p;
   c->colours = int(ipow(c->D, dim));
   c->m = n; c->n1 = n1; c->N = N; c->opts = o;
@@ -996,6 +1029,115 @@ int iga2l_solve(iga2l_ctx *c, const double *b, double *x, double rtol, int maxit
     if (int rc = S_gather(c, xd)) return rc;
   if (int rc = stage_out(c, x, sx, c->N)) return rc;
   if (rk > rtol * r0) return fail(IGA2L_NOTCONV, "maxit reached before rtol");
+  return IGA2L_OK;
+}
+
+int iga2l_iterate_batch(int n, iga2l_ctx *const *ctxs, const double *const *b, double *const *x, int iters) {
+  if (n < 1 || !ctxs || !b || !x) return fail(IGA2L_EPARAM, "iterate_batch: n >= 1 and non-NULL arrays");
+  if (iters < 0) return fail(IGA2L_EPARAM, "iters must be >= 0");
+  for (int j = 0; j < n; ++j) {
+    if (int rc = check_ctx(ctxs[j])) return rc;
+    if (!b[j] || !x[j]) return fail(IGA2L_EPARAM, "iterate_batch: NULL vector");
+    for (int k = 0; k < j; ++k)
+      if (ctxs[k] == ctxs[j] || x[k] == x[j]) return fail(IGA2L_EPARAM, "iterate_batch: contexts and x must be distinct");
+  }
+  // fused colour launches need: <= kBatchMax 2D single-domain DMMA contexts and device vectors
+  const char *v = std::getenv("IGA2L_S2D_VARIANT");
+  const char *tb = std::getenv("IGA2L_TB");
+  bool fuse = n <= kBatchMax && !(v && std::atoi(v) != 0 && std::atoi(v) != 9) && !(tb && std::atoi(tb) >= 2);
+  for (int j = 0; j < n && fuse; ++j) {
+    const iga2l_ctx *c = ctxs[j];
+    fuse = c->dim == 2 && c->nranks == 1 && c->persist_tiles == 0 && batch_ps_index(c->p, c->s) >= 0 &&
+           is_device_ptr(b[j]) && is_device_ptr(x[j]);
+  }
+  if (!fuse) {   // independent iterations, one context after the other
+    for (int j = 0; j < n; ++j)
+      if (int rc = iga2l_iterate(ctxs[j], b[j], x[j], iters, nullptr)) return rc;
+    return IGA2L_OK;
+  }
+  if (iters == 0) return IGA2L_OK;
+  iga2l_ctx *c0 = ctxs[0];
+  if (!c0->batch_st) CU(cudaStreamCreateWithFlags(&c0->batch_st, cudaStreamNonBlocking));
+  std::vector<uintptr_t> key{uintptr_t(n)};
+  for (int j = 0; j < n; ++j) {
+    key.push_back(uintptr_t(ctxs[j]->gen));
+    key.push_back(reinterpret_cast<uintptr_t>(b[j]));
+    key.push_back(reinterpret_cast<uintptr_t>(x[j]));
+  }
+  cudaGraphExec_t exec = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_batch_mu);
+    auto it = g_batch_graphs.find(key);
+    if (it != g_batch_graphs.end()) exec = it->second;
+  }
+  if (!exec) {
+    cudaStream_t main = c0->st, side = c0->batch_st;
+    std::vector<cudaEvent_t> evs;
+    auto ev = [&]() {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      evs.push_back(e);
+      return e;
+    };
+    CU(cudaStreamBeginCapture(main, cudaStreamCaptureModeThreadLocal));
+    cudaEvent_t fork = ev();
+    cudaEventRecord(fork, main);
+    cudaStreamWaitEvent(side, fork, 0);
+    for (int j = 1; j < n; ++j) cudaStreamWaitEvent(ctxs[j]->st, fork, 0);
+    int maxcol = 0;
+    size_t smem = 0;
+    for (int j = 0; j < n; ++j) {
+      maxcol = std::max(maxcol, ctxs[j]->colours);
+      smem = std::max(smem, batch_smem_bytes(batch_ps_index(ctxs[j]->p, ctxs[j]->s)));   // per warp
+    }
+    for (int i = 0; i < maxcol; ++i) {
+      BatchDesc d{};
+      d.n = n;
+      d.beg[0] = 0;
+      for (int j = 0; j < n; ++j) {
+        const iga2l_ctx *c = ctxs[j];
+        BatchProb &q = d.pr[j];
+        int nblk = 0;
+        if (i < c->colours) {
+          const int n1 = int(c->n1), D = c->D, cc0 = i % D, cc1 = i / D;
+          const int nb0 = cc0 < n1 ? (n1 - cc0 + D - 1) / D : 0, nb1 = cc1 < n1 ? (n1 - cc1 + D - 1) / D : 0;
+          nblk = nb0 * nb1;
+          const int m = n1 - c->p + 2;
+          q = BatchProb{batch_ps_index(c->p, c->s), n1, cc0, cc1, D, std::max(nb0, 1), nblk, 2 * c->p - 1,
+                        m - 2 - c->p, c->K1, c->M1, c->V, c->lam, b[j], c->frags, x[j]};
+        }
+        d.beg[j + 1] = d.beg[j] + nblk;
+      }
+      launch_schwarz2d_batch(d, smem, side);
+      for (int j = 0; j < n; ++j) ctxs[j]->launch_counter += (j == 0);
+      for (int j = 0; j < n; ++j)
+        if (i == ctxs[j]->colours - 1) {   // problem j's sweep is complete: its post-sweep phase may start
+          cudaEvent_t done = ev();
+          cudaEventRecord(done, side);
+          cudaStreamWaitEvent(ctxs[j]->st, done, 0);
+          L_post(ctxs[j], b[j], x[j]);
+        }
+    }
+    cudaEvent_t side_end = ev();
+    cudaEventRecord(side_end, side);
+    cudaStreamWaitEvent(main, side_end, 0);
+    for (int j = 1; j < n; ++j) {
+      cudaEvent_t e = ev();
+      cudaEventRecord(e, ctxs[j]->st);
+      cudaStreamWaitEvent(main, e, 0);
+    }
+    cudaGraph_t graph;
+    cudaError_t e = cudaStreamEndCapture(main, &graph);
+    for (cudaEvent_t x_ : evs) cudaEventDestroy(x_);
+    if (e != cudaSuccess) return fail(IGA2L_ECUDA, std::string("batch graph capture: ") + cudaGetErrorString(e));
+    cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) return fail(IGA2L_ECUDA, std::string("batch graph instantiate: ") + cudaGetErrorString(ei));
+    std::lock_guard<std::mutex> lk(g_batch_mu);
+    g_batch_graphs[key] = exec;
+  }
+  for (int k = 0; k < iters; ++k) CU(cudaGraphLaunch(exec, c0->st));
+  CU(cudaGetLastError());
   return IGA2L_OK;
 }
 

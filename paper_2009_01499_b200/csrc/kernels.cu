@@ -2638,21 +2638,17 @@ __device__ __forceinline__ void load_frags(const double *__restrict__ fb, FragX<
   for (int k = 0; k < NY; ++k) c[k] = __ldg(fb + (NX + k) * 32 + lane);
 }
 
-template <int P, int S, int WPC>
-__global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma(int n1, const double *__restrict__ K,
-                                                            const double *__restrict__ M,
-                                                            const double *__restrict__ Vt,
-                                                            const double *__restrict__ lamt,
-                                                            const double *__restrict__ b, double *__restrict__ x,
-                                                            int c0, int c1, int D, int nb0, int nblk, int zoff,
-                                                            const double *__restrict__ fb, int tlo, int thi) {
+// Body of one colour's block solve for block `bid` by the calling warp (per-warp shared memory X).
+template <int P, int S>
+__device__ __forceinline__ void mma_colour_block(double *__restrict__ X, int bid, int n1, const double *__restrict__ K,
+                                                 const double *__restrict__ M, const double *__restrict__ Vt,
+                                                 const double *__restrict__ lamt, const double *__restrict__ b,
+                                                 double *__restrict__ x, int c0, int c1, int D, int nb0, int nblk,
+                                                 int zoff, const double *__restrict__ fb, int tlo, int thi) {
   using G = Mma2<P, S>;
   constexpr int Wn = G::Wn, w = G::w, MT = G::MT, WN4 = G::WN4, LDX = G::LDX;
-  extern __shared__ double sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bid = blockIdx.x * WPC + warp;
-  if (bid >= nblk) return;                                   // whole warp exits together
-  double *X = sm + warp * G::PER, *Pab = X + MT * 8 * LDX;
+  const int lane = threadIdx.x & 31;
+  double *Pab = X + MT * 8 * LDX;
   const int j1 = bid / nb0, j0 = bid - j1 * nb0;
   const int cx = c0 + D * j0, cy = c1 + D * j1;
   const int bx = cx - w, by = cy - w, ox = bx - P, oy = by - P;
@@ -2783,6 +2779,52 @@ __global__ void __launch_bounds__(WPC * 32) k_schwarz2d_tb(int n1, const double 
     const int cy = i / T, cx = i - cy * T, gx = X0 + cx, gy = Y0 + cy;
     if (gx < n1 && gy < n1) x[(int64_t)gy * n1 + gx] = Rg[(cy + H) * LDR + cx + H];
   }
+}
+
+
+template <int P, int S, int WPC>
+__global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma(int n1, const double *__restrict__ K,
+                                                            const double *__restrict__ M,
+                                                            const double *__restrict__ Vt,
+                                                            const double *__restrict__ lamt,
+                                                            const double *__restrict__ b, double *__restrict__ x,
+                                                            int c0, int c1, int D, int nb0, int nblk, int zoff,
+                                                            const double *__restrict__ fb, int tlo, int thi) {
+  extern __shared__ double sm[];
+  const int warp = threadIdx.x >> 5;
+  const int bid = blockIdx.x * WPC + warp;
+  if (bid >= nblk) return;                                   // whole warp exits together
+  mma_colour_block<P, S>(sm + warp * Mma2<P, S>::PER, bid, n1, K, M, Vt, lamt, b, x, c0, c1, D, nb0, nblk, zoff, fb,
+                         tlo, thi);
+}
+
+// ---------------- batched colour launch: one colour of up to kBatchMax independent problems ----------
+// CTA = one warp = one block; CTAs [beg[j], beg[j+1]) belong to problem j, whose (p, s) selects the body.
+// WPC warps per CTA, one block per warp (block index over the concatenated problems); MAXPS limits the
+// (p, s) bodies compiled in (registers / shared memory are the maximum over them).
+template <int WPC, int MAXPS>
+__global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma_batch(const BatchDesc d, int per) {
+  extern __shared__ double sm[];
+  const int warp = threadIdx.x >> 5;
+  const int g = int(blockIdx.x) * WPC + warp;
+  if (g >= d.beg[d.n]) return;
+  int j = 0;
+  while (j + 1 < d.n && g >= d.beg[j + 1]) ++j;
+  const BatchProb &q = d.pr[j];
+  const int bid = g - d.beg[j];
+  double *X = sm + warp * per;
+#define IGA2L_B(I, P_, S_)                                                                                    \
+  case I:                                                                                                     \
+    if (I <= MAXPS)                                                                                           \
+      mma_colour_block<P_, S_>(X, bid, q.n1, q.K, q.M, q.V, q.lam, q.b, q.x, q.c0, q.c1, q.D, q.nb0, q.nblk, 0, \
+                               q.fb, q.tlo, q.thi);                                                           \
+    break;
+  switch (q.ps) {
+    IGA2L_B(0, 1, 3) IGA2L_B(1, 2, 3) IGA2L_B(2, 3, 3) IGA2L_B(3, 4, 3)
+    IGA2L_B(4, 5, 5) IGA2L_B(5, 6, 5) IGA2L_B(6, 7, 7) IGA2L_B(7, 8, 7)
+    default: break;
+  }
+#undef IGA2L_B
 }
 
 // Several blocks per warp (BPW consecutive blocks of the colour): interior fragments (A27) built once
@@ -3372,6 +3414,43 @@ int export_interior_frags(int p, int s, int64_t n1, const double *K, const doubl
   IGA2L_EXP(8, 7)
 #undef IGA2L_EXP
   return -1;
+}
+
+int batch_ps_index(int p, int s) {
+  const int tab[8][2] = {{1, 3}, {2, 3}, {3, 3}, {4, 3}, {5, 5}, {6, 5}, {7, 7}, {8, 7}};
+  for (int i = 0; i < 8; ++i)
+    if (tab[i][0] == p && tab[i][1] == s) return i;
+  return -1;
+}
+
+size_t batch_smem_bytes(int ps) {
+  const size_t per[8] = {Mma2<1, 3>::PER, Mma2<2, 3>::PER, Mma2<3, 3>::PER, Mma2<4, 3>::PER,
+                         Mma2<5, 5>::PER, Mma2<6, 5>::PER, Mma2<7, 7>::PER, Mma2<8, 7>::PER};
+  return ps >= 0 && ps < 8 ? per[ps] * sizeof(double) : 0;
+}
+
+void launch_schwarz2d_batch(const BatchDesc &d, size_t smem, cudaStream_t st) {
+  const int nb = d.beg[d.n];
+  if (nb <= 0) return;
+  int maxps = 0;
+  for (int j = 0; j < d.n; ++j)
+    if (d.beg[j + 1] > d.beg[j]) maxps = std::max(maxps, d.pr[j].ps);
+  const char *e = std::getenv("IGA2L_BATCH_WPC");
+  const int wpc = e ? std::atoi(e) : 4;
+  const int per = int(smem / sizeof(double));
+  auto go = [&](auto kern, int w) {
+    ensure_smem(kern, smem * w);
+    kern<<<(nb + w - 1) / w, w * 32, smem * w, st>>>(d, per);
+  };
+  if (maxps <= 5) {
+    if (wpc == 1) go(k_schwarz2d_mma_batch<1, 5>, 1);
+    else if (wpc == 2) go(k_schwarz2d_mma_batch<2, 5>, 2);
+    else go(k_schwarz2d_mma_batch<4, 5>, 4);
+  } else {
+    if (wpc == 1) go(k_schwarz2d_mma_batch<1, 7>, 1);
+    else if (wpc == 2) go(k_schwarz2d_mma_batch<2, 7>, 2);
+    else go(k_schwarz2d_mma_batch<4, 7>, 4);
+  }
 }
 
 void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumulate, cudaStream_t st,

@@ -88,6 +88,24 @@ int export_interior_frags(int p, int s, int64_t n1, const double *K, const doubl
 // copy of x).  False if (p, s, kc) is not specialised.
 bool launch_schwarz2d_tb(int p, int s, int64_t n1, const double *K, const double *M, const double *V,
                          const double *lam, const double *b, double *x, int col0, int ncol, int kc, cudaStream_t st);
+// Batched colour launch (2D DMMA path): one colour of up to kBatchMax independent problems in ONE launch,
+// one warp-CTA per Schwarz block; CTAs [beg[j], beg[j+1]) belong to problem j.  Same block arithmetic
+// as the per-problem launches (bitwise equal).
+struct BatchProb {
+  int ps;                                   // batch_ps_index(p, s)
+  int n1, c0, c1, D, nb0, nblk, tlo, thi;
+  const double *K, *M, *V, *lam, *b, *fb;
+  double *x;
+};
+constexpr int kBatchMax = 4;
+struct BatchDesc {
+  int n, beg[kBatchMax + 1];
+  BatchProb pr[kBatchMax];
+};
+int batch_ps_index(int p, int s);           // -1 if (p, s) has no DMMA specialisation
+size_t batch_smem_bytes(int ps);
+void launch_schwarz2d_batch(const BatchDesc &d, size_t smem, cudaStream_t st);
+
 // Persistent 2D sweep (all D^2 colours in one cooperative launch, per-tile progress counters).
 // ctl: 2 unsigned (zeroed once), done: one unsigned per tile (zeroed once).  launch = false returns the
 // tile count (0: cannot be co-resident or more than max_tiles; -1: (p, s) not specialised).

@@ -406,3 +406,39 @@ def test_multiblock_warps_bitwise(p, s, m, bpw, monkeypatch):
     monkeypatch.setenv("IGA2L_MMA_BPW", bpw)
     ctx.sweep(b, x2)
     assert torch.equal(x1, x2)
+
+
+# ---- batched iterations of independent problems (fused colour launches): bitwise equal to separate calls ----
+@pytest.mark.parametrize("combo", [((3, 3, 48), (4, 3, 40), (5, 5, 32)), ((2, 3, 32), (8, 7, 32)),
+                                   ((3, 3, 256), (4, 3, 256), (5, 5, 256))], ids=["p345", "p28", "C2"])
+def test_iterate_batch_bitwise(combo):
+    ctxs, bs, xs, refs = [], [], [], []
+    for i, (p, s, m) in enumerate(combo):
+        st = torch.cuda.Stream(DEV)
+        c = pkg.Context(2, p, 1, m, s, coarse_mode=pkg.COARSE_VCYCLE, coarse_h_factor=2, stream=st.cuda_stream)
+        ctxs.append(c)
+        bs.append(cu(random_rhs(c.N, seed=10 + i)))
+        x0 = cu(initial_guess(c.N, seed=20 + i))
+        xs.append(x0.clone())
+        refs.append(x0.clone())
+    torch.cuda.synchronize()
+    pkg.iterate_batch(ctxs, bs, xs, iters=3)
+    torch.cuda.synchronize()
+    for c, b, xr in zip(ctxs, bs, refs):
+        c.iterate(b, xr, iters=3)
+    torch.cuda.synchronize()
+    for xb, xr in zip(xs, refs):
+        assert torch.equal(xb, xr)
+
+
+def test_iterate_batch_fallback_mixed_dims():
+    c2 = make_ctx(2, 3, 1, 48, 3, "vcycle", 2)
+    c3 = make_ctx(3, 3, 1, 16, 3, "vcycle", 2)
+    b2, b3 = cu(random_rhs(c2.N)), cu(random_rhs(c3.N))
+    x2, x3 = cu(initial_guess(c2.N)), cu(initial_guess(c3.N))
+    r2, r3 = x2.clone(), x3.clone()
+    pkg.iterate_batch([c2, c3], [b2, b3], [x2, x3], iters=2)
+    c2.iterate(b2, r2, iters=2)
+    c3.iterate(b3, r3, iters=2)
+    torch.cuda.synchronize()
+    assert torch.equal(x2, r2) and torch.equal(x3, r3)
