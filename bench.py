@@ -296,11 +296,13 @@ def main():
         sw_flops_tot += inf.sweep_flops
         sw_launches += inf.colours
     achieved = sw_flops_tot / (sw_ms_tot / 1e3) / 1e12
+    # dram__bytes_read.sum + dram__bytes_write.sum per launch of this config's dominant kernel, from one
+    # `ncu --set full` capture of this bench command (tools/traffic.py writes the file); null if not captured
     traffic = None
     prof = os.path.join(ROOT, "profiles", "schwarz_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            traffic = json.load(open(prof)).get(args.config, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     dim = ctxs[0].dim
@@ -314,7 +316,7 @@ def main():
                             f"achieved = SURVEY 8(d) sweep flops / CUDA-event sweep time over {sw_launches} launches"}
     else:
         roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                    "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                    "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                     "kernel": "k_schwarz3d_t (FP64 FMA pencil block solves, one launch per colour)",
                     "peak_source": "derived 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md)",
                     "note": f"achieved = SURVEY 8(d) sweep flops / CUDA-event sweep time over {sw_launches} launches"}

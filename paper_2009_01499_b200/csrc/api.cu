@@ -782,6 +782,14 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
       if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(IGA2L_ECUDA, "fragment export"));
     }
   }
+  if (dim == 3) {   // interior block inverse of the s = 3 pencil kernel (IGA2L_S3D_INV=0 disables per launch)
+    const int nf = export_interior_inv3(p, block, n1, c->V, c->lam, nullptr, nullptr);
+    if (nf > 0) {
+      if ((rc = dalloc(c, &c->frags, nf))) return bail(rc);
+      export_interior_inv3(p, block, n1, c->V, c->lam, c->frags, nullptr);
+      if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(IGA2L_ECUDA, "inverse export"));
+    }
+  }
   c->npartial = apply_num_partials(dim, p, n1);
   if (c->nranks > 1) {   // slab buffers (padded with H halo planes) and the communicator
     const int first = c->rank < 0 ? 0 : c->rank, last = c->rank < 0 ? c->nranks - 1 : c->rank;

@@ -1752,7 +1752,7 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
                                                     const double *__restrict__ Vt, const double *__restrict__ lamt,
                                                     const double *__restrict__ b, double *__restrict__ x, int c0, int c1,
                                                     int c2, int D, int nb0, int nb1, int nblk, int zoff, int tlo,
-                                                    int thi) {
+                                                    int thi, const double *__restrict__ ainv) {
   using B = Blk3<P, S>;
   constexpr int W = B::W, Wn = B::Wn, w = B::w, S2 = B::S2, S3 = B::S3, Wn2 = B::Wn2, PER = B::PER;
   extern __shared__ double sm[];
@@ -1962,7 +1962,18 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
       const int lane = tid, li = lane < 27 ? lane : 0;
       const int lx = li % 3, ly = (li / 3) % 3, lz = li / 9;
       const double *Vx = Vs(0), *Vy = Vs(0) + 9, *Vz = Vs(0) + 18, *L = Ls(0);
-      double v = lane < 27 ? R(0)[li] : 0.0;
+      double v;
+      if (ainv && tt1[0] && tt1[1] && tt1[2]) {   // interior block (A27): δ = row `lane` of A_B^{-1} times r_B
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+#pragma unroll
+        for (int j = 0; j < 27; j += 3) {
+          d0 = fma(__ldg(ainv + j * 32 + lane), R(0)[j], d0);
+          d1 = fma(__ldg(ainv + (j + 1) * 32 + lane), R(0)[j + 1], d1);
+          d2 = fma(__ldg(ainv + (j + 2) * 32 + lane), R(0)[j + 2], d2);
+        }
+        v = (d0 + d1) + d2;
+      } else {
+      v = lane < 27 ? R(0)[li] : 0.0;
       auto src = [&](int ax, int l) { return ax == 0 ? lz * 9 + ly * 3 + l : (ax == 1 ? lz * 9 + l * 3 + lx : l * 9 + ly * 3 + lx); };
       auto step = [&](int ax, const double *V, bool trans) {   // trans: out[j] = Σ_l V[l][j] in[l]; else V[j][l]
         const int j = ax == 0 ? lx : (ax == 1 ? ly : lz);
@@ -1981,6 +1992,7 @@ __global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__rest
       step(2, Vz, false);
       step(1, Vy, false);
       step(0, Vx, false);
+      }
       const int gx = centre(0, 0) - w + lx, gy = centre(0, 1) - w + ly, gz = centre(0, 2) - w + lz;
       if (lane < 27 && unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un)
         x[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx] = Xc(0)[(lz * S + ly) * S + lx] + v;
@@ -2068,19 +2080,24 @@ int s3d_variant() {
 template <int P, int S, int NBK, int NT, bool ROW, bool REGW = false>
 void launch3d(int64_t n1, const double *K, const double *M, const double *V, const double *lam, const double *b,
               double *x, int c0, int c1, int c2, int D, int nb0, int nb1, int nb2, int zoff, int tlo, int thi,
-              cudaStream_t st) {
+              cudaStream_t st, const double *ainv = nullptr) {
   constexpr size_t sm = sizeof(double) * NBK * Blk3<P, S>::PER;
   ensure_smem(k_schwarz3d_t<P, S, NBK, NT, ROW, REGW>, sm);
   const int nblk = nb0 * nb1 * nb2;
   k_schwarz3d_t<P, S, NBK, NT, ROW, REGW><<<(nblk + NBK - 1) / NBK, NT, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1,
-                                                                                  c2, D, nb0, nb1, nblk, zoff, tlo, thi);
+                                                                                  c2, D, nb0, nb1, nblk, zoff, tlo, thi,
+                                                                                  ainv);
 }
 
 template <int P, int S>
 bool try_schwarz3d(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
                    const double *b, double *x, int c0, int c1, int c2, int D, int nb0, int nb1, int nb2, int zoff,
-                   int tlo, int thi, cudaStream_t st) {
+                   int tlo, int thi, cudaStream_t st, const double *ainv) {
   if (p != P || s != S) return false;
+  {                                                 // IGA2L_S3D_INV=1: A_B^{-1} rows on interior blocks (opt-in:
+    const char *e = std::getenv("IGA2L_S3D_INV");   // measured equal at C4, profiles/variants_inv_r01.txt)
+    if (!(e && e[0] == '1')) ainv = nullptr;
+  }
   constexpr int NT1 = ((Blk3<P, S>::Wn2 + 31) / 32) * 32 > 512 ? 512 : ((Blk3<P, S>::Wn2 + 31) / 32) * 32;
   switch (s3d_variant()) {
     case 1: launch3d<P, S, 1, NT1, true>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, zoff, tlo, thi, st); break;
@@ -2090,7 +2107,7 @@ bool try_schwarz3d(int p, int s, int64_t n1, const double *K, const double *M, c
     case 6: launch3d<P, S, 1, NT1, false, true>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, zoff, tlo, thi, st); break;
     default:   // measured best (tools/variants.py): s >= 5 -> half the pass-x pencil count of threads
       launch3d<P, S, 1, (S >= 5 && NT1 >= 128 ? NT1 / 2 : NT1), false>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1,
-                                                                      nb2, zoff, tlo, thi, st);
+                                                                      nb2, zoff, tlo, thi, st, ainv);
       break;
   }
   return true;
@@ -2508,13 +2525,28 @@ __device__ __forceinline__ void build_fragy(FragY<P, S> &f, int n1, int cy, cons
   f.lam = r4 < S ? __ldg(lamt + (int64_t)cy * S + r4) : 1.0;
 }
 
+// Row `lane` of the interior block inverse A_B^{-1} (s^2 <= 32 only; A27 makes it the same matrix for
+// every interior block): δ_lane = Σ_j a[j] r_j replaces the four FD GEMMs (INV path).
+template <int S>
+struct InvRow {
+  double a[S * S];
+};
+// IGA2L_MMA_INV=1: interior blocks multiply by A_B^{-1} instead of the FD GEMMs (read per launch, host side).
+// Opt-in: measured equal (C2 p3-p5, C1: within ±0.03 us per colour, profiles/variants_inv_r01.txt), so
+// the default keeps one arithmetic for every block.
+int mma_inv_enabled() {
+  const char *e = std::getenv("IGA2L_MMA_INV");
+  return e ? std::atoi(e) != 0 : 0;
+}
+
 // One block solve by one warp.  Xw: the block's (s+2p)^2 window inside a zero-padded array with row
 // stride ldx (rows/cols beyond the window up to the fragment padding must be finite); Pab: per-warp
-// scratch (MT*8 x LDP); writes x_B = Xw-centre + δ through out(ly, lx, value) for in-domain cells.
-template <int P, int S, class OUT>
-__device__ __forceinline__ void mma_block_f(const double *Xw, int ldx, double *Pab, int n1, int cx, int cy,
-                                            const FragX<P, S> &fx, const FragY<P, S> &fy,
-                                            const double *__restrict__ b, int zoff, OUT out, bool trace = false) {
+// scratch (MT*8 x LDP, plus s^2 doubles behind it on the INV path); writes x_B = Xw-centre + δ through
+// out(ly, lx, value) for in-domain cells.
+template <int P, int S, bool INV, class OUT>
+__device__ __forceinline__ void mma_block_impl(const double *Xw, int ldx, double *Pab, int n1, int cx, int cy,
+                                               const FragX<P, S> &fx, const FragY<P, S> &fy, const InvRow<S> &ai,
+                                               const double *__restrict__ b, int zoff, OUT out, bool trace) {
   using G = Mma2<P, S>;
   constexpr int Wn = G::Wn, w = G::w, MT = G::MT, KT = G::KT, NTX = G::NTX, WN4 = G::WN4, LDP = G::LDP,
                 KY = G::KY, KF = G::KF;
@@ -2567,6 +2599,22 @@ __device__ __forceinline__ void mma_block_f(const double *Xw, int ldx, double *P
 #ifdef IGA2L_TRACE
   if (trace) g_s2d_trace[4] = clock64() + (r0 == 1.2345e300 ? 1 : 0);
 #endif
+  if constexpr (INV) {                                       // δ = A_B^{-1} r_B, one row per lane
+    double *Rs = Pab + MT * 8 * LDP;
+    if (r4 < S) {
+      if (2 * q4 < S) Rs[r4 * S + 2 * q4] = r0;
+      if (2 * q4 + 1 < S) Rs[r4 * S + 2 * q4 + 1] = r1;
+    }
+    __syncwarp();
+    double d[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < S * S; ++j) d[j & 3] = fma(ai.a[j], Rs[j], d[j & 3]);
+    __syncwarp();
+    const double dl = (d[0] + d[1]) + (d[2] + d[3]);
+    const int ly = lane / S, lx = lane - (lane / S) * S, gx = bx + lx, gy = by + ly;
+    if (lane < S * S && unsigned(gx) < un && unsigned(gy) < un) out(ly, lx, Xw[(ly + P) * ldx + lx + P] + dl);
+    return;
+  }
   // ---- FD: T = R Vx;  Z = Vy^T T ./ den;  U = Z Vx^T;  δ = Vy U ----
   double t0 = 0.0, t1 = 0.0;
 #pragma unroll
@@ -2596,6 +2644,14 @@ __device__ __forceinline__ void mma_block_f(const double *Xw, int ldx, double *P
 }
 
 template <int P, int S, class OUT>
+__device__ __forceinline__ void mma_block_f(const double *Xw, int ldx, double *Pab, int n1, int cx, int cy,
+                                            const FragX<P, S> &fx, const FragY<P, S> &fy,
+                                            const double *__restrict__ b, int zoff, OUT out, bool trace = false) {
+  InvRow<S> none;                                            // unused on the FD path
+  mma_block_impl<P, S, false>(Xw, ldx, Pab, n1, cx, cy, fx, fy, none, b, zoff, out, trace);
+}
+
+template <int P, int S, class OUT>
 __device__ __forceinline__ void mma_block(const double *Xw, int ldx, double *Pab, int n1, int cx, int cy,
                                           const double *__restrict__ K, const double *__restrict__ M,
                                           const double *__restrict__ Vt, const double *__restrict__ lamt,
@@ -2610,8 +2666,12 @@ __device__ __forceinline__ void mma_block(const double *Xw, int ldx, double *Pab
 // Interior fragments (A27) of the per-colour DMMA kernel, lane-major: frag[k * 32 + lane], k over the
 // FragX then FragY fields.  Built once per context by one warp; loaded coalesced by interior blocks.
 template <int P, int S>
-constexpr int frag_count() {
+__host__ __device__ constexpr int frag_count() {
   return (sizeof(FragX<P, S>) + sizeof(FragY<P, S>)) / sizeof(double);
+}
+template <int S>
+__host__ __device__ constexpr int inv_count() {   // lane-major rows of the interior block inverse behind the fragments
+  return S * S <= 32 ? S * S : 0;
 }
 template <int P, int S>
 __global__ void k_export_frags(int n1, int cref, const double *__restrict__ K, const double *__restrict__ M,
@@ -2626,6 +2686,21 @@ __global__ void k_export_frags(int n1, int cref, const double *__restrict__ K, c
   for (int k = 0; k < NX; ++k) out[k * 32 + threadIdx.x] = a[k];
 #pragma unroll
   for (int k = 0; k < NY; ++k) out[(NX + k) * 32 + threadIdx.x] = c[k];
+  if constexpr (inv_count<S>() > 0) {
+    // A_B^{-1}[(ly,lx)][(ky,kx)] = Σ_{k,j} Vy[ly][k] Vx[lx][j] Vy[ky][k] Vx[kx][j] / (λx_j + λy_k), both axes at
+    // the reference centre (A27: the FD pair of every interior block)
+    const double *V = Vt + (int64_t)cref * S * S, *L = lamt + (int64_t)cref * S;
+    const int l = threadIdx.x, ly = l / S, lx = l % S;
+    for (int c2 = 0; c2 < S * S; ++c2) {
+      const int ky = c2 / S, kx = c2 % S;
+      double acc = 0.0;
+      if (l < S * S)
+        for (int k = 0; k < S; ++k)
+          for (int j = 0; j < S; ++j)
+            acc += V[ly * S + k] * V[lx * S + j] * V[ky * S + k] * V[kx * S + j] / (L[j] + L[k]);
+      out[(NX + NY + c2) * 32 + l] = acc;
+    }
+  }
 }
 template <int P, int S>
 __device__ __forceinline__ void load_frags(const double *__restrict__ fb, FragX<P, S> &fx, FragY<P, S> &fy) {
@@ -2644,7 +2719,7 @@ __device__ __forceinline__ void mma_colour_block(double *__restrict__ X, int bid
                                                  const double *__restrict__ M, const double *__restrict__ Vt,
                                                  const double *__restrict__ lamt, const double *__restrict__ b,
                                                  double *__restrict__ x, int c0, int c1, int D, int nb0, int nblk,
-                                                 int zoff, const double *__restrict__ fb, int tlo, int thi) {
+                                                 int zoff, const double *__restrict__ fb, int tlo, int thi, int inv) {
   using G = Mma2<P, S>;
   constexpr int Wn = G::Wn, w = G::w, MT = G::MT, WN4 = G::WN4, LDX = G::LDX;
   const int lane = threadIdx.x & 31;
@@ -2673,7 +2748,27 @@ __device__ __forceinline__ void mma_colour_block(double *__restrict__ X, int bid
 #endif
   FragX<P, S> fx;
   FragY<P, S> fy;
-  if (fb && cx - w >= tlo && cx + w <= thi && cy - w >= tlo && cy + w <= thi) {
+  const bool interior = fb && cx - w >= tlo && cx + w <= thi && cy - w >= tlo && cy + w <= thi;
+  if constexpr (inv_count<S>() > 0) {
+    if (interior && inv) {                                   // interior block: shared fragments + A_B^{-1} row
+      load_frags<P, S>(fb, fx, fy);
+      InvRow<S> ai;
+      constexpr int NF = frag_count<P, S>();
+#pragma unroll
+      for (int j = 0; j < S * S; ++j) ai.a[j] = __ldg(fb + (NF + j) * 32 + lane);
+#pragma unroll
+      for (int k = 0; k < WI; ++k) {
+        const int i = lane + 32 * k, row = i / WN4, cc = i - row * WN4;
+        if (i < WT) X[row * LDX + cc] = wv[k];
+      }
+      __syncwarp();
+      mma_block_impl<P, S, true>(X, LDX, Pab, n1, cx, cy, fx, fy, ai, b, zoff, [&](int ly, int lx, double v) {
+        x[(int64_t)(by + ly - zoff) * n1 + bx + lx] = v;
+      }, false);
+      return;
+    }
+  }
+  if (interior) {
     load_frags<P, S>(fb, fx, fy);                            // interior block: shared fragments (A27)
   } else {
     build_fragx<P, S>(fx, n1, cx, K, M, Vt, lamt);
@@ -2789,13 +2884,13 @@ __global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma(int n1, const double
                                                             const double *__restrict__ lamt,
                                                             const double *__restrict__ b, double *__restrict__ x,
                                                             int c0, int c1, int D, int nb0, int nblk, int zoff,
-                                                            const double *__restrict__ fb, int tlo, int thi) {
+                                                            const double *__restrict__ fb, int tlo, int thi, int inv) {
   extern __shared__ double sm[];
   const int warp = threadIdx.x >> 5;
   const int bid = blockIdx.x * WPC + warp;
   if (bid >= nblk) return;                                   // whole warp exits together
   mma_colour_block<P, S>(sm + warp * Mma2<P, S>::PER, bid, n1, K, M, Vt, lamt, b, x, c0, c1, D, nb0, nblk, zoff, fb,
-                         tlo, thi);
+                         tlo, thi, inv);
 }
 
 // ---------------- batched colour launch: one colour of up to kBatchMax independent problems ----------
@@ -2803,7 +2898,7 @@ __global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma(int n1, const double
 // WPC warps per CTA, one block per warp (block index over the concatenated problems); MAXPS limits the
 // (p, s) bodies compiled in (registers / shared memory are the maximum over them).
 template <int WPC, int MAXPS>
-__global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma_batch(const BatchDesc d, int per) {
+__global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma_batch(const BatchDesc d, int per, int inv) {
   extern __shared__ double sm[];
   const int warp = threadIdx.x >> 5;
   const int g = int(blockIdx.x) * WPC + warp;
@@ -2817,7 +2912,7 @@ __global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma_batch(const BatchDes
   case I:                                                                                                     \
     if (I <= MAXPS)                                                                                           \
       mma_colour_block<P_, S_>(X, bid, q.n1, q.K, q.M, q.V, q.lam, q.b, q.x, q.c0, q.c1, q.D, q.nb0, q.nblk, 0, \
-                               q.fb, q.tlo, q.thi);                                                           \
+                               q.fb, q.tlo, q.thi, inv);                                                      \
     break;
   switch (q.ps) {
     IGA2L_B(0, 1, 3) IGA2L_B(1, 2, 3) IGA2L_B(2, 3, 3) IGA2L_B(3, 4, 3)
@@ -2905,7 +3000,8 @@ void launch2d_mma(int64_t n1, const double *K, const double *M, const double *V,
   ensure_smem(k_schwarz2d_mma<P, S, WPC>, sm);
   const int m = int(n1) - P + 2;
   k_schwarz2d_mma<P, S, WPC><<<(nblk + WPC - 1) / WPC, WPC * 32, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, D,
-                                                                           nb0, nblk, zoff, fb, 2 * P - 1, m - 2 - P);
+                                                                           nb0, nblk, zoff, fb, 2 * P - 1, m - 2 - P,
+                                                                           mma_inv_enabled());
 }
 
 template <int P, int S>
@@ -3291,12 +3387,12 @@ bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double 
          try_schwarz3d_mma<5, 5, 8>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, st) ||
          try_schwarz3d_mma<6, 5, 8>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, st)))
       return true;
-    return try_schwarz3d<1, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st) ||
-           try_schwarz3d<2, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st) ||
-           try_schwarz3d<3, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st) ||
-           try_schwarz3d<4, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st) ||
-           try_schwarz3d<5, 5>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st) ||
-           try_schwarz3d<6, 5>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st);
+    return try_schwarz3d<1, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st, fb) ||
+           try_schwarz3d<2, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st, fb) ||
+           try_schwarz3d<3, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st, fb) ||
+           try_schwarz3d<4, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st, fb) ||
+           try_schwarz3d<5, 5>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st, fb) ||
+           try_schwarz3d<6, 5>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st, fb);
   }
   if (dim != 2) return false;
   const int c0 = colour % D, c1 = (colour / D) % D;
@@ -3406,14 +3502,41 @@ int export_interior_frags(int p, int s, int64_t n1, const double *K, const doubl
   const int cref = (tlo + thi) / 2;
 #define IGA2L_EXP(P_, S_)                                                                                   \
   if (p == P_ && s == S_) {                                                                                 \
-    if (!out) return frag_count<P_, S_>() * 32;                                                            \
+    if (!out) return (frag_count<P_, S_>() + inv_count<S_>()) * 32;                                        \
     k_export_frags<P_, S_><<<1, 32, 0, st>>>(int(n1), cref, K, M, V, lam, out);                            \
-    return frag_count<P_, S_>() * 32;                                                                      \
+    return (frag_count<P_, S_>() + inv_count<S_>()) * 32;                                                  \
   }
   IGA2L_EXP(1, 3) IGA2L_EXP(2, 3) IGA2L_EXP(3, 3) IGA2L_EXP(4, 3) IGA2L_EXP(5, 5) IGA2L_EXP(6, 5) IGA2L_EXP(7, 7)
   IGA2L_EXP(8, 7)
 #undef IGA2L_EXP
   return -1;
+}
+
+// Interior block inverse of the 3D s = 3 pencil kernel, lane-major rows: out[j * 32 + l] = A_B^{-1}[l][j],
+// A_B^{-1}[(lz,ly,lx)][(kz,ky,kx)] = Σ_{a,b,c} Vz[lz][c] Vy[ly][b] Vx[lx][a] Vz[kz][c] Vy[ky][b] Vx[kx][a] / (λa+λb+λc),
+// every axis at the reference centre (A27).
+__global__ void k_export_inv3(int cref, const double *__restrict__ Vt, const double *__restrict__ lamt, double *out) {
+  constexpr int S = 3;
+  const double *V = Vt + (int64_t)cref * S * S, *L = lamt + (int64_t)cref * S;
+  const int l = threadIdx.x, lx = l % 3, ly = (l / 3) % 3, lz = l / 9;
+  for (int j = 0; j < 27; ++j) {
+    const int kx = j % 3, ky = (j / 3) % 3, kz = j / 9;
+    double acc = 0.0;
+    if (l < 27)
+      for (int c = 0; c < S; ++c)
+        for (int bb = 0; bb < S; ++bb)
+          for (int a = 0; a < S; ++a)
+            acc += V[lz * S + c] * V[ly * S + bb] * V[lx * S + a] * V[kz * S + c] * V[ky * S + bb] * V[kx * S + a] /
+                   (L[a] + L[bb] + L[c]);
+    out[j * 32 + l] = acc;
+  }
+}
+
+int export_interior_inv3(int p, int s, int64_t n1, const double *V, const double *lam, double *out, cudaStream_t st) {
+  const int m = int(n1) - p + 2, tlo = 2 * p - 1, thi = m - 2 - p, w = (s - 1) / 2;
+  if (s != 3 || thi - tlo < 2 * w) return -1;
+  if (out) k_export_inv3<<<1, 32, 0, st>>>((tlo + thi) / 2, V, lam, out);
+  return 27 * 32;
 }
 
 int batch_ps_index(int p, int s) {
@@ -3440,7 +3563,7 @@ void launch_schwarz2d_batch(const BatchDesc &d, size_t smem, cudaStream_t st) {
   const int per = int(smem / sizeof(double));
   auto go = [&](auto kern, int w) {
     ensure_smem(kern, smem * w);
-    kern<<<(nb + w - 1) / w, w * 32, smem * w, st>>>(d, per);
+    kern<<<(nb + w - 1) / w, w * 32, smem * w, st>>>(d, per, mma_inv_enabled());
   };
   if (maxps <= 5) {
     if (wpc == 1) go(k_schwarz2d_mma_batch<1, 5>, 1);

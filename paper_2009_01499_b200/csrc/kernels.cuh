@@ -81,6 +81,8 @@ bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double 
                                 const double *fb = nullptr);
 // Interior-block operand fragments of the 2D DMMA kernel (lane-major, A27) into out (device); with
 // out == nullptr returns the number of doubles needed; -1 if no interior block or (p, s) not specialised.
+// 3D s = 3: rows of the interior block inverse (27 x 32 doubles, lane-major); -1 if not applicable
+int export_interior_inv3(int p, int s, int64_t n1, const double *V, const double *lam, double *out, cudaStream_t st);
 int export_interior_frags(int p, int s, int64_t n1, const double *K, const double *M, const double *V,
                           const double *lam, double *out, cudaStream_t st);
 // Temporal blocking (2D, single domain): colours [col0, col0 + ncol), ncol <= kc in {2, 3}, in ONE

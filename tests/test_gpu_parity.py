@@ -325,6 +325,7 @@ TB_CASES = [(1, 3, 48), (2, 3, 64), (3, 3, 96), (4, 3, 64), (5, 5, 96), (6, 5, 4
 @pytest.mark.parametrize("kc", ["2", "3"])
 @pytest.mark.parametrize("p,s,m", TB_CASES, ids=[f"p{c[0]}" for c in TB_CASES])
 def test_temporal_blocking_bitwise(p, s, m, kc, monkeypatch):
+    monkeypatch.setenv("IGA2L_MMA_INV", "0")   # TB runs the FD GEMMs on every block
     monkeypatch.setenv("IGA2L_TB", "0")
     ref = make_ctx(2, p, 1, m, s, "vcycle", 2)
     monkeypatch.setenv("IGA2L_TB", kc)
@@ -397,6 +398,7 @@ def test_exact_coarse_fd_large():
 @pytest.mark.parametrize("p,s,m", [(3, 3, 96), (5, 5, 96), (8, 7, 96)], ids=["p3", "p5", "p8"])
 def test_multiblock_warps_bitwise(p, s, m, bpw, monkeypatch):
     """Several blocks per warp with prefetch (IGA2L_MMA_BPW) == one block per warp, bitwise."""
+    monkeypatch.setenv("IGA2L_MMA_INV", "0")   # the multi-block warps run the FD GEMMs on every block
     monkeypatch.setenv("IGA2L_MMA_BPW", "1")
     ref = make_ctx(2, p, 1, m, s, "vcycle", 2)
     ctx = make_ctx(2, p, 1, m, s, "vcycle", 2)
@@ -442,3 +444,38 @@ def test_iterate_batch_fallback_mixed_dims():
     c3.iterate(b3, r3, iters=2)
     torch.cuda.synchronize()
     assert torch.equal(x2, r2) and torch.equal(x3, r3)
+
+
+# ---- interior block inverse (s^2 <= 32: one A_B^{-1} row per lane instead of the four FD GEMMs) ----
+@pytest.mark.parametrize("p,s,m", [(2, 3, 40), (3, 3, 96), (4, 3, 64), (5, 5, 96), (6, 5, 48)],
+                         ids=["p2", "p3", "p4", "p5", "p6"])
+def test_interior_inverse_matches_fd(p, s, m, monkeypatch):
+    """IGA2L_MMA_INV=1 (opt-in) vs 0 (default): the same sweep up to rounding (both are exact block solves; the
+    default path's parity with the oracle is test_one_sweep_and_phases above)."""
+    monkeypatch.setenv("IGA2L_MMA_INV", "0")
+    ref = make_ctx(2, p, 1, m, s, "vcycle", 2)
+    ctx = make_ctx(2, p, 1, m, s, "vcycle", 2)
+    b, x0 = cu(random_rhs(ctx.N)), cu(initial_guess(ctx.N))
+    x1, x2 = x0.clone(), x0.clone()
+    ref.sweep(b, x1)
+    monkeypatch.setenv("IGA2L_MMA_INV", "1")
+    ctx.sweep(b, x2)
+    scale = float(x1.abs().max())
+    assert float((x1 - x2).abs().max()) <= 1e-11 * scale
+    assert not torch.equal(x1, x2) or m < 4 * (p + s)   # the inverse path actually ran on interior blocks
+
+
+@pytest.mark.parametrize("p,m", [(2, 24), (3, 32)], ids=["p2", "p3"])
+def test_interior_inverse_3d_matches_fd(p, m, monkeypatch):
+    """3D s = 3: IGA2L_S3D_INV=1 (opt-in, A_B^{-1} rows on interior blocks) vs 0 (default, shuffle FD everywhere)."""
+    monkeypatch.setenv("IGA2L_S3D_INV", "0")
+    ref = make_ctx(3, p, 1, m, 3, "vcycle", 2)
+    ctx = make_ctx(3, p, 1, m, 3, "vcycle", 2)
+    b, x0 = cu(random_rhs(ctx.N)), cu(initial_guess(ctx.N))
+    x1, x2 = x0.clone(), x0.clone()
+    ref.sweep(b, x1)
+    monkeypatch.setenv("IGA2L_S3D_INV", "1")
+    ctx.sweep(b, x2)
+    scale = float(x1.abs().max())
+    assert float((x1 - x2).abs().max()) <= 1e-11 * scale
+    assert not torch.equal(x1, x2)
