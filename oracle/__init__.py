@@ -19,6 +19,7 @@ transfer   lumped L2-projection degree transfer, knot-insertion mesh transfer (P
 schwarz    overlapping multiplicative Schwarz: lex and multicolour orders
 multigrid  multicolour Gauss–Seidel V(1,1) on the q-level
 twolevel   Algorithm 1, solve loop, asymptotic rate, dense error operator
+lfa        block local Fourier analysis of the multicolour two-grid         (reading A28)
 
 Parity status: every function is pinned by a ``-m "not gpu"`` test in
 ``tests/test_oracle_*.py``.  Table 4 iteration
