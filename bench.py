@@ -298,17 +298,19 @@ def main():
     achieved = sw_flops_tot / (sw_ms_tot / 1e3) / 1e12
     # dram__bytes_read.sum + dram__bytes_write.sum per launch of this config's dominant kernel, from one
     # `ncu --set full` capture of this bench command (tools/traffic.py writes the file); null if not captured
-    traffic = None
+    traffic, traffic_kernel = None, None
     prof = os.path.join(ROOT, "profiles", "schwarz_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(args.config, {}).get("dram_bytes_per_launch")
+            rec = json.load(open(prof)).get(args.config, {})
+            traffic = rec.get("dram_bytes_per_launch")
+            traffic_kernel = (rec.get("kernel") or [None])[0]
         except Exception:
             traffic = None
     dim = ctxs[0].dim
     if dim == 2:
         roofline = {"bound": "tensor", "achieved": achieved, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                    "frac": achieved / DMMA_PEAK_TFLOPS, "traffic": traffic,
+                    "frac": achieved / DMMA_PEAK_TFLOPS, "traffic": traffic, "traffic_kernel": traffic_kernel,
                     "kernel": "k_schwarz2d_mma (FP64 DMMA block solves, one launch per colour)",
                     "peak_source": "measured FP64 DMMA peak, tools/microbench.cu (profiles/microbench_r01.txt)",
                     "note": ("C2 is latency bound (36/49/100 dependent colours of ~0.7-1.8k blocks); " if args.config == "C2"
@@ -316,7 +318,7 @@ def main():
                             f"achieved = SURVEY 8(d) sweep flops / CUDA-event sweep time over {sw_launches} launches"}
     else:
         roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                    "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                    "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic, "traffic_kernel": traffic_kernel,
                     "kernel": "k_schwarz3d_t (FP64 FMA pencil block solves, one launch per colour)",
                     "peak_source": "derived 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md)",
                     "note": f"achieved = SURVEY 8(d) sweep flops / CUDA-event sweep time over {sw_launches} launches"}
