@@ -135,9 +135,9 @@ int upload(iga2l_ctx *c, T **ptr, const std::vector<T> &v) {
 int upload_band(iga2l_ctx *c, DevBand &d, const BandOp &h) {
   int rc = upload(c, &d.lo, h.lo);
   if (!rc) rc = upload(c, &d.c, h.c);
-  auto span_of = [&](int t) {   // tile input span for the separable 2D transfer (t-row tiles)
-    int sp = 0;
-    for (int r0 = 0; r0 < h.rows; r0 += t) {
+  auto span_of = [&](int t) {   // tile input span for the separable 2D transfer (t-row tiles starting
+    int sp = 0;                 // at ANY row: slab views launch tiles from an arbitrary first row)
+    for (int r0 = 0; r0 < h.rows; ++r0) {
       const int r1 = std::min(h.rows, r0 + t) - 1;
       sp = std::max(sp, h.lo[r1] - h.lo[r0]);
     }
@@ -164,8 +164,19 @@ bool is_device_ptr(const void *p) {
 }
 
 // ---- launch helpers (count our kernel launches) ----
-void L_apply(iga2l_ctx *c, const double *x, const double *b, double *y, double *partial, int mode) {
-  launch_apply(c->dim, c->p, c->n1, c->K1, c->M1, x, b, y, partial, mode, c->st, nullptr, kFull, &c->toe);
+// returns the number of per-CTA partial sums the launch wrote (the count to reduce)
+int L_apply(iga2l_ctx *c, const double *x, const double *b, double *y, double *partial, int mode) {
+  int np = 0;
+  launch_apply(c->dim, c->p, c->n1, c->K1, c->M1, x, b, y, partial, mode, c->st, &np, kFull, &c->toe);
+  c->launch_counter++;
+  return np;
+}
+
+// ||b - A x||^2 -> c->norm (and hist[*count]++ if push_hist): sums exactly the partials written
+void L_norm(iga2l_ctx *c, const double *x, const double *b, bool push_hist) {
+  const int np = L_apply(c, x, b, c->r, c->partial, 1);
+  launch_sum_partials(c->partial, np, c->norm, push_hist ? c->hist : nullptr, push_hist ? c->hist_count : nullptr,
+                      c->hist_cap, c->st);
   c->launch_counter++;
 }
 
@@ -263,9 +274,7 @@ void L_iteration(iga2l_ctx *c, const double *b, double *x, bool with_norm) {
   L_vcycle(c, 0);                                            // A_q e_q = d_q (exact or one V(1,1))
   L_tensor(c, c->dim, c->RT.b, c->lev[0].x, x, c->t1, c->t2, 1);     // u^1 += I_q^p e_q
   if (with_norm) {
-    L_apply(c, x, b, c->r, c->partial, 1);
-    launch_sum_partials(c->partial, c->npartial, c->norm, c->hist, c->hist_count, c->hist_cap, c->st);
-    c->launch_counter++;
+    L_norm(c, x, b, true);
   }
 }
 
@@ -821,7 +830,9 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
       (rc = dalloc(c, &c->hist_count, 1)) || (rc = dalloc(c, &c->hist, 4096)))
     return bail(rc);
   c->hist_cap = 4096;
-  if (cudaMemset(c->hist_count, 0, sizeof(int)) != cudaSuccess) return bail(fail(IGA2L_ECUDA, "cudaMemset"));
+  if (cudaMemset(c->hist_count, 0, sizeof(int)) != cudaSuccess ||
+      cudaMemset(c->partial, 0, size_t(c->npartial) * sizeof(double)) != cudaSuccess)
+    return bail(fail(IGA2L_ECUDA, "cudaMemset"));
   if (cudaMallocHost(&c->pinned, 64 * sizeof(double)) != cudaSuccess) return bail(fail(IGA2L_ENOMEM, "cudaMallocHost"));
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return bail(fail(IGA2L_ECUDA, std::string("setup: ") + cudaGetErrorString(e)));
@@ -945,8 +956,7 @@ int iga2l_residual_norm(iga2l_ctx *c, const double *b, const double *x, double *
     if (int rc = S_scatter(c, sb.ptr, sx.ptr)) return rc;
     if (int rc = S_norm(c, false)) return rc;
   } else {
-    L_apply(c, sx.ptr, sb.ptr, c->r, c->partial, 1);
-    launch_sum_partials(c->partial, c->npartial, c->norm, nullptr, nullptr, 0, c->st);
+    L_norm(c, sx.ptr, sb.ptr, false);
   }
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(c->pinned, c->norm, sizeof(double), cudaMemcpyDeviceToHost, c->st));
@@ -980,8 +990,7 @@ int iga2l_iterate(iga2l_ctx *c, const double *b, double *x, int iters, double *r
   } else {
     if (res_hist) {
       CU(cudaMemsetAsync(c->hist_count, 0, sizeof(int), c->st));
-      L_apply(c, xd, sb.ptr, c->r, c->partial, 1);
-      launch_sum_partials(c->partial, c->npartial, c->norm, c->hist, c->hist_count, c->hist_cap, c->st);
+      L_norm(c, xd, sb.ptr, true);
     }
     if (int rc = run_iterations(c, sb.ptr, xd, iters, res_hist != nullptr)) return rc;
   }
@@ -1010,8 +1019,7 @@ int iga2l_solve(iga2l_ctx *c, const double *b, double *x, double rtol, int maxit
     if (int rc = S_scatter(c, sb.ptr, xd)) return rc;
     if (int rc = S_norm(c, false)) return rc;
   } else {
-    L_apply(c, xd, sb.ptr, c->r, c->partial, 1);
-    launch_sum_partials(c->partial, c->npartial, c->norm, nullptr, nullptr, 0, c->st);
+    L_norm(c, xd, sb.ptr, false);
   }
   CU(cudaMemcpyAsync(c->pinned, c->norm, sizeof(double), cudaMemcpyDeviceToHost, c->st));
   CU(cudaStreamSynchronize(c->st));
