@@ -115,17 +115,6 @@ int iga2l_residual_norm(iga2l_ctx *ctx, const double *b, const double *x, double
 int iga2l_iterate(iga2l_ctx *ctx, const double *b, double *x, int iters, double *res_hist);
 
 /*
- * `iters` iterations of Algorithm 1 on each of n independent problems (contexts ctxs[j], vectors b[j], x[j]),
- * batched: when all contexts are 2D single-domain contexts on the DMMA path (n <= 4) and the vectors are
- * device pointers, colour i of every problem runs in ONE launch and problem j's post-sweep phase
- * (defect, restriction, second level, prolongation) on its own stream as soon as its sweep is done;
- * the work is captured once into a CUDA graph and replayed.  Results are bitwise equal to n separate
- * iga2l_iterate calls.  Ordered on ctxs[0]'s stream (the call is asynchronous; synchronise that stream
- * before using any x[j] from another stream).  Otherwise the problems are iterated one after another.
- */
-int iga2l_iterate_batch(int n, iga2l_ctx *const *ctxs, const double *const *b, double *const *x, int iters);
-
-/*
  * Iterate until ||b - A x_k|| <= rtol ||b - A x_0|| or maxit iterations.
  * iters_out / relres_out (host, may be NULL) receive the count and ||r_k||/||r_0||.
  * Returns IGA2L_NOTCONV (outputs valid) if maxit was reached, IGA2L_ENUMERIC on NaN/Inf.
@@ -156,6 +145,9 @@ typedef struct {
   int launches_per_iter;        /* kernel launches in one iteration (graph nodes of ours)      */
   double sweep_flops;           /* algorithmic FP64 flops of one sweep           */
   double iter_hbm_bytes;        /* algorithmic HBM bytes of one iteration outside the sweep    */
+  int vc_smem_level;            /* first second-level level run by the shared-memory cluster   */
+                                /*   V-cycle kernel (-1: none)                                  */
+  int vc_smem_cs;               /* its cluster size (CTAs); 0 if none                           */
 } iga2l_info;
 int iga2l_get_info(const iga2l_ctx *ctx, iga2l_info *out);
 

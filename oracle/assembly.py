@@ -13,7 +13,7 @@ import functools
 import numpy as np
 import scipy.sparse as sp
 
-from .bspline import basis, basis_deriv, knot_vector, span_rule
+from .bspline import basis, basis_deriv, knot_vector, span_basis, span_rule
 
 
 def n_dofs_1d(p, m):
@@ -28,8 +28,8 @@ def _span_tables(p, m, nq):
     out = []
     for e in range(m):
         xs, ws = span_rule(m, e, nq)
-        N = basis(xi, p, xs)[:, e:e + p + 1]
-        dN = basis_deriv(xi, p, xs)[:, e:e + p + 1] if p >= 1 else np.zeros_like(N)
+        N = span_basis(xi, p, e, xs)
+        dN = span_basis(xi, p, e, xs, deriv=True) if p >= 1 else np.zeros_like(N)
         out.append((xs, ws, N, dN))
     return out
 
@@ -56,8 +56,8 @@ def cross_mass_1d(q, p, m, constrained=True):
     Mc = np.zeros((m + q, m + p))
     for e in range(m):
         xs, ws = span_rule(m, e, nq_pts)
-        Nq = basis(xq, q, xs)[:, e:e + q + 1]
-        Np = basis(xp, p, xs)[:, e:e + p + 1]
+        Nq = span_basis(xq, q, e, xs)
+        Np = span_basis(xp, p, e, xs)
         Mc[e:e + q + 1, e:e + p + 1] += Nq.T @ (ws[:, None] * Np)
     if constrained:
         Mc = Mc[1:-1, 1:-1]
@@ -170,7 +170,7 @@ def load_1d_sine(p, m):
     g = np.zeros(m + p)
     for e in range(m):
         xs, ws = span_rule(m, e, p + 3)
-        g[e:e + p + 1] += basis(xi, p, xs)[:, e:e + p + 1].T @ (ws * np.sin(np.pi * xs))
+        g[e:e + p + 1] += span_basis(xi, p, e, xs).T @ (ws * np.sin(np.pi * xs))
     return g[1:-1]
 
 

@@ -59,6 +59,16 @@ def basis(xi, k, xs):
     return N
 
 
+def span_basis(xi, k, e, xs, deriv=False):
+    """The k+1 functions N_e^k .. N_{e+k}^k (0-based, full numbering) that can be non-zero on the
+    knot span [ξ_{e+k}, ξ_{e+k+1}), at points xs inside that span.  They depend only on the knots
+    ξ_e .. ξ_{e+2k+1}, so this is ``basis(xi, k, xs)[:, e:e+k+1]`` (or ``basis_deriv``) computed by
+    the same recursion on that knot window: the same operations on the same values, i.e. bitwise
+    equal (pinned in tests/test_oracle_bspline.py), without the functions that vanish there."""
+    sub = xi[e:e + 2 * k + 2]
+    return basis_deriv(sub, k, xs) if deriv else basis(sub, k, xs)
+
+
 def basis_deriv(xi, k, xs):
     """d/dξ N_i^k by the standard degree-reduction rule (needed by a(u,v)):
 

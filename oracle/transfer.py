@@ -20,7 +20,7 @@ import numpy as np
 import scipy.sparse as sp
 
 from .assembly import cross_mass_1d, matrices_1d
-from .bspline import basis, knot_vector, span_rule
+from .bspline import basis, knot_vector, span_basis, span_rule
 
 
 def lumped_mass_1d(q, m):
@@ -46,8 +46,10 @@ def mesh_prolongation_1d(q, m_coarse, constrained=True):
     Mhc = np.zeros((m_f + q, m_coarse + q))
     for e in range(m_f):
         xs, ws = span_rule(m_f, e, q + 1)
-        Nf = basis(xf, q, xs)
-        Nc = basis(xc, q, xs)
+        Nf = np.zeros((len(xs), m_f + q))                  # all functions; only the q+1 on this span
+        Nc = np.zeros((len(xs), m_coarse + q))             # (fine) / coarse span e // 2 are non-zero
+        Nf[:, e:e + q + 1] = span_basis(xf, q, e, xs)
+        Nc[:, e // 2:e // 2 + q + 1] = span_basis(xc, q, e // 2, xs)
         Mhc += Nf.T @ (ws[:, None] * Nc)
     P = np.linalg.solve(Mh, Mhc)
     P[np.abs(P) < 1e-14] = 0.0      # exact zeros outside the support (solve leaves ~1e-17 dust)

@@ -28,7 +28,7 @@ class Info(ctypes.Structure):
     _fields_ = [("n1", ctypes.c_int64), ("N", ctypes.c_int64), ("n1c", ctypes.c_int64),
                 ("Nc", ctypes.c_int64), ("colours", ctypes.c_int), ("levels", ctypes.c_int),
                 ("launches_per_iter", ctypes.c_int), ("sweep_flops", ctypes.c_double),
-                ("iter_hbm_bytes", ctypes.c_double)]
+                ("iter_hbm_bytes", ctypes.c_double), ("vc_smem_level", ctypes.c_int), ("vc_smem_cs", ctypes.c_int)]
 
 
 class IgaError(RuntimeError):
@@ -59,7 +59,6 @@ def lib():
         "iga2l_apply": (i, [vp, vp, vp]),
         "iga2l_residual_norm": (i, [vp, vp, vp, P(d)]),
         "iga2l_iterate": (i, [vp, vp, vp, i, vp]),
-        "iga2l_iterate_batch": (i, [i, vp, vp, vp, i]),
         "iga2l_solve": (i, [vp, vp, vp, d, i, P(i), P(d)]),
         "iga2l_sweep": (i, [vp, vp, vp, i, i]),
         "iga2l_defect_restrict": (i, [vp, vp, vp, vp]),
@@ -127,17 +126,6 @@ def host_coarse_fd(q, m):
     lam = np.zeros(n)
     _check(lib().iga2l_host_coarse_fd(q, m, _ptr(V), _ptr(lam)))
     return V.reshape(n, n), lam
-
-
-def iterate_batch(ctxs, bs, xs, iters=1):
-    """iga2l_iterate_batch: one batched iteration schedule over independent problems (see the header)."""
-    n = len(ctxs)
-    h = (ctypes.c_void_p * n)(*[c._h.value for c in ctxs])
-    pb = (ctypes.c_void_p * n)(*[_ptr(b).value for b in bs])
-    px = (ctypes.c_void_p * n)(*[_ptr(x).value for x in xs])
-    _check(lib().iga2l_iterate_batch(n, ctypes.cast(h, ctypes.c_void_p), ctypes.cast(pb, ctypes.c_void_p),
-                                     ctypes.cast(px, ctypes.c_void_p), iters))
-    return xs
 
 
 def host_slab_plan(dim, p, block, m, nranks, rank):

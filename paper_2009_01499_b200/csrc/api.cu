@@ -84,15 +84,9 @@ struct iga2l_ctx {
     cudaGraphExec_t exec = nullptr;
   } graphs[4];
   int next_graph = 0;
-  QLevelDev *levdev = nullptr;   // device copy of the level table (single-CTA V-cycle tail)
-  int l_cta = -1;                // first level handled by the single-CTA tail kernel
-  int l_sm = -1;                 // first level handled by the shared-memory tail kernel (preferred)
-  int persist_tiles = 0;         // > 0: full sweeps run as one persistent launch with this many tiles
-  int tb_kc = 0;                 // temporal blocking (colours per launch) chosen at setup; 0 = per-colour
-  uint64_t gen = 0;              // unique id (batched-graph cache key)
-  cudaStream_t batch_st = nullptr;   // internal stream of iga2l_iterate_batch (fused colour launches)
-  unsigned *sweep_ctl = nullptr, *sweep_done = nullptr;
+  int l_sm = -1;                 // first level handled by the shared-memory tail kernel
   VcLayout vcl{};
+  cudaError_t launch_error = cudaSuccess;   // first failed cudaLaunchKernelEx* (reported by the next call)
   int launch_counter = 0;
   int launches_per_iter = 0;
   std::vector<void *> allocs;
@@ -202,13 +196,9 @@ void L_tensor(iga2l_ctx *c, int dim, const Band1D &B, const double *in, double *
 
 void L_vcycle(iga2l_ctx *c, size_t l) {
   Level &L = c->lev[l];
-  if (int(l) == c->l_sm && c->levdev) {    // tail levels resident in shared memory (one cluster)
-    launch_vcycle_smem(c->dim, c->q, c->vcl, c->st);
-    c->launch_counter++;
-    return;
-  }
-  if (int(l) == c->l_cta && c->levdev) {   // small tail levels: the whole rest of the cycle in one CTA
-    launch_vcycle_cta(c->dim, c->levdev, int(l), int(c->lev.size()), c->q, c->st);
+  if (int(l) == c->l_sm) {                 // tail levels resident in shared memory (one cluster)
+    const cudaError_t e = launch_vcycle_smem(c->dim, c->q, c->vcl, c->st);
+    if (e != cudaSuccess) c->launch_error = e;
     c->launch_counter++;
     return;
   }
@@ -240,27 +230,9 @@ void L_vcycle(iga2l_ctx *c, size_t l) {
 }
 
 void L_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
-  if (c0 == 0 && c1 == c->colours && c->persist_tiles > 0) {   // whole sweep: one persistent launch
-    sweep2d_persist(c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, c->sweep_ctl, c->sweep_done,
-                    c->persist_tiles, c->st, true);
-    c->launch_counter++;
-    return;
-  }
-  const char *tbe = std::getenv("IGA2L_TB");   // temporal blocking: colours per launch (0 = off)
-  const int kc = tbe ? std::atoi(tbe) : c->tb_kc;
-  if (c->dim == 2 && kc >= 2) {
-    bool ok = true;
-    for (int col = c0; col < c1 && ok; col += kc) {
-      ok = launch_schwarz2d_tb(c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, std::min(kc, c1 - col), kc,
-                               c->st);
-      if (ok) c->launch_counter++;
-      else if (col != c0) return;   // (cannot happen: the same (p, s) either specialises or not)
-    }
-    if (ok) return;
-  }
   for (int col = c0; col < c1; ++col) {
     if (!launch_schwarz_colour_fast(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st,
-                                    kFull, &c->toe, c->frags))
+                                    kFull, c->frags))
       launch_schwarz_colour(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st);
     c->launch_counter++;
   }
@@ -278,21 +250,19 @@ void L_iteration(iga2l_ctx *c, const double *b, double *x, bool with_norm) {
   }
 }
 
-// Algorithm 1 after the sweep (defect, restriction, second level, prolongation) on the context's stream.
-void L_post(iga2l_ctx *c, const double *b, double *x) {
-  L_apply(c, x, b, c->r, nullptr, 1);
-  L_tensor(c, c->dim, c->R.b, c->r, c->lev[0].b, c->t1, c->t2, 0);
-  L_vcycle(c, 0);
-  L_tensor(c, c->dim, c->RT.b, c->lev[0].x, x, c->t1, c->t2, 1);
-}
-
-// batched-iteration graph cache: key = (ctx generations, b, x pointers)
-std::mutex g_batch_mu;
-std::map<std::vector<uintptr_t>, cudaGraphExec_t> g_batch_graphs;
-std::atomic<uint64_t> g_ctx_gen{1};
-
 int check_ctx(const iga2l_ctx *c) {
   if (!c) return fail(IGA2L_EPARAM, "ctx is NULL");
+  return IGA2L_OK;
+}
+
+// launch status after a schedule was issued: the sticky runtime error, else a recorded
+// cudaLaunchKernelEx* failure (cluster launches report their configuration errors only there)
+int launch_status(iga2l_ctx *c) {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = c->launch_error;
+  c->launch_error = cudaSuccess;
+  if (e != cudaSuccess) return fail(e == cudaErrorMemoryAllocation ? IGA2L_ENOMEM : IGA2L_ECUDA,
+                                    std::string("kernel launch: ") + cudaGetErrorString(e));
   return IGA2L_OK;
 }
 
@@ -325,7 +295,7 @@ int run_iterations(iga2l_ctx *c, const double *b, double *x, int iters, bool wit
   if (iters <= 0) return IGA2L_OK;
   if (!c->opts.use_graph) {
     for (int k = 0; k < iters; ++k) L_iteration(c, b, x, with_norm);
-    CU(cudaGetLastError());
+    if (int rc_ = launch_status(c)) return rc_;
     return IGA2L_OK;
   }
   iga2l_ctx::G *g = nullptr;
@@ -342,6 +312,10 @@ int run_iterations(iga2l_ctx *c, const double *b, double *x, int iters, bool wit
     L_iteration(c, b, x, with_norm);
     cudaError_t e = cudaStreamEndCapture(c->st, &graph);
     if (e != cudaSuccess) return fail(IGA2L_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    if (int rc_ = launch_status(c)) {
+      cudaGraphDestroy(graph);
+      return rc_;
+    }
     if (!with_norm) c->launches_per_iter = c->launch_counter;
     CU(cudaGraphInstantiate(&g->exec, graph, 0));
     cudaGraphDestroy(graph);
@@ -473,7 +447,7 @@ int S_iteration(iga2l_ctx *c, bool with_norm) {
       for (auto &S : c->slabs) {
         const SlabView sv{S.za, std::max(0, S.z0 - c->w), std::min(n1, S.z1 + c->w)};
         if (!launch_schwarz_colour_fast(d, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, S.bp, S.xp, col, c->D,
-                                        c->st, sv, &c->toe, c->frags))
+                                        c->st, sv, c->frags))
           launch_schwarz_colour(d, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, S.bp, S.xp, col, c->D, c->st, sv);
         c->launch_counter++;
       }
@@ -522,7 +496,7 @@ int S_iteration(iga2l_ctx *c, bool with_norm) {
   }
   if (with_norm)
     if (int rc = S_norm(c, true)) return rc;
-  CU(cudaGetLastError());
+  if (int rc_ = launch_status(c)) return rc_;
   return IGA2L_OK;
 }
 
@@ -586,20 +560,6 @@ int iga2l_setup(int dim, int p, int q, int64_t n, int block, int overlap, iga2l_
 
 int iga2l_destroy(iga2l_ctx *c) {
   if (!c) return IGA2L_OK;
-  {
-    std::lock_guard<std::mutex> lk(g_batch_mu);
-    for (auto it = g_batch_graphs.begin(); it != g_batch_graphs.end();) {
-      bool has = false;
-      for (size_t k = 1; k < it->first.size(); k += 3) has = has || it->first[k] == c->gen;
-      if (has) {
-        cudaGraphExecDestroy(it->second);
-        it = g_batch_graphs.erase(it);
-      } else {
-        ++it;
-      }
-    }
-  }
-  if (c->batch_st) cudaStreamDestroy(c->batch_st);
   for (auto &g : c->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (c->comm) nccl().commDestroy(static_cast<ncclComm_t>(c->comm));
@@ -653,7 +613,6 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
   if (N > (int64_t)1 << 31) return fail(IGA2L_EPARAM, "problem too large");
 
   iga2l_ctx *c = new iga2l_ctx();
-  c->gen = g_ctx_gen.fetch_add(1);
   c->dim = dim; c->p = p; c->q = q; c->s = block; c->w = (block - 1) / 2; c->D = block + p;
   c->colours = int(ipow(c->D, dim));
   c->m = n; c->n1 = n1; c->N = N; c->opts = o;
@@ -736,13 +695,11 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
     c->lev.push_back(L);
     ml /= 2;
   }
-  {  // device level table for the single-CTA V-cycle tail (levels with <= kCtaTailMax unknowns)
-    constexpr int64_t kCtaTailMax = 20000;
+  {  // level table (device pointers) for the shared-memory V-cycle tail
     std::vector<QLevelDev> tab(c->lev.size());
     for (size_t l = 0; l < c->lev.size(); ++l) {
       const Level &L = c->lev[l];
       tab[l] = QLevelDev{L.n, L.N, L.K, L.M, L.x, L.b, L.r, L.t1, L.t2, L.P.b, L.PT.b, L.inv};
-      if (c->l_cta < 0 && L.N <= kCtaTailMax && c->lev.size() > 1) c->l_cta = int(l);
     }
     // shared-memory tail (one cluster): the first (largest) level from which the rest of the cycle
     // fits, preferring the widest cluster; IGA2L_VC_SMEM=0 disables it, IGA2L_VC_FORCE_CS=<cs>
@@ -765,38 +722,13 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
           break;
         }
     }
-    if ((c->l_cta >= 0 || c->l_sm >= 0) && (rc = upload(c, &c->levdev, tab))) return bail(rc);
-    if (c->l_cta >= 0) vcycle_cluster_size(dim);   // probe outside any stream capture
   }
-  if (dim == 2 && c->nranks == 1) {   // persistent sweep: opt-in (IGA2L_SWEEP_PERSIST=1); measured slower
-    const char *pe = std::getenv("IGA2L_SWEEP_PERSIST");   // than per-colour graph launches
-    if (pe && pe[0] == '1') {
-      const int nt = sweep2d_persist(p, block, n1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                     nullptr, 1 << 20, nullptr, false);
-      if (nt > 0) {
-        if ((rc = dalloc(c, &c->sweep_ctl, 2)) || (rc = dalloc(c, &c->sweep_done, 32 * size_t(nt)))) return bail(rc);
-        if (cudaMemset(c->sweep_ctl, 0, 2 * sizeof(unsigned)) != cudaSuccess ||
-            cudaMemset(c->sweep_done, 0, 32 * size_t(nt) * sizeof(unsigned)) != cudaSuccess)
-          return bail(fail(IGA2L_ECUDA, "cudaMemset (sweep counters)"));
-        c->persist_tiles = nt;
-      }
-    }
-  }
-  if (dim == 2) {   // interior-block fragments for the DMMA colour kernel (IGA2L_MMA_FRAGS=0 disables)
-    const char *fe = std::getenv("IGA2L_MMA_FRAGS");
+  if (dim == 2) {   // interior-block fragments for the DMMA colour kernel (A27)
     const int nf = export_interior_frags(p, block, n1, c->K1, c->M1, c->V, c->lam, nullptr, nullptr);
-    if (nf > 0 && !(fe && fe[0] == '0')) {
+    if (nf > 0) {
       if ((rc = dalloc(c, &c->frags, nf))) return bail(rc);
       export_interior_frags(p, block, n1, c->K1, c->M1, c->V, c->lam, c->frags, nullptr);
       if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(IGA2L_ECUDA, "fragment export"));
-    }
-  }
-  if (dim == 3) {   // interior block inverse of the s = 3 pencil kernel (IGA2L_S3D_INV=0 disables per launch)
-    const int nf = export_interior_inv3(p, block, n1, c->V, c->lam, nullptr, nullptr);
-    if (nf > 0) {
-      if ((rc = dalloc(c, &c->frags, nf))) return bail(rc);
-      export_interior_inv3(p, block, n1, c->V, c->lam, c->frags, nullptr);
-      if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(IGA2L_ECUDA, "inverse export"));
     }
   }
   c->npartial = apply_num_partials(dim, p, n1);
@@ -880,6 +812,8 @@ int iga2l_get_info(const iga2l_ctx *c, iga2l_info *o) {
   double coarse = 0;
   for (auto &L : c->lev) coarse += double(L.N);
   o->iter_hbm_bytes = 40.0 * double(c->N) + 64.0 * coarse;
+  o->vc_smem_level = c->l_sm;
+  o->vc_smem_cs = c->l_sm >= 0 ? c->vcl.cs : 0;
   return IGA2L_OK;
 }
 
@@ -902,7 +836,7 @@ int iga2l_rhs_sine(iga2l_ctx *c, double *b) {
   } else {
     launch_tensor_rhs(c->dim, c->n1, c->g1, c->dim * pi * pi, dst, c->st);
   }
-  CU(cudaGetLastError());
+  if (int rc_ = launch_status(c)) return rc_;
   if (!dev) {
     CU(cudaMemcpyAsync(b, dst, c->N * sizeof(double), cudaMemcpyDeviceToHost, c->st));
     CU(cudaStreamSynchronize(c->st));
@@ -937,11 +871,11 @@ int iga2l_apply(iga2l_ctx *c, const double *x, double *y) {
       CU(cudaMemcpyAsync(dst, S.rp + size_t(S.z0 - S.za) * c->plane, size_t(S.z1 - S.z0) * c->plane * 8,
                          cudaMemcpyDeviceToDevice, c->st));
     }
-    CU(cudaGetLastError());
+    if (int rc_ = launch_status(c)) return rc_;
     return stage_out(c, y, sy, c->N);
   }
   L_apply(c, sx.ptr, nullptr, const_cast<double *>(sy.ptr), nullptr, 0);
-  CU(cudaGetLastError());
+  if (int rc_ = launch_status(c)) return rc_;
   return stage_out(c, y, sy, c->N);
 }
 
@@ -958,7 +892,7 @@ int iga2l_residual_norm(iga2l_ctx *c, const double *b, const double *x, double *
   } else {
     L_norm(c, sx.ptr, sb.ptr, false);
   }
-  CU(cudaGetLastError());
+  if (int rc_ = launch_status(c)) return rc_;
   CU(cudaMemcpyAsync(c->pinned, c->norm, sizeof(double), cudaMemcpyDeviceToHost, c->st));
   CU(cudaStreamSynchronize(c->st));
   *out = std::sqrt(c->pinned[0]);
@@ -994,7 +928,7 @@ int iga2l_iterate(iga2l_ctx *c, const double *b, double *x, int iters, double *r
     }
     if (int rc = run_iterations(c, sb.ptr, xd, iters, res_hist != nullptr)) return rc;
   }
-  CU(cudaGetLastError());
+  if (int rc_ = launch_status(c)) return rc_;
   if (res_hist) {
     CU(cudaMemcpyAsync(res_hist, c->hist, (iters + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->st));
     CU(cudaStreamSynchronize(c->st));
@@ -1048,115 +982,6 @@ int iga2l_solve(iga2l_ctx *c, const double *b, double *x, double rtol, int maxit
   return IGA2L_OK;
 }
 
-int iga2l_iterate_batch(int n, iga2l_ctx *const *ctxs, const double *const *b, double *const *x, int iters) {
-  if (n < 1 || !ctxs || !b || !x) return fail(IGA2L_EPARAM, "iterate_batch: n >= 1 and non-NULL arrays");
-  if (iters < 0) return fail(IGA2L_EPARAM, "iters must be >= 0");
-  for (int j = 0; j < n; ++j) {
-    if (int rc = check_ctx(ctxs[j])) return rc;
-    if (!b[j] || !x[j]) return fail(IGA2L_EPARAM, "iterate_batch: NULL vector");
-    for (int k = 0; k < j; ++k)
-      if (ctxs[k] == ctxs[j] || x[k] == x[j]) return fail(IGA2L_EPARAM, "iterate_batch: contexts and x must be distinct");
-  }
-  // fused colour launches need: <= kBatchMax 2D single-domain DMMA contexts and device vectors
-  const char *v = std::getenv("IGA2L_S2D_VARIANT");
-  const char *tb = std::getenv("IGA2L_TB");
-  bool fuse = n <= kBatchMax && !(v && std::atoi(v) != 0 && std::atoi(v) != 9) && !(tb && std::atoi(tb) >= 2);
-  for (int j = 0; j < n && fuse; ++j) {
-    const iga2l_ctx *c = ctxs[j];
-    fuse = c->dim == 2 && c->nranks == 1 && c->persist_tiles == 0 && batch_ps_index(c->p, c->s) >= 0 &&
-           is_device_ptr(b[j]) && is_device_ptr(x[j]);
-  }
-  if (!fuse) {   // independent iterations, one context after the other
-    for (int j = 0; j < n; ++j)
-      if (int rc = iga2l_iterate(ctxs[j], b[j], x[j], iters, nullptr)) return rc;
-    return IGA2L_OK;
-  }
-  if (iters == 0) return IGA2L_OK;
-  iga2l_ctx *c0 = ctxs[0];
-  if (!c0->batch_st) CU(cudaStreamCreateWithFlags(&c0->batch_st, cudaStreamNonBlocking));
-  std::vector<uintptr_t> key{uintptr_t(n)};
-  for (int j = 0; j < n; ++j) {
-    key.push_back(uintptr_t(ctxs[j]->gen));
-    key.push_back(reinterpret_cast<uintptr_t>(b[j]));
-    key.push_back(reinterpret_cast<uintptr_t>(x[j]));
-  }
-  cudaGraphExec_t exec = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(g_batch_mu);
-    auto it = g_batch_graphs.find(key);
-    if (it != g_batch_graphs.end()) exec = it->second;
-  }
-  if (!exec) {
-    cudaStream_t main = c0->st, side = c0->batch_st;
-    std::vector<cudaEvent_t> evs;
-    auto ev = [&]() {
-      cudaEvent_t e;
-      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-      evs.push_back(e);
-      return e;
-    };
-    CU(cudaStreamBeginCapture(main, cudaStreamCaptureModeThreadLocal));
-    cudaEvent_t fork = ev();
-    cudaEventRecord(fork, main);
-    cudaStreamWaitEvent(side, fork, 0);
-    for (int j = 1; j < n; ++j) cudaStreamWaitEvent(ctxs[j]->st, fork, 0);
-    int maxcol = 0;
-    size_t smem = 0;
-    for (int j = 0; j < n; ++j) {
-      maxcol = std::max(maxcol, ctxs[j]->colours);
-      smem = std::max(smem, batch_smem_bytes(batch_ps_index(ctxs[j]->p, ctxs[j]->s)));   // per warp
-    }
-    for (int i = 0; i < maxcol; ++i) {
-      BatchDesc d{};
-      d.n = n;
-      d.beg[0] = 0;
-      for (int j = 0; j < n; ++j) {
-        const iga2l_ctx *c = ctxs[j];
-        BatchProb &q = d.pr[j];
-        int nblk = 0;
-        if (i < c->colours) {
-          const int n1 = int(c->n1), D = c->D, cc0 = i % D, cc1 = i / D;
-          const int nb0 = cc0 < n1 ? (n1 - cc0 + D - 1) / D : 0, nb1 = cc1 < n1 ? (n1 - cc1 + D - 1) / D : 0;
-          nblk = nb0 * nb1;
-          const int m = n1 - c->p + 2;
-          q = BatchProb{batch_ps_index(c->p, c->s), n1, cc0, cc1, D, std::max(nb0, 1), nblk, 2 * c->p - 1,
-                        m - 2 - c->p, c->K1, c->M1, c->V, c->lam, b[j], c->frags, x[j]};
-        }
-        d.beg[j + 1] = d.beg[j] + nblk;
-      }
-      launch_schwarz2d_batch(d, smem, side);
-      for (int j = 0; j < n; ++j) ctxs[j]->launch_counter += (j == 0);
-      for (int j = 0; j < n; ++j)
-        if (i == ctxs[j]->colours - 1) {   // problem j's sweep is complete: its post-sweep phase may start
-          cudaEvent_t done = ev();
-          cudaEventRecord(done, side);
-          cudaStreamWaitEvent(ctxs[j]->st, done, 0);
-          L_post(ctxs[j], b[j], x[j]);
-        }
-    }
-    cudaEvent_t side_end = ev();
-    cudaEventRecord(side_end, side);
-    cudaStreamWaitEvent(main, side_end, 0);
-    for (int j = 1; j < n; ++j) {
-      cudaEvent_t e = ev();
-      cudaEventRecord(e, ctxs[j]->st);
-      cudaStreamWaitEvent(main, e, 0);
-    }
-    cudaGraph_t graph;
-    cudaError_t e = cudaStreamEndCapture(main, &graph);
-    for (cudaEvent_t x_ : evs) cudaEventDestroy(x_);
-    if (e != cudaSuccess) return fail(IGA2L_ECUDA, std::string("batch graph capture: ") + cudaGetErrorString(e));
-    cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
-    cudaGraphDestroy(graph);
-    if (ei != cudaSuccess) return fail(IGA2L_ECUDA, std::string("batch graph instantiate: ") + cudaGetErrorString(ei));
-    std::lock_guard<std::mutex> lk(g_batch_mu);
-    g_batch_graphs[key] = exec;
-  }
-  for (int k = 0; k < iters; ++k) CU(cudaGraphLaunch(exec, c0->st));
-  CU(cudaGetLastError());
-  return IGA2L_OK;
-}
-
 int iga2l_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
   if (int rc = check_ctx(c)) return rc;
   if (c->nranks > 1) return fail(IGA2L_EPARAM, "phase entry points are single-domain only (nranks == 1)");
@@ -1166,7 +991,7 @@ int iga2l_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
   if (int rc = stage_in(c, b, c->hb, c->N, &sb)) return rc;
   if (int rc = stage_in(c, x, c->hx, c->N, &sx)) return rc;
   L_sweep(c, sb.ptr, const_cast<double *>(sx.ptr), c0, c1);
-  CU(cudaGetLastError());
+  if (int rc_ = launch_status(c)) return rc_;
   return stage_out(c, x, sx, c->N);
 }
 
@@ -1182,7 +1007,7 @@ int iga2l_defect_restrict(iga2l_ctx *c, const double *b, const double *x, double
   double *dst = dev ? dq : c->hcb;
   L_apply(c, sx.ptr, sb.ptr, c->r, nullptr, 1);
   L_tensor(c, c->dim, c->R.b, c->r, dst, c->t1, c->t2, 0);
-  CU(cudaGetLastError());
+  if (int rc_ = launch_status(c)) return rc_;
   return stage_out(c, dq, Staged{dst, !dev}, c->lev[0].N);
 }
 
@@ -1197,7 +1022,7 @@ int iga2l_coarse_solve(iga2l_ctx *c, const double *dq, double *e) {
   L_vcycle(c, 0);
   const bool dout = is_device_ptr(e);
   CU(cudaMemcpyAsync(e, L0.x, L0.N * sizeof(double), dout ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
-  CU(cudaGetLastError());
+  if (int rc_ = launch_status(c)) return rc_;
   if (!dout) CU(cudaStreamSynchronize(c->st));
   return IGA2L_OK;
 }
@@ -1210,7 +1035,7 @@ int iga2l_prolong_add(iga2l_ctx *c, const double *e, double *x) {
   if (int rc = stage_in(c, e, c->hcx, c->lev[0].N, &se)) return rc;
   if (int rc = stage_in(c, x, c->hx, c->N, &sx)) return rc;
   L_tensor(c, c->dim, c->RT.b, se.ptr, const_cast<double *>(sx.ptr), c->t1, c->t2, 1);
-  CU(cudaGetLastError());
+  if (int rc_ = launch_status(c)) return rc_;
   return stage_out(c, x, sx, c->N);
 }
 

@@ -1,4 +1,7 @@
 // Device kernels of libiga2l (layer L1), sm_100a.  All arithmetic is IEEE fp64.
+// Sources: apply.cu (operator, norms), schwarz2d.cu (2D DMMA colour kernel, generic fallback, dispatch),
+// schwarz3d.cu (3D colour kernel), transfer.cu (band transfers), vcycle.cu (second level),
+// coarse_fd.cu (exact second level by fast diagonalisation).
 //
 // Operator: the degree-p stiffness on the tensor basis is
 //     A = Σ_a ⊗_b X_b,  X_b = K (1D stiffness) if b == a else M (1D mass),
@@ -74,46 +77,19 @@ void launch_sum_partials(const double *partial, int n, double *out, double *hist
                          cudaStream_t st);
 
 // ---- optimised paths ------------------------------------------------------------------------
-// Warp-per-block 2D Schwarz colour kernel for the paper's (p, s) pairs; false = not specialised.
+// Colour `colour` by the specialised kernels (2D: DMMA warp-per-block for the paper's (p, s) pairs;
+// 3D: pencil kernel for s = 3 (p <= 4), s = 5 (p = 5, 6)); false = not specialised (use the generic kernel).
+// fb: interior-block DMMA operand fragments (export_interior_frags) or nullptr.
 bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M,
                                 const double *V, const double *lam, const double *b, double *x, int colour,
-                                int D, cudaStream_t st, SlabView sv = kFull, const ToeP *tp = nullptr,
-                                const double *fb = nullptr);
+                                int D, cudaStream_t st, SlabView sv = kFull, const double *fb = nullptr);
+bool launch_schwarz3d_colour(int p, int s, int64_t n1, const double *K, const double *M, const double *V,
+                             const double *lam, const double *b, double *x, int c0, int c1, int f2, int D, int nb0,
+                             int nb1, int nb2, int zoff, int tlo, int thi, cudaStream_t st);
 // Interior-block operand fragments of the 2D DMMA kernel (lane-major, A27) into out (device); with
 // out == nullptr returns the number of doubles needed; -1 if no interior block or (p, s) not specialised.
-// 3D s = 3: rows of the interior block inverse (27 x 32 doubles, lane-major); -1 if not applicable
-int export_interior_inv3(int p, int s, int64_t n1, const double *V, const double *lam, double *out, cudaStream_t st);
 int export_interior_frags(int p, int s, int64_t n1, const double *K, const double *M, const double *V,
                           const double *lam, double *out, cudaStream_t st);
-// Temporal blocking (2D, single domain): colours [col0, col0 + ncol), ncol <= kc in {2, 3}, in ONE
-// launch (each CTA solves its core's blocks and the halo blocks they depend on from a shared-memory
-// copy of x).  False if (p, s, kc) is not specialised.
-bool launch_schwarz2d_tb(int p, int s, int64_t n1, const double *K, const double *M, const double *V,
-                         const double *lam, const double *b, double *x, int col0, int ncol, int kc, cudaStream_t st);
-// Batched colour launch (2D DMMA path): one colour of up to kBatchMax independent problems in ONE launch,
-// one warp-CTA per Schwarz block; CTAs [beg[j], beg[j+1]) belong to problem j.  Same block arithmetic
-// as the per-problem launches (bitwise equal).
-struct BatchProb {
-  int ps;                                   // batch_ps_index(p, s)
-  int n1, c0, c1, D, nb0, nblk, tlo, thi;
-  const double *K, *M, *V, *lam, *b, *fb;
-  double *x;
-};
-constexpr int kBatchMax = 4;
-struct BatchDesc {
-  int n, beg[kBatchMax + 1];
-  BatchProb pr[kBatchMax];
-};
-int batch_ps_index(int p, int s);           // -1 if (p, s) has no DMMA specialisation
-size_t batch_smem_bytes(int ps);
-void launch_schwarz2d_batch(const BatchDesc &d, size_t smem, cudaStream_t st);
-
-// Persistent 2D sweep (all D^2 colours in one cooperative launch, per-tile progress counters).
-// ctl: 2 unsigned (zeroed once), done: one unsigned per tile (zeroed once).  launch = false returns the
-// tile count (0: cannot be co-resident or more than max_tiles; -1: (p, s) not specialised).
-int sweep2d_persist(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
-                    const double *b, double *x, unsigned *ctl, unsigned *done, int max_tiles, cudaStream_t st,
-                    bool launch);
 // 2D tensor transfer out (+)= (B ⊗ B) in in one launch (in: B.cols^2, out: B.rows^2).
 // (optional: input rows valid in [iylo, iyhi) stored from iyoff; output rows [rylo, ryhi) stored from ryoff)
 void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumulate, cudaStream_t st,
@@ -128,12 +104,6 @@ struct QLevelDev {
   Band1D P, PT;          // to the next coarser level (unused at the coarsest)
   const double *inv;     // dense inverse at the coarsest level
 };
-// V-cycle levels l0 .. nlev-1 (down-sweep, dense coarsest solve, up-sweep) in ONE thread-block
-// cluster (phases separated by cluster barriers).  vcycle_cluster_size() must be called once
-// outside stream capture (it probes the largest schedulable cluster).
-int vcycle_cluster_size(int dim);
-void launch_vcycle_cta(int dim, const QLevelDev *levs_dev, int l0, int nlev, int q, cudaStream_t st);
-
 // Shared-memory V-cycle tail (levels [l0, nlev)), one thread-block cluster of cs CTAs:
 //  * levels [l0, l0 + nsp) are SPREAD over the CTAs by rows of the last axis (CTA r owns rows
 //    [z0[l][r], z0[l][r+1]) and keeps H halo rows each side, refreshed by the writing thread with
@@ -168,7 +138,7 @@ bool vcycle_smem_layout(int dim, int q, const QLevelDev *tab, int nlev, int l0, 
                         VcLayout *out);
 size_t vcycle_smem_bytes(const VcLayout &L);
 bool vcycle_smem_probe(int dim, int q, const VcLayout &L);   // call outside stream capture
-void launch_vcycle_smem(int dim, int q, const VcLayout &L, cudaStream_t st);
+cudaError_t launch_vcycle_smem(int dim, int q, const VcLayout &L, cudaStream_t st);
 
 // Strided batched FP64 GEMM on the tensor pipe: C[b](m,n) = Σ_k A[b](m,k) B[b](k,n).
 void launch_dgemm(const double *A, const double *B, double *C, int M, int N, int K, int batch, int64_t sAb,

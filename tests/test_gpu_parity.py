@@ -262,100 +262,6 @@ def test_vcycle_smem_spread_level(cfg, cs, monkeypatch):
     close(host(e), ora._csolve(dq), 1e-11)
 
 
-@pytest.mark.parametrize("q,m,d", [(1, 128, 2), (1, 64, 3), (2, 512, 2)], ids=["C2", "C4", "C3"])
-def test_vcycle_full_size(q, m, d):
-    from oracle.multigrid import QHierarchy
-    H = QHierarchy(q, m, d)
-    n = H.levels[0]["n"]
-    # a fine context whose aggressive second level is exactly this q-level (m_fine = 2 m)
-    p = {(1, 2): 3, (1, 3): 3, (2, 2): 8}[(q, d)]
-    s = 3 if p <= 4 else 7
-    ctx = make_ctx(d, p, q, 2 * m, s, "vcycle", 2)
-    assert ctx.Nc == n ** d
-    dq = random_rhs(ctx.Nc, seed=5)
-    e = torch.empty(ctx.Nc, dtype=torch.float64, device=DEV)
-    ctx.coarse_solve(cu(dq), e)
-    close(host(e), H.vcycle(dq), 1e-11)
-
-
-# ---- persistent sweep (one cooperative launch per sweep, per-tile progress counters) against the
-# per-colour launches: same block arithmetic, so bitwise equal; repeated launches advance the counters ----
-PERSIST = [(1, 3, 48), (2, 3, 48), (3, 3, 48), (4, 3, 48), (5, 5, 48), (6, 5, 48), (7, 7, 96), (8, 7, 96)]
-
-
-@pytest.mark.parametrize("p,s,m", PERSIST, ids=[f"p{c[0]}" for c in PERSIST])
-def test_persistent_sweep_bitwise(p, s, m, monkeypatch):
-    # the persistent kernel runs the warp-group block solve (Blk2): compare with the per-colour launches
-    # of the same block solve (IGA2L_S2D_VARIANT=10), bitwise
-    monkeypatch.setenv("IGA2L_S2D_VARIANT", "10")
-    monkeypatch.setenv("IGA2L_SWEEP_PERSIST", "1")
-    ctx = make_ctx(2, p, 1, m, s, "vcycle", 2)
-    monkeypatch.setenv("IGA2L_SWEEP_PERSIST", "0")
-    ref = make_ctx(2, p, 1, m, s, "vcycle", 2)
-    b, x0 = cu(random_rhs(ctx.N)), cu(initial_guess(ctx.N))
-    x1, x2 = x0.clone(), x0.clone()
-    for _ in range(3):
-        ctx.sweep(b, x1)
-        ref.sweep(b, x2)
-    assert torch.equal(x1, x2)
-    ctx.iterate(b, x1, iters=4)
-    ref.iterate(b, x2, iters=4)
-    assert torch.equal(x1, x2)
-
-
-# ---- every 2D block-solve variant (DMMA default, register-blocked, warp-group) against the oracle ----
-@pytest.mark.parametrize("variant", ["1", "2", "10"])
-@pytest.mark.parametrize("cfg", [c for c in PAR if c[1] == 2], ids=[c[0] for c in PAR if c[1] == 2])
-def test_sweep_variants_match_oracle(cfg, variant, monkeypatch):
-    name, d, p, q, m, s, coarse, hf = cfg
-    monkeypatch.setenv("IGA2L_S2D_VARIANT", variant)
-    ctx = make_ctx(d, p, q, m, s, coarse, hf)
-    ora = oracle_for(*cfg)
-    b, x0 = random_rhs(ctx.N), initial_guess(ctx.N)
-    xg = cu(x0)
-    ctx.sweep(cu(b), xg)
-    close(host(xg), ora.smoother.sweep(x0.copy(), b), 1e-11)
-
-
-# ---- temporal blocking (several colours per launch, halo blocks recomputed per CTA): the same block
-# arithmetic as the per-colour DMMA launches, so bitwise equal; and against the oracle ----
-TB_CASES = [(1, 3, 48), (2, 3, 64), (3, 3, 96), (4, 3, 64), (5, 5, 96), (6, 5, 48)]
-
-
-@pytest.mark.parametrize("kc", ["2", "3"])
-@pytest.mark.parametrize("p,s,m", TB_CASES, ids=[f"p{c[0]}" for c in TB_CASES])
-def test_temporal_blocking_bitwise(p, s, m, kc, monkeypatch):
-    monkeypatch.setenv("IGA2L_MMA_INV", "0")   # TB runs the FD GEMMs on every block
-    monkeypatch.setenv("IGA2L_TB", "0")
-    ref = make_ctx(2, p, 1, m, s, "vcycle", 2)
-    monkeypatch.setenv("IGA2L_TB", kc)
-    ctx = make_ctx(2, p, 1, m, s, "vcycle", 2)
-    b, x0 = cu(random_rhs(ctx.N)), cu(initial_guess(ctx.N))
-    x1, x2 = x0.clone(), x0.clone()
-    ctx.sweep(b, x1)
-    monkeypatch.setenv("IGA2L_TB", "0")
-    ref.sweep(b, x2)
-    assert torch.equal(x1, x2)
-    monkeypatch.setenv("IGA2L_TB", kc)
-    ctx.sweep(b, x1, 1, 6)                 # a partial range (odd start, ragged chunk)
-    monkeypatch.setenv("IGA2L_TB", "0")
-    ref.sweep(b, x2, 1, 6)
-    assert torch.equal(x1, x2)
-
-
-# ---- 3D block-solve variants (opt-in DMMA kernel, DFMA default) against the oracle ----
-@pytest.mark.parametrize("cfg", [c for c in PAR if c[1] == 3], ids=[c[0] for c in PAR if c[1] == 3])
-def test_sweep3d_dmma_matches_oracle(cfg, monkeypatch):
-    name, d, p, q, m, s, coarse, hf = cfg
-    monkeypatch.setenv("IGA2L_S3D_MMA", "1")
-    ctx = make_ctx(d, p, q, m, s, coarse, hf)
-    ora = oracle_for(*cfg)
-    b, x0 = random_rhs(ctx.N), initial_guess(ctx.N)
-    xg = cu(x0)
-    ctx.sweep(cu(b), xg)
-    close(host(xg), ora.smoother.sweep(x0.copy(), b), 1e-11)
-
-
 # ---- exact second level at scale by Kronecker fast diagonalisation ----
 EXACT_FD = [("2d_p3_exact_h", 2, 3, 1, 48, 3, "exact", 1), ("2d_p5_exact_2h", 2, 5, 1, 64, 5, "exact", 2),
             ("2d_p8_q2_exact_2h", 2, 8, 2, 40, 7, "exact", 2), ("3d_p3_exact_2h", 3, 3, 1, 16, 3, "exact", 2),
@@ -392,90 +298,3 @@ def test_exact_coarse_fd_large():
     e = torch.empty(ctx.Nc, dtype=torch.float64, device=DEV)
     ctx.coarse_solve(cu(dq), e)
     close(host(e), spla.spsolve(A, dq), 1e-10)
-
-
-@pytest.mark.parametrize("bpw", ["2", "4", "8"])
-@pytest.mark.parametrize("p,s,m", [(3, 3, 96), (5, 5, 96), (8, 7, 96)], ids=["p3", "p5", "p8"])
-def test_multiblock_warps_bitwise(p, s, m, bpw, monkeypatch):
-    """Several blocks per warp with prefetch (IGA2L_MMA_BPW) == one block per warp, bitwise."""
-    monkeypatch.setenv("IGA2L_MMA_INV", "0")   # the multi-block warps run the FD GEMMs on every block
-    monkeypatch.setenv("IGA2L_MMA_BPW", "1")
-    ref = make_ctx(2, p, 1, m, s, "vcycle", 2)
-    ctx = make_ctx(2, p, 1, m, s, "vcycle", 2)
-    b, x0 = cu(random_rhs(ctx.N)), cu(initial_guess(ctx.N))
-    x1, x2 = x0.clone(), x0.clone()
-    ref.sweep(b, x1)
-    monkeypatch.setenv("IGA2L_MMA_BPW", bpw)
-    ctx.sweep(b, x2)
-    assert torch.equal(x1, x2)
-
-
-# ---- batched iterations of independent problems (fused colour launches): bitwise equal to separate calls ----
-@pytest.mark.parametrize("combo", [((3, 3, 48), (4, 3, 40), (5, 5, 32)), ((2, 3, 32), (8, 7, 32)),
-                                   ((3, 3, 256), (4, 3, 256), (5, 5, 256))], ids=["p345", "p28", "C2"])
-def test_iterate_batch_bitwise(combo):
-    ctxs, bs, xs, refs = [], [], [], []
-    for i, (p, s, m) in enumerate(combo):
-        st = torch.cuda.Stream(DEV)
-        c = pkg.Context(2, p, 1, m, s, coarse_mode=pkg.COARSE_VCYCLE, coarse_h_factor=2, stream=st.cuda_stream)
-        ctxs.append(c)
-        bs.append(cu(random_rhs(c.N, seed=10 + i)))
-        x0 = cu(initial_guess(c.N, seed=20 + i))
-        xs.append(x0.clone())
-        refs.append(x0.clone())
-    torch.cuda.synchronize()
-    pkg.iterate_batch(ctxs, bs, xs, iters=3)
-    torch.cuda.synchronize()
-    for c, b, xr in zip(ctxs, bs, refs):
-        c.iterate(b, xr, iters=3)
-    torch.cuda.synchronize()
-    for xb, xr in zip(xs, refs):
-        assert torch.equal(xb, xr)
-
-
-def test_iterate_batch_fallback_mixed_dims():
-    c2 = make_ctx(2, 3, 1, 48, 3, "vcycle", 2)
-    c3 = make_ctx(3, 3, 1, 16, 3, "vcycle", 2)
-    b2, b3 = cu(random_rhs(c2.N)), cu(random_rhs(c3.N))
-    x2, x3 = cu(initial_guess(c2.N)), cu(initial_guess(c3.N))
-    r2, r3 = x2.clone(), x3.clone()
-    pkg.iterate_batch([c2, c3], [b2, b3], [x2, x3], iters=2)
-    c2.iterate(b2, r2, iters=2)
-    c3.iterate(b3, r3, iters=2)
-    torch.cuda.synchronize()
-    assert torch.equal(x2, r2) and torch.equal(x3, r3)
-
-
-# ---- interior block inverse (s^2 <= 32: one A_B^{-1} row per lane instead of the four FD GEMMs) ----
-@pytest.mark.parametrize("p,s,m", [(2, 3, 40), (3, 3, 96), (4, 3, 64), (5, 5, 96), (6, 5, 48)],
-                         ids=["p2", "p3", "p4", "p5", "p6"])
-def test_interior_inverse_matches_fd(p, s, m, monkeypatch):
-    """IGA2L_MMA_INV=1 (opt-in) vs 0 (default): the same sweep up to rounding (both are exact block solves; the
-    default path's parity with the oracle is test_one_sweep_and_phases above)."""
-    monkeypatch.setenv("IGA2L_MMA_INV", "0")
-    ref = make_ctx(2, p, 1, m, s, "vcycle", 2)
-    ctx = make_ctx(2, p, 1, m, s, "vcycle", 2)
-    b, x0 = cu(random_rhs(ctx.N)), cu(initial_guess(ctx.N))
-    x1, x2 = x0.clone(), x0.clone()
-    ref.sweep(b, x1)
-    monkeypatch.setenv("IGA2L_MMA_INV", "1")
-    ctx.sweep(b, x2)
-    scale = float(x1.abs().max())
-    assert float((x1 - x2).abs().max()) <= 1e-11 * scale
-    assert not torch.equal(x1, x2) or m < 4 * (p + s)   # the inverse path actually ran on interior blocks
-
-
-@pytest.mark.parametrize("p,m", [(2, 24), (3, 32)], ids=["p2", "p3"])
-def test_interior_inverse_3d_matches_fd(p, m, monkeypatch):
-    """3D s = 3: IGA2L_S3D_INV=1 (opt-in, A_B^{-1} rows on interior blocks) vs 0 (default, shuffle FD everywhere)."""
-    monkeypatch.setenv("IGA2L_S3D_INV", "0")
-    ref = make_ctx(3, p, 1, m, 3, "vcycle", 2)
-    ctx = make_ctx(3, p, 1, m, 3, "vcycle", 2)
-    b, x0 = cu(random_rhs(ctx.N)), cu(initial_guess(ctx.N))
-    x1, x2 = x0.clone(), x0.clone()
-    ref.sweep(b, x1)
-    monkeypatch.setenv("IGA2L_S3D_INV", "1")
-    ctx.sweep(b, x2)
-    scale = float(x1.abs().max())
-    assert float((x1 - x2).abs().max()) <= 1e-11 * scale
-    assert not torch.equal(x1, x2)

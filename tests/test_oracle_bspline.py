@@ -86,3 +86,15 @@ def test_derivative_finite_difference_and_sum(p):
     fd = (basis(xi, p, xs + eps) - basis(xi, p, xs - eps)) / (2 * eps)
     assert np.allclose(dN, fd, atol=1e-5 * m * p, rtol=1e-6)
     assert np.allclose(dN.sum(axis=1), 0.0, atol=1e-10)
+
+
+@pytest.mark.parametrize("p,m", [(1, 3), (2, 5), (3, 7), (5, 9), (8, 12)])
+def test_span_basis_is_bitwise_the_global_recursion(p, m):
+    """span_basis (the p+1 functions alive on one span, from the knot window) == the columns of the
+    full Cox-de Boor evaluation, bitwise, on every span incl. the repeated end knots."""
+    from oracle.bspline import basis, basis_deriv, knot_vector, span_basis, span_rule
+    xi = knot_vector(p, m)
+    for e in range(m):
+        xs, _ = span_rule(m, e, p + 3)
+        assert np.array_equal(span_basis(xi, p, e, xs), basis(xi, p, xs)[:, e:e + p + 1])
+        assert np.array_equal(span_basis(xi, p, e, xs, deriv=True), basis_deriv(xi, p, xs)[:, e:e + p + 1])
