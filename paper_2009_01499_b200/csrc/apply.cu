@@ -497,15 +497,25 @@ __global__ void k_axpy(double *__restrict__ y, const double *__restrict__ x, int
 }  // namespace
 
 int apply_num_partials(int dim, int p, int64_t n1) {
-  (void)p;
   if (dim == 2) {   // the most tiles any 2D apply variant launches
     const int64_t v1 = ((n1 + A2X - 1) / A2X) * ((n1 + A2Y - 1) / A2Y), v2 = ((n1 + 15) / 16) * ((n1 + 15) / 16);
-    return int(std::max(v1, v2));
+    int v3 = 0;
+    launch_apply_stream(dim, p, n1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, &v3, kFull,
+                        nullptr, true);
+    return int(std::max<int64_t>(std::max(v1, v2), v3));
   }
   const int64_t v1 = ((n1 + A3X - 1) / A3X) * ((n1 + A3Y - 1) / A3Y) * ((n1 + A3Z - 1) / A3Z);
   const int64_t v2 = ((n1 + A3TX - 1) / A3TX) * ((n1 + A3TY - 1) / A3TY) * apply3d_zchunks(n1, int(n1));
-  return int(std::max(v1, v2));
+  int v3 = 0;
+  launch_apply_stream(dim, p, n1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, &v3, kFull, nullptr,
+                      true);
+  return int(std::max<int64_t>(std::max(v1, v2), v3));
 }
+
+static const bool g_apply_stream = [] {
+  const char *e = std::getenv("IGA2L_APPLY_STREAM");   // 0: the tiled kernels below (A/B and fallback)
+  return !(e && e[0] == '0');
+}();
 
 void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, const double *x, const double *b,
                   double *y, double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv, const ToeP *tp) {
@@ -513,6 +523,8 @@ void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, 
   const int nz = sv.zhi - sv.zlo;
   const size_t sm = apply_smem(dim, p);
   if (nz <= 0) return;
+  if (g_apply_stream && launch_apply_stream(dim, p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp, false))
+    return;
   if (dim == 2 &&
       (try_apply2d<1>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
        try_apply2d<2>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||

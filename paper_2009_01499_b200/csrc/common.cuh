@@ -41,6 +41,39 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
+// ---- TMA (cp.async.bulk.tensor) + mbarrier ------------------------------------------------------
+// Vectors are addressed through 1D tensor maps (element-granular coordinates, so rows of any length n1
+// -- odd n1 makes 2D/3D maps impossible: their strides must be multiples of 16 bytes); coordinates
+// outside [0, N) are zero-filled by the hardware.  Destination rows in shared memory are 128-byte aligned.
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return unsigned(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// count doubles from element c0 of the vector behind `map` -> dst (box = the map's box size)
+__device__ __forceinline__ void tma_load_1d(double *dst, const void *map, int c0, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// host: 1D tensor map over n doubles at ptr with a box of `box` elements (box * 8 % 16 == 0, box <= 256).
+// Returns false if the driver entry point is missing or the encode fails.
+bool make_tmap_1d(void *map64, const double *ptr, int64_t n, int box);
+
 template <typename F>
 inline void ensure_smem(F *kernel, size_t bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));

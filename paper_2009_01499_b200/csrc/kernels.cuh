@@ -45,6 +45,11 @@ void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, 
                   const double *b, double *y, double *partial, int mode, cudaStream_t st, int *nparts,
                   SlabView sv = kFull, const ToeP *tp = nullptr);
 int apply_num_partials(int dim, int p, int64_t n1);
+// The TMA streaming apply (stream.cu), used by launch_apply for 1 <= p <= 8 unless IGA2L_APPLY_STREAM=0.
+// count_only: only report *nparts.  False if not launched (p unsupported, tensor map encode failed).
+bool launch_apply_stream(int dim, int p, int64_t n1, const double *K, const double *M, const double *x, const double *b,
+                         double *y, double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv,
+                         const ToeP *tp, bool count_only);
 
 // ---- multicolour Schwarz: one colour ---------------------------------------------------------
 // Blocks centred at c = col + D*j (per axis) are solved in parallel (A-decoupled, reading A4):

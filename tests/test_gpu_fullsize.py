@@ -134,8 +134,8 @@ def test_vcycle_smem_spread_3d_q2(m, cs, monkeypatch):
 # ---- C3 transfers at full size (the separable 32x32-tile kernel bench.py runs) and that kernel forced
 # at small sizes, against the oracle's Kronecker R ----
 @pytest.mark.parametrize("force", [None, "32"], ids=["auto", "sep32"])
-@pytest.mark.parametrize("d,p,q,m,s", [(2, 8, 2, 1024, 7), (2, 8, 2, 32, 7), (2, 3, 1, 48, 3), (2, 5, 1, 36, 5)],
-                         ids=["C3", "p8_m32", "p3_m48", "p5_m36"])
+@pytest.mark.parametrize("d,p,q,m,s", [(2, 8, 2, 1024, 7), (2, 8, 2, 32, 7), (2, 3, 1, 48, 3), (2, 5, 1, 40, 5)],
+                         ids=["C3", "p8_m32", "p3_m48", "p5_m40"])
 def test_transfers_2d(d, p, q, m, s, force, monkeypatch):
     if force:
         monkeypatch.setenv("IGA2L_TRANSFER_SEP", force)
