@@ -10,75 +10,6 @@ namespace cg = cooperative_groups;
 namespace iga2l {
 namespace {
 
-// =============================== q-level kernels ==========================================
-template <int DIM>
-__device__ __forceinline__ double q_apply_point(int q, int n, const double *K, const double *M, const double *x,
-                                                int ix, int iy, int iz, double *diag) {
-  const int W = 2 * q + 1;
-  double acc = 0.0;
-  const double *kx = K + (int64_t)ix * W, *mx = M + (int64_t)ix * W;
-  const double *ky = K + (int64_t)iy * W, *my = M + (int64_t)iy * W;
-  if (DIM == 2) {
-    for (int u = 0; u < W; ++u) {
-      const int jy = iy + u - q;
-      if (jy < 0 || jy >= n) continue;
-      for (int t = 0; t < W; ++t) {
-        const int jx = ix + t - q;
-        if (jx < 0 || jx >= n) continue;
-        acc = fma(kx[t] * my[u] + mx[t] * ky[u], x[(int64_t)jy * n + jx], acc);
-      }
-    }
-    *diag = kx[q] * my[q] + mx[q] * ky[q];
-  } else {
-    const double *kz = K + (int64_t)iz * W, *mz = M + (int64_t)iz * W;
-    for (int v = 0; v < W; ++v) {
-      const int jz = iz + v - q;
-      if (jz < 0 || jz >= n) continue;
-      for (int u = 0; u < W; ++u) {
-        const int jy = iy + u - q;
-        if (jy < 0 || jy >= n) continue;
-        for (int t = 0; t < W; ++t) {
-          const int jx = ix + t - q;
-          if (jx < 0 || jx >= n) continue;
-          const double a = kx[t] * my[u] * mz[v] + mx[t] * ky[u] * mz[v] + mx[t] * my[u] * kz[v];
-          acc = fma(a, x[((int64_t)jz * n + jy) * n + jx], acc);
-        }
-      }
-    }
-    *diag = kx[q] * my[q] * mz[q] + mx[q] * ky[q] * mz[q] + mx[q] * my[q] * kz[q];
-  }
-  return acc;
-}
-
-template <int DIM>
-__global__ void k_q_gs(int q, int n, const double *__restrict__ K, const double *__restrict__ M,
-                       const double *__restrict__ b, double *__restrict__ x, int c0, int c1, int c2, int na0,
-                       int na1, int64_t total) {
-  const int st = q + 1;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int ix = c0 + st * int(idx % na0);
-    const int iy = c1 + st * int((idx / na0) % na1);
-    const int iz = (DIM == 3) ? c2 + st * int(idx / ((int64_t)na0 * na1)) : 0;
-    double dg;
-    const double ax = q_apply_point<DIM>(q, n, K, M, x, ix, iy, iz, &dg);
-    const int64_t g = ((int64_t)iz * n + iy) * n + ix;
-    x[g] += (b[g] - ax) / dg;
-  }
-}
-
-template <int DIM>
-__global__ void k_q_resid(int q, int n, const double *__restrict__ K, const double *__restrict__ M,
-                          const double *__restrict__ b, const double *__restrict__ x, double *__restrict__ r,
-                          int64_t total) {
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int ix = int(idx % n), iy = int((idx / n) % n), iz = (DIM == 3) ? int(idx / ((int64_t)n * n)) : 0;
-    double dg;
-    r[idx] = b[idx] - q_apply_point<DIM>(q, n, K, M, x, ix, iy, iz, &dg);
-  }
-}
-
 __global__ void k_dense_mv(int N, const double *__restrict__ A, const double *__restrict__ b, double *__restrict__ x) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= N) return;
@@ -89,29 +20,6 @@ __global__ void k_dense_mv(int N, const double *__restrict__ A, const double *__
 }
 
 }  // namespace
-
-void launch_q_gs_colour(int dim, int q, int n, const double *K, const double *M, const double *b, double *x,
-                        int colour, cudaStream_t st) {
-  const int st_ = q + 1;
-  const int c0 = colour % st_, c1 = (colour / st_) % st_, c2 = (dim == 3) ? colour / (st_ * st_) : 0;
-  if (c0 >= n || c1 >= n || c2 >= n) return;
-  const int na0 = (n - c0 + q) / st_, na1 = (n - c1 + q) / st_, na2 = (dim == 3) ? (n - c2 + q) / st_ : 1;
-  const int64_t total = (int64_t)na0 * na1 * na2;
-  if (dim == 2)
-    k_q_gs<2><<<grid_for(total, 128), 128, 0, st>>>(q, n, K, M, b, x, c0, c1, c2, na0, na1, total);
-  else
-    k_q_gs<3><<<grid_for(total, 128), 128, 0, st>>>(q, n, K, M, b, x, c0, c1, c2, na0, na1, total);
-}
-
-void launch_q_residual(int dim, int q, int n, const double *K, const double *M, const double *b, const double *x,
-                       double *r, cudaStream_t st) {
-  int64_t total = (int64_t)n * n;
-  if (dim == 3) total *= n;
-  if (dim == 2)
-    k_q_resid<2><<<grid_for(total, 128), 128, 0, st>>>(q, n, K, M, b, x, r, total);
-  else
-    k_q_resid<3><<<grid_for(total, 128), 128, 0, st>>>(q, n, K, M, b, x, r, total);
-}
 
 void launch_dense_mv(int N, const double *Ainv, const double *b, double *x, cudaStream_t st) {
   const int warps_per_block = 8;
@@ -248,6 +156,41 @@ __device__ __forceinline__ double tensor_point_acc(const XA &xa, int nin, int W,
     s = fma(cz[kz], u, s);
   }
   return s;
+}
+
+// ---- level-by-level kernels for the q-levels above the shared-memory tail (same point arithmetic as the
+// tail kernel: q_point_acc, compile-time q, unrolled stencil) ----
+// one (q+1)^d Gauss-Seidel colour (A11): every point of the colour, x_i += (b_i - (A x)_i) / a_ii
+template <int DIM, int Q>
+__global__ void __launch_bounds__(128) k_q_gs(int n, const double *__restrict__ K, const double *__restrict__ M,
+                                              const double *__restrict__ b, double *__restrict__ x, int c0, int c1,
+                                              int c2, int na0, int na1, int64_t total) {
+  constexpr int st = Q + 1;
+  const XOff<DIM> xa{x, n, 0};
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int ix = c0 + st * int(idx % na0);
+    const int iy = c1 + st * int((idx / na0) % na1);
+    const int iz = (DIM == 3) ? c2 + st * int(idx / ((int64_t)na0 * na1)) : 0;
+    double dg;
+    const double ax = q_point_acc<DIM, Q>(n, K, M, xa, ix, iy, iz, &dg);
+    const int64_t g = ((int64_t)iz * n + iy) * n + ix;
+    x[g] += (b[g] - ax) / dg;
+  }
+}
+
+// r = b - A x on a whole level
+template <int DIM, int Q>
+__global__ void __launch_bounds__(128) k_q_resid(int n, const double *__restrict__ K, const double *__restrict__ M,
+                                                 const double *__restrict__ b, const double *__restrict__ x,
+                                                 double *__restrict__ r, int64_t total) {
+  const XOff<DIM> xa{x, n, 0};
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int ix = int(idx % n), iy = int((idx / n) % n), iz = (DIM == 3) ? int(idx / ((int64_t)n * n)) : 0;
+    double dg;
+    r[idx] = b[idx] - q_point_acc<DIM, Q>(n, K, M, xa, ix, iy, iz, &dg);
+  }
 }
 
 // Thread-level work distribution over the points of a box of rows [zlo, zhi) of the last axis;
@@ -566,6 +509,31 @@ __global__ void __launch_bounds__(512, 1) k_vcycle_smem(const VcLayout L) {
 }
 
 }  // namespace
+
+void launch_q_gs_colour(int dim, int q, int n, const double *K, const double *M, const double *b, double *x,
+                        int colour, cudaStream_t st) {
+  const int st_ = q + 1;
+  const int c0 = colour % st_, c1 = (colour / st_) % st_, c2 = (dim == 3) ? colour / (st_ * st_) : 0;
+  if (c0 >= n || c1 >= n || c2 >= n) return;
+  const int na0 = (n - c0 + q) / st_, na1 = (n - c1 + q) / st_, na2 = (dim == 3) ? (n - c2 + q) / st_ : 1;
+  const int64_t total = (int64_t)na0 * na1 * na2;
+  const int g = grid_for(total, 128);
+  if (dim == 2 && q == 1) k_q_gs<2, 1><<<g, 128, 0, st>>>(n, K, M, b, x, c0, c1, c2, na0, na1, total);
+  else if (dim == 2) k_q_gs<2, 2><<<g, 128, 0, st>>>(n, K, M, b, x, c0, c1, c2, na0, na1, total);
+  else if (q == 1) k_q_gs<3, 1><<<g, 128, 0, st>>>(n, K, M, b, x, c0, c1, c2, na0, na1, total);
+  else k_q_gs<3, 2><<<g, 128, 0, st>>>(n, K, M, b, x, c0, c1, c2, na0, na1, total);
+}
+
+void launch_q_residual(int dim, int q, int n, const double *K, const double *M, const double *b, const double *x,
+                       double *r, cudaStream_t st) {
+  int64_t total = (int64_t)n * n;
+  if (dim == 3) total *= n;
+  const int g = grid_for(total, 128);
+  if (dim == 2 && q == 1) k_q_resid<2, 1><<<g, 128, 0, st>>>(n, K, M, b, x, r, total);
+  else if (dim == 2) k_q_resid<2, 2><<<g, 128, 0, st>>>(n, K, M, b, x, r, total);
+  else if (q == 1) k_q_resid<3, 1><<<g, 128, 0, st>>>(n, K, M, b, x, r, total);
+  else k_q_resid<3, 2><<<g, 128, 0, st>>>(n, K, M, b, x, r, total);
+}
 
 bool vcycle_smem_layout(int dim, int q, const QLevelDev *tab, int nlev, int l0, int cs, size_t max_bytes,
                         VcLayout *out) {
