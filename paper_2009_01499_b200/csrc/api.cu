@@ -217,7 +217,10 @@ void L_vcycle(iga2l_ctx *c, size_t l) {
     launch_q_gs_colour(c->dim, c->q, L.n, L.K, L.M, L.b, L.x, col, c->st);
     c->launch_counter++;
   }
-  launch_q_residual(c->dim, c->q, L.n, L.K, L.M, L.b, L.x, L.r, c->st);
+  if (c->dim == 3)   // r = b - A_q x: the streaming sum-factorised operator kernel (degree q tables, no partials)
+    launch_apply(3, c->q, L.n, L.K, L.M, L.x, L.b, L.r, nullptr, 1, c->st, nullptr, kFull, nullptr);
+  else
+    launch_q_residual(c->dim, c->q, L.n, L.K, L.M, L.b, L.x, L.r, c->st);
   c->launch_counter++;
   Level &C = c->lev[l + 1];
   L_tensor(c, c->dim, L.PT.b, L.r, C.b, L.t1, L.t2, 0);   // restriction P^T (reading A8)
