@@ -235,7 +235,7 @@ void L_vcycle(iga2l_ctx *c, size_t l) {
 void L_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
   for (int col = c0; col < c1; ++col) {
     if (!launch_schwarz_colour_fast(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st,
-                                    kFull, c->frags))
+                                    kFull, c->frags, &c->toe))
       launch_schwarz_colour(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st);
     c->launch_counter++;
   }
@@ -450,7 +450,7 @@ int S_iteration(iga2l_ctx *c, bool with_norm) {
       for (auto &S : c->slabs) {
         const SlabView sv{S.za, std::max(0, S.z0 - c->w), std::min(n1, S.z1 + c->w)};
         if (!launch_schwarz_colour_fast(d, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, S.bp, S.xp, col, c->D,
-                                        c->st, sv, c->frags))
+                                        c->st, sv, c->frags, &c->toe))
           launch_schwarz_colour(d, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, S.bp, S.xp, col, c->D, c->st, sv);
         c->launch_counter++;
       }

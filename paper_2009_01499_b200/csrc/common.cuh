@@ -73,6 +73,9 @@ __device__ __forceinline__ void tma_load_1d(double *dst, const void *map, int c0
 // host: 1D tensor map over n doubles at ptr with a box of `box` elements (box * 8 % 16 == 0, box <= 256).
 // Returns false if the driver entry point is missing or the encode fails.
 bool make_tmap_1d(void *map64, const double *ptr, int64_t n, int box);
+// the same with 128-byte swizzle (box * 8 <= 128): chunk c of a row landing at a 128-byte aligned shared
+// address A goes to chunk c ^ ((A >> 7) & 7)
+bool make_tmap_1d_swz128(void *map64, const double *ptr, int64_t n, int box);
 
 template <typename F>
 inline void ensure_smem(F *kernel, size_t bytes) {

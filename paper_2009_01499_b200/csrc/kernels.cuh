@@ -87,10 +87,11 @@ void launch_sum_partials(const double *partial, int n, double *out, double *hist
 // fb: interior-block DMMA operand fragments (export_interior_frags) or nullptr.
 bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M,
                                 const double *V, const double *lam, const double *b, double *x, int colour,
-                                int D, cudaStream_t st, SlabView sv = kFull, const double *fb = nullptr);
+                                int D, cudaStream_t st, SlabView sv = kFull, const double *fb = nullptr,
+                                const ToeP *tp = nullptr);
 bool launch_schwarz3d_colour(int p, int s, int64_t n1, const double *K, const double *M, const double *V,
                              const double *lam, const double *b, double *x, int c0, int c1, int f2, int D, int nb0,
-                             int nb1, int nb2, int zoff, int tlo, int thi, cudaStream_t st);
+                             int nb1, int nb2, int zoff, int tlo, int thi, cudaStream_t st, const ToeP *tp);
 // Interior-block operand fragments of the 2D DMMA kernel (lane-major, A27) into out (device); with
 // out == nullptr returns the number of doubles needed; -1 if no interior block or (p, s) not specialised.
 int export_interior_frags(int p, int s, int64_t n1, const double *K, const double *M, const double *V,

@@ -517,7 +517,7 @@ void launch_schwarz_colour(int dim, int p, int s, int64_t n1, const double *K, c
 
 bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M, const double *V,
                                 const double *lam, const double *b, double *x, int colour, int D, cudaStream_t st,
-                                SlabView sv, const double *fb) {
+                                SlabView sv, const double *fb, const ToeP *tp) {
   if (sv.zhi < 0) sv = SlabView{0, 0, int(n1)};
   if (dim == 3) {
     const int c0 = colour % D, c1 = (colour / D) % D, c2 = colour / (D * D);
@@ -528,7 +528,7 @@ bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double 
     const int m = int(n1) - p + 2;
     const int tlo = 2 * p - 1, thi = m - 2 - p;            // translation-invariant rows (toeplitz_rows)
     const int z = sv.zoff;
-    return launch_schwarz3d_colour(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st);
+    return launch_schwarz3d_colour(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, z, tlo, thi, st, tp);
   }
   if (dim != 2) return false;
   const int c0 = colour % D, c1 = (colour / D) % D;

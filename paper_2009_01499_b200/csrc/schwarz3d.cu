@@ -1,42 +1,60 @@
 // 3D multicolour Schwarz colour kernel (reading A4, A25): one CTA per block, register-blocked
 // pencil passes for the sum-factorised block residual, then fast diagonalisation.  See kernels.cuh.
+#include <cuda.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace iga2l {
 namespace {
 
-// ---------------- 3D Schwarz colour kernel, compile-time (p, s): one CTA per block ------------
-// Same arithmetic as k_schwarz<3> (sum-factorised block residual over the (s+2p)^3 window, then
-// fast diagonalisation), register-blocked: every pass maps one thread to a PENCIL (a line of the
-// window along the contracted axis), loads it once into registers and produces all s outputs of that
-// line.  A pass along an axis whose s block rows are all translation-invariant rows (tlo..thi, made
-// bitwise equal at setup) keeps the 2(2p+1) band coefficients in registers; otherwise they are read
-// per row from shared memory.
+// ---------------- v4: one block per CTA, per-thread roles fixed up front ----------------------------
+// Sum-factorised block residual (pencil passes x, y, z) and fast diagonalisation; per block:
+// the window is staged by rows (one division per row, Wn 8-byte cp.async with a per-block column range),
+// band rows / FD tables of Toeplitz axes (reading A27) come from the kernel parameter (constant bank) and
+// are only loaded for boundary axes, and every index is decoded once per thread.
+template <int P, int S>
+struct B4 {
+  static constexpr int W = 2 * P + 1, Wn = S + 2 * P, w = (S - 1) / 2, S2 = S * S, S3 = S2 * S, Wn2 = Wn * Wn;
+  static constexpr int OPa = Wn2 * Wn, OPb = OPa + Wn2 * S, OXc = OPb + Wn2 * S, OR = OXc + S3, OQ = OR + S3,
+                       OBb = OQ + S3, OTk = OBb + S3, OTm = OTk + 3 * S * W, OVs = OTm + 3 * S * W, OLs = OVs + 3 * S2;
+  static constexpr int PER = OLs + 3 * S;
+  // TMA window: one 128-byte (16-double) row per window row, 128B-swizzled (chunk c of row r lands at
+  // chunk c ^ (r & 7): conflict-free pencil reads); a row is loaded from the even element at or below its
+  // first element (TMA starts are 16-byte aligned) and read with that parity shift
+  static constexpr int BOX = ((Wn + 2) / 2) * 2, RW = 16, XT = Wn2 * RW;
+  static constexpr bool TMA_OK = BOX * 8 <= 128;
+  static constexpr int OFF = TMA_OK ? (XT > OPa ? XT - OPa : 0) : 0;   // window area grows to Wn2 x 16
+  static constexpr int PERT = PER + OFF;
+  static constexpr int NT0 = ((Wn2 + 31) / 32) * 32 > 512 ? 512 : ((Wn2 + 31) / 32) * 32;
+  static constexpr int NT = (S >= 5 && NT0 >= 128) ? NT0 / 2 : NT0;
+  static_assert(2 * Wn * S2 <= Wn2 * Wn, "Pc/Pe must fit in the window");
+  static_assert(S3 <= NT || S == 3, "one FD point per thread");
+};
+
 template <int S, int W, int Wn, bool TOE>
-__device__ __forceinline__ void band_pencil(const double *in, int stride, const double *ck, const double *cm,
-                                            double (&oa)[S], double (&ob)[S]) {
+__device__ __forceinline__ void pencil_x(const double *xr, const double *ck, const double *cm, const ToeP &tp,
+                                         double *oa, double *ob, int ostride) {
   double v[Wn];
 #pragma unroll
-  for (int k = 0; k < Wn; ++k) v[k] = in[k * stride];
+  for (int k = 0; k < Wn; ++k) v[k] = xr[k];
 #pragma unroll
   for (int l = 0; l < S; ++l) {
     double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
 #pragma unroll
     for (int t = 0; t < W; ++t) {
-      const double kc = TOE ? ck[t] : ck[l * W + t], mc = TOE ? cm[t] : cm[l * W + t];
+      const double kc = TOE ? tp.k[t] : ck[l * W + t], mc = TOE ? tp.m[t] : cm[l * W + t];
       if (t & 1) { a1 = fma(kc, v[l + t], a1); b1 = fma(mc, v[l + t], b1); }
       else { a0 = fma(kc, v[l + t], a0); b0 = fma(mc, v[l + t], b0); }
     }
-    oa[l] = a0 + a1;
-    ob[l] = b0 + b1;
+    oa[l * ostride] = a0 + a1;
+    ob[l * ostride] = b0 + b1;
   }
 }
 
-// pass y: from pencils pa, pb (stride) -> c = My pa + Ky pb, e = My pb
 template <int S, int W, int Wn, bool TOE>
-__device__ __forceinline__ void band_pencil2(const double *pa_, const double *pb_, int stride, const double *ck,
-                                             const double *cm, double (&oc)[S], double (&oe)[S]) {
+__device__ __forceinline__ void pencil_yz(const double *pa_, const double *pb_, int stride, const double *ck,
+                                          const double *cm, const ToeP &tp, double (&oc)[S], double (&oe)[S]) {
   double pa[Wn], pb[Wn];
 #pragma unroll
   for (int k = 0; k < Wn; ++k) { pa[k] = pa_[k * stride]; pb[k] = pb_[k * stride]; }
@@ -45,7 +63,7 @@ __device__ __forceinline__ void band_pencil2(const double *pa_, const double *pb
     double c0 = 0.0, c1 = 0.0, e0 = 0.0;
 #pragma unroll
     for (int t = 0; t < W; ++t) {
-      const double kc = TOE ? ck[t] : ck[l * W + t], mc = TOE ? cm[t] : cm[l * W + t];
+      const double kc = TOE ? tp.k[t] : ck[l * W + t], mc = TOE ? tp.m[t] : cm[l * W + t];
       c0 = fma(mc, pa[l + t], c0);
       c1 = fma(kc, pb[l + t], c1);
       e0 = fma(mc, pb[l + t], e0);
@@ -55,339 +73,253 @@ __device__ __forceinline__ void band_pencil2(const double *pa_, const double *pb
   }
 }
 
-template <int P, int S>
-struct Blk3 {
-  static constexpr int W = 2 * P + 1, Wn = S + 2 * P, w = (S - 1) / 2, S2 = S * S, S3 = S2 * S, Wn2 = Wn * Wn;
-  // per-block layout; Pc/Pe alias the window X (dead after pass x once its s^3 centre values are in Xc)
-  static constexpr int OPa = Wn2 * Wn, OPb = OPa + Wn2 * S, OXc = OPb + Wn2 * S, OR = OXc + S3, OQ = OR + S3,
-                       OBb = OQ + S3, OTk = OBb + S3, OTm = OTk + 3 * S * W, OVs = OTm + 3 * S * W, OLs = OVs + 3 * S2;
-  static constexpr int PER = OLs + 3 * S;
-  static_assert(2 * Wn * S2 <= Wn2 * Wn, "Pc/Pe must fit in the window");
-};
-
-// NBK blocks per CTA (block g = blockIdx.x * NBK + k of the colour's nb0 x nb1 x nb2 grid); every phase
-// runs over (block, pencil) pairs so that the short phases still occupy the CTA.
-template <int P, int S, int NBK, int NT, bool ROW, bool REGW = false>
-__global__ void __launch_bounds__(NT) k_schwarz3d_t(int n1, const double *__restrict__ K, const double *__restrict__ M,
-                                                    const double *__restrict__ Vt, const double *__restrict__ lamt,
-                                                    const double *__restrict__ b, double *__restrict__ x, int c0, int c1,
-                                                    int c2, int D, int nb0, int nb1, int nblk, int zoff, int tlo,
-                                                    int thi) {
-  using B = Blk3<P, S>;
-  constexpr int W = B::W, Wn = B::Wn, w = B::w, S2 = B::S2, S3 = B::S3, Wn2 = B::Wn2, PER = B::PER;
-  extern __shared__ double sm[];
+template <int P, int S, bool TMA>
+__global__ void __launch_bounds__(B4<P, S>::NT) k_schwarz3d_v4(const __grid_constant__ CUtensorMap xmap, int n1,
+                                                                const double *__restrict__ K,
+                                                                const double *__restrict__ M,
+                                                                const double *__restrict__ Vt,
+                                                                const double *__restrict__ lamt,
+                                                                const double *__restrict__ b, double *__restrict__ x,
+                                                                int c0, int c1, int c2, int D, int nb0, int nb1,
+                                                                int zoff, int tlo, int thi, const ToeP tp) {
+  using B = B4<P, S>;
+  constexpr int W = B::W, Wn = B::Wn, w = B::w, S2 = B::S2, S3 = B::S3, Wn2 = B::Wn2, NT = B::NT;
+  constexpr int O = TMA ? B::OFF : 0;
+  extern __shared__ __align__(1024) double sm[];
+  double *X = sm, *Pa = sm + O + B::OPa, *Pb = sm + O + B::OPb, *Pc = sm, *Pe = sm + Wn * S2, *Xc = sm + O + B::OXc;
+  double *R = sm + O + B::OR, *Q = sm + O + B::OQ, *Bb = sm + O + B::OBb, *Tk = sm + O + B::OTk, *Tm = sm + O + B::OTm;
+  double *Vs = sm + O + B::OVs, *Ls = sm + O + B::OLs;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sm + O + B::PER);
   const int tid = threadIdx.x;
   const unsigned un = unsigned(n1);
-  // per-block regions: X [z][y][x] window, Pa/Pb [wz][wy][lx], Pc/Pe [wz][ly][lx], R, Q, Bb,
-  // Tk/Tm [axis][row][t], Vs [axis][l][j], Ls [axis][j]
-  auto X = [&](int k) { return sm + k * PER; };
-  auto Pa = [&](int k) { return sm + k * PER + B::OPa; };
-  auto Pb = [&](int k) { return sm + k * PER + B::OPb; };
-  auto Pc = [&](int k) { return sm + k * PER; };                     // aliases X (see Blk3)
-  auto Pe = [&](int k) { return sm + k * PER + Wn * S2; };
-  auto Xc = [&](int k) { return sm + k * PER + B::OXc; };
-  auto R = [&](int k) { return sm + k * PER + B::OR; };
-  auto Q = [&](int k) { return sm + k * PER + B::OQ; };
-  auto Bb = [&](int k) { return sm + k * PER + B::OBb; };
-  auto Tk = [&](int k) { return sm + k * PER + B::OTk; };
-  auto Tm = [&](int k) { return sm + k * PER + B::OTm; };
-  auto Vs = [&](int k) { return sm + k * PER + B::OVs; };
-  auto Ls = [&](int k) { return sm + k * PER + B::OLs; };
-  __shared__ int sC[NBK][3];
-  __shared__ bool sT[NBK][3];
-  if (NBK > 1 && tid < NBK) {                               // block centres, Toeplitz flags per axis
-    const int g = blockIdx.x * NBK + tid;
-    const int cc[3] = {c0 + D * (g % nb0), c1 + D * ((g / nb0) % nb1), c2 + D * (g / (nb0 * nb1))};
+  const int g = blockIdx.x;
+  const int cc[3] = {c0 + D * (g % nb0), c1 + D * ((g / nb0) % nb1), c2 + D * (g / (nb0 * nb1))};
+  const bool tv = tp.valid != 0;
+  bool toe[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      sC[tid][a] = cc[a];
-      sT[tid][a] = (cc[a] - w >= tlo) && (cc[a] + w <= thi);
+  for (int a = 0; a < 3; ++a) toe[a] = tv && cc[a] - w >= tlo && cc[a] + w <= thi;
+  const int ox = cc[0] - w - P, oy = cc[1] - w - P, oz = cc[2] - w - P;
+  // ---- window rows r = (wz, wy) ----
+  const int64_t wbase = (int64_t(oz - zoff) * n1 + oy) * n1 + ox;   // global index of window element (0,0,0)
+  if constexpr (TMA) {                                            // one TMA per row (swizzled, see B4)
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      mbar_fence_init();
+      mbar_expect_tx(bar, Wn2 * B::BOX * 8);
+    }
+    __syncthreads();
+    for (int r = tid; r < Wn2; r += NT) {
+      const int wz = r / Wn, wy = r - wz * Wn;
+      tma_load_1d(X + r * B::RW, &xmap, int(wbase + (int64_t(wz) * n1 + wy) * n1) & ~1, bar);
+    }
+  } else {                                                        // LG lanes per row: coalesced row copies
+    // (zero outside the domain)                                                               // LG lanes per row: coalesced row copies
+    constexpr int LG = Wn <= 16 ? 16 : 32, RPI = NT / LG;           // rows per iteration of the CTA
+    const int col = tid % LG, r0 = tid / LG;
+    const bool colok = col < Wn && unsigned(ox + col) < un;
+    for (int r = r0; r < Wn2; r += RPI) {
+      const int wz = r / Wn, wy = r - wz * Wn, gy = oy + wy, gz = oz + wz;
+      const bool ok = colok && unsigned(gy) < un && unsigned(gz) < un;
+      if (col < Wn) cp_async8(X + r * Wn + col, ok ? x + (int64_t(gz - zoff) * n1 + gy) * n1 + ox + col : x, ok);
     }
   }
-  __syncthreads();
-  int cc1[3];                                               // NBK == 1: the centre in registers
-  bool tt1[3];
-  if (NBK == 1) {
-    const int g = blockIdx.x;
-    cc1[0] = c0 + D * (g % nb0);
-    cc1[1] = c1 + D * ((g / nb0) % nb1);
-    cc1[2] = c2 + D * (g / (nb0 * nb1));
-#pragma unroll
-    for (int a = 0; a < 3; ++a) tt1[a] = (cc1[a] - w >= tlo) && (cc1[a] + w <= thi);
-  }
-  auto centre = [&](int k, int a) { return NBK == 1 ? cc1[a] : sC[k][a]; };
-  const int nk = min(NBK, nblk - int(blockIdx.x) * NBK);   // blocks of this CTA
-  // ---- loads: band rows, FD tables, b_B (through registers when one block per CTA: the 8-byte cp.async
-  // issue cost dominated this phase), x windows ----
-  if (NBK == 1 && !ROW) {
-    constexpr int NTAB = 2 * 3 * S * W + 3 * S2 + 3 * S + S3;   // Tk, Tm, Vs, Ls, Bb
-    constexpr int IT = (NTAB + NT - 1) / NT;
-    double v[IT];
-#pragma unroll
-    for (int k = 0; k < IT; ++k) {
-      const int i = tid + k * NT;
-      double val = 0.0;
-      if (i < 2 * 3 * S * W) {
-        const int r = i % (3 * S * W), a = r / (S * W), l = (r / W) % S, t = r % W;
-        const int g = centre(0, a) - w + l;
-        if (unsigned(g) < un) val = (i < 3 * S * W ? K : M)[(int64_t)g * W + t];
-      } else if (i < 2 * 3 * S * W + 3 * S2) {
-        const int r = i - 2 * 3 * S * W;
-        val = Vt[(int64_t)centre(0, r / S2) * S2 + r % S2];
-      } else if (i < 2 * 3 * S * W + 3 * S2 + 3 * S) {
-        const int r = i - 2 * 3 * S * W - 3 * S2;
-        val = lamt[(int64_t)centre(0, r / S) * S + r % S];
-      } else if (i < NTAB) {
-        const int r = i - 2 * 3 * S * W - 3 * S2 - 3 * S;
-        const int gx = centre(0, 0) - w + r % S, gy = centre(0, 1) - w + (r / S) % S, gz = centre(0, 2) - w + r / S2;
-        if (unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un)
-          val = b[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx];
-      }
-      v[k] = val;
-    }
-#pragma unroll
-    for (int k = 0; k < IT; ++k) {
-      const int i = tid + k * NT;
-      if (i < 3 * S * W) Tk(0)[i] = v[k];
-      else if (i < 2 * 3 * S * W) Tm(0)[i - 3 * S * W] = v[k];
-      else if (i < 2 * 3 * S * W + 3 * S2) Vs(0)[i - 2 * 3 * S * W] = v[k];
-      else if (i < 2 * 3 * S * W + 3 * S2 + 3 * S) Ls(0)[i - 2 * 3 * S * W - 3 * S2] = v[k];
-      else if (i < NTAB) Bb(0)[i - 2 * 3 * S * W - 3 * S2 - 3 * S] = v[k];
-    }
-  } else {
-  for (int i = tid; i < nk * 3 * S * W; i += NT) {
-    const int k = NBK == 1 ? 0 : i / (3 * S * W), r = NBK == 1 ? i : i % (3 * S * W);
-    const int a = r / (S * W), l = (r / W) % S, t = r % W;
-    const int g = centre(k, a) - w + l;
-    const bool ok = unsigned(g) < un;
-    cp_async8(Tk(k) + r, K + (ok ? (int64_t)g * W + t : 0), ok);
-    cp_async8(Tm(k) + r, M + (ok ? (int64_t)g * W + t : 0), ok);
-  }
-  for (int i = tid; i < nk * 3 * S2; i += NT) {
-    const int k = NBK == 1 ? 0 : i / (3 * S2), r = NBK == 1 ? i : i % (3 * S2);
-    cp_async8(Vs(k) + r, Vt + (int64_t)centre(k, r / S2) * S2 + r % S2, true);
-  }
-  for (int i = tid; i < nk * 3 * S; i += NT) {
-    const int k = NBK == 1 ? 0 : i / (3 * S), r = NBK == 1 ? i : i % (3 * S);
-    cp_async8(Ls(k) + r, lamt + (int64_t)centre(k, r / S) * S + r % S, true);
-  }
-  for (int i = tid; i < nk * S3; i += NT) {
-    const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3;
-    const int gx = centre(k, 0) - w + r % S, gy = centre(k, 1) - w + (r / S) % S, gz = centre(k, 2) - w + r / S2;
+  // ---- b_B, and band rows / FD tables of the boundary axes ----
+  int lx = 0, ly = 0, lz = 0;                                     // this thread's FD / update point
+  if (tid < S3) {
+    lz = tid / S2;
+    ly = (tid - lz * S2) / S;
+    lx = tid - lz * S2 - ly * S;
+    const int gx = cc[0] - w + lx, gy = cc[1] - w + ly, gz = cc[2] - w + lz;
     const bool ok = unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un;
-    cp_async8(Bb(k) + r, b + (ok ? ((int64_t)(gz - zoff) * n1 + gy) * n1 + gx : 0), ok);
+    cp_async8(Bb + tid, b + (ok ? (int64_t(gz - zoff) * n1 + gy) * n1 + gx : 0), ok);
   }
-  }
-  if (!ROW && NBK == 1 && (REGW || Wn2 * Wn <= 1024)) {   // x window through registers, batches of 16 loads
-                                                   // (measured: C4 40.6 -> 36.6 us/colour; C5 slower)
-    constexpr int TOT = Wn2 * Wn, BATCH = 16;      // (8-byte cp.async issue costs ~95 cycles each)
-    const int ox = centre(0, 0) - w - P, oy = centre(0, 1) - w - P, oz = centre(0, 2) - w - P;
-    for (int i0 = 0; i0 < TOT; i0 += NT * BATCH) {
-      double v[BATCH];
 #pragma unroll
-      for (int k = 0; k < BATCH; ++k) {
-        const int r = i0 + tid + k * NT;
-        const int gx = ox + r % Wn, gy = oy + (r / Wn) % Wn, gz = oz + r / Wn2;
-        const bool ok = r < TOT && unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un;
-        v[k] = ok ? x[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx] : 0.0;
-      }
-#pragma unroll
-      for (int k = 0; k < BATCH; ++k) {
-        const int r = i0 + tid + k * NT;
-        if (r < TOT) X(0)[r] = v[k];
-      }
+  for (int a = 0; a < 3; ++a) {
+    if (toe[a]) continue;
+    for (int i = tid; i < S * W; i += NT) {
+      const int l = i / W, t = i - l * W, gr = cc[a] - w + l;
+      const bool ok = unsigned(gr) < un;
+      cp_async8(Tk + a * S * W + i, K + (ok ? int64_t(gr) * W + t : 0), ok);
+      cp_async8(Tm + a * S * W + i, M + (ok ? int64_t(gr) * W + t : 0), ok);
     }
-  } else if (!ROW) {                               // x windows, element by element
-    for (int i = tid; i < nk * Wn2 * Wn; i += NT) {
-      const int k = NBK == 1 ? 0 : i / (Wn2 * Wn), r = NBK == 1 ? i : i % (Wn2 * Wn);
-      const int gx = centre(k, 0) - w - P + r % Wn, gy = centre(k, 1) - w - P + (r / Wn) % Wn,
-                gz = centre(k, 2) - w - P + r / Wn2;
-      const bool ok = unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un;
-      cp_async8(X(k) + r, x + (ok ? ((int64_t)(gz - zoff) * n1 + gy) * n1 + gx : 0), ok);
-    }
-  } else {                                          // x windows: one window row per 16 lanes
-    const int lane16 = tid & 15;
-    for (int row = tid >> 4; row < nk * Wn2; row += NT / 16) {
-      const int k = NBK == 1 ? 0 : row / Wn2, rr = row - k * Wn2, wz = rr / Wn, wy = rr - wz * Wn;
-      const int ox = centre(k, 0) - w - P, gy = centre(k, 1) - w - P + wy, gz = centre(k, 2) - w - P + wz;
-      const bool okyz = unsigned(gy) < un && unsigned(gz) < un;
-      const double *src = x + (okyz ? ((int64_t)(gz - zoff) * n1 + gy) * n1 : 0);
-      double *dst = X(k) + rr * Wn;
-#pragma unroll
-      for (int wx = lane16; wx < Wn; wx += 16) {
-        const int gx = ox + wx;
-        const bool ok = okyz && unsigned(gx) < un;
-        cp_async8(dst + wx, ok ? src + gx : x, ok);
-      }
-    }
+    for (int i = tid; i < S2; i += NT) cp_async8(Vs + a * S2 + i, Vt + int64_t(cc[a]) * S2 + i, true);
+    if (tid < S) cp_async8(Ls + a * S + tid, lamt + int64_t(cc[a]) * S + tid, true);
   }
   cp_async_wait_all();
-  auto toe = [&](int k, int a) { return NBK == 1 ? tt1[a] : sT[k][a]; };
+  if constexpr (TMA) mbar_wait(bar, 0);
   __syncthreads();
   // ---- pass x: pencils (wy, wz) along x -> Pa = Kx X, Pb = Mx X ----
-  for (int i = tid; i < nk * Wn2; i += NT) {
-    const int k = NBK == 1 ? 0 : i / Wn2, pi = NBK == 1 ? i : i % Wn2;
-    double oa[S], ob[S];
-    if (toe(k, 0)) band_pencil<S, W, Wn, true>(X(k) + pi * Wn, 1, Tk(k), Tm(k), oa, ob);
-    else band_pencil<S, W, Wn, false>(X(k) + pi * Wn, 1, Tk(k), Tm(k), oa, ob);
+  if constexpr (TMA) {
+    for (int pi = tid; pi < Wn2; pi += NT) {
+      const int wz = pi / Wn, wy = pi - wz * Wn;
+      const int sh = int(wbase + (int64_t(wz) * n1 + wy) * n1) & 1;
+      const double2 *row = reinterpret_cast<const double2 *>(X + pi * B::RW);
+      double v[B::BOX];
 #pragma unroll
-    for (int l = 0; l < S; ++l) { Pa(k)[pi * S + l] = oa[l]; Pb(k)[pi * S + l] = ob[l]; }
-  }
-  for (int i = tid; i < nk * S3; i += NT) {        // the block's centre values, before Pc/Pe overwrite X
-    const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3;
-    const int lx = r % S, ly = (r / S) % S, lz = r / S2;
-    Xc(k)[r] = X(k)[((lz + P) * Wn + ly + P) * Wn + lx + P];
+      for (int c = 0; c < B::BOX / 2; ++c) {
+        const double2 t = row[c ^ (pi & 7)];
+        v[2 * c] = t.x;
+        v[2 * c + 1] = t.y;
+      }
+      double u[Wn];
+#pragma unroll
+      for (int k = 0; k < Wn; ++k) u[k] = sh ? v[k + 1] : v[k];
+      if (toe[0]) pencil_x<S, W, Wn, true>(u, Tk, Tm, tp, Pa + pi * S, Pb + pi * S, 1);
+      else pencil_x<S, W, Wn, false>(u, Tk, Tm, tp, Pa + pi * S, Pb + pi * S, 1);
+    }
+    if (tid < S3) {
+      const int pr = (lz + P) * Wn + ly + P;
+      const int e = lx + P + (int(wbase + (int64_t(lz + P) * n1 + ly + P) * n1) & 1);
+      Xc[tid] = X[pr * B::RW + (((e >> 1) ^ (pr & 7)) << 1) + (e & 1)];
+    }
+  } else {
+    for (int pi = tid; pi < Wn2; pi += NT) {
+      if (toe[0]) pencil_x<S, W, Wn, true>(X + pi * Wn, Tk, Tm, tp, Pa + pi * S, Pb + pi * S, 1);
+      else pencil_x<S, W, Wn, false>(X + pi * Wn, Tk, Tm, tp, Pa + pi * S, Pb + pi * S, 1);
+    }
+    if (tid < S3) Xc[tid] = X[((lz + P) * Wn + ly + P) * Wn + lx + P];   // before Pc/Pe overwrite X
   }
   __syncthreads();
   // ---- pass y: pencils (wz, lx) along y -> Pc = My Pa + Ky Pb, Pe = My Pb ----
-  for (int i = tid; i < nk * Wn * S; i += NT) {
-    const int k = NBK == 1 ? 0 : i / (Wn * S), pi = NBK == 1 ? i : i % (Wn * S);
-    const int wz = pi / S, lx = pi % S;
+  for (int pi = tid; pi < Wn * S; pi += NT) {
+    const int wz = pi / S, px = pi - wz * S;
     double oc[S], oe[S];
-    const double *pa = Pa(k) + wz * Wn * S + lx, *pb = Pb(k) + wz * Wn * S + lx;
-    if (toe(k, 1)) band_pencil2<S, W, Wn, true>(pa, pb, S, Tk(k) + S * W, Tm(k) + S * W, oc, oe);
-    else band_pencil2<S, W, Wn, false>(pa, pb, S, Tk(k) + S * W, Tm(k) + S * W, oc, oe);
+    if (toe[1]) pencil_yz<S, W, Wn, true>(Pa + wz * Wn * S + px, Pb + wz * Wn * S + px, S, Tk + S * W, Tm + S * W, tp, oc, oe);
+    else pencil_yz<S, W, Wn, false>(Pa + wz * Wn * S + px, Pb + wz * Wn * S + px, S, Tk + S * W, Tm + S * W, tp, oc, oe);
 #pragma unroll
-    for (int l = 0; l < S; ++l) { Pc(k)[(wz * S + l) * S + lx] = oc[l]; Pe(k)[(wz * S + l) * S + lx] = oe[l]; }
+    for (int l = 0; l < S; ++l) { Pc[(wz * S + l) * S + px] = oc[l]; Pe[(wz * S + l) * S + px] = oe[l]; }
   }
   __syncthreads();
   // ---- pass z: pencils (ly, lx) along z -> r_B = b_B - (Mz Pc + Kz Pe) ----
-  for (int i = tid; i < nk * S2; i += NT) {
-    const int k = NBK == 1 ? 0 : i / S2, pi = NBK == 1 ? i : i % S2;
+  if (tid < S2) {
     double oc[S], oe[S];
-    if (toe(k, 2)) band_pencil2<S, W, Wn, true>(Pc(k) + pi, Pe(k) + pi, S2, Tk(k) + 2 * S * W, Tm(k) + 2 * S * W, oc, oe);
-    else band_pencil2<S, W, Wn, false>(Pc(k) + pi, Pe(k) + pi, S2, Tk(k) + 2 * S * W, Tm(k) + 2 * S * W, oc, oe);
+    if (toe[2]) pencil_yz<S, W, Wn, true>(Pc + tid, Pe + tid, S2, Tk + 2 * S * W, Tm + 2 * S * W, tp, oc, oe);
+    else pencil_yz<S, W, Wn, false>(Pc + tid, Pe + tid, S2, Tk + 2 * S * W, Tm + 2 * S * W, tp, oc, oe);
 #pragma unroll
-    for (int l = 0; l < S; ++l) R(k)[l * S2 + pi] = Bb(k)[l * S2 + pi] - oc[l];
+    for (int l = 0; l < S; ++l) R[l * S2 + tid] = Bb[l * S2 + tid] - oc[l];
   }
   __syncthreads();
-  // ---- δ = (⊗V) Λ^{-1} (⊗V)^T r ----
-  if constexpr (S == 3 && NBK == 1) {   // s^3 = 27 values: the whole FD in one warp's registers (shuffles)
+  // ---- δ = (⊗V) Λ^{-1} (⊗V)^T r_B (fast diagonalisation), x_B = X_c + δ ----
+  auto Vax = [&](int a, int l, int j) { return toe[a] ? tp.v[l * S + j] : Vs[a * S2 + l * S + j]; };
+  auto Lax = [&](int a, int j) { return toe[a] ? tp.lam[j] : Ls[a * S + j]; };
+  if constexpr (S == 3) {                                         // 27 values: one warp, shuffles
     if (tid < 32) {
-      const int lane = tid, li = lane < 27 ? lane : 0;
-      const int lx = li % 3, ly = (li / 3) % 3, lz = li / 9;
-      const double *Vx = Vs(0), *Vy = Vs(0) + 9, *Vz = Vs(0) + 18, *L = Ls(0);
-      double v;
-      {
-      v = lane < 27 ? R(0)[li] : 0.0;
-      auto src = [&](int ax, int l) { return ax == 0 ? lz * 9 + ly * 3 + l : (ax == 1 ? lz * 9 + l * 3 + lx : l * 9 + ly * 3 + lx); };
-      auto step = [&](int ax, const double *V, bool trans) {   // trans: out[j] = Σ_l V[l][j] in[l]; else V[j][l]
-        const int j = ax == 0 ? lx : (ax == 1 ? ly : lz);
+      const int li = tid < 27 ? tid : 0;
+      const int fx = li % 3, fy = (li / 3) % 3, fz = li / 9;
+      double v = tid < 27 ? R[li] : 0.0;
+      auto src = [&](int ax, int l) { return ax == 0 ? fz * 9 + fy * 3 + l : (ax == 1 ? fz * 9 + l * 3 + fx : l * 9 + fy * 3 + fx); };
+      auto step = [&](int ax, bool trans) {
+        const int j = ax == 0 ? fx : (ax == 1 ? fy : fz);
         double o = 0.0;
 #pragma unroll
         for (int l = 0; l < 3; ++l) {
           const double in = __shfl_sync(0xffffffffu, v, src(ax, l));
-          o = fma(trans ? V[l * 3 + j] : V[j * 3 + l], in, o);
+          o = fma(trans ? Vax(ax, l, j) : Vax(ax, j, l), in, o);
         }
         v = o;
       };
-      step(0, Vx, true);
-      step(1, Vy, true);
-      step(2, Vz, true);
-      v /= (L[lx] + L[3 + ly] + L[6 + lz]);
-      step(2, Vz, false);
-      step(1, Vy, false);
-      step(0, Vx, false);
-      }
-      const int gx = centre(0, 0) - w + lx, gy = centre(0, 1) - w + ly, gz = centre(0, 2) - w + lz;
-      if (lane < 27 && unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un)
-        x[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx] = Xc(0)[(lz * S + ly) * S + lx] + v;
+      step(0, true);
+      step(1, true);
+      step(2, true);
+      v /= (Lax(0, fx) + Lax(1, fy) + Lax(2, fz));
+      step(2, false);
+      step(1, false);
+      step(0, false);
+      const int gx = cc[0] - w + fx, gy = cc[1] - w + fy, gz = cc[2] - w + fz;
+      if (tid < 27 && unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un)
+        x[(int64_t(gz - zoff) * n1 + gy) * n1 + gx] = Xc[(fz * S + fy) * S + fx] + v;
     }
-    return;
-  }
-  if constexpr (!(S == 3 && NBK == 1)) {   // general FD (s >= 5 or several blocks per CTA)
-  for (int i = tid; i < nk * S3; i += NT) {         // along x (transposed)
-    const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3, j = r % S, rest = r - j;
-    const double *Vx = Vs(k);
-    double a0 = 0.0;
+  } else {
+    const int r = tid;
+    const bool act = tid < S3;
+    if (act) {                                                    // along x (transposed)
+      double a0 = 0.0;
 #pragma unroll
-    for (int l = 0; l < S; ++l) a0 = fma(Vx[l * S + j], R(k)[rest + l], a0);
-    Q(k)[r] = a0;
-  }
-  __syncthreads();
-  for (int i = tid; i < nk * S3; i += NT) {         // along y (transposed)
-    const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3, j = r % S, kk = (r / S) % S, lz = r / S2;
-    const double *Vy = Vs(k) + S2;
-    double a0 = 0.0;
+      for (int l = 0; l < S; ++l) a0 = fma(Vax(0, l, lx), R[r - lx + l], a0);
+      Q[r] = a0;
+    }
+    __syncthreads();
+    if (act) {                                                    // along y (transposed)
+      double a0 = 0.0;
 #pragma unroll
-    for (int l = 0; l < S; ++l) a0 = fma(Vy[l * S + kk], Q(k)[(lz * S + l) * S + j], a0);
-    R(k)[r] = a0;
-  }
-  __syncthreads();
-  for (int i = tid; i < nk * S3; i += NT) {         // along z (transposed), then / (λx + λy + λz)
-    const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3, j = r % S, kk = (r / S) % S, l3 = r / S2;
-    const double *Vz = Vs(k) + 2 * S2, *L = Ls(k);
-    double a0 = 0.0;
+      for (int l = 0; l < S; ++l) a0 = fma(Vax(1, l, ly), Q[(lz * S + l) * S + lx], a0);
+      R[r] = a0;
+    }
+    __syncthreads();
+    if (act) {                                                    // along z (transposed), / (λx + λy + λz)
+      double a0 = 0.0;
 #pragma unroll
-    for (int l = 0; l < S; ++l) a0 = fma(Vz[l * S + l3], R(k)[(l * S + kk) * S + j], a0);
-    Q(k)[r] = a0 / (L[j] + L[S + kk] + L[2 * S + l3]);
-  }
-  __syncthreads();
-  for (int i = tid; i < nk * S3; i += NT) {         // along z
-    const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3, j = r % S, kk = (r / S) % S, lz = r / S2;
-    const double *Vz = Vs(k) + 2 * S2;
-    double a0 = 0.0;
+      for (int l = 0; l < S; ++l) a0 = fma(Vax(2, l, lz), R[(l * S + ly) * S + lx], a0);
+      Q[r] = a0 / (Lax(0, lx) + Lax(1, ly) + Lax(2, lz));
+    }
+    __syncthreads();
+    if (act) {                                                    // along z
+      double a0 = 0.0;
 #pragma unroll
-    for (int l = 0; l < S; ++l) a0 = fma(Vz[lz * S + l], Q(k)[(l * S + kk) * S + j], a0);
-    R(k)[r] = a0;
-  }
-  __syncthreads();
-  for (int i = tid; i < nk * S3; i += NT) {         // along y
-    const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3, j = r % S, ly = (r / S) % S, lz = r / S2;
-    const double *Vy = Vs(k) + S2;
-    double a0 = 0.0;
+      for (int l = 0; l < S; ++l) a0 = fma(Vax(2, lz, l), Q[(l * S + ly) * S + lx], a0);
+      R[r] = a0;
+    }
+    __syncthreads();
+    if (act) {                                                    // along y
+      double a0 = 0.0;
 #pragma unroll
-    for (int l = 0; l < S; ++l) a0 = fma(Vy[ly * S + l], R(k)[(lz * S + l) * S + j], a0);
-    Q(k)[r] = a0;
-  }
-  __syncthreads();
-  for (int i = tid; i < nk * S3; i += NT) {         // along x, and x_B += δ
-    const int k = NBK == 1 ? 0 : i / S3, r = NBK == 1 ? i : i % S3, lx = r % S, ly = (r / S) % S, lz = r / S2, rest = r - lx;
-    const double *Vx = Vs(k);
-    double a0 = 0.0;
+      for (int l = 0; l < S; ++l) a0 = fma(Vax(1, ly, l), R[(lz * S + l) * S + lx], a0);
+      Q[r] = a0;
+    }
+    __syncthreads();
+    if (act) {                                                    // along x, and x_B += δ
+      double a0 = 0.0;
 #pragma unroll
-    for (int l = 0; l < S; ++l) a0 = fma(Vx[lx * S + l], Q(k)[rest + l], a0);
-    const int gx = centre(k, 0) - w + lx, gy = centre(k, 1) - w + ly, gz = centre(k, 2) - w + lz;
-    if (unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un)
-      x[((int64_t)(gz - zoff) * n1 + gy) * n1 + gx] = Xc(k)[r] + a0;
-  }
+      for (int l = 0; l < S; ++l) a0 = fma(Vax(0, lx, l), Q[r - lx + l], a0);
+      const int gx = cc[0] - w + lx, gy = cc[1] - w + ly, gz = cc[2] - w + lz;
+      if (unsigned(gx) < un && unsigned(gy) < un && unsigned(gz) < un)
+        x[(int64_t(gz - zoff) * n1 + gy) * n1 + gx] = Xc[r] + a0;
+    }
   }
 }
 
-template <int P, int S, int NBK, int NT, bool ROW, bool REGW = false>
-void launch3d(int64_t n1, const double *K, const double *M, const double *V, const double *lam, const double *b,
-              double *x, int c0, int c1, int c2, int D, int nb0, int nb1, int nb2, int zoff, int tlo, int thi,
-              cudaStream_t st) {
-  constexpr size_t sm = sizeof(double) * NBK * Blk3<P, S>::PER;
-  ensure_smem(k_schwarz3d_t<P, S, NBK, NT, ROW, REGW>, sm);
-  const int nblk = nb0 * nb1 * nb2;
-  k_schwarz3d_t<P, S, NBK, NT, ROW, REGW><<<(nblk + NBK - 1) / NBK, NT, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1,
-                                                                                  c2, D, nb0, nb1, nblk, zoff, tlo, thi);
-}
-
+static const bool g_s3d_tma = [] {                  // IGA2L_S3D_TMA=0: window by cp.async rows
+  const char *e = std::getenv("IGA2L_S3D_TMA");
+  return !(e && e[0] == '0');
+}();
 template <int P, int S>
 bool try_schwarz3d(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
                    const double *b, double *x, int c0, int c1, int c2, int D, int nb0, int nb1, int nb2, int zoff,
-                   int tlo, int thi, cudaStream_t st) {
+                   int tlo, int thi, cudaStream_t st, const ToeP *tpp) {
   if (p != P || s != S) return false;
-  constexpr int NT1 = ((Blk3<P, S>::Wn2 + 31) / 32) * 32 > 512 ? 512 : ((Blk3<P, S>::Wn2 + 31) / 32) * 32;
-  // measured best (profiles/variants_s3d_r01.txt): one block per CTA; s >= 5: half the pass-x pencil count of threads
-  launch3d<P, S, 1, (S >= 5 && NT1 >= 128 ? NT1 / 2 : NT1), false>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2,
-                                                                  zoff, tlo, thi, st);
-  return true;
+  {
+    using B = B4<P, S>;
+    ToeP tp{};
+    if (tpp) tp = *tpp;
+    CUtensorMap map{};
+    const int w = (S - 1) / 2;
+    const int64_t stored = (std::min<int64_t>(n1, c2 + int64_t(D) * (nb2 - 1) + w + P + 1) - zoff) * n1 * n1;
+    if (B::TMA_OK && g_s3d_tma && make_tmap_1d_swz128(&map, x, stored, B::BOX)) {
+      constexpr size_t sm = sizeof(double) * B::PERT + 16 + 1024;
+      ensure_smem(k_schwarz3d_v4<P, S, true>, sm);
+      k_schwarz3d_v4<P, S, true><<<nb0 * nb1 * nb2, B::NT, sm, st>>>(map, int(n1), K, M, V, lam, b, x, c0, c1, c2, D,
+                                                                     nb0, nb1, zoff, tlo, thi, tp);
+    } else {
+      constexpr size_t sm = sizeof(double) * B::PER + 16 + 1024;
+      ensure_smem(k_schwarz3d_v4<P, S, false>, sm);
+      k_schwarz3d_v4<P, S, false><<<nb0 * nb1 * nb2, B::NT, sm, st>>>(map, int(n1), K, M, V, lam, b, x, c0, c1, c2, D,
+                                                                      nb0, nb1, zoff, tlo, thi, tp);
+    }
+    return true;
+  }
 }
 
 }  // namespace
 
 bool launch_schwarz3d_colour(int p, int s, int64_t n1, const double *K, const double *M, const double *V,
                              const double *lam, const double *b, double *x, int c0, int c1, int f2, int D, int nb0,
-                             int nb1, int nb2, int zoff, int tlo, int thi, cudaStream_t st) {
-  return try_schwarz3d<1, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, zoff, tlo, thi, st) ||
-         try_schwarz3d<2, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, zoff, tlo, thi, st) ||
-         try_schwarz3d<3, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, zoff, tlo, thi, st) ||
-         try_schwarz3d<4, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, zoff, tlo, thi, st) ||
-         try_schwarz3d<5, 5>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, zoff, tlo, thi, st) ||
-         try_schwarz3d<6, 5>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, zoff, tlo, thi, st);
+                             int nb1, int nb2, int zoff, int tlo, int thi, cudaStream_t st, const ToeP *tp) {
+  return try_schwarz3d<1, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, zoff, tlo, thi, st, tp) ||
+         try_schwarz3d<2, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, zoff, tlo, thi, st, tp) ||
+         try_schwarz3d<3, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, zoff, tlo, thi, st, tp) ||
+         try_schwarz3d<4, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, zoff, tlo, thi, st, tp) ||
+         try_schwarz3d<5, 5>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, zoff, tlo, thi, st, tp) ||
+         try_schwarz3d<6, 5>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, zoff, tlo, thi, st, tp);
 }
 
 }  // namespace iga2l

@@ -20,7 +20,17 @@
 
 namespace iga2l {
 
+static bool encode_1d(void *map64, const double *ptr, int64_t n, int box, CUtensorMapSwizzle swz);
+
 bool make_tmap_1d(void *map64, const double *ptr, int64_t n, int box) {
+  return encode_1d(map64, ptr, n, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+bool make_tmap_1d_swz128(void *map64, const double *ptr, int64_t n, int box) {
+  return box * 8 <= 128 && encode_1d(map64, ptr, n, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+static bool encode_1d(void *map64, const double *ptr, int64_t n, int box, CUtensorMapSwizzle swz) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
     void *fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -37,7 +47,7 @@ bool make_tmap_1d(void *map64, const double *ptr, int64_t n, int box) {
   cuuint32_t boxd[1] = {cuuint32_t(box)};
   cuuint32_t es[1] = {1};
   return enc(static_cast<CUtensorMap *>(map64), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, const_cast<double *>(ptr), dims,
-             strides, boxd, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             strides, boxd, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
