@@ -70,12 +70,25 @@ __device__ __forceinline__ void tma_load_1d(double *dst, const void *map, int c0
       : "memory");
 }
 
+// 2D box load: element (c0, c1) of the box origin (c0 = column, c1 = row)
+__device__ __forceinline__ void tma_load_2d(double *dst, const void *map, int c0, int c1, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // host: 1D tensor map over n doubles at ptr with a box of `box` elements (box * 8 % 16 == 0, box <= 256).
 // Returns false if the driver entry point is missing or the encode fails.
 bool make_tmap_1d(void *map64, const double *ptr, int64_t n, int box);
 // the same with 128-byte swizzle (box * 8 <= 128): chunk c of a row landing at a 128-byte aligned shared
 // address A goes to chunk c ^ ((A >> 7) & 7)
 bool make_tmap_1d_swz128(void *map64, const double *ptr, int64_t n, int box);
+// 2D map of `rows` rows of `cols` doubles, consecutive rows `stride` elements apart (stride * 8 % 16 == 0),
+// box = box_cols x box_rows, 128B swizzle
+bool make_tmap_rows_swz128(void *map64, const double *ptr, int64_t cols, int64_t rows, int64_t stride, int box_cols,
+                           int box_rows);
 
 template <typename F>
 inline void ensure_smem(F *kernel, size_t bytes) {

@@ -19,12 +19,15 @@ struct B4 {
   static constexpr int OPa = Wn2 * Wn, OPb = OPa + Wn2 * S, OXc = OPb + Wn2 * S, OR = OXc + S3, OQ = OR + S3,
                        OBb = OQ + S3, OTk = OBb + S3, OTm = OTk + 3 * S * W, OVs = OTm + 3 * S * W, OLs = OVs + 3 * S2;
   static constexpr int PER = OLs + 3 * S;
-  // TMA window: one 128-byte (16-double) row per window row, 128B-swizzled (chunk c of row r lands at
-  // chunk c ^ (r & 7): conflict-free pencil reads); a row is loaded from the even element at or below its
-  // first element (TMA starts are 16-byte aligned) and read with that parity shift
-  static constexpr int BOX = ((Wn + 2) / 2) * 2, RW = 16, XT = Wn2 * RW;
-  static constexpr bool TMA_OK = BOX * 8 <= 128;
-  static constexpr int OFF = TMA_OK ? (XT > OPa ? XT - OPa : 0) : 0;   // window area grows to Wn2 x 16
+  // TMA window.  Grid rows J (the n1-element x-rows, counted from the stored base) of one parity are
+  // 2 n1 elements apart -- a 16-byte multiple even for odd n1 -- so the even rows and the odd rows each form
+  // a 2D tensor (two maps; the odd one based one element early so that its base stays 16-byte aligned).
+  // A window plane is then TWO box loads of BR rows x BOX columns into consecutive 128-byte shared rows
+  // with 128B swizzle (chunk c of shared row R lands at chunk c ^ (R & 7): conflict-free pencil reads).  Boxes start at the
+  // even column at or below the first needed one; rows are read with that parity shift.
+  static constexpr int BOX = ((Wn + 2) / 2) * 2, RW = 16, BR = (Wn + 1) / 2, XT = Wn * 2 * BR * RW;
+  static constexpr bool TMA_OK = BOX * 8 <= 128 && BR <= 8;
+  static constexpr int OFF = TMA_OK ? (XT > OPa ? XT - OPa : 0) : 0;   // window area grows to Wn x 2 tiles
   static constexpr int PERT = PER + OFF;
   static constexpr int NT0 = ((Wn2 + 31) / 32) * 32 > 512 ? 512 : ((Wn2 + 31) / 32) * 32;
   static constexpr int NT = (S >= 5 && NT0 >= 128) ? NT0 / 2 : NT0;
@@ -74,7 +77,8 @@ __device__ __forceinline__ void pencil_yz(const double *pa_, const double *pb_, 
 }
 
 template <int P, int S, bool TMA>
-__global__ void __launch_bounds__(B4<P, S>::NT) k_schwarz3d_v4(const __grid_constant__ CUtensorMap xmap, int n1,
+__global__ void __launch_bounds__(B4<P, S>::NT) k_schwarz3d_v4(const __grid_constant__ CUtensorMap xmap_e,
+                                                                const __grid_constant__ CUtensorMap xmap_o, int n1,
                                                                 const double *__restrict__ K,
                                                                 const double *__restrict__ M,
                                                                 const double *__restrict__ Vt,
@@ -100,17 +104,20 @@ __global__ void __launch_bounds__(B4<P, S>::NT) k_schwarz3d_v4(const __grid_cons
   for (int a = 0; a < 3; ++a) toe[a] = tv && cc[a] - w >= tlo && cc[a] + w <= thi;
   const int ox = cc[0] - w - P, oy = cc[1] - w - P, oz = cc[2] - w - P;
   // ---- window rows r = (wz, wy) ----
-  const int64_t wbase = (int64_t(oz - zoff) * n1 + oy) * n1 + ox;   // global index of window element (0,0,0)
-  if constexpr (TMA) {                                            // one TMA per row (swizzled, see B4)
+  if constexpr (TMA) {                                            // two box loads per plane (see B4)
     if (tid == 0) {
       mbar_init(bar, 1);
       mbar_fence_init();
-      mbar_expect_tx(bar, Wn2 * B::BOX * 8);
+      mbar_expect_tx(bar, Wn * 2 * B::BR * B::BOX * 8);
     }
     __syncthreads();
-    for (int r = tid; r < Wn2; r += NT) {
-      const int wz = r / Wn, wy = r - wz * Wn;
-      tma_load_1d(X + r * B::RW, &xmap, int(wbase + (int64_t(wz) * n1 + wy) * n1) & ~1, bar);
+    if (tid < 2 * Wn) {
+      const int wz = tid >> 1, par = tid & 1;                   // plane, row parity (of J)
+      const int J0 = (oz + wz - zoff) * n1 + oy;                // first window row of the plane
+      const int Jf = J0 + ((J0 ^ par) & 1);                     // first window row of parity par
+      double *dst = X + (wz * 2 + par) * B::BR * B::RW;
+      if (par == 0) tma_load_2d(dst, &xmap_e, ox & ~1, Jf >> 1, bar);
+      else tma_load_2d(dst, &xmap_o, (ox + 1) & ~1, Jf >> 1, bar);
     }
   } else {                                                        // LG lanes per row: coalesced row copies
     // (zero outside the domain)                                                               // LG lanes per row: coalesced row copies
@@ -149,15 +156,24 @@ __global__ void __launch_bounds__(B4<P, S>::NT) k_schwarz3d_v4(const __grid_cons
   if constexpr (TMA) mbar_wait(bar, 0);
   __syncthreads();
   // ---- pass x: pencils (wy, wz) along x -> Pa = Kx X, Pb = Mx X ----
+  // window row (wz, wy) -> tile row: parity of J = J0 + wy, index among the plane's rows of that parity
+  auto trow = [&](int wz, int wy, int *k, int *sh) {
+    const int J0 = (oz + wz - zoff) * n1 + oy, par = (J0 + wy) & 1, d0 = J0 & 1;
+    *k = par == 0 ? ((wy + d0) >> 1) - d0 : (wy - 1 + d0) >> 1;
+    *sh = par == 0 ? (ox & 1) : ((ox + 1) & 1);
+    return (wz * 2 + par) * B::BR;
+  };
   if constexpr (TMA) {
     for (int pi = tid; pi < Wn2; pi += NT) {
       const int wz = pi / Wn, wy = pi - wz * Wn;
-      const int sh = int(wbase + (int64_t(wz) * n1 + wy) * n1) & 1;
-      const double2 *row = reinterpret_cast<const double2 *>(X + pi * B::RW);
+      int k, sh;
+      const int t0 = trow(wz, wy, &k, &sh);
+      const double2 *row = reinterpret_cast<const double2 *>(X + (t0 + k) * B::RW);
+      const int sw = (t0 + k) & 7;
       double v[B::BOX];
 #pragma unroll
       for (int c = 0; c < B::BOX / 2; ++c) {
-        const double2 t = row[c ^ (pi & 7)];
+        const double2 t = row[c ^ sw];
         v[2 * c] = t.x;
         v[2 * c + 1] = t.y;
       }
@@ -168,9 +184,10 @@ __global__ void __launch_bounds__(B4<P, S>::NT) k_schwarz3d_v4(const __grid_cons
       else pencil_x<S, W, Wn, false>(u, Tk, Tm, tp, Pa + pi * S, Pb + pi * S, 1);
     }
     if (tid < S3) {
-      const int pr = (lz + P) * Wn + ly + P;
-      const int e = lx + P + (int(wbase + (int64_t(lz + P) * n1 + ly + P) * n1) & 1);
-      Xc[tid] = X[pr * B::RW + (((e >> 1) ^ (pr & 7)) << 1) + (e & 1)];
+      int k, sh;
+      const int t0 = trow(lz + P, ly + P, &k, &sh);
+      const int e = lx + P + sh;
+      Xc[tid] = X[(t0 + k) * B::RW + (((e >> 1) ^ ((t0 + k) & 7)) << 1) + (e & 1)];
     }
   } else {
     for (int pi = tid; pi < Wn2; pi += NT) {
@@ -291,19 +308,20 @@ bool try_schwarz3d(int p, int s, int64_t n1, const double *K, const double *M, c
     using B = B4<P, S>;
     ToeP tp{};
     if (tpp) tp = *tpp;
-    CUtensorMap map{};
+    CUtensorMap me{}, mo{};
     const int w = (S - 1) / 2;
-    const int64_t stored = (std::min<int64_t>(n1, c2 + int64_t(D) * (nb2 - 1) + w + P + 1) - zoff) * n1 * n1;
-    if (B::TMA_OK && g_s3d_tma && make_tmap_1d_swz128(&map, x, stored, B::BOX)) {
+    const int64_t rows = (std::min<int64_t>(n1, c2 + int64_t(D) * (nb2 - 1) + w + P + 1) - zoff) * n1;   // stored rows
+    if (B::TMA_OK && g_s3d_tma && rows >= 2 && make_tmap_rows_swz128(&me, x, n1, (rows + 1) / 2, 2 * n1, B::BOX, B::BR) &&
+        make_tmap_rows_swz128(&mo, x + n1 - 1, n1 + 1, rows / 2, 2 * n1, B::BOX, B::BR)) {
       constexpr size_t sm = sizeof(double) * B::PERT + 16 + 1024;
       ensure_smem(k_schwarz3d_v4<P, S, true>, sm);
-      k_schwarz3d_v4<P, S, true><<<nb0 * nb1 * nb2, B::NT, sm, st>>>(map, int(n1), K, M, V, lam, b, x, c0, c1, c2, D,
-                                                                     nb0, nb1, zoff, tlo, thi, tp);
+      k_schwarz3d_v4<P, S, true><<<nb0 * nb1 * nb2, B::NT, sm, st>>>(me, mo, int(n1), K, M, V, lam, b, x, c0, c1, c2,
+                                                                     D, nb0, nb1, zoff, tlo, thi, tp);
     } else {
       constexpr size_t sm = sizeof(double) * B::PER + 16 + 1024;
       ensure_smem(k_schwarz3d_v4<P, S, false>, sm);
-      k_schwarz3d_v4<P, S, false><<<nb0 * nb1 * nb2, B::NT, sm, st>>>(map, int(n1), K, M, V, lam, b, x, c0, c1, c2, D,
-                                                                      nb0, nb1, zoff, tlo, thi, tp);
+      k_schwarz3d_v4<P, S, false><<<nb0 * nb1 * nb2, B::NT, sm, st>>>(me, mo, int(n1), K, M, V, lam, b, x, c0, c1,
+                                                                      c2, D, nb0, nb1, zoff, tlo, thi, tp);
     }
     return true;
   }

@@ -30,7 +30,7 @@ bool make_tmap_1d_swz128(void *map64, const double *ptr, int64_t n, int box) {
   return box * 8 <= 128 && encode_1d(map64, ptr, n, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-static bool encode_1d(void *map64, const double *ptr, int64_t n, int box, CUtensorMapSwizzle swz) {
+static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
     void *fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -41,6 +41,26 @@ static bool encode_1d(void *map64, const double *ptr, int64_t n, int box, CUtens
     }
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }();
+  return enc;
+}
+
+bool make_tmap_rows_swz128(void *map64, const double *ptr, int64_t cols, int64_t rows, int64_t stride, int box_cols,
+                           int box_rows) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = encoder();
+  if (!enc || rows <= 0 || cols <= 0 || box_cols * 8 > 128 || (box_cols * 8) % 16 || box_rows > 256 ||
+      (stride * 8) % 16 || (reinterpret_cast<uintptr_t>(ptr) & 15))
+    return false;
+  cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(stride * 8)};
+  cuuint32_t boxd[2] = {cuuint32_t(box_cols), cuuint32_t(box_rows)};
+  cuuint32_t es[2] = {1, 1};
+  return enc(static_cast<CUtensorMap *>(map64), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(ptr), dims,
+             strides, boxd, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool encode_1d(void *map64, const double *ptr, int64_t n, int box, CUtensorMapSwizzle swz) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = encoder();
   if (!enc || n <= 0 || box <= 0 || box > 256 || (box * 8) % 16 || (reinterpret_cast<uintptr_t>(ptr) & 15)) return false;
   cuuint64_t dims[1] = {cuuint64_t(n)};
   cuuint64_t strides[1] = {0};
