@@ -10,6 +10,10 @@ iteration of each of the three problems (the three p of the config), inputs resi
 metric value = DOF-iterations per second over the whole job = Σ_p N_p / step time (x n_gpus).
 L2 is flushed (a 256 MiB write) before every timed step; the flush is outside the event pair.
 
+--shard slab (with --config C3|C4|C5 under torchrun) runs ONE problem slab-partitioned along its last
+axis over the ranks (halo exchange per last-axis colour class over NCCL, allreduce of the
+coarse defect, replicated second level); "scaling" is then "strong".  Default (C2, --gpus N): N replicas.
+
 --impl reference runs the CPU oracle (oracle/, the parity reference) as the reference arm.
 """
 import argparse
@@ -33,6 +37,19 @@ FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # SMs x FP64 FMA/clk/SM x 2 x
 # FP64 tensor pipe (DMMA, mma.sync m8n8k4 f64): measured 37.09 TFLOP/s by tools/microbench.cu on this
 # pool's B200 (profiles/microbench_r01.txt); MEASURED_PEAKS.json has no FP64 entry
 DMMA_PEAK_TFLOPS = 37.09
+
+
+def hbm_peak():
+    """Measured HBM GB/s (MEASURED_PEAKS.json, driver-written), else the profiling guide's fallback."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# The paper's own numbers for the C2 cells (Table 4, P:418-422, 256^2 row; laptop i7-8550U, Fortran,
+# "cpu" = seconds to 1e-8): context only, another machine and an iteration count, not the target
+PAPER_C2 = {"p3": {"it": 6, "cpu_s": 0.55}, "p4": {"it": 7, "cpu_s": 0.79}, "p5": {"it": 5, "cpu_s": 1.45}}
 
 
 def env_rank():
@@ -103,71 +120,134 @@ def make_ctx(pkg, name, stream):
 
 
 class OracleSample:
-    """The oracle, as it stands, on a bounded sample of the workload: full-size C2 (p=3) built once
-    (assembly and the factorisations of the timed blocks are setup, not timed); one sample = the first
-    `colours_timed` of the D^2 Schwarz colours, timed and scaled to the whole sweep, plus the complete
-    defect / restriction / V(1,1) / prolongation."""
+    """The oracle, as it stands, on the bench workload: oracle.kron.KronTwoLevel (Algorithm 1 with the
+    Kronecker-form operator and colour-by-colour multicolour sweep, pinned to the assembled sequential
+    oracle) for each problem of the config, BLAS threads = all host cores of this process.  One sample
+    = ONE full iteration of every problem of the step (median of `reps`); setup (operators, V-cycle
+    hierarchy, first-sweep block inverses) is excluded."""
 
-    def __init__(self, p=3, colours_timed=2):
-        os.environ.setdefault("OMP_NUM_THREADS", "1")
-        from oracle.schwarz import colour_of
-        from oracle.twolevel import TwoLevel
+    def __init__(self, config="C2", reps=3):
+        from oracle.kron import KronTwoLevel
+        from oracle.multigrid import QHierarchy
         from oracle.assembly import load_sine
-        from synthetic_inputs import initial_guess
+        from synthetic_inputs import CONFIGS, initial_guess
         t0 = time.perf_counter()
-        self.p, self.ct = p, colours_timed
-        self.tl = TwoLevel(2, p, 1, 256, s=3, coarse="vcycle", h_factor=2, order="multicolour")
-        self.D = self.tl.s + p
-        self.b = load_sine(p, 256, 2)
-        self.x = initial_guess(self.tl.N)
-        self.sel = [c for c in self.tl.smoother.seq if colour_of(c, self.D) < colours_timed]
-        for c in self.sel:
-            self.tl.smoother._factor(c)
+        self.cores = len(os.sched_getaffinity(0))
+        self.reps = reps
+        self.probs = []
+        mgs = {}
+        for name in CONFIG_PROBLEMS[config]:
+            c = CONFIGS[name]
+            key = (c["q"], c["m"] // c["h_factor"], c["d"])
+            if c["coarse"] == "vcycle" and key not in mgs:
+                mgs[key] = QHierarchy(*key)
+            kt = KronTwoLevel(c["d"], c["p"], c["q"], c["m"], c["s"], c["coarse"], c["h_factor"], mg=mgs.get(key))
+            b, x = load_sine(c["p"], c["m"], c["d"]), initial_guess(kt.N)
+            kt.iterate(x, b)                          # first sweep forms the kept block inverses (setup)
+            self.probs.append((name, kt, b, x))
+        self.N = sum(kt.N for _, kt, _, _ in self.probs)
         self.setup_s = time.perf_counter() - t0
 
     def sample(self):
-        """Returns (DOF*it/s, seconds of timed CPU work)."""
-        tl, x, b = self.tl, self.x, self.b
-        t0 = time.perf_counter()
-        tl.smoother.sweep(x, b, self.sel)
-        t_sw = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        dq = tl.R @ (b - tl.A @ x)
-        e = tl._csolve(dq)
-        x += tl.RT @ e
-        t_rest = time.perf_counter() - t0
-        t_iter = t_sw * (self.D * self.D) / self.ct + t_rest
-        return tl.N / t_iter, t_iter
+        """Returns (DOF*it/s, seconds per step): the step's iterations, each the median of `reps`."""
+        t_step = 0.0
+        for _, kt, b, x in self.probs:
+            ts = []
+            for _ in range(self.reps):
+                t0 = time.perf_counter()
+                kt.iterate(x, b)
+                ts.append(time.perf_counter() - t0)
+            t_step += float(np.median(ts))
+        return self.N / t_step, t_step
 
     def describe(self):
-        return (f"oracle (NumPy/SciPy, 1 thread) on full-size C2 p={self.p}: {self.ct}/{self.D * self.D} Schwarz "
-                f"colours timed and scaled x{self.D * self.D / self.ct:.0f}, plus full defect+restriction+V(1,1)+"
-                f"prolongation; setup ({self.setup_s:.1f} s: assembly, block factorisations) excluded")
+        names = ",".join(n for n, _, _, _ in self.probs)
+        return (f"oracle.kron.KronTwoLevel (NumPy/SciPy, BLAS threads = {self.cores} host cores) on the full-size "
+                f"{names}: one complete two-level iteration per problem, median of {self.reps}; setup "
+                f"({self.setup_s:.1f} s: operators, V-cycle hierarchy, block inverses) excluded")
 
 
-def cpu_baseline_sample(p=3, colours_timed=2):
-    o = OracleSample(p, colours_timed)
+def cpu_baseline_sample(config="C2"):
+    o = OracleSample(config)
     v, t = o.sample()
-    return v, t, o.describe()
+    return v, t, o.describe(), o.cores
 
 
 def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    o = OracleSample()
+    o = OracleSample(args.config, reps=1)
     for _ in range(args.warmup):
         o.sample()
-    vals = [o.sample()[0] for _ in range(max(args.steps, 1))]
-    value = float(np.median(vals))
-    ms = float(1e3 * o.tl.N / value)
+    steps = [o.sample()[1] for _ in range(max(args.steps, 1))]
+    ms = float(1e3 * np.mean(steps))
+    value = o.N / (ms / 1e3)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD + " (reference arm: the CPU oracle, p=3 sample per step)"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": o.describe()},
+            "config": {"workload": CONFIG_TEXT[args.config] + " (reference arm: the CPU oracle, full iterations)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": o.cores, "kind": "oracle", "sample": o.describe()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def graph_time(fn, stream, reps, flush=None):
+    """Mean device time (ms) of fn()'s launches replayed from a CUDA graph captured on `stream` (the
+    launch mode of the bench step: iga2l_iterate replays its own graph); L2 flushed before every replay
+    (outside the event pair) when `flush` is given."""
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ms = 0.0
+    for _ in range(reps):
+        if flush is not None:
+            flush.fill_(1.0)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+    return ms / reps
+
+
+def kernel_rooflines(ctxs, bs, xs, info, side, flush, reps):
+    """Per kernel class of the iteration (Algorithm 1 phases), CUDA-graph-replayed, L2 flushed:
+    the Schwarz sweep against the FP64 peak (SURVEY §8(d) algorithmic flops), the HBM phases against
+    the measured HBM copy bandwidth (SURVEY §8(d) algorithmic bytes: defect + restriction 16 B per fine
+    DOF + 8 per coarse DOF; prolongation 16 B per fine DOF + 8 per coarse DOF; the V(1,1) ~64 B per DOF of
+    every second-level grid)."""
+    import torch
+    peak, src = hbm_peak()
+    out = {"sweep": {"ms": 0.0, "flops": 0.0, "launches": 0}, "defect_restrict": {"ms": 0.0, "bytes": 0.0},
+           "coarse_vcycle": {"ms": 0.0, "bytes": 0.0}, "prolong": {"ms": 0.0, "bytes": 0.0}}
+    for c, b, x, inf, st in zip(ctxs, bs, xs, info, side):
+        dq = torch.zeros(c.Nc, dtype=torch.float64, device=x.device)
+        e = torch.zeros_like(dq)
+        out["sweep"]["ms"] += graph_time(lambda: c.sweep(b, x), st, reps, flush)
+        out["sweep"]["flops"] += inf.sweep_flops
+        out["sweep"]["launches"] += inf.colours
+        out["defect_restrict"]["ms"] += graph_time(lambda: c.defect_restrict(b, x, dq), st, reps, flush)
+        out["defect_restrict"]["bytes"] += 16.0 * c.N + 8.0 * c.Nc
+        out["coarse_vcycle"]["ms"] += graph_time(lambda: c.coarse_solve(dq, e), st, reps, flush)
+        out["coarse_vcycle"]["bytes"] += inf.iter_hbm_bytes - 40.0 * c.N
+        out["prolong"]["ms"] += graph_time(lambda: c.prolong_add(e, x), st, reps, flush)
+        out["prolong"]["bytes"] += 16.0 * c.N + 8.0 * c.Nc
+    for k, v in out.items():
+        if k == "sweep":
+            v["tflops"] = v["flops"] / (v["ms"] / 1e3) / 1e12
+        else:
+            v["GBps"] = v["bytes"] / (v["ms"] / 1e3) / 1e9
+            v["frac_of_hbm"] = v["GBps"] / peak
+    out["hbm_peak_GBps"] = peak
+    out["hbm_peak_source"] = src
+    return out
 
 
 def main():
@@ -178,6 +258,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", default="C2", choices=sorted(CONFIG_PROBLEMS))
+    ap.add_argument("--shard", default="replicas", choices=["replicas", "slab"])
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -196,7 +277,8 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.Stream(dev)         # one stream for torch ops, library calls and events
     torch.cuda.set_stream(stream)
-    sh = stream.cuda_stream
+    if args.shard == "slab":
+        return run_slab(args, pkg, dist, rank, world, local, dev, stream)
 
     # the three problems of the workload are independent: each context runs on its own stream and a
     # step forks them from the main stream and joins them back (events), so their latency-bound
@@ -278,24 +360,12 @@ def main():
             ms += e0.elapsed_time(e1)
         ms /= reps
         per_p[f"p{p}"] = {"N": c.N, "it_per_s": 1e3 / ms, "dof_per_s": c.N * 1e3 / ms, "ms_per_iter": ms}
+        if args.config == "C2":
+            per_p[f"p{p}"]["paper_table4_256sq"] = dict(PAPER_C2[f"p{p}"], note="P:420, laptop i7-8550U, to 1e-8")
 
-    # dominant kernel: the Schwarz colour kernel (all D^2 launches of one sweep), timed live
-    sw_ms_tot, sw_flops_tot, sw_launches = 0.0, 0.0, 0
-    for i, (c, b, x, inf) in enumerate(zip(ctxs, bs, xs, info)):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = max(args.steps, 5)
-        ms = 0.0
-        for _ in range(reps):
-            flush.fill_(2.0)
-            e0.record(stream)
-            on_side(i, lambda: c.sweep(b, x))
-            e1.record(stream)
-            torch.cuda.synchronize()
-            ms += e0.elapsed_time(e1)
-        sw_ms_tot += ms / reps
-        sw_flops_tot += inf.sweep_flops
-        sw_launches += inf.colours
-    achieved = sw_flops_tot / (sw_ms_tot / 1e3) / 1e12
+    # per kernel class, graph-replayed (the launch mode of the step), L2 flushed before every replay
+    kr = kernel_rooflines(ctxs, bs, xs, info, side, flush, max(min(args.steps, 50), 5))
+    achieved = kr["sweep"]["tflops"]
     # dram__bytes_read.sum + dram__bytes_write.sum per launch of this config's dominant kernel, from one
     # `ncu --set full` capture of this bench command (tools/traffic.py writes the file); null if not captured
     traffic, traffic_kernel = None, None
@@ -308,20 +378,28 @@ def main():
         except Exception:
             traffic = None
     dim = ctxs[0].dim
+    note = ("C2 is latency bound (36/49/100 dependent colours of 0.7-1.8k blocks); " if args.config == "C2" else "")
+    note += (f"achieved = SURVEY 8(d) sweep flops / CUDA-graph-replayed sweep time over {kr['sweep']['launches']} "
+             f"launches (L2 flushed before each replay)")
     if dim == 2:
         roofline = {"bound": "tensor", "achieved": achieved, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                     "frac": achieved / DMMA_PEAK_TFLOPS, "traffic": traffic, "traffic_kernel": traffic_kernel,
                     "kernel": "k_schwarz2d_mma (FP64 DMMA block solves, one launch per colour)",
                     "peak_source": "measured FP64 DMMA peak, tools/microbench.cu (profiles/microbench_r01.txt)",
-                    "note": ("C2 is latency bound (36/49/100 dependent colours of ~0.7-1.8k blocks); " if args.config == "C2"
-                             else "") +
-                            f"achieved = SURVEY 8(d) sweep flops / CUDA-event sweep time over {sw_launches} launches"}
+                    "note": note}
     else:
         roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic, "traffic_kernel": traffic_kernel,
-                    "kernel": "k_schwarz3d_t (FP64 FMA pencil block solves, one launch per colour)",
-                    "peak_source": "derived 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md)",
-                    "note": f"achieved = SURVEY 8(d) sweep flops / CUDA-event sweep time over {sw_launches} launches"}
+                    "kernel": "k_schwarz3d_v4 (FP64 FMA pencil block solves, TMA windows, one launch per colour)",
+                    "peak_source": "derived 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md)", "note": note}
+    roofline["hbm_kernels"] = {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
+                               for k, v in kr.items() if k not in ("sweep", "hbm_peak_GBps", "hbm_peak_source")}
+    roofline["hbm_peak_GBps"] = kr["hbm_peak_GBps"]
+    roofline["hbm_peak_source"] = kr["hbm_peak_source"]
+    # whole-iteration HBM fraction: the iteration's algorithmic bytes outside the sweep +
+    # 24 B per DOF for the sweep, over the step time
+    it_bytes = sum(i.iter_hbm_bytes + 24.0 * n for i, n in zip(info, Ns))
+    roofline["iteration_hbm_frac"] = it_bytes / (ms_per_step / 1e3) / 1e9 / kr["hbm_peak_GBps"]
 
     # convergence factor (b = 0, 20 iterations, last 10 ratios) and iterations to 1e-8
     conv = {}
@@ -391,14 +469,98 @@ def main():
                     "how": "iga2l_iterate with pinned HOST b, x per problem (H2D, one iteration, D2H inside the "
                            "call), the step's problems on concurrent host threads; host wall clock"},
             "wall_s_timed": t_wall}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == "C2":
-        v, t, desc = cpu_baseline_sample()
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
-                                "host_cores_available": len(os.sched_getaffinity(0))}
+    if args.config == "C2":
+        line["paper_context"] = {"table4_256sq_dof_it_per_s": sum(Ns) / sum(v["cpu_s"] / v["it"] for v in PAPER_C2.values()),
+                                 "source": "P:420 (it, cpu) for p=3,4,5 at 256^2; laptop, another machine: context only"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, t, desc, cores = cpu_baseline_sample(args.config)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
     if rank == 0:
         print(json.dumps(line), flush=True)
     for c in ctxs:
         c.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_slab(args, pkg, dist, rank, world, local, dev, stream):
+    """One problem of the config slab-partitioned over the ranks; every rank owns the
+    planes [z0, z1) of the last axis.  The NCCL unique id comes from rank 0's library and is broadcast
+    over torch.distributed.  Timed like the replica mode (barrier + synchronize, CUDA events on every
+    rank, max over ranks)."""
+    import torch
+    from synthetic_inputs import CONFIGS, initial_guess
+    name = CONFIG_PROBLEMS[args.config][0]
+    c = CONFIGS[name]
+    nid = [pkg.nccl_unique_id() if (rank == 0 and world > 1) else None]
+    if world > 1:
+        dist.broadcast_object_list(nid, src=0)
+    ctx = pkg.Context(c["d"], c["p"], c["q"], c["m"], c["s"],
+                      coarse_mode=pkg.COARSE_EXACT if c["coarse"] == "exact" else pkg.COARSE_VCYCLE,
+                      coarse_h_factor=c["h_factor"], stream=stream.cuda_stream, nranks=world,
+                      rank=rank if world > 1 else 0, nccl_id=nid[0] if world > 1 else None)
+    print(f"iga2l: rank {rank} of {world}: {'NCCL communicator initialised, ' if world > 1 else ''}"
+          f"owned planes [{ctx.z0}, {ctx.z1}) of {ctx.n1}", file=sys.stderr, flush=True)
+    n1, d = ctx.n1, ctx.dim
+    plane = n1 ** (d - 1)
+    xg = initial_guess(n1 ** d)
+    x = torch.tensor(xg[ctx.z0 * plane:ctx.z1 * plane], device=dev)
+    b = torch.empty(ctx.N_local, dtype=torch.float64, device=dev)
+    ctx.rhs_sine(b)
+    torch.cuda.synchronize()
+    for _ in range(max(args.warmup, 3)):
+        ctx.iterate(b, x, 1)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            evs[k][0].record(stream)
+            ctx.iterate(b, x, 1)
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    tot = torch.tensor([sum(a.elapsed_time(e) for a, e in evs)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms_per_step = float(tot.item()) / args.steps
+    Ntot = n1 ** d
+    # e2e through the C-ABI with this rank's HOST (pinned) slab vectors: H2D, one iteration, D2H in the call
+    hb, hx = b.cpu().pin_memory(), x.cpu().pin_memory()
+    ctx.iterate(hb, hx, 1)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ctx.iterate(hb, hx, 1)
+    e2e_t = torch.tensor([(time.perf_counter() - t0) * 1e3 / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    # residual history (3 iterations) as a health check of the distributed iteration
+    hist = np.zeros(4)
+    ctx.iterate(b, x, 3, hist)
+    line = {"metric": METRIC, "value": Ntot / (ms_per_step / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIG_TEXT[args.config], "global_batch": 1, "dofs": [Ntot],
+                       "l2": "flushed before every timed step (256 MiB write)", "parallelism": f"slab{world}",
+                       "halo_planes": c["s"] - 1 + c["p"],
+                       "graph": "eager launches (NCCL calls inside the schedule)"},
+            "residual_check": [float(v) for v in hist], "clocks": clk.summary(),
+            "gpu_launches": ctx.info().launches_per_iter * args.steps,
+            "e2e": {"value": Ntot / (float(e2e_t.item()) / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": 2 * 8 * ctx.N_local, "d2h_bytes_per_step": 8 * ctx.N_local,
+                    "how": "per rank: iga2l_iterate with pinned HOST slab b, x (H2D, iteration, D2H in the call); "
+                           "host wall clock, max over ranks; bytes per rank"}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -119,7 +119,7 @@ def _block_matrices(Kd, Md, lo, ln, d):
 class KronTwoLevel:
     """Algorithm 1, multicolour Schwarz order, matrix-free (see module docstring)."""
 
-    def __init__(self, d, p, q, m, s, coarse="vcycle", h_factor=2, coarsest_m=8, cache_bytes=6e9):
+    def __init__(self, d, p, q, m, s, coarse="vcycle", h_factor=2, coarsest_m=8, cache_bytes=6e9, mg=None):
         self.d, self.p, self.q, self.m, self.s = d, p, q, m, s
         self.n1 = m + p - 2
         self.N = self.n1 ** d
@@ -133,8 +133,8 @@ class KronTwoLevel:
         self.R1T = sp.csr_matrix(R1.T)
         self.nc1 = R1.shape[0]
         self.Nc = self.nc1 ** d
-        if coarse == "vcycle":
-            self.mg = QHierarchy(q, self.mc, d, coarsest_m)
+        if coarse == "vcycle":          # (a QHierarchy of the same (q, m_c, d) may be shared: it is read-only)
+            self.mg = mg if mg is not None else QHierarchy(q, self.mc, d, coarsest_m)
             self._csolve = self.mg.vcycle
         elif coarse == "exact":
             self._csolve = spla.factorized(stiffness(q, self.mc, d).tocsc())
