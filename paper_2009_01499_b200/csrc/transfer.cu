@@ -9,29 +9,40 @@ namespace {
 // =============================== band transform along one axis ===========================
 // Columns valid in [clo, chi), stored from column coff on (nin stored columns per outer slice);
 // output rows r in [rlo, rhi), stored from row rlo on (rhi - rlo rows per outer slice).
-__global__ void k_band_axis(const double *__restrict__ in, double *__restrict__ out, int64_t outer, int nin,
-                            int64_t inner, int rows, int W, const int *__restrict__ lo,
-                            const double *__restrict__ c, int acc, int clo, int chi, int coff, int rlo, int rhi) {
+// One thread per output, no index divisions: inner > 1 -> threads along the contiguous inner index,
+// blockIdx.y = output row, blockIdx.z = outer slice; inner == 1 -> threads along the output rows,
+// blockIdx.y + gridDim.y * blockIdx.z = outer slice.
+__global__ void __launch_bounds__(256) k_band_axis(const double *__restrict__ in, double *__restrict__ out,
+                                                   int64_t outer, int nin, int64_t inner, int W,
+                                                   const int *__restrict__ lo, const double *__restrict__ c, int acc,
+                                                   int clo, int chi, int coff, int rlo, int rhi) {
   const int nr = rhi - rlo;
-  const int64_t total = outer * nr * inner;
-  (void)rows;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = idx % inner;
-    const int r = rlo + int((idx / inner) % nr);
-    const int64_t o = idx / (inner * nr);
-    const int l0 = lo[r];
-    double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {            // all gathers independent (W <= 16 checked at setup)
-      const int col = l0 + k;
-      const bool ok = k < W && col >= clo && col < chi;
-      const double v = ok ? c[(int64_t)r * W + k] * in[(o * nin + (col - coff)) * inner + i] : 0.0;
-      if (k & 1) s1 += v; else s0 += v;
-    }
-    const double s = s0 + s1;
-    out[idx] = acc ? out[idx] + s : s;
+  int64_t i, o;
+  int r;
+  if (inner == 1) {
+    r = rlo + int(blockIdx.x * blockDim.x + threadIdx.x);
+    o = blockIdx.y + int64_t(gridDim.y) * blockIdx.z;
+    i = 0;
+    if (r >= rhi || o >= outer) return;
+  } else {
+    i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    r = rlo + int(blockIdx.y);
+    o = blockIdx.z;
+    if (i >= inner) return;
   }
+  const int l0 = lo[r];
+  const double *src = in + (o * nin - coff) * inner + i;
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {              // all gathers independent (W <= 16 checked at setup)
+    const int col = l0 + k;
+    const bool ok = k < W && col >= clo && col < chi;
+    const double v = ok ? c[int64_t(r) * W + k] * src[int64_t(col) * inner] : 0.0;
+    if (k & 1) s1 += v; else s0 += v;
+  }
+  const double s = s0 + s1;
+  const int64_t idx = (o * nr + (r - rlo)) * inner + i;
+  out[idx] = acc ? out[idx] + s : s;
 }
 
 // 2D tensor transfer, direct: out[ry][rx] (+)= Σ_{ky,kx} c[ry][ky] c[rx][kx] in[lo[ry]+ky][lo[rx]+kx].
@@ -152,8 +163,15 @@ void launch_band_axis(const double *in, double *out, int64_t outer, int nin, int
   if (rhi < 0) { rlo = 0; rhi = B.rows; }
   const int64_t total = outer * (rhi - rlo) * inner;
   if (total <= 0) return;
-  k_band_axis<<<grid_for(total, 256), 256, 0, st>>>(in, out, outer, nin, inner, B.rows, B.W, B.lo, B.c, accumulate,
-                                                   clo, chi, coff, rlo, rhi);
+  const int nr = rhi - rlo;
+  if (inner == 1) {
+    const unsigned gy = unsigned(std::min<int64_t>(outer, 32768)), gz = unsigned((outer + gy - 1) / gy);
+    k_band_axis<<<dim3((nr + 127) / 128, gy, gz), 128, 0, st>>>(in, out, outer, nin, inner, B.W, B.lo, B.c,
+                                                                accumulate, clo, chi, coff, rlo, rhi);
+  } else {
+    k_band_axis<<<dim3(unsigned((inner + 255) / 256), unsigned(nr), unsigned(outer)), 256, 0, st>>>(
+        in, out, outer, nin, inner, B.W, B.lo, B.c, accumulate, clo, chi, coff, rlo, rhi);
+  }
 }
 
 void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumulate, cudaStream_t st,
