@@ -55,6 +55,14 @@ typedef enum {
   IGA2L_COARSE_VCYCLE = 1  /* one V(1,1) h-multigrid cycle, zero initial guess     */
 } iga2l_coarse_mode;
 
+typedef enum {
+  IGA2L_GEOM_SQUARE = 0,            /* Ω = (0,1)^d, B-splines (the benchmark workloads)      */
+  IGA2L_GEOM_QUARTER_ANNULUS = 1    /* Ω = {0.3² <= x²+y² <= 0.5², x,y >= 0}: F = ρ(η)c(ξ), */
+                                    /*   NURBS in ξ (exact arc), B-splines in η.  2D only,  */
+                                    /*   q = 2, p >= 2, nranks 1.  Orthogonal map, so          */
+                                    /*   A = My ⊗ Kx + Ky ⊗ Mx with weighted 1D tables per axis       */
+} iga2l_geometry;
+
 typedef struct {
   int coarse_mode;       /* iga2l_coarse_mode; default VCYCLE                                    */
   int coarse_h_factor;   /* 1: q-level on the same mesh h (Algorithm 1); 2: aggressive   */
@@ -72,6 +80,7 @@ typedef struct {
                          /*     (global vectors; halo exchange by device copies; nccl_id NULL)   */
   const void *nccl_id;   /* 128-byte ncclUniqueId from iga2l_nccl_unique_id() on one rank,       */
                          /*   broadcast by the caller (NULL unless rank >= 0 and nranks > 1)     */
+  int geometry;          /* iga2l_geometry; default SQUARE                                        */
 } iga2l_opts;
 
 /* Fill *o with the defaults above. */
@@ -99,6 +108,10 @@ int iga2l_sizes(const iga2l_ctx *ctx, int64_t *n_local, int64_t *z0, int64_t *z1
 /* b_i = (f, φ_i) for f = d π² ∏ sin(π x_a) (exact solution u = ∏ sin(π x_a); P:397-405 for d=2),
  * Gauss quadrature with p+3 points per span (reading A17).  b: N fp64 (output). */
 int iga2l_rhs_sine(iga2l_ctx *ctx, double *b);
+/* The paper's right-hand side for the context's geometry: square -> iga2l_rhs_sine; quarter annulus ->
+ * b_ik = (f, φ_ik), f = -Δu for u = sin(πx) sin(πy)(x²+y²-r²)(x²+y²-R²), (p+3)² Gauss points
+ * per element (host quadrature, then copied).  b: N fp64, host or device. */
+int iga2l_rhs(iga2l_ctx *ctx, double *b);
 
 /* y = A_p x, matrix-free ((2p+1)^d-point operator).  x, y: N fp64, must not alias. */
 int iga2l_apply(iga2l_ctx *ctx, const double *x, double *y);
@@ -173,6 +186,16 @@ int iga2l_host_restriction_1d(int p, int q, int64_t m, int h_factor, double *R);
  * index, column = eigen index); lam: host n doubles.  Then A_q^{-1} = (⊗V) (Σ_a lam)^{-1} (⊗V)^T
  * (SURVEY §8(f) row 1).  ENUMERIC if M or K is not SPD. */
 int iga2l_host_coarse_fd(int q, int64_t m, double *V, double *lam);
+
+/* Host-only helpers of the quarter annulus (no GPU needed):
+ *  tables: per-axis constrained band tables, K and M each [2][n1][2p+1] (axis 0 = ξ: ∫R'R'/s, ∫R R s;
+ *          axis 1 = η: ∫N'N' ρ/ρ', ∫N N ρ'/ρ), so that A = My ⊗ Kx + Ky ⊗ Mx;
+ *  restriction_1d: one axis of the restriction (lumped L2 on the map, composed with the exact NURBS /
+ *          B-spline embedding for h_factor 2), dense row-major (n1c x n1), q = 2;
+ *  load: the load vector of iga2l_rhs, n1*n1 (x = ξ fastest). */
+int iga2l_host_annulus_tables(int p, int64_t m, double *K, double *M);
+int iga2l_host_annulus_restriction_1d(int axis, int p, int q, int64_t m, int h_factor, double *R);
+int iga2l_host_annulus_load(int p, int64_t m, double *b);
 
 int iga2l_destroy(iga2l_ctx *ctx);
 const char *iga2l_last_error(void);

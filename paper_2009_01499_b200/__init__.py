@@ -15,13 +15,14 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "iga2l.h")
 
 OK, EPARAM, ENUMERIC, NOTCONV, ECUDA, ENCCL, ENOMEM = range(7)
 COARSE_EXACT, COARSE_VCYCLE = 0, 1
+GEOM_SQUARE, GEOM_QUARTER_ANNULUS = 0, 1
 
 
 class Opts(ctypes.Structure):
     _fields_ = [("coarse_mode", ctypes.c_int), ("coarse_h_factor", ctypes.c_int),
                 ("vcycle_coarsest_m", ctypes.c_int), ("stream", ctypes.c_void_p),
                 ("use_graph", ctypes.c_int), ("nranks", ctypes.c_int), ("rank", ctypes.c_int),
-                ("nccl_id", ctypes.c_void_p)]
+                ("nccl_id", ctypes.c_void_p), ("geometry", ctypes.c_int)]
 
 
 class Info(ctypes.Structure):
@@ -56,6 +57,7 @@ def lib():
         "iga2l_setup_ex": (i, [i, i, i, i64, i, i, P(Opts), P(vp)]),
         "iga2l_sizes": (i, [vp, P(i64), P(i64), P(i64), P(i64)]),
         "iga2l_rhs_sine": (i, [vp, vp]),
+        "iga2l_rhs": (i, [vp, vp]),
         "iga2l_apply": (i, [vp, vp, vp]),
         "iga2l_residual_norm": (i, [vp, vp, vp, P(d)]),
         "iga2l_iterate": (i, [vp, vp, vp, i, vp]),
@@ -69,6 +71,9 @@ def lib():
         "iga2l_host_coarse_fd": (i, [i, i64, vp, vp]),
         "iga2l_host_restriction_1d": (i, [i, i, i64, i, vp]),
         "iga2l_host_slab_plan": (i, [i, i, i, i64, i, i, vp]),
+        "iga2l_host_annulus_tables": (i, [i, i64, vp, vp]),
+        "iga2l_host_annulus_restriction_1d": (i, [i, i, i, i64, i, vp]),
+        "iga2l_host_annulus_load": (i, [i, i64, vp]),
         "iga2l_nccl_unique_id": (i, [vp]),
         "iga2l_destroy": (i, [vp]),
         "iga2l_last_error": (ctypes.c_char_p, []),
@@ -151,11 +156,38 @@ def host_restriction_1d(p, q, m, h_factor):
     return R.reshape(n1c, n1)
 
 
+def host_annulus_tables(p, m):
+    """Quarter-annulus per-axis band tables (host-only): (Kx, Mx, Ky, My), each (n1, 2p+1)."""
+    import numpy as np
+    n1 = m + p - 2
+    K = np.zeros(2 * n1 * (2 * p + 1))
+    M = np.zeros_like(K)
+    _check(lib().iga2l_host_annulus_tables(p, m, _ptr(K), _ptr(M)))
+    K, M = K.reshape(2, n1, 2 * p + 1), M.reshape(2, n1, 2 * p + 1)
+    return K[0], M[0], K[1], M[1]
+
+
+def host_annulus_restriction_1d(axis, p, q, m, h_factor):
+    import numpy as np
+    n1, n1c = m + p - 2, m // h_factor + q - 2
+    R = np.zeros(n1c * n1)
+    _check(lib().iga2l_host_annulus_restriction_1d(axis, p, q, m, h_factor, _ptr(R)))
+    return R.reshape(n1c, n1)
+
+
+def host_annulus_load(p, m):
+    import numpy as np
+    b = np.zeros((m + p - 2) ** 2)
+    _check(lib().iga2l_host_annulus_load(p, m, _ptr(b)))
+    return b
+
+
 class Context:
     """One iga2l context (iga2l_setup_ex).  Methods mirror the C entry points."""
 
     def __init__(self, dim, p, q, m, block, overlap=None, coarse_mode=COARSE_VCYCLE, coarse_h_factor=2,
-                 vcycle_coarsest_m=8, stream=None, use_graph=True, nranks=1, rank=0, nccl_id=None):
+                 vcycle_coarsest_m=8, stream=None, use_graph=True, nranks=1, rank=0, nccl_id=None,
+                 geometry="square"):
         L = lib()
         o = Opts()
         L.iga2l_default_opts(ctypes.byref(o))
@@ -169,6 +201,7 @@ class Context:
                 stream = None
         o.stream = stream or None
         o.nranks, o.rank = nranks, rank
+        o.geometry = {"square": GEOM_SQUARE, "annulus": GEOM_QUARTER_ANNULUS}[geometry]
         self._id = None
         if nccl_id is not None:
             self._id = ctypes.create_string_buffer(bytes(nccl_id), 128)
@@ -187,6 +220,11 @@ class Context:
         inf = Info()
         _check(lib().iga2l_get_info(self._h, ctypes.byref(inf)))
         return inf
+
+    def rhs(self, b):
+        """The paper's right-hand side for this geometry (square: sine; annulus: P:439-447)."""
+        _check(lib().iga2l_rhs(self._h, _ptr(b)))
+        return b
 
     def rhs_sine(self, b):
         _check(lib().iga2l_rhs_sine(self._h, _ptr(b)))

@@ -52,6 +52,7 @@ struct Level {
   double *K = nullptr, *M = nullptr;   // band tables [n][2q+1]
   double *x = nullptr, *b = nullptr, *r = nullptr, *t1 = nullptr, *t2 = nullptr;
   DevBand P, PT;      // to the next coarser level: P (n x n_c), PT (n_c x n)
+  DevBand Py, PTy;    // y-axis factors when the context has per-axis tables (quarter annulus)
   double *inv = nullptr;               // dense inverse at the coarsest level
   double *fdV = nullptr, *fdLam = nullptr;   // exact solve by Kronecker fast diagonalisation (large levels)
 };
@@ -60,12 +61,14 @@ struct Level {
 
 struct iga2l_ctx {
   int dim = 2, p = 1, q = 1, s = 1, w = 0, D = 1, colours = 1;
+  int ax = 0;                    // 1: per-axis 1D tables [2][n][.] (quarter annulus, A = My ⊗ Kx + Ky ⊗ Mx)
   int64_t m = 0, n1 = 0, N = 0;
   iga2l_opts opts{};
   cudaStream_t st = nullptr;
   bool own_stream = false;
   double *K1 = nullptr, *M1 = nullptr, *V = nullptr, *lam = nullptr, *g1 = nullptr;
   DevBand R, RT;
+  DevBand Ry, RTy;               // y-axis transfer factors (ax = 1)
   ToeP toe{};                    // interior 1D data (A27) for the kernels' constant-bank path
   double *frags = nullptr;       // interior-block DMMA operand fragments, lane-major (A27)
   std::vector<Level> lev;
@@ -161,7 +164,8 @@ bool is_device_ptr(const void *p) {
 // returns the number of per-CTA partial sums the launch wrote (the count to reduce)
 int L_apply(iga2l_ctx *c, const double *x, const double *b, double *y, double *partial, int mode) {
   int np = 0;
-  launch_apply(c->dim, c->p, c->n1, c->K1, c->M1, x, b, y, partial, mode, c->st, &np, kFull, &c->toe);
+  launch_apply(c->dim, c->p, c->n1, c->K1, c->M1, x, b, y, partial, mode, c->st, &np, kFull, &c->toe,
+               c->ax ? c->n1 * (2 * c->p + 1) : 0);
   c->launch_counter++;
   return np;
 }
@@ -174,12 +178,12 @@ void L_norm(iga2l_ctx *c, const double *x, const double *b, bool push_hist) {
   c->launch_counter++;
 }
 
-// Tensor-product transform out = (⊗_a B) in (all axes the same 1D band B), passes axis 0, 1, 2.
-// n_in per axis = B.cols, n_out = B.rows.  acc: add into out on the last pass.
+// Tensor-product transform out = (⊗_a B) in (all axes the same 1D band B; 2D: By on the y axis if
+// given), passes axis 0, 1, 2.  n_in per axis = B.cols, n_out = B.rows.  acc: add into out on the last pass.
 void L_tensor(iga2l_ctx *c, int dim, const Band1D &B, const double *in, double *out, double *t1, double *t2,
-              int acc) {
-  if (dim == 2) {            // one direct launch: out (+)= (B ⊗ B) in
-    launch_tensor2d(in, out, B, acc, c->st);
+              int acc, const Band1D *By = nullptr) {
+  if (dim == 2) {            // one direct launch: out (+)= (By ⊗ B) in
+    launch_tensor2d(in, out, B, acc, c->st, 0, -1, 0, 0, -1, 0, By);
     c->launch_counter++;
     return;
   }
@@ -203,7 +207,7 @@ void L_vcycle(iga2l_ctx *c, size_t l) {
     return;
   }
   if (L.fdV) {   // exact: (⊗V)(Σλ)^{-1}(⊗V)^T on the tensor pipe
-    c->launch_counter += launch_coarse_fd(c->dim, L.n, L.fdV, L.fdLam, L.b, L.x, L.t1, L.t2, c->st);
+    c->launch_counter += launch_coarse_fd(c->dim, L.n, L.fdV, L.fdLam, L.b, L.x, L.t1, L.t2, c->st, c->ax);
     return;
   }
   if (L.inv) {
@@ -212,22 +216,23 @@ void L_vcycle(iga2l_ctx *c, size_t l) {
     return;
   }
   const int ncol = int(ipow(c->q + 1, c->dim));
+  const int64_t ays = c->ax ? int64_t(L.n) * (2 * c->q + 1) : 0;   // per-axis level tables
   cudaMemsetAsync(L.x, 0, L.N * sizeof(double), c->st);   // zero initial guess (reading A13)
   for (int col = 0; col < ncol; ++col) {                 // pre-smoothing: (q+1)^d-colour GS (A11)
-    launch_q_gs_colour(c->dim, c->q, L.n, L.K, L.M, L.b, L.x, col, c->st);
+    launch_q_gs_colour(c->dim, c->q, L.n, L.K, L.M, L.b, L.x, col, c->st, ays);
     c->launch_counter++;
   }
   if (c->dim == 3)   // r = b - A_q x: the streaming sum-factorised operator kernel (degree q tables, no partials)
     launch_apply(3, c->q, L.n, L.K, L.M, L.x, L.b, L.r, nullptr, 1, c->st, nullptr, kFull, nullptr);
   else
-    launch_q_residual(c->dim, c->q, L.n, L.K, L.M, L.b, L.x, L.r, c->st);
+    launch_q_residual(c->dim, c->q, L.n, L.K, L.M, L.b, L.x, L.r, c->st, ays);
   c->launch_counter++;
   Level &C = c->lev[l + 1];
-  L_tensor(c, c->dim, L.PT.b, L.r, C.b, L.t1, L.t2, 0);   // restriction P^T (reading A8)
+  L_tensor(c, c->dim, L.PT.b, L.r, C.b, L.t1, L.t2, 0, c->ax ? &L.PTy.b : nullptr);   // restriction P^T (A8)
   L_vcycle(c, l + 1);
-  L_tensor(c, c->dim, L.P.b, C.x, L.x, L.t1, L.t2, 1);    // x += P e
+  L_tensor(c, c->dim, L.P.b, C.x, L.x, L.t1, L.t2, 1, c->ax ? &L.Py.b : nullptr);     // x += P e
   for (int col = 0; col < ncol; ++col) {                 // post-smoothing, same order
-    launch_q_gs_colour(c->dim, c->q, L.n, L.K, L.M, L.b, L.x, col, c->st);
+    launch_q_gs_colour(c->dim, c->q, L.n, L.K, L.M, L.b, L.x, col, c->st, ays);
     c->launch_counter++;
   }
 }
@@ -235,8 +240,9 @@ void L_vcycle(iga2l_ctx *c, size_t l) {
 void L_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
   for (int col = c0; col < c1; ++col) {
     if (!launch_schwarz_colour_fast(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st,
-                                    kFull, c->frags, &c->toe))
-      launch_schwarz_colour(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st);
+                                    kFull, c->frags, &c->toe, c->ax))
+      launch_schwarz_colour(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st, kFull,
+                            c->ax);
     c->launch_counter++;
   }
 }
@@ -245,9 +251,10 @@ void L_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
 void L_iteration(iga2l_ctx *c, const double *b, double *x, bool with_norm) {
   L_sweep(c, b, x, 0, c->colours);                           // u^1 = u^0 + S_p(b - A_p u^0)
   L_apply(c, x, b, c->r, nullptr, 1);                        // d_p = b - A_p u^1
-  L_tensor(c, c->dim, c->R.b, c->r, c->lev[0].b, c->t1, c->t2, 0);   // d_q = I_p^q d_p
+  const Band1D *Ry = c->ax ? &c->Ry.b : nullptr, *RTy = c->ax ? &c->RTy.b : nullptr;
+  L_tensor(c, c->dim, c->R.b, c->r, c->lev[0].b, c->t1, c->t2, 0, Ry);   // d_q = I_p^q d_p
   L_vcycle(c, 0);                                            // A_q e_q = d_q (exact or one V(1,1))
-  L_tensor(c, c->dim, c->RT.b, c->lev[0].x, x, c->t1, c->t2, 1);     // u^1 += I_q^p e_q
+  L_tensor(c, c->dim, c->RT.b, c->lev[0].x, x, c->t1, c->t2, 1, RTy);     // u^1 += I_q^p e_q
   if (with_norm) {
     L_norm(c, x, b, true);
   }
@@ -553,6 +560,7 @@ void iga2l_default_opts(iga2l_opts *o) {
   o->nranks = 1;
   o->rank = 0;
   o->nccl_id = nullptr;
+  o->geometry = IGA2L_GEOM_SQUARE;
 }
 
 int iga2l_setup(int dim, int p, int q, int64_t n, int block, int overlap, iga2l_ctx **out) {
@@ -594,6 +602,11 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
   if (o.coarse_h_factor == 2 && n % 2) return fail(IGA2L_EPARAM, "aggressive coarsening needs n even (S:358)");
   if (o.vcycle_coarsest_m < 1) return fail(IGA2L_EPARAM, "opts.vcycle_coarsest_m must be >= 1");
   if (o.nranks < 1) return fail(IGA2L_EPARAM, "opts.nranks must be >= 1");
+  if (o.geometry != IGA2L_GEOM_SQUARE && o.geometry != IGA2L_GEOM_QUARTER_ANNULUS)
+    return fail(IGA2L_EPARAM, "opts.geometry");
+  const bool annulus = o.geometry == IGA2L_GEOM_QUARTER_ANNULUS;
+  if (annulus && (dim != 2 || q != 2 || p < 2 || o.nranks != 1))
+    return fail(IGA2L_EPARAM, "quarter annulus: dim 2, q = 2 (the geometry's degree, P:453), p >= 2, nranks 1");
   if (o.nranks == 1 && (o.rank != 0 || o.nccl_id)) return fail(IGA2L_EPARAM, "opts.rank must be 0 and opts.nccl_id NULL when nranks == 1");
   if (o.nranks > 1 && !((o.rank == -1 && !o.nccl_id) || (o.rank >= 0 && o.rank < o.nranks && o.nccl_id)))
     return fail(IGA2L_EPARAM, "opts.rank: -1 (all slabs in this process, nccl_id NULL) or 0..nranks-1 with nccl_id");
@@ -619,6 +632,7 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
   c->dim = dim; c->p = p; c->q = q; c->s = block; c->w = (block - 1) / 2; c->D = block + p;
   c->colours = int(ipow(c->D, dim));
   c->m = n; c->n1 = n1; c->N = N; c->opts = o;
+  c->ax = annulus ? 1 : 0;
   c->nranks = o.nranks;
   c->rank = o.nranks > 1 ? o.rank : 0;
   c->H = block - 1 + p;
@@ -635,9 +649,21 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
   int rc;
   // fine level tables (P:83 via Gauss quadrature on Cox–de Boor)
   std::vector<double> K, M, V, lam;
-  band_tables(p, n, K, M);
-  if (!fd_tables(p, block, n1, K, M, V, lam)) return bail(fail(IGA2L_ENUMERIC, "Schwarz block matrix not SPD"));
-  {  // interior (translation-invariant) band row and FD tables, passed to kernels by value (A27)
+  if (annulus) {   // per-axis weighted NURBS / B-spline tables (geometry.cpp), FD tables per axis
+    annulus_band_tables(p, n, K, M);
+    const size_t tw = size_t(n1) * (2 * p + 1);
+    for (int a = 0; a < 2; ++a) {
+      std::vector<double> Ka(K.begin() + a * tw, K.begin() + (a + 1) * tw), Ma(M.begin() + a * tw, M.begin() + (a + 1) * tw);
+      std::vector<double> Va, la;
+      if (!fd_tables(p, block, n1, Ka, Ma, Va, la)) return bail(fail(IGA2L_ENUMERIC, "Schwarz block matrix not SPD"));
+      V.insert(V.end(), Va.begin(), Va.end());
+      lam.insert(lam.end(), la.begin(), la.end());
+    }
+  } else {
+    band_tables(p, n, K, M);
+    if (!fd_tables(p, block, n1, K, M, V, lam)) return bail(fail(IGA2L_ENUMERIC, "Schwarz block matrix not SPD"));
+  }
+  if (!annulus) {  // interior (translation-invariant) band row and FD tables, passed to kernels by value (A27)
     int64_t tlo, thi;
     toeplitz_rows(p, n, &tlo, &thi);
     const int W = 2 * p + 1, w = (block - 1) / 2;
@@ -653,12 +679,13 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
       (rc = upload(c, &c->lam, lam)) || (rc = upload(c, &c->g1, load_1d_sine(p, n))))
     return bail(rc);
   // transfers (aggressive P:263)
-  BandOp R1 = degree_restriction(p, q, n);
-  if (o.coarse_h_factor == 2) R1 = multiply(transpose(mesh_prolongation(q, mc)), R1);
-  {
+  for (int a = 0; a < (annulus ? 2 : 1); ++a) {
+    BandOp R1 = annulus ? annulus_degree_restriction(a, p, q, n) : degree_restriction(p, q, n);
+    if (o.coarse_h_factor == 2)
+      R1 = multiply(transpose(annulus ? annulus_embedding(a, q, mc) : mesh_prolongation(q, mc)), R1);
     const BandOp R1T = transpose(R1);
     if (R1.W > 16 || R1T.W > 16) return bail(fail(IGA2L_EPARAM, "transfer bandwidth > 16 (p + q too large)"));
-    if ((rc = upload_band(c, c->R, R1)) || (rc = upload_band(c, c->RT, R1T))) return bail(rc);
+    if ((rc = upload_band(c, a ? c->Ry : c->R, R1)) || (rc = upload_band(c, a ? c->RTy : c->RT, R1T))) return bail(rc);
   }
   // second-level hierarchy
   int64_t ml = mc;
@@ -668,7 +695,8 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
     L.n = int(ml + q - 2);
     L.N = ipow(L.n, dim);
     std::vector<double> Kq, Mq;
-    band_tables(q, ml, Kq, Mq);
+    if (annulus) annulus_band_tables(q, ml, Kq, Mq);   // [2][n][2q+1]
+    else band_tables(q, ml, Kq, Mq);
     if ((rc = upload(c, &L.K, Kq)) || (rc = upload(c, &L.M, Mq)) || (rc = dalloc(c, &L.x, L.N)) ||
         (rc = dalloc(c, &L.b, L.N)) || (rc = dalloc(c, &L.r, L.N)) || (rc = dalloc(c, &L.t1, L.N)) ||
         (rc = dalloc(c, &L.t2, L.N)))
@@ -679,7 +707,18 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
                         (fde ? fde[0] == '1' : L.N > 4096) && L.n <= 2048;
     if (use_fd) {   // exact second level at any size: Kronecker fast diagonalisation (host eigensolve)
       std::vector<double> V, lam;
-      if (!coarse_fd_tables(q, ml, V, lam)) return bail(fail(IGA2L_ENUMERIC, "coarse matrix not SPD"));
+      if (annulus) {       // per-axis decompositions [2][n][n], [2][n]
+        const size_t tw = size_t(L.n) * (2 * q + 1);
+        for (int a = 0; a < 2; ++a) {
+          std::vector<double> Va, la;
+          if (!band_fd_tables(q, L.n, Kq.data() + a * tw, Mq.data() + a * tw, Va, la))
+            return bail(fail(IGA2L_ENUMERIC, "coarse matrix not SPD"));
+          V.insert(V.end(), Va.begin(), Va.end());
+          lam.insert(lam.end(), la.begin(), la.end());
+        }
+      } else if (!coarse_fd_tables(q, ml, V, lam)) {
+        return bail(fail(IGA2L_ENUMERIC, "coarse matrix not SPD"));
+      }
       if ((rc = upload(c, &L.fdV, V)) || (rc = upload(c, &L.fdLam, lam))) return bail(rc);
       c->lev.push_back(L);
       break;
@@ -687,14 +726,19 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
     if (direct) {
       if (L.N > 4096) return bail(fail(IGA2L_EPARAM, "exact second level: dense inverse limited to 4096 unknowns, FD to n <= 2048 per axis"));
       std::vector<double> inv;
-      if (!dense_kron_inverse(dim, q, L.n, Kq, Mq, inv)) return bail(fail(IGA2L_ENUMERIC, "coarse matrix not SPD"));
+      if (!dense_kron_inverse(dim, q, L.n, Kq, Mq, inv, annulus ? int64_t(L.n) * (2 * q + 1) : 0))
+        return bail(fail(IGA2L_ENUMERIC, "coarse matrix not SPD"));
       if ((rc = upload(c, &L.inv, inv))) return bail(rc);
       c->lev.push_back(L);
       break;
     }
     if (ml % 2) return bail(fail(IGA2L_EPARAM, "V-cycle needs the second-level m divisible by 2 down to opts.vcycle_coarsest_m"));
-    BandOp P = mesh_prolongation(q, ml / 2);
+    BandOp P = annulus ? annulus_embedding(0, q, ml / 2) : mesh_prolongation(q, ml / 2);
     if ((rc = upload_band(c, L.P, P)) || (rc = upload_band(c, L.PT, transpose(P)))) return bail(rc);
+    if (annulus) {
+      BandOp Py = annulus_embedding(1, q, ml / 2);
+      if ((rc = upload_band(c, L.Py, Py)) || (rc = upload_band(c, L.PTy, transpose(Py)))) return bail(rc);
+    }
     c->lev.push_back(L);
     ml /= 2;
   }
@@ -709,7 +753,8 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
     // forces level 0 on a cluster of cs CTAs (test knob)
     const char *vc_env = std::getenv("IGA2L_VC_SMEM");
     const char *force = std::getenv("IGA2L_VC_FORCE_CS");
-    const bool want_sm = !(vc_env && vc_env[0] == '0') && c->lev.size() > 1;
+    // (per-axis tables: level-by-level kernels only)
+    const bool want_sm = !(vc_env && vc_env[0] == '0') && c->lev.size() > 1 && !annulus;
     const size_t cap = 227 * 1024;
     for (int l0 = 0; want_sm && c->l_sm < 0 && l0 + 1 < int(c->lev.size()); ++l0) {
       VcLayout vl;
@@ -726,7 +771,7 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
         }
     }
   }
-  if (dim == 2) {   // interior-block fragments for the DMMA colour kernel (A27)
+  if (dim == 2 && !annulus) {   // interior-block fragments for the DMMA colour kernel (A27)
     const int nf = export_interior_frags(p, block, n1, c->K1, c->M1, c->V, c->lam, nullptr, nullptr);
     if (nf > 0) {
       if ((rc = dalloc(c, &c->frags, nf))) return bail(rc);
@@ -820,9 +865,20 @@ int iga2l_get_info(const iga2l_ctx *c, iga2l_info *o) {
   return IGA2L_OK;
 }
 
+int iga2l_rhs(iga2l_ctx *c, double *b) {
+  if (int rc = check_ctx(c)) return rc;
+  if (!c->ax) return iga2l_rhs_sine(c, b);
+  if (!b) return fail(IGA2L_EPARAM, "b is NULL");
+  const std::vector<double> h = annulus_load(c->p, c->m);   // host quadrature (setup-like)
+  CU(cudaMemcpyAsync(b, h.data(), h.size() * sizeof(double), cudaMemcpyDefault, c->st));
+  CU(cudaStreamSynchronize(c->st));
+  return IGA2L_OK;
+}
+
 int iga2l_rhs_sine(iga2l_ctx *c, double *b) {
   if (int rc = check_ctx(c)) return rc;
   if (!b) return fail(IGA2L_EPARAM, "b is NULL");
+  if (c->ax) return fail(IGA2L_EPARAM, "iga2l_rhs_sine: square geometry only (use iga2l_rhs)");
   const double pi = 3.14159265358979323846;
   const bool dev = is_device_ptr(b);
   if (!dev && !c->hy && dalloc(c, &c->hy, c->N)) return IGA2L_ENOMEM;
@@ -1009,7 +1065,7 @@ int iga2l_defect_restrict(iga2l_ctx *c, const double *b, const double *x, double
   const bool dev = is_device_ptr(dq);
   double *dst = dev ? dq : c->hcb;
   L_apply(c, sx.ptr, sb.ptr, c->r, nullptr, 1);
-  L_tensor(c, c->dim, c->R.b, c->r, dst, c->t1, c->t2, 0);
+  L_tensor(c, c->dim, c->R.b, c->r, dst, c->t1, c->t2, 0, c->ax ? &c->Ry.b : nullptr);
   if (int rc_ = launch_status(c)) return rc_;
   return stage_out(c, dq, Staged{dst, !dev}, c->lev[0].N);
 }
@@ -1037,7 +1093,7 @@ int iga2l_prolong_add(iga2l_ctx *c, const double *e, double *x) {
   Staged se, sx;
   if (int rc = stage_in(c, e, c->hcx, c->lev[0].N, &se)) return rc;
   if (int rc = stage_in(c, x, c->hx, c->N, &sx)) return rc;
-  L_tensor(c, c->dim, c->RT.b, se.ptr, const_cast<double *>(sx.ptr), c->t1, c->t2, 1);
+  L_tensor(c, c->dim, c->RT.b, se.ptr, const_cast<double *>(sx.ptr), c->t1, c->t2, 1, c->ax ? &c->RTy.b : nullptr);
   if (int rc_ = launch_status(c)) return rc_;
   return stage_out(c, x, sx, c->N);
 }
@@ -1095,6 +1151,34 @@ int iga2l_host_restriction_1d(int p, int q, int64_t m, int h_factor, double *R) 
   if (h_factor == 2) R1 = multiply(transpose(mesh_prolongation(q, m / 2)), R1);
   for (int r = 0; r < R1.rows; ++r)
     for (int col = 0; col < R1.cols; ++col) R[(size_t)r * R1.cols + col] = R1.at(r, col);
+  return IGA2L_OK;
+}
+
+
+int iga2l_host_annulus_tables(int p, int64_t m, double *K, double *M) {
+  if (p < 2 || p > 8 || m < 1 || m + p - 2 < 1 || !K || !M) return fail(IGA2L_EPARAM, "host_annulus_tables arguments");
+  std::vector<double> k, mm;
+  annulus_band_tables(p, m, k, mm);
+  std::memcpy(K, k.data(), k.size() * sizeof(double));
+  std::memcpy(M, mm.data(), mm.size() * sizeof(double));
+  return IGA2L_OK;
+}
+
+int iga2l_host_annulus_restriction_1d(int axis, int p, int q, int64_t m, int h_factor, double *R) {
+  if ((axis != 0 && axis != 1) || p < 2 || p > 8 || q != 2 || q > p || m < 2 || (h_factor != 1 && h_factor != 2) ||
+      !R || (h_factor == 2 && m % 2))
+    return fail(IGA2L_EPARAM, "host_annulus_restriction_1d arguments");
+  BandOp R1 = annulus_degree_restriction(axis, p, q, m);
+  if (h_factor == 2) R1 = multiply(transpose(annulus_embedding(axis, q, m / 2)), R1);
+  for (int r = 0; r < R1.rows; ++r)
+    for (int col = 0; col < R1.cols; ++col) R[(size_t)r * R1.cols + col] = R1.at(r, col);
+  return IGA2L_OK;
+}
+
+int iga2l_host_annulus_load(int p, int64_t m, double *b) {
+  if (p < 2 || p > 8 || m < 1 || m + p - 2 < 1 || !b) return fail(IGA2L_EPARAM, "host_annulus_load arguments");
+  const std::vector<double> h = annulus_load(p, m);
+  std::memcpy(b, h.data(), h.size() * sizeof(double));
   return IGA2L_OK;
 }
 

@@ -14,7 +14,8 @@ template <int TX, int TY>
 __global__ void __launch_bounds__(256) k_apply2d(int p, int n1, const double *__restrict__ K,
                                                  const double *__restrict__ M, const double *__restrict__ x,
                                                  const double *__restrict__ b, double *__restrict__ y,
-                                                 double *__restrict__ partial, int mode, int zoff, int zlo, int zhi) {
+                                                 double *__restrict__ partial, int mode, int zoff, int zlo, int zhi,
+                                                 int64_t ys) {
   extern __shared__ double sm[];
   const int W = 2 * p + 1, WX = TX + 2 * p, WY = TY + 2 * p;
   double *X = sm;              // [WY][WX]
@@ -48,7 +49,7 @@ __global__ void __launch_bounds__(256) k_apply2d(int p, int n1, const double *__
   for (int i = threadIdx.x; i < TY * TX; i += blockDim.x) {   // pass along y: M_y Tk + K_y Tm
     const int ly = i / TX, lx = i - ly * TX, gx = x0 + lx, gy = y0 + ly;
     if (gx >= n1 || gy >= zhi) continue;
-    const double *kr = K + (int64_t)gy * W, *mr = M + (int64_t)gy * W;
+    const double *kr = K + ys + (int64_t)gy * W, *mr = M + ys + (int64_t)gy * W;   // y-axis tables
     double acc = 0.0;
     for (int u = 0; u < W; ++u) {
       acc = fma(mr[u], Tk[(ly + u) * TX + lx], acc);
@@ -199,7 +200,8 @@ template <int P, int AT>
 __global__ void __launch_bounds__(AT * AT / ARY, 2) k_apply2d_t(int n1, const double *__restrict__ K, const double *__restrict__ M,
                                                    const double *__restrict__ x, const double *__restrict__ b,
                                                    double *__restrict__ y, double *__restrict__ partial, int mode,
-                                                   int zoff, int zlo, int zhi, int tlo, int thi, const ToeP tp) {
+                                                   int zoff, int zlo, int zhi, int tlo, int thi, const ToeP tp,
+                                                   int64_t ys) {
   using A = Apl2<P, AT>;
   constexpr int NT = AT * AT / ARY;
   constexpr int W = A::W, WN = A::WN, ARX = A::ARX;
@@ -228,8 +230,8 @@ __global__ void __launch_bounds__(AT * AT / ARY, 2) k_apply2d_t(int n1, const do
       cp_async8(Mx + i, M + (okx ? (int64_t)gx * W + t : 0), okx);
     }
     if (!ty) {
-      cp_async8(Ky + i, K + (oky ? (int64_t)gy * W + t : 0), oky);
-      cp_async8(My + i, M + (oky ? (int64_t)gy * W + t : 0), oky);
+      cp_async8(Ky + i, K + ys + (oky ? (int64_t)gy * W + t : 0), oky);   // y-axis tables (ys: per-axis)
+      cp_async8(My + i, M + ys + (oky ? (int64_t)gy * W + t : 0), oky);
     }
   }
   cp_async_wait_all();
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(AT * AT / ARY, 2) k_apply2d_t(int n1, const do
 
 template <int P>
 bool try_apply2d(int p, int64_t n1, const double *K, const double *M, const double *x, const double *b, double *y,
-                 double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv, const ToeP *tpp) {
+                 double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv, const ToeP *tpp, int64_t ys) {
   if (p != P) return false;
   ToeP tp{};
   if (tpp) tp = *tpp;
@@ -284,7 +286,7 @@ bool try_apply2d(int p, int64_t n1, const double *K, const double *M, const doub
     ensure_smem(kern, sm);
     dim3 grid((unsigned)((n1 + at - 1) / at), (unsigned)((nz + at - 1) / at));
     kern<<<grid, at * at / ARY, sm, st>>>(int(n1), K, M, x, b, y, partial, mode, sv.zoff, sv.zlo, sv.zhi, 2 * P - 1,
-                                          m - 2 - P, tp);
+                                          m - 2 - P, tp, ys);
     if (nparts) *nparts = int(grid.x * grid.y);
   };
   // 32x32 tiles; 16x16 when that would leave fewer than two CTAs per SM
@@ -518,22 +520,23 @@ static const bool g_apply_stream = [] {
 }();
 
 void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, const double *x, const double *b,
-                  double *y, double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv, const ToeP *tp) {
+                  double *y, double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv, const ToeP *tp,
+                  int64_t ys) {
   if (sv.zhi < 0) sv = SlabView{0, 0, int(n1)};
   const int nz = sv.zhi - sv.zlo;
   const size_t sm = apply_smem(dim, p);
   if (nz <= 0) return;
-  if (g_apply_stream && launch_apply_stream(dim, p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp, false))
+  if (g_apply_stream && ys == 0 && launch_apply_stream(dim, p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp, false))
     return;
   if (dim == 2 &&
-      (try_apply2d<1>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
-       try_apply2d<2>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
-       try_apply2d<3>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
-       try_apply2d<4>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
-       try_apply2d<5>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
-       try_apply2d<6>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
-       try_apply2d<7>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
-       try_apply2d<8>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp)))
+      (try_apply2d<1>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp, ys) ||
+       try_apply2d<2>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp, ys) ||
+       try_apply2d<3>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp, ys) ||
+       try_apply2d<4>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp, ys) ||
+       try_apply2d<5>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp, ys) ||
+       try_apply2d<6>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp, ys) ||
+       try_apply2d<7>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp, ys) ||
+       try_apply2d<8>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp, ys)))
     return;
   if (dim == 3 &&
       (try_apply3d<1>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp) ||
@@ -546,7 +549,7 @@ void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, 
   if (dim == 2) {
     dim3 grid((unsigned)((n1 + A2X - 1) / A2X), (unsigned)((nz + A2Y - 1) / A2Y));
     ensure_smem(k_apply2d<A2X, A2Y>, sm);
-    k_apply2d<A2X, A2Y><<<grid, 256, sm, st>>>(p, int(n1), K, M, x, b, y, partial, mode, sv.zoff, sv.zlo, sv.zhi);
+    k_apply2d<A2X, A2Y><<<grid, 256, sm, st>>>(p, int(n1), K, M, x, b, y, partial, mode, sv.zoff, sv.zlo, sv.zhi, ys);
     if (nparts) *nparts = int(grid.x * grid.y);
   } else {
     const unsigned nbx = unsigned((n1 + A3X - 1) / A3X), nby = unsigned((n1 + A3Y - 1) / A3Y);

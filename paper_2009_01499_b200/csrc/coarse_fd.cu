@@ -81,10 +81,11 @@ __global__ void __launch_bounds__(128) k_dgemm_mma(const GemmArgs g) {
 }
 
 // T[idx] /= Σ_a lam[i_a]  (x-fastest multi-index over n^dim)
-__global__ void k_eig_divide(double *__restrict__ T, const double *__restrict__ lam, int n, int dim, int64_t total) {
+__global__ void k_eig_divide(double *__restrict__ T, const double *__restrict__ lam, int n, int dim, int64_t total,
+                             int64_t lys) {
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    double den = lam[idx % n] + lam[(idx / n) % n];
+    double den = lam[idx % n] + lam[lys + (idx / n) % n];
     if (dim == 3) den += lam[idx / ((int64_t)n * n)];
     T[idx] /= den;
   }
@@ -101,21 +102,22 @@ void launch_dgemm(const double *A, const double *B, double *C, int M, int N, int
 }
 
 int launch_coarse_fd(int dim, int n, const double *V, const double *lam, const double *d, double *e, double *t1,
-                     double *t2, cudaStream_t st) {
+                     double *t2, cudaStream_t st, int ax) {
   const int64_t n1 = n, n2 = n1 * n1, n3 = n2 * n1;
-  if (dim == 2) {   // D[y][x]: S = V^T D V ./ (λ_j + λ_k);  E = V S V^T
-    launch_dgemm(d, V, t1, n, n, n, 1, 0, n1, 1, 0, n1, 1, 0, n1, 1, st);      // T1[y][j] = Σ_x D[y][x] V[x][j]
-    launch_dgemm(V, t1, t2, n, n, n, 1, 0, 1, n1, 0, n1, 1, 0, n1, 1, st);     // S[k][j] = Σ_y V[y][k] T1[y][j]
-    k_eig_divide<<<int(std::min<int64_t>((n2 + 255) / 256, 148 * 16)), 256, 0, st>>>(t2, lam, n, 2, n2);
-    launch_dgemm(t2, V, t1, n, n, n, 1, 0, n1, 1, 0, 1, n1, 0, n1, 1, st);     // T2[k][x] = Σ_j S[k][j] V[x][j]
-    launch_dgemm(V, t1, e, n, n, n, 1, 0, n1, 1, 0, n1, 1, 0, n1, 1, st);      // E[y][x] = Σ_k V[y][k] T2[k][x]
+  if (dim == 2) {   // D[y][x]: S = Vy^T D Vx ./ (λx_j + λy_k);  E = Vy S Vx^T
+    const double *Vx = V, *Vy = V + (ax ? n2 : 0);
+    launch_dgemm(d, Vx, t1, n, n, n, 1, 0, n1, 1, 0, n1, 1, 0, n1, 1, st);     // T1[y][j] = Σ_x D[y][x] Vx[x][j]
+    launch_dgemm(Vy, t1, t2, n, n, n, 1, 0, 1, n1, 0, n1, 1, 0, n1, 1, st);    // S[k][j] = Σ_y Vy[y][k] T1[y][j]
+    k_eig_divide<<<int(std::min<int64_t>((n2 + 255) / 256, 148 * 16)), 256, 0, st>>>(t2, lam, n, 2, n2, ax ? n1 : 0);
+    launch_dgemm(t2, Vx, t1, n, n, n, 1, 0, n1, 1, 0, 1, n1, 0, n1, 1, st);    // T2[k][x] = Σ_j S[k][j] Vx[x][j]
+    launch_dgemm(Vy, t1, e, n, n, n, 1, 0, n1, 1, 0, n1, 1, 0, n1, 1, st);     // E[y][x] = Σ_k Vy[y][k] T2[k][x]
     return 5;
   }
   // D[z][y][x]: forward x, y, z with V^T, divide by λ_x + λ_y + λ_z, back z, y, x with V
   launch_dgemm(d, V, t1, int(n2), n, n, 1, 0, n1, 1, 0, n1, 1, 0, n1, 1, st);          // x
   launch_dgemm(V, t1, t2, n, n, n, n, 0, 1, n1, n2, n1, 1, n2, n1, 1, st);             // y (batch z)
   launch_dgemm(V, t2, t1, n, int(n2), n, 1, 0, 1, n1, 0, n2, 1, 0, n2, 1, st);         // z
-  k_eig_divide<<<int(std::min<int64_t>((n3 + 255) / 256, 148 * 16)), 256, 0, st>>>(t1, lam, n, 3, n3);
+  k_eig_divide<<<int(std::min<int64_t>((n3 + 255) / 256, 148 * 16)), 256, 0, st>>>(t1, lam, n, 3, n3, 0);
   launch_dgemm(V, t1, t2, n, int(n2), n, 1, 0, n1, 1, 0, n2, 1, 0, n2, 1, st);         // z back
   launch_dgemm(V, t2, t1, n, n, n, n, 0, n1, 1, n2, n1, 1, n2, n1, 1, st);             // y back (batch z)
   launch_dgemm(t1, V, e, int(n2), n, n, 1, 0, n1, 1, 0, 1, n1, 0, n1, 1, st);          // x back

@@ -383,14 +383,14 @@ bool fd_tables(int p, int s, int64_t n1, const std::vector<double> &K, const std
 }
 
 bool dense_kron_inverse(int dim, int q, int n, const std::vector<double> &K, const std::vector<double> &M,
-                        std::vector<double> &inv) {
+                        std::vector<double> &inv, int64_t ays) {
   const int W = 2 * q + 1;
   int N = 1;
   for (int a = 0; a < dim; ++a) N *= n;
   std::vector<double> A((size_t)N * N, 0.0);
-  auto band = [&](const std::vector<double> &T, int i, int j) -> double {
+  auto band = [&](const std::vector<double> &T, int a, int i, int j) -> double {   // axis a's table
     const int t = j - i;
-    return (t < -q || t > q) ? 0.0 : T[(size_t)i * W + t + q];
+    return (t < -q || t > q) ? 0.0 : T[(size_t)(a * ays) + (size_t)i * W + t + q];
   };
   for (int g = 0; g < N; ++g)
     for (int h = 0; h < N; ++h) {
@@ -401,7 +401,7 @@ bool dense_kron_inverse(int dim, int q, int n, const std::vector<double> &K, con
       double v = 0.0;  // Σ_a ⊗(K on axis a, M elsewhere) (tensor-product basis)
       for (int a = 0; a < dim; ++a) {
         double t = 1.0;
-        for (int b = 0; b < dim; ++b) t *= (a == b) ? band(K, ig[b], ih[b]) : band(M, ig[b], ih[b]);
+        for (int b = 0; b < dim; ++b) t *= (a == b) ? band(K, b, ig[b], ih[b]) : band(M, b, ig[b], ih[b]);
         v += t;
       }
       A[(size_t)g * N + h] = v;
@@ -507,11 +507,15 @@ static void sym_eigen(std::vector<double> &A, int n, std::vector<double> &Q, std
 }
 
 bool coarse_fd_tables(int q, int64_t m, std::vector<double> &V, std::vector<double> &lam) {
-  // generalized problem K V = M V Λ with V^T M V = I for the constrained degree-q tables on m spans:
-  // M = L L^T, C = L^{-1} K L^{-T} = Q Λ Q^T, V = L^{-T} Q  (then A_q^{-1} = (⊗V)(Σ_a λ)^{-1}(⊗V)^T)
   std::vector<double> Kb, Mb;
   band_tables(q, m, Kb, Mb);
-  const int n = int(m + q - 2), W = 2 * q + 1;
+  return band_fd_tables(q, int(m + q - 2), Kb.data(), Mb.data(), V, lam);
+}
+
+bool band_fd_tables(int q, int n, const double *Kb, const double *Mb, std::vector<double> &V, std::vector<double> &lam) {
+  // generalized problem K V = M V Λ with V^T M V = I for constrained degree-q band tables:
+  // M = L L^T, C = L^{-1} K L^{-T} = Q Λ Q^T, V = L^{-T} Q  (then A_q^{-1} = (⊗V)(Σ_a λ)^{-1}(⊗V)^T)
+  const int W = 2 * q + 1;
   if (n < 1) return false;
   std::vector<double> Kd((size_t)n * n, 0.0), L((size_t)n * n, 0.0);
   for (int i = 0; i < n; ++i)

@@ -58,10 +58,29 @@ bool fd_tables(int p, int s, int64_t n1, const std::vector<double> &K, const std
 // Fast diagonalisation of the degree-q level on m spans (exact coarse solve at any size, SURVEY
 // §8(f) row 1): K V = M V Λ, V^T M V = I; V row-major n x n (row = 1D index, column = eigen index).
 bool coarse_fd_tables(int q, int64_t m, std::vector<double> &V, std::vector<double> &lam);
+// The same from given band tables (bandwidth 2q+1, n rows): K V = M V Λ, V^T M V = I.
+bool band_fd_tables(int q, int n, const double *K, const double *M, std::vector<double> &V, std::vector<double> &lam);
 
 // Dense inverse of the d-dim operator Σ_a ⊗ (K on axis a, M elsewhere) from band tables of
 // degree q (bandwidth 2q+1) on n points per axis.  Returns false if not SPD.  Row-major N x N.
+// ays > 0: per-axis tables, axis a's rows at K[a * ays ...] (the quarter annulus, A = My ⊗ Kx + Ky ⊗ Mx).
 bool dense_kron_inverse(int dim, int q, int n, const std::vector<double> &K, const std::vector<double> &M,
-                        std::vector<double> &inv);
+                        std::vector<double> &inv, int64_t ays = 0);
+
+// ---- quarter annulus (geometry.cpp) ----
+// Coefficients w of the arc's weight function W(ξ) in the degree-p (p >= 2) basis on m spans (nf = m+p).
+std::vector<double> nurbs_weights(int p, int64_t m);
+// NURBS R_r = w_{e+r} N_{e+r} / W and dR_r/dξ (r = 0..p) on span e at x.
+void nurbs_on_span(const std::vector<double> &U, const std::vector<double> &w, int p, int64_t e, double x, double *R,
+                   double *dR);
+// Per-axis constrained band tables [2][n1][2p+1]: axis 0 (ξ): Kx = ∫R'R'/s, Mx = ∫R R s; axis 1 (η):
+// Ky = ∫N'N'ρ/ρ', My = ∫N N ρ'/ρ, so that A = My ⊗ Kx + Ky ⊗ Mx (x = ξ fastest).
+void annulus_band_tables(int p, int64_t m, std::vector<double> &K, std::vector<double> &M);
+// One axis (0: ξ, 1: η) of the lumped L2 degree restriction on the map (weights s and ρρ').
+BandOp annulus_degree_restriction(int axis, int p, int q, int64_t m);
+// One axis of the exact embedding of the degree-q space on mc spans into the one on 2 mc spans.
+BandOp annulus_embedding(int axis, int q, int64_t mc);
+// Load vector (f, φ_ik) of the manufactured solution, n1*n1 (x = ξ fastest).
+std::vector<double> annulus_load(int p, int64_t m);
 
 }  // namespace iga2l

@@ -41,9 +41,11 @@ struct ToeP {
 
 // ---- fine operator: apply / residual -------------------------------------------------------
 // mode 0: y = A x;  mode 1: y = b - A x.  If partial != nullptr, partial[cta] = Σ y^2 over the tile.
+// ys: offset (doubles) of the y-axis tables from the x-axis ones (2D; 0 = the same tables; the quarter
+// annulus stores [2][n1][2p+1] per-axis tables, A = My ⊗ Kx + Ky ⊗ Mx, and passes ys = n1 (2p+1)).
 void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, const double *x,
                   const double *b, double *y, double *partial, int mode, cudaStream_t st, int *nparts,
-                  SlabView sv = kFull, const ToeP *tp = nullptr);
+                  SlabView sv = kFull, const ToeP *tp = nullptr, int64_t ys = 0);
 int apply_num_partials(int dim, int p, int64_t n1);
 // The TMA streaming apply (stream.cu), used by launch_apply for 1 <= p <= 8 unless IGA2L_APPLY_STREAM=0.
 // count_only: only report *nparts.  False if not launched (p unsupported, tensor map encode failed).
@@ -58,7 +60,7 @@ bool launch_apply_stream(int dim, int p, int64_t n1, const double *K, const doub
 // (slab: blocks with last-axis centre in [sv.zlo, sv.zhi); x, b stored from plane sv.zoff)
 void launch_schwarz_colour(int dim, int p, int s, int64_t n1, const double *K, const double *M,
                            const double *V, const double *lam, const double *b, double *x,
-                           int colour, int D, cudaStream_t st, SlabView sv = kFull);
+                           int colour, int D, cudaStream_t st, SlabView sv = kFull, int ax = 0);
 
 // ---- tensor-product band transform along one axis ------------------------------------------
 // in: [outer][nin][inner]  ->  out: [outer][B.rows][inner],  out (+)= Σ_k B.c[r,k] in[.., lo[r]+k, ..]
@@ -68,10 +70,11 @@ void launch_band_axis(const double *in, double *out, int64_t outer, int nin, int
                       int coff = 0, int rlo = 0, int rhi = -1);
 
 // ---- q-level (V-cycle) kernels, direct (2q+1)^d stencil --------------------------------------
+// ays: offset of axis a's band tables = a * ays (0: shared tables; per-axis for the quarter annulus).
 void launch_q_gs_colour(int dim, int q, int n, const double *K, const double *M, const double *b,
-                        double *x, int colour, cudaStream_t st);
+                        double *x, int colour, cudaStream_t st, int64_t ays = 0);
 void launch_q_residual(int dim, int q, int n, const double *K, const double *M, const double *b,
-                       const double *x, double *r, cudaStream_t st);
+                       const double *x, double *r, cudaStream_t st, int64_t ays = 0);
 
 // x = Ainv b (dense, N <= 4096), one warp per row.
 void launch_dense_mv(int N, const double *Ainv, const double *b, double *x, cudaStream_t st);
@@ -88,7 +91,9 @@ void launch_sum_partials(const double *partial, int n, double *out, double *hist
 bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M,
                                 const double *V, const double *lam, const double *b, double *x, int colour,
                                 int D, cudaStream_t st, SlabView sv = kFull, const double *fb = nullptr,
-                                const ToeP *tp = nullptr);
+                                const ToeP *tp = nullptr, int ax = 0);
+// ax = 1 (2D): per-axis tables -- K, M [2][n1][2p+1], V [2][n1][s*s], lam [2][n1][s], y after x
+// (the quarter annulus, A = My ⊗ Kx + Ky ⊗ Mx); fb must be nullptr then.
 bool launch_schwarz3d_colour(int p, int s, int64_t n1, const double *K, const double *M, const double *V,
                              const double *lam, const double *b, double *x, int c0, int c1, int f2, int D, int nb0,
                              int nb1, int nb2, int zoff, int tlo, int thi, cudaStream_t st, const ToeP *tp);
@@ -96,10 +101,12 @@ bool launch_schwarz3d_colour(int p, int s, int64_t n1, const double *K, const do
 // out == nullptr returns the number of doubles needed; -1 if no interior block or (p, s) not specialised.
 int export_interior_frags(int p, int s, int64_t n1, const double *K, const double *M, const double *V,
                           const double *lam, double *out, cudaStream_t st);
-// 2D tensor transfer out (+)= (B ⊗ B) in in one launch (in: B.cols^2, out: B.rows^2).
+// 2D tensor transfer out (+)= (By ⊗ B) in in one launch (in: B.cols^2, out: B.rows^2).
 // (optional: input rows valid in [iylo, iyhi) stored from iyoff; output rows [rylo, ryhi) stored from ryoff)
+// By: the y-axis band if it differs from the x-axis one (per-axis transfers of the quarter annulus).
 void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumulate, cudaStream_t st,
-                     int iylo = 0, int iyhi = -1, int iyoff = 0, int rylo = 0, int ryhi = -1, int ryoff = 0);
+                     int iylo = 0, int iyhi = -1, int iyoff = 0, int rylo = 0, int ryhi = -1, int ryoff = 0,
+                     const Band1D *By = nullptr);
 
 // One q-level of the V-cycle hierarchy, as seen by the single-CTA tail kernel (device array).
 struct QLevelDev {
@@ -152,8 +159,9 @@ void launch_dgemm(const double *A, const double *B, double *C, int M, int N, int
                   int64_t sCn, cudaStream_t st);
 // Exact second-level solve by Kronecker fast diagonalisation: e = (⊗V)(Σ_a λ)^{-1}(⊗V)^T d
 // (V: n x n row-major, K V = M V Λ, V^T M V = I).  t1, t2: n^dim scratch.  Returns the launch count.
+// ax = 1 (2D): per-axis decompositions, V [2][n][n], lam [2][n] (x then y; the quarter annulus).
 int launch_coarse_fd(int dim, int n, const double *V, const double *lam, const double *d, double *e, double *t1,
-                     double *t2, cudaStream_t st);
+                     double *t2, cudaStream_t st, int ax = 0);
 
 // y += x (fixed-order sums of the slab partial coarse vectors in local multi-slab mode)
 void launch_axpy(double *y, const double *x, int64_t n, cudaStream_t st);

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(128) k_schwarz(int p, int s, int n1, const dou
                                                  const double *__restrict__ M, const double *__restrict__ Vt,
                                                  const double *__restrict__ lamt, const double *__restrict__ b,
                                                  double *__restrict__ x, int c0, int c1, int c2, int D, int nb0,
-                                                 int nb1, int zoff) {
+                                                 int nb1, int zoff, int ax) {
   extern __shared__ double sm[];
   // memory index of global point (gx, gy, gz); the last axis is stored from plane zoff on
 #define SIDX(gx, gy, gz) ((DIM == 3) ? (((int64_t)((gz) - zoff) * n1 + (gy)) * n1 + (gx)) \
@@ -56,15 +56,18 @@ __global__ void __launch_bounds__(128) k_schwarz(int p, int s, int n1, const dou
   double *Q0 = R + sd, *Q1 = Q0 + sd;
   double *Vx = Q1 + sd, *Vy = Vx + s2, *Vz = Vy + s2;
   double *Lx = Vz + s2, *Ly = Lx + s, *Lz = Ly + s;
+  // 2D per-axis tables (ax = 1, quarter annulus): the y axis's band / FD tables follow the x axis's
+  const int64_t ys = (DIM == 2 && ax) ? (int64_t)n1 * W : 0, vys = (DIM == 2 && ax) ? (int64_t)n1 * s2 : 0,
+                lys = (DIM == 2 && ax) ? (int64_t)n1 * s : 0;
 
   for (int i = threadIdx.x; i < s2; i += blockDim.x) {
     Vx[i] = Vt[(int64_t)cx * s2 + i];
-    Vy[i] = Vt[(int64_t)cy * s2 + i];
+    Vy[i] = Vt[vys + (int64_t)cy * s2 + i];
     if (DIM == 3) Vz[i] = Vt[(int64_t)cz * s2 + i];
   }
   for (int i = threadIdx.x; i < s; i += blockDim.x) {
     Lx[i] = lamt[(int64_t)cx * s + i];
-    Ly[i] = lamt[(int64_t)cy * s + i];
+    Ly[i] = lamt[lys + (int64_t)cy * s + i];
     if (DIM == 3) Lz[i] = lamt[(int64_t)cz * s + i];
   }
   // window of x (zero outside the domain: the band tables vanish there too)
@@ -96,7 +99,7 @@ __global__ void __launch_bounds__(128) k_schwarz(int p, int s, int n1, const dou
       const int lx = i % s, ly = i / s, gx = bx + lx, gy = by + ly;
       double r = 0.0;
       if (gx >= 0 && gx < n1 && gy >= 0 && gy < n1) {
-        const double *kr = K + (int64_t)gy * W, *mr = M + (int64_t)gy * W;
+        const double *kr = K + ys + (int64_t)gy * W, *mr = M + ys + (int64_t)gy * W;
         double acc = 0.0;
         for (int u = 0; u < W; ++u) {
           acc = fma(mr[u], Pa[(ly + u) * s + lx], acc);
@@ -407,7 +410,7 @@ __device__ __forceinline__ void mma_colour_block(double *__restrict__ X, int bid
                                                  const double *__restrict__ M, const double *__restrict__ Vt,
                                                  const double *__restrict__ lamt, const double *__restrict__ b,
                                                  double *__restrict__ x, int c0, int c1, int D, int nb0, int nblk,
-                                                 int zoff, const double *__restrict__ fb, int tlo, int thi) {
+                                                 int zoff, const double *__restrict__ fb, int tlo, int thi, int ax) {
   using G = Mma2<P, S>;
   constexpr int Wn = G::Wn, w = G::w, MT = G::MT, WN4 = G::WN4, LDX = G::LDX;
   const int lane = threadIdx.x & 31;
@@ -434,7 +437,12 @@ __device__ __forceinline__ void mma_colour_block(double *__restrict__ X, int bid
     load_frags<P, S>(fb, fx, fy);                            // interior block: shared fragments (A27)
   } else {
     build_fragx<P, S>(fx, n1, cx, K, M, Vt, lamt);
-    build_fragy<P, S>(fy, n1, cy, K, M, Vt, lamt);
+    if (ax) {                                                // per-axis tables (quarter annulus)
+      const int64_t ys = (int64_t)n1 * G::W;
+      build_fragy<P, S>(fy, n1, cy, K + ys, M + ys, Vt + (int64_t)n1 * S * S, lamt + (int64_t)n1 * S);
+    } else {
+      build_fragy<P, S>(fy, n1, cy, K, M, Vt, lamt);
+    }
   }
 #pragma unroll
   for (int k = 0; k < WI; ++k) {
@@ -454,32 +462,33 @@ __global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma(int n1, const double
                                                             const double *__restrict__ lamt,
                                                             const double *__restrict__ b, double *__restrict__ x,
                                                             int c0, int c1, int D, int nb0, int nblk, int zoff,
-                                                            const double *__restrict__ fb, int tlo, int thi) {
+                                                            const double *__restrict__ fb, int tlo, int thi, int ax) {
   extern __shared__ double sm[];
   const int warp = threadIdx.x >> 5;
   const int bid = blockIdx.x * WPC + warp;
   if (bid >= nblk) return;                                   // whole warp exits together
   mma_colour_block<P, S>(sm + warp * Mma2<P, S>::PER, bid, n1, K, M, Vt, lamt, b, x, c0, c1, D, nb0, nblk, zoff, fb,
-                         tlo, thi);
+                         tlo, thi, ax);
 }
 
 template <int P, int S, int WPC>
 void launch2d_mma(int64_t n1, const double *K, const double *M, const double *V, const double *lam, const double *b,
-                  double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st, const double *fb) {
+                  double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st, const double *fb,
+                  int ax) {
   constexpr size_t sm = sizeof(double) * WPC * Mma2<P, S>::PER;
   ensure_smem(k_schwarz2d_mma<P, S, WPC>, sm);
   const int m = int(n1) - P + 2;
   k_schwarz2d_mma<P, S, WPC><<<(nblk + WPC - 1) / WPC, WPC * 32, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, D,
-                                                                           nb0, nblk, zoff, fb, 2 * P - 1, m - 2 - P);
+                                                                           nb0, nblk, zoff, fb, 2 * P - 1, m - 2 - P, ax);
 }
 
 template <int P, int S>
 bool try_schwarz2d_mma(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
                        const double *b, double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st,
-                       const double *fb) {
+                       const double *fb, int ax) {
   if (p != P || s != S) return false;
   constexpr int wpc = S >= 5 ? 1 : 4;   // warps (blocks) per CTA, measured best (profiles/variants_wpc_r01.txt)
-  launch2d_mma<P, S, wpc>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st, fb);
+  launch2d_mma<P, S, wpc>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st, fb, ax);
   return true;
 }
 
@@ -494,7 +503,7 @@ void centre_range(int c, int D, int lo, int hi, int *first, int *count) {
 
 void launch_schwarz_colour(int dim, int p, int s, int64_t n1, const double *K, const double *M, const double *V,
                            const double *lam, const double *b, double *x, int colour, int D, cudaStream_t st,
-                           SlabView sv) {
+                           SlabView sv, int ax) {
   if (sv.zhi < 0) sv = SlabView{0, 0, int(n1)};
   const int c0 = colour % D, c1 = (colour / D) % D, c2 = (dim == 3) ? colour / (D * D) : 0;
   int fl, nl;   // last axis: first centre and count inside the slab's centre range
@@ -508,16 +517,16 @@ void launch_schwarz_colour(int dim, int p, int s, int64_t n1, const double *K, c
   const unsigned nblk = unsigned(nb0) * unsigned(nb1) * unsigned(nb2);
   if (dim == 2) {
     ensure_smem(k_schwarz<2>, sm);
-    k_schwarz<2><<<nblk, 128, sm, st>>>(p, s, int(n1), K, M, V, lam, b, x, c0, fl, 0, D, nb0, nb1, sv.zoff);
+    k_schwarz<2><<<nblk, 128, sm, st>>>(p, s, int(n1), K, M, V, lam, b, x, c0, fl, 0, D, nb0, nb1, sv.zoff, ax);
   } else {
     ensure_smem(k_schwarz<3>, sm);
-    k_schwarz<3><<<nblk, 128, sm, st>>>(p, s, int(n1), K, M, V, lam, b, x, c0, c1, fl, D, nb0, nb1, sv.zoff);
+    k_schwarz<3><<<nblk, 128, sm, st>>>(p, s, int(n1), K, M, V, lam, b, x, c0, c1, fl, D, nb0, nb1, sv.zoff, 0);
   }
 }
 
 bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double *K, const double *M, const double *V,
                                 const double *lam, const double *b, double *x, int colour, int D, cudaStream_t st,
-                                SlabView sv, const double *fb, const ToeP *tp) {
+                                SlabView sv, const double *fb, const ToeP *tp, int ax) {
   if (sv.zhi < 0) sv = SlabView{0, 0, int(n1)};
   if (dim == 3) {
     const int c0 = colour % D, c1 = (colour / D) % D, c2 = colour / (D * D);
@@ -537,14 +546,14 @@ bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double 
   if (c0 >= n1 || nb1 == 0) return true;   // empty colour
   const int nb0 = int((n1 - c0 + D - 1) / D), nblk = nb0 * nb1;
   const int z = sv.zoff;
-  return try_schwarz2d_mma<1, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb) ||
-         try_schwarz2d_mma<2, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb) ||
-         try_schwarz2d_mma<3, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb) ||
-         try_schwarz2d_mma<4, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb) ||
-         try_schwarz2d_mma<5, 5>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb) ||
-         try_schwarz2d_mma<6, 5>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb) ||
-         try_schwarz2d_mma<7, 7>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb) ||
-         try_schwarz2d_mma<8, 7>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb);
+  return try_schwarz2d_mma<1, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb, ax) ||
+         try_schwarz2d_mma<2, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb, ax) ||
+         try_schwarz2d_mma<3, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb, ax) ||
+         try_schwarz2d_mma<4, 3>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb, ax) ||
+         try_schwarz2d_mma<5, 5>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb, ax) ||
+         try_schwarz2d_mma<6, 5>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb, ax) ||
+         try_schwarz2d_mma<7, 7>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb, ax) ||
+         try_schwarz2d_mma<8, 7>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb, ax);
 }
 
 int export_interior_frags(int p, int s, int64_t n1, const double *K, const double *M, const double *V,

@@ -52,13 +52,14 @@ __global__ void __launch_bounds__(256) k_band_axis(const double *__restrict__ in
 template <int WMAX>
 __device__ __forceinline__ double tensor2d_point(const double *__restrict__ in, int nin, int iylo, int iyhi, int iyoff,
                                                  int W, const int *__restrict__ lo, const double *__restrict__ c,
+                                                 int Wy, const int *__restrict__ loy, const double *__restrict__ cyt,
                                                  int ry, int rx) {
-  const int ly = lo[ry], lx = lo[rx];
+  const int ly = loy[ry], lx = lo[rx];
   double cy[WMAX], cx[WMAX];
 #pragma unroll
   for (int k = 0; k < WMAX; ++k) {
-    const bool oky = k < W && ly + k >= iylo && ly + k < iyhi, okx = k < W && unsigned(lx + k) < unsigned(nin);
-    cy[k] = oky ? c[(int64_t)ry * W + k] : 0.0;
+    const bool oky = k < Wy && ly + k >= iylo && ly + k < iyhi, okx = k < W && unsigned(lx + k) < unsigned(nin);
+    cy[k] = oky ? cyt[(int64_t)ry * Wy + k] : 0.0;
     cx[k] = okx ? c[(int64_t)rx * W + k] : 0.0;
   }
   double s0 = 0.0, s1 = 0.0;
@@ -79,13 +80,14 @@ __device__ __forceinline__ double tensor2d_point(const double *__restrict__ in, 
 // Output rows ry in [rylo, ryhi) are stored from row ryoff on (all rows.x columns).
 template <int WMAX>
 __global__ void k_tensor2d(const double *__restrict__ in, double *__restrict__ out, int nin, int rows, int W,
-                           const int *__restrict__ lo, const double *__restrict__ c, int acc, int iylo, int iyhi,
+                           const int *__restrict__ lo, const double *__restrict__ c, int Wy,
+                           const int *__restrict__ loy, const double *__restrict__ cyt, int acc, int iylo, int iyhi,
                            int iyoff, int rylo, int ryhi, int ryoff) {
   const int64_t total = (int64_t)(ryhi - rylo) * rows;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int ry = rylo + int(idx / rows), rx = int(idx % rows);
-    const double s = tensor2d_point<WMAX>(in, nin, iylo, iyhi, iyoff, W, lo, c, ry, rx);
+    const double s = tensor2d_point<WMAX>(in, nin, iylo, iyhi, iyoff, W, lo, c, Wy, loy, cyt, ry, rx);
     const int64_t o = (int64_t)(ry - ryoff) * rows + rx;
     out[o] = acc ? out[o] + s : s;
   }
@@ -99,17 +101,19 @@ __global__ void k_tensor2d(const double *__restrict__ in, double *__restrict__ o
 template <int TO>
 __global__ void __launch_bounds__(256) k_transfer2d_sep(const double *__restrict__ in, double *__restrict__ out, int nin,
                                                         int rows, int W, const int *__restrict__ lo,
-                                                        const double *__restrict__ c, int acc, int iylo, int iyhi,
-                                                        int iyoff, int rylo, int ryhi, int ryoff, int LI) {
+                                                        const double *__restrict__ c, int Wy,
+                                                        const int *__restrict__ loy, const double *__restrict__ cyt,
+                                                        int acc, int iylo, int iyhi, int iyoff, int rylo, int ryhi,
+                                                        int ryoff, int LI) {
   extern __shared__ double sm[];
   const int rx0 = blockIdx.x * TO, ry0 = rylo + blockIdx.y * TO;
   const int nrx = min(TO, rows - rx0), nry = min(TO, ryhi - ry0);
   if (nrx <= 0 || nry <= 0) return;
-  const int ix0 = lo[rx0], iy0 = lo[ry0];                 // first input column / row of the tile
+  const int ix0 = lo[rx0], iy0 = loy[ry0];                 // first input column / row of the tile
   double *X = sm;                                           // [LI][LI] input window
   double *T = X + LI * LI;                                  // [LI][TO]
   double *cx = T + LI * TO, *cy = cx + TO * W;              // coefficient rows of the tile
-  int *lx = reinterpret_cast<int *>(cy + TO * W), *ly = lx + TO;
+  int *lx = reinterpret_cast<int *>(cy + TO * Wy), *ly = lx + TO;
   const int tid = threadIdx.x;
   for (int i = tid; i < LI * LI; i += 256) {
     const int wy = i / LI, wx = i - wy * LI, gx = ix0 + wx, gy = iy0 + wy;
@@ -118,18 +122,22 @@ __global__ void __launch_bounds__(256) k_transfer2d_sep(const double *__restrict
   }
   for (int i = tid; i < TO * W; i += 256) {
     const int r = i / W;
-    const bool okx = r < nrx, oky = r < nry;
+    const bool okx = r < nrx;
     cp_async8(cx + i, c + (okx ? (int64_t)(rx0 + r) * W + i % W : 0), okx);
-    cp_async8(cy + i, c + (oky ? (int64_t)(ry0 + r) * W + i % W : 0), oky);
+  }
+  for (int i = tid; i < TO * Wy; i += 256) {
+    const int r = i / Wy;
+    const bool oky = r < nry;
+    cp_async8(cy + i, cyt + (oky ? (int64_t)(ry0 + r) * Wy + i % Wy : 0), oky);
   }
   if (tid < TO) {
     lx[tid] = tid < nrx ? lo[rx0 + tid] - ix0 : 0;
-    ly[tid] = tid < nry ? lo[ry0 + tid] - iy0 : 0;
+    ly[tid] = tid < nry ? loy[ry0 + tid] - iy0 : 0;
   }
   cp_async_wait_all();
   __syncthreads();
   // pass 1: rows of the window that pass 2 reads: [0, ly[nry-1] + W)
-  const int nrow = min(LI, ly[nry - 1] + W);
+  const int nrow = min(LI, ly[nry - 1] + Wy);
   for (int i = tid; i < nrow * TO; i += 256) {
     const int wy = i / TO, r = i - wy * TO;
     double s0 = 0.0, s1 = 0.0;
@@ -145,9 +153,9 @@ __global__ void __launch_bounds__(256) k_transfer2d_sep(const double *__restrict
   for (int i = tid; i < TO * TO; i += 256) {
     const int ry = i / TO, r = i - ry * TO;
     if (ry >= nry || r >= nrx) continue;
-    const double *tc = T + ly[ry] * TO + r, *cr = cy + ry * W;
+    const double *tc = T + ly[ry] * TO + r, *cr = cy + ry * Wy;
     double s0 = 0.0, s1 = 0.0;
-    for (int k = 0; k < W; ++k) {
+    for (int k = 0; k < Wy; ++k) {
       if (k & 1) s1 = fma(cr[k], tc[k * TO], s1); else s0 = fma(cr[k], tc[k * TO], s0);
     }
     const int64_t o = (int64_t)(ry0 + ry - ryoff) * rows + rx0 + r;
@@ -175,47 +183,46 @@ void launch_band_axis(const double *in, double *out, int64_t outer, int nin, int
 }
 
 void launch_tensor2d(const double *in, double *out, const Band1D &B, int accumulate, cudaStream_t st,
-                     int iylo, int iyhi, int iyoff, int rylo, int ryhi, int ryoff) {
-  if (iyhi < 0) { iylo = 0; iyhi = B.cols; iyoff = 0; }
-  if (ryhi < 0) { rylo = 0; ryhi = B.rows; ryoff = 0; }
+                     int iylo, int iyhi, int iyoff, int rylo, int ryhi, int ryoff, const Band1D *Byp) {
+  const Band1D &By = Byp ? *Byp : B;        // y-axis band (per-axis transfers: the quarter annulus)
+  if (iyhi < 0) { iylo = 0; iyhi = By.cols; iyoff = 0; }
+  if (ryhi < 0) { rylo = 0; ryhi = By.rows; ryoff = 0; }
   const int64_t total = (int64_t)(ryhi - rylo) * B.rows;
   if (total <= 0) return;
+  const int Wm = std::max(B.W, By.W);
   // test knob: IGA2L_TRANSFER_SEP=32|16 forces that separable tile at any size (the C3 path at PAR sizes)
   const char *fs = std::getenv("IGA2L_TRANSFER_SEP");
   const int force = fs ? std::atoi(fs) : 0;
-  if (force == 32 && B.lo_max_span > 0) {
-    const int LI = B.lo_max_span + B.W;
-    const size_t sm = sizeof(double) * (size_t(LI) * LI + size_t(LI) * 32 + 2 * 32 * B.W) + 2 * 32 * sizeof(int);
-    ensure_smem(k_transfer2d_sep<32>, sm);
-    dim3 grid((unsigned)((B.rows + 31) / 32), (unsigned)((ryhi - rylo + 31) / 32));
-    k_transfer2d_sep<32><<<grid, 256, sm, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate, iylo, iyhi, iyoff,
-                                                rylo, ryhi, ryoff, LI);
-    return;
-  }
-  if (B.lo_max_span > 0) {   // separable two-pass
-    auto go = [&](auto kern, int TO, int span) {
-      const int LI = span + B.W;
-      const size_t sm = sizeof(double) * (size_t(LI) * LI + size_t(LI) * TO + 2 * TO * B.W) + 2 * TO * sizeof(int);
-      if (sm > 200 * 1024) return false;
-      ensure_smem(kern, sm);
-      dim3 grid((unsigned)((B.rows + TO - 1) / TO), (unsigned)((ryhi - rylo + TO - 1) / TO));
-      kern<<<grid, 256, sm, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate, iylo, iyhi, iyoff, rylo, ryhi,
-                                  ryoff, LI);
-      return true;
-    };
+  auto go = [&](auto kern, int TO, int span) {
+    const int LI = span + Wm;
+    const size_t sm = sizeof(double) * (size_t(LI) * LI + size_t(LI) * TO + TO * size_t(B.W + By.W)) + 2 * TO * sizeof(int);
+    if (sm > 200 * 1024) return false;
+    ensure_smem(kern, sm);
+    dim3 grid((unsigned)((B.rows + TO - 1) / TO), (unsigned)((ryhi - rylo + TO - 1) / TO));
+    kern<<<grid, 256, sm, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, By.W, By.lo, By.c, accumulate, iylo, iyhi,
+                                iyoff, rylo, ryhi, ryoff, LI);
+    return true;
+  };
+  const int span32 = (B.lo_max_span > 0 && By.lo_max_span > 0) ? std::max(B.lo_max_span, By.lo_max_span) : 0;
+  const int span16 = (B.lo_max_span16 > 0 && By.lo_max_span16 > 0) ? std::max(B.lo_max_span16, By.lo_max_span16) : 0;
+  if (force == 32 && span32 > 0 && go(k_transfer2d_sep<32>, 32, span32)) return;
+  if (span32 > 0) {   // separable two-pass
     if (total >= 200000) {
-      if (go(k_transfer2d_sep<32>, 32, B.lo_max_span)) return;
-    } else if (B.lo_max_span16 > 0 && go(k_transfer2d_sep<16>, 16, B.lo_max_span16)) {
+      if (go(k_transfer2d_sep<32>, 32, span32)) return;
+    } else if (span16 > 0 && go(k_transfer2d_sep<16>, 16, span16)) {
       return;
     }
   }
   const int g = grid_for(total, 128);
-  if (B.W <= 4)
-    k_tensor2d<4><<<g, 128, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate, iylo, iyhi, iyoff, rylo, ryhi, ryoff);
-  else if (B.W <= 8)
-    k_tensor2d<8><<<g, 128, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate, iylo, iyhi, iyoff, rylo, ryhi, ryoff);
+  if (Wm <= 4)
+    k_tensor2d<4><<<g, 128, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, By.W, By.lo, By.c, accumulate, iylo, iyhi,
+                                     iyoff, rylo, ryhi, ryoff);
+  else if (Wm <= 8)
+    k_tensor2d<8><<<g, 128, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, By.W, By.lo, By.c, accumulate, iylo, iyhi,
+                                     iyoff, rylo, ryhi, ryoff);
   else
-    k_tensor2d<16><<<g, 128, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, accumulate, iylo, iyhi, iyoff, rylo, ryhi, ryoff);
+    k_tensor2d<16><<<g, 128, 0, st>>>(in, out, B.cols, B.rows, B.W, B.lo, B.c, By.W, By.lo, By.c, accumulate, iylo,
+                                      iyhi, iyoff, rylo, ryhi, ryoff);
 }
 
 }  // namespace iga2l

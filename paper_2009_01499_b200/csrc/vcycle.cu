@@ -46,17 +46,18 @@ struct XOff {               // level values in shared memory; last-axis row j st
   }
 };
 
-// Σ_j a_ij x_j over the (2Q+1)^d stencil of point (ix, iy, iz) and a_ii (tables in shared memory)
+// Σ_j a_ij x_j over the (2Q+1)^d stencil of point (ix, iy, iz) and a_ii.  ays: offset of axis a's
+// tables = a * ays (0: one table pair for all axes; per-axis tables of the quarter annulus otherwise)
 template <int DIM, int Q, class XA>
 __device__ __forceinline__ double q_point_acc(int n, const double *sK, const double *sM, const XA &xa, int ix,
-                                              int iy, int iz, double *diag) {
+                                              int iy, int iz, double *diag, int64_t ays = 0) {
   constexpr int W = 2 * Q + 1;
   const unsigned un = unsigned(n);
   double kx[W], mx[W], ky[W], my[W];
 #pragma unroll
   for (int t = 0; t < W; ++t) {
     kx[t] = sK[ix * W + t]; mx[t] = sM[ix * W + t];
-    ky[t] = sK[iy * W + t]; my[t] = sM[iy * W + t];
+    ky[t] = sK[ays + iy * W + t]; my[t] = sM[ays + iy * W + t];
   }
   double acc0 = 0.0, acc1 = 0.0;
   if (DIM == 2) {
@@ -79,7 +80,7 @@ __device__ __forceinline__ double q_point_acc(int n, const double *sK, const dou
   } else {
     double kz[W], mz[W];
 #pragma unroll
-    for (int t = 0; t < W; ++t) { kz[t] = sK[iz * W + t]; mz[t] = sM[iz * W + t]; }
+    for (int t = 0; t < W; ++t) { kz[t] = sK[2 * ays + iz * W + t]; mz[t] = sM[2 * ays + iz * W + t]; }
 #pragma unroll
     for (int v = 0; v < W; ++v) {
       const int jz = iz + v - Q;
@@ -164,7 +165,7 @@ __device__ __forceinline__ double tensor_point_acc(const XA &xa, int nin, int W,
 template <int DIM, int Q>
 __global__ void __launch_bounds__(128) k_q_gs(int n, const double *__restrict__ K, const double *__restrict__ M,
                                               const double *__restrict__ b, double *__restrict__ x, int c0, int c1,
-                                              int c2, int na0, int na1, int64_t total) {
+                                              int c2, int na0, int na1, int64_t total, int64_t ays) {
   constexpr int st = Q + 1;
   const XOff<DIM> xa{x, n, 0};
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(128) k_q_gs(int n, const double *__restrict__ 
     const int iy = c1 + st * int((idx / na0) % na1);
     const int iz = (DIM == 3) ? c2 + st * int(idx / ((int64_t)na0 * na1)) : 0;
     double dg;
-    const double ax = q_point_acc<DIM, Q>(n, K, M, xa, ix, iy, iz, &dg);
+    const double ax = q_point_acc<DIM, Q>(n, K, M, xa, ix, iy, iz, &dg, ays);
     const int64_t g = ((int64_t)iz * n + iy) * n + ix;
     x[g] += (b[g] - ax) / dg;
   }
@@ -183,13 +184,13 @@ __global__ void __launch_bounds__(128) k_q_gs(int n, const double *__restrict__ 
 template <int DIM, int Q>
 __global__ void __launch_bounds__(128) k_q_resid(int n, const double *__restrict__ K, const double *__restrict__ M,
                                                  const double *__restrict__ b, const double *__restrict__ x,
-                                                 double *__restrict__ r, int64_t total) {
+                                                 double *__restrict__ r, int64_t total, int64_t ays) {
   const XOff<DIM> xa{x, n, 0};
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int ix = int(idx % n), iy = int((idx / n) % n), iz = (DIM == 3) ? int(idx / ((int64_t)n * n)) : 0;
     double dg;
-    r[idx] = b[idx] - q_point_acc<DIM, Q>(n, K, M, xa, ix, iy, iz, &dg);
+    r[idx] = b[idx] - q_point_acc<DIM, Q>(n, K, M, xa, ix, iy, iz, &dg, ays);
   }
 }
 
@@ -511,28 +512,28 @@ __global__ void __launch_bounds__(512, 1) k_vcycle_smem(const VcLayout L) {
 }  // namespace
 
 void launch_q_gs_colour(int dim, int q, int n, const double *K, const double *M, const double *b, double *x,
-                        int colour, cudaStream_t st) {
+                        int colour, cudaStream_t st, int64_t ays) {
   const int st_ = q + 1;
   const int c0 = colour % st_, c1 = (colour / st_) % st_, c2 = (dim == 3) ? colour / (st_ * st_) : 0;
   if (c0 >= n || c1 >= n || c2 >= n) return;
   const int na0 = (n - c0 + q) / st_, na1 = (n - c1 + q) / st_, na2 = (dim == 3) ? (n - c2 + q) / st_ : 1;
   const int64_t total = (int64_t)na0 * na1 * na2;
   const int g = grid_for(total, 128);
-  if (dim == 2 && q == 1) k_q_gs<2, 1><<<g, 128, 0, st>>>(n, K, M, b, x, c0, c1, c2, na0, na1, total);
-  else if (dim == 2) k_q_gs<2, 2><<<g, 128, 0, st>>>(n, K, M, b, x, c0, c1, c2, na0, na1, total);
-  else if (q == 1) k_q_gs<3, 1><<<g, 128, 0, st>>>(n, K, M, b, x, c0, c1, c2, na0, na1, total);
-  else k_q_gs<3, 2><<<g, 128, 0, st>>>(n, K, M, b, x, c0, c1, c2, na0, na1, total);
+  if (dim == 2 && q == 1) k_q_gs<2, 1><<<g, 128, 0, st>>>(n, K, M, b, x, c0, c1, c2, na0, na1, total, ays);
+  else if (dim == 2) k_q_gs<2, 2><<<g, 128, 0, st>>>(n, K, M, b, x, c0, c1, c2, na0, na1, total, ays);
+  else if (q == 1) k_q_gs<3, 1><<<g, 128, 0, st>>>(n, K, M, b, x, c0, c1, c2, na0, na1, total, ays);
+  else k_q_gs<3, 2><<<g, 128, 0, st>>>(n, K, M, b, x, c0, c1, c2, na0, na1, total, ays);
 }
 
 void launch_q_residual(int dim, int q, int n, const double *K, const double *M, const double *b, const double *x,
-                       double *r, cudaStream_t st) {
+                       double *r, cudaStream_t st, int64_t ays) {
   int64_t total = (int64_t)n * n;
   if (dim == 3) total *= n;
   const int g = grid_for(total, 128);
-  if (dim == 2 && q == 1) k_q_resid<2, 1><<<g, 128, 0, st>>>(n, K, M, b, x, r, total);
-  else if (dim == 2) k_q_resid<2, 2><<<g, 128, 0, st>>>(n, K, M, b, x, r, total);
-  else if (q == 1) k_q_resid<3, 1><<<g, 128, 0, st>>>(n, K, M, b, x, r, total);
-  else k_q_resid<3, 2><<<g, 128, 0, st>>>(n, K, M, b, x, r, total);
+  if (dim == 2 && q == 1) k_q_resid<2, 1><<<g, 128, 0, st>>>(n, K, M, b, x, r, total, ays);
+  else if (dim == 2) k_q_resid<2, 2><<<g, 128, 0, st>>>(n, K, M, b, x, r, total, ays);
+  else if (q == 1) k_q_resid<3, 1><<<g, 128, 0, st>>>(n, K, M, b, x, r, total, ays);
+  else k_q_resid<3, 2><<<g, 128, 0, st>>>(n, K, M, b, x, r, total, ays);
 }
 
 bool vcycle_smem_layout(int dim, int q, const QLevelDev *tab, int nlev, int l0, int cs, size_t max_bytes,

@@ -93,3 +93,48 @@ def test_host_coarse_fd_diagonalises_the_oracle_matrices(q, m):
     A = stiffness(q, m, 2).tocsc()
     ref = spla.spsolve(A, d)
     assert np.abs(E.ravel() - ref).max() <= 1e-11 * np.abs(ref).max()
+
+
+# ---- quarter annulus: the library's host setup against the oracle's 2D assembly ----
+def _dense_band(B, p):
+    n1, W = B.shape
+    D = np.zeros((n1, n1))
+    for i in range(n1):
+        for t in range(W):
+            j = i + t - p
+            if 0 <= j < n1:
+                D[i, j] = B[i, t]
+    return D
+
+
+@pytest.mark.parametrize("p,m", [(2, 4), (3, 6), (5, 8), (8, 12)])
+def test_host_annulus_tables_give_the_assembled_operator(p, m):
+    """My ⊗ Kx + Ky ⊗ Mx from the library's per-axis tables equals the oracle's element-by-element 2D
+    stiffness on the exact geometry (NURBS weights from the blossom here, L2 projection there)."""
+    from oracle import annulus as an
+    Kx, Mx, Ky, My = (_dense_band(T, p) for T in pkg.host_annulus_tables(p, m))
+    A = an.assemble(p, m)["A"].toarray()
+    assert np.abs(np.kron(My, Kx) + np.kron(Ky, Mx) - A).max() <= 1e-12 * np.abs(A).max()
+
+
+@pytest.mark.parametrize("p,m,hf", [(3, 8, 2), (5, 8, 1), (4, 12, 2)])
+def test_host_annulus_restriction_matches_oracle(p, m, hf):
+    """Ry ⊗ Rx (per-axis lumped L2 restriction, composed with the NURBS / B-spline embedding) equals the
+    oracle's 2D R = P^T D^{-1} C."""
+    import scipy.sparse as sp
+    from oracle import annulus as an
+    Rx = pkg.host_annulus_restriction_1d(0, p, 2, m, hf)
+    Ry = pkg.host_annulus_restriction_1d(1, p, 2, m, hf)
+    C = an.assemble(p, m, q=2, want=("C",))["C"]
+    R = sp.diags(1.0 / an.lumped_q_mass(2, m)) @ C
+    if hf == 2:
+        R = an.embedding(2, m // 2).T @ R
+    R = R.toarray()
+    assert np.abs(np.kron(Ry, Rx) - R).max() <= 1e-13 * np.abs(R).max()
+
+
+def test_host_annulus_load_matches_oracle():
+    from oracle import annulus as an
+    b = pkg.host_annulus_load(3, 8)
+    ref = an.assemble(3, 8, want=("b",))["b"]
+    assert np.abs(b - ref).max() <= 1e-13 * np.abs(ref).max()
