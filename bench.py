@@ -119,14 +119,30 @@ def make_ctx(pkg, name, stream):
                        coarse_h_factor=c["h_factor"], stream=stream)
 
 
+class _NoSecondLevel:
+    """Stands in for the V-cycle hierarchy when the sample times only the sweep (large configs)."""
+
+    def vcycle(self, d):
+        raise RuntimeError("second level not part of this sample")
+
+
 class OracleSample:
     """The oracle, as it stands, on the bench workload: oracle.kron.KronTwoLevel (Algorithm 1 with the
     Kronecker-form operator and colour-by-colour multicolour sweep, pinned to the assembled sequential
-    oracle) for each problem of the config, BLAS threads = all host cores of this process.  One sample
-    = ONE full iteration of every problem of the step (median of `reps`); setup (operators, V-cycle
-    hierarchy, first-sweep block inverses) is excluded."""
+    oracle) for each problem of the config, BLAS threads = all host cores of this process.
 
-    def __init__(self, config="C2", reps=3):
+    Bounded sample (about `budget_s` of timed CPU work): when a complete iteration of every problem fits
+    the budget (C1, C2), one sample = one full iteration per problem (median of `reps`); otherwise
+    (C3-C5) a sample = an evenly spaced subset of the sweep's colour steps (each a full-grid residual plus
+    every block solve of that colour), extrapolated to the D^d colours, plus -- for problems up to 3M DOF --
+    the rest of the iteration (defect, restriction, second level, prolongation) timed once.  Above 3M DOF
+    (C5) the rest is not timed (the oracle's assembled 3D q-hierarchy does not fit a bounded sample); the
+    sweep is >= 95% of the oracle iteration at C3/C4, so the figure is an upper bound on the oracle's
+    throughput.  Setup (operators, hierarchy, the first pass that forms kept block inverses) is excluded."""
+
+    FULL_REST_LIMIT = 3_000_000
+
+    def __init__(self, config="C2", reps=3, budget_s=20.0):
         from oracle.kron import KronTwoLevel
         from oracle.multigrid import QHierarchy
         from oracle.assembly import load_sine
@@ -136,35 +152,85 @@ class OracleSample:
         self.reps = reps
         self.probs = []
         mgs = {}
-        for name in CONFIG_PROBLEMS[config]:
+        names = CONFIG_PROBLEMS[config]
+        per = budget_s / len(names)
+        for name in names:
             c = CONFIGS[name]
+            N = (c["m"] + c["p"] - 2) ** c["d"]
+            with_rest = N <= self.FULL_REST_LIMIT
             key = (c["q"], c["m"] // c["h_factor"], c["d"])
-            if c["coarse"] == "vcycle" and key not in mgs:
-                mgs[key] = QHierarchy(*key)
-            kt = KronTwoLevel(c["d"], c["p"], c["q"], c["m"], c["s"], c["coarse"], c["h_factor"], mg=mgs.get(key))
+            mg = None
+            if c["coarse"] == "vcycle":
+                if not with_rest:
+                    mg = _NoSecondLevel()
+                elif key not in mgs:
+                    mgs[key] = QHierarchy(*key)
+                mg = mg or mgs.get(key)
+            kt = KronTwoLevel(c["d"], c["p"], c["q"], c["m"], c["s"], c["coarse"], c["h_factor"], mg=mg)
             b, x = load_sine(c["p"], c["m"], c["d"]), initial_guess(kt.N)
-            kt.iterate(x, b)                          # first sweep forms the kept block inverses (setup)
-            self.probs.append((name, kt, b, x))
-        self.N = sum(kt.N for _, kt, _, _ in self.probs)
+            nc = kt.D ** kt.d
+            tc = time.perf_counter()
+            kt.colour_step(x, b, 0)                     # (forms colour 0's kept inverses)
+            t1 = time.perf_counter() - tc
+            n_col = int(min(nc, max(2, per / max(t1, 1e-6) / 2)))
+            cols = sorted(set(int(round(v)) for v in np.linspace(0, nc - 1, n_col)))
+            rest = 0.0
+            if with_rest:
+                tr = time.perf_counter()
+                self._rest(kt, x, b)
+                rest = time.perf_counter() - tr
+            full = (t1 * nc + rest) * reps <= per
+            if full:
+                kt.iterate(x, b)                        # first sweep forms all kept block inverses (setup)
+            else:
+                for col in cols:                        # forms the sampled colours' kept inverses (setup)
+                    kt.colour_step(x, b, col)
+            self.probs.append(dict(name=name, kt=kt, b=b, x=x, full=full, cols=cols, with_rest=with_rest))
+        self.N = sum(p["kt"].N for p in self.probs)
         self.setup_s = time.perf_counter() - t0
 
+    @staticmethod
+    def _rest(kt, x, b):
+        dq = kt.restrict(b - kt.A.apply(x))
+        x += kt.prolong(kt._csolve(dq))
+
     def sample(self):
-        """Returns (DOF*it/s, seconds per step): the step's iterations, each the median of `reps`."""
+        """Returns (DOF*it/s, seconds per step): the step's iterations (measured or extrapolated)."""
         t_step = 0.0
-        for _, kt, b, x in self.probs:
-            ts = []
-            for _ in range(self.reps):
+        for p in self.probs:
+            kt, b, x = p["kt"], p["b"], p["x"]
+            if p["full"]:
+                ts = []
+                for _ in range(self.reps):
+                    t0 = time.perf_counter()
+                    kt.iterate(x, b)
+                    ts.append(time.perf_counter() - t0)
+                t_step += float(np.median(ts))
+                continue
+            t0 = time.perf_counter()
+            for col in p["cols"]:
+                kt.colour_step(x, b, col)
+            t_sweep = (time.perf_counter() - t0) / len(p["cols"]) * kt.D ** kt.d
+            t_rest = 0.0
+            if p["with_rest"]:
                 t0 = time.perf_counter()
-                kt.iterate(x, b)
-                ts.append(time.perf_counter() - t0)
-            t_step += float(np.median(ts))
+                self._rest(kt, x, b)
+                t_rest = time.perf_counter() - t0
+            t_step += t_sweep + t_rest
         return self.N / t_step, t_step
 
     def describe(self):
-        names = ",".join(n for n, _, _, _ in self.probs)
-        return (f"oracle.kron.KronTwoLevel (NumPy/SciPy, BLAS threads = {self.cores} host cores) on the full-size "
-                f"{names}: one complete two-level iteration per problem, median of {self.reps}; setup "
-                f"({self.setup_s:.1f} s: operators, V-cycle hierarchy, block inverses) excluded")
+        parts = []
+        for p in self.probs:
+            kt = p["kt"]
+            if p["full"]:
+                parts.append(f"{p['name']}: complete iterations (median of {self.reps})")
+            else:
+                parts.append(f"{p['name']}: {len(p['cols'])} of {kt.D ** kt.d} colour steps extrapolated to the "
+                             f"sweep" + (" + the rest of the iteration once" if p["with_rest"] else
+                                         " (rest of the iteration not timed: upper bound)"))
+        return (f"oracle.kron.KronTwoLevel (NumPy/SciPy, BLAS threads = {self.cores} host cores), full-size "
+                f"grids; " + "; ".join(parts) + f"; setup ({self.setup_s:.1f} s) excluded")
 
 
 def cpu_baseline_sample(config="C2"):
