@@ -50,8 +50,9 @@ typedef enum {
 } iga2l_status;
 
 typedef enum {
-  IGA2L_COARSE_EXACT = 0,  /* A_q e = d_q solved exactly: dense inverse (Nc <= 4096) or, above,  */
+  IGA2L_COARSE_EXACT = 0,  /* A_q e = d_q solved exactly: dense inverse (Nc <= 1024) or, above,  */
                            /* Kronecker fast diagonalisation (⊗V)(Σλ)^{-1}(⊗V)^T, n <= 2048/axis */
+                           /* (IGA2L_COARSE_FD=0/1 forces dense (Nc <= 4096) / FD)              */
   IGA2L_COARSE_VCYCLE = 1  /* one V(1,1) h-multigrid cycle, zero initial guess     */
 } iga2l_coarse_mode;
 

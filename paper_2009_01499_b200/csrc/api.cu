@@ -704,7 +704,7 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
     const bool direct = (o.coarse_mode == IGA2L_COARSE_EXACT) || ml <= o.vcycle_coarsest_m;
     const char *fde = std::getenv("IGA2L_COARSE_FD");   // force / forbid the FD exact solve (tests)
     const bool use_fd = direct && o.coarse_mode == IGA2L_COARSE_EXACT &&
-                        (fde ? fde[0] == '1' : L.N > 4096) && L.n <= 2048;
+                        (fde ? fde[0] == '1' : L.N > 1024) && L.n <= 2048;
     if (use_fd) {   // exact second level at any size: Kronecker fast diagonalisation (host eigensolve)
       std::vector<double> V, lam;
       if (annulus) {       // per-axis decompositions [2][n][n], [2][n]

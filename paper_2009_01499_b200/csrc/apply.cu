@@ -514,10 +514,10 @@ int apply_num_partials(int dim, int p, int64_t n1) {
   return int(std::max<int64_t>(std::max(v1, v2), v3));
 }
 
-static const bool g_apply_stream = [] {
-  const char *e = std::getenv("IGA2L_APPLY_STREAM");   // 0: the tiled kernels below (A/B and fallback)
+inline bool apply_stream_on() {                      // IGA2L_APPLY_STREAM=0: the tiled kernels below (read per call)
+  const char *e = std::getenv("IGA2L_APPLY_STREAM");
   return !(e && e[0] == '0');
-}();
+}
 
 void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, const double *x, const double *b,
                   double *y, double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv, const ToeP *tp,
@@ -526,7 +526,7 @@ void launch_apply(int dim, int p, int64_t n1, const double *K, const double *M, 
   const int nz = sv.zhi - sv.zlo;
   const size_t sm = apply_smem(dim, p);
   if (nz <= 0) return;
-  if (g_apply_stream && ys == 0 && launch_apply_stream(dim, p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp, false))
+  if (ys == 0 && apply_stream_on() && launch_apply_stream(dim, p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp, false))
     return;
   if (dim == 2 &&
       (try_apply2d<1>(p, n1, K, M, x, b, y, partial, mode, st, nparts, sv, tp, ys) ||

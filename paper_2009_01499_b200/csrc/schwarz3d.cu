@@ -295,10 +295,11 @@ __global__ void __launch_bounds__(B4<P, S>::NT) k_schwarz3d_v4(const __grid_cons
   }
 }
 
-static const bool g_s3d_tma = [] {                  // IGA2L_S3D_TMA=0: window by cp.async rows
-  const char *e = std::getenv("IGA2L_S3D_TMA");
+// IGA2L_S3D_TMA=0: window by cp.async rows.  Read per launch (tests switch it within one process).
+inline bool env_on(const char *name) {
+  const char *e = std::getenv(name);
   return !(e && e[0] == '0');
-}();
+}
 template <int P, int S>
 bool try_schwarz3d(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
                    const double *b, double *x, int c0, int c1, int c2, int D, int nb0, int nb1, int nb2, int zoff,
@@ -311,7 +312,7 @@ bool try_schwarz3d(int p, int s, int64_t n1, const double *K, const double *M, c
     CUtensorMap me{}, mo{};
     const int w = (S - 1) / 2;
     const int64_t rows = (std::min<int64_t>(n1, c2 + int64_t(D) * (nb2 - 1) + w + P + 1) - zoff) * n1;   // stored rows
-    if (B::TMA_OK && g_s3d_tma && rows >= 2 && make_tmap_rows_swz128(&me, x, n1, (rows + 1) / 2, 2 * n1, B::BOX, B::BR) &&
+    if (B::TMA_OK && env_on("IGA2L_S3D_TMA") && rows >= 2 && make_tmap_rows_swz128(&me, x, n1, (rows + 1) / 2, 2 * n1, B::BOX, B::BR) &&
         make_tmap_rows_swz128(&mo, x + n1 - 1, n1 + 1, rows / 2, 2 * n1, B::BOX, B::BR)) {
       constexpr size_t sm = sizeof(double) * B::PERT + 16 + 1024;
       ensure_smem(k_schwarz3d_v4<P, S, true>, sm);

@@ -282,12 +282,9 @@ inline int chunks_for(int64_t tiles, int nz, int target, int minlen) {
 }
 
 // A/B knob IGA2L_STREAM_CFG: 1 = TY 8 / 256 threads, 2 = TY 16 / 256 threads, 3 = TY 16 / 512 threads
-int stream_cfg() {
-  static const int v = [] {
-    const char *e = std::getenv("IGA2L_STREAM_CFG");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
+int stream_cfg() {                                   // read per call (tests switch it within one process)
+  const char *e = std::getenv("IGA2L_STREAM_CFG");
+  return e ? std::atoi(e) : 0;
 }
 
 template <int P, int TY, int NT>
@@ -317,6 +314,14 @@ bool try_stream3d(int p, int64_t n1, const double *K, const double *M, const dou
                   double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv, const ToeP *tpp, bool count) {
   if (p != P) return false;
   // measured (C4 p = 3, C5 p = 5): TY 8 / 256 threads for p <= 4, TY 16 / 256 threads above
+  if (count) {                                        // partial-buffer sizing: the most any config writes
+    int a = 0, c = 0, d = 0;
+    go_stream3d<P, 8, 256>(n1, K, M, x, b, y, partial, mode, st, &a, sv, tpp, true);
+    go_stream3d<P, 16, 256>(n1, K, M, x, b, y, partial, mode, st, &c, sv, tpp, true);
+    go_stream3d<P, 16, 512>(n1, K, M, x, b, y, partial, mode, st, &d, sv, tpp, true);
+    if (nparts) *nparts = std::max(a, std::max(c, d));
+    return true;
+  }
   const int cfg = stream_cfg() ? stream_cfg() : (P <= 4 ? 1 : 2);
   if (cfg == 1) return go_stream3d<P, 8, 256>(n1, K, M, x, b, y, partial, mode, st, nparts, sv, tpp, count);
   if (cfg == 2) return go_stream3d<P, 16, 256>(n1, K, M, x, b, y, partial, mode, st, nparts, sv, tpp, count);

@@ -298,3 +298,46 @@ def test_exact_coarse_fd_large():
     e = torch.empty(ctx.Nc, dtype=torch.float64, device=DEV)
     ctx.coarse_solve(cu(dq), e)
     close(host(e), spla.spsolve(A, dq), 1e-10)
+
+
+# ---- every kernel variant a knob selects gives the oracle's result ----
+@pytest.mark.parametrize("cfg", [PAR[7], PAR[8]], ids=["3d_p3", "3d_p5_q2"])
+def test_3d_sweep_variants_bitwise_equal(cfg, monkeypatch):
+    """3D colour kernel: window by TMA boxes (default) and by cp.async rows (IGA2L_S3D_TMA=0): the same
+    arithmetic in the same order -> bitwise equal sweeps, and equal to the oracle's multicolour sweep."""
+    name, d, p, q, m, s, coarse, hf = cfg
+    ctx = make_ctx(d, p, q, m, s, coarse, hf)
+    b, x0 = random_rhs(ctx.N), initial_guess(ctx.N)
+    outs = []
+    for env in ({}, {"IGA2L_S3D_TMA": "0"}):
+        monkeypatch.delenv("IGA2L_S3D_TMA", raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        xg = cu(x0)
+        ctx.sweep(cu(b), xg)
+        outs.append(host(xg))
+    assert np.array_equal(outs[0], outs[1])
+    ora = oracle_for(*cfg)
+    xo = x0.copy()
+    ora.smoother.sweep(xo, b)
+    assert np.abs(outs[0] - xo).max() <= 1e-11 * np.abs(xo).max()
+
+
+@pytest.mark.parametrize("p,m", [(3, 20), (5, 12)])
+@pytest.mark.parametrize("env", [{"IGA2L_APPLY_STREAM": "0"}, {"IGA2L_STREAM_CFG": "1"}, {"IGA2L_STREAM_CFG": "2"},
+                                 {"IGA2L_STREAM_CFG": "3"}], ids=["tiled", "cfg1", "cfg2", "cfg3"])
+def test_3d_apply_variants(p, m, env, monkeypatch):
+    """3D residual: the tiled kernel and every streaming configuration against the assembled operator,
+    and the residual norm over exactly the partials each variant writes."""
+    from oracle.assembly import stiffness
+    ctx = make_ctx(3, p, 1, m, 3 if p <= 4 else 5, "vcycle", 2)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    x, b = initial_guess(ctx.N, seed=2), random_rhs(ctx.N, seed=3)
+    y = torch.empty(ctx.N, dtype=torch.float64, device=DEV)
+    ctx.apply(cu(x), y)
+    ref = stiffness(p, m, 3) @ x
+    assert np.abs(host(y) - ref).max() <= 1e-13 * np.abs(ref).max()
+    rn = ctx.residual_norm(cu(b), cu(x))
+    assert abs(rn - np.linalg.norm(b - ref)) <= 1e-12 * np.linalg.norm(b - ref)
+

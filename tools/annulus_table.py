@@ -24,7 +24,7 @@ dev = torch.device("cuda:0")
 st = torch.cuda.Stream(dev)
 torch.cuda.set_stream(st)
 print(f"{'grid':>6} {'p':>2} | {'DS it':>5} {'MG it':>5} | paper DS MG | {'DS us/it':>9} {'MG us/it':>9}")
-for m in sorted(PAPER):
+for m in [int(v) for v in (sys.argv[1].split(",") if len(sys.argv) > 1 else sorted(PAPER))]:
     for i, p in enumerate(range(3, 9)):
         res = []
         for mode in (pkg.COARSE_EXACT, pkg.COARSE_VCYCLE):

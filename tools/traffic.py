@@ -33,7 +33,8 @@ def scale(v, unit):
 
 res = {}
 for arg in sys.argv[1:]:
-    cfg, rep = arg.split("=", 1)
+    cfg, rep = arg.split("=", 1)          # cfg=path[@profile name for the source note]
+    rep, _, note = rep.partition("@")
     hdr, units, data = rows(rep)
     i_n = hdr.index("Kernel Name")
     i_r, i_w, i_t = (hdr.index(m) for m in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"))
@@ -42,6 +43,6 @@ for arg in sys.argv[1:]:
                 "dram_bytes_per_launch": sum(p[1] for p in per) / len(per),
                 "launches_captured": len(per),
                 "cold_us_per_launch": [round(p[2], 2) for p in per],
-                "source": f"ncu --set full --clock-control none -k regex:k_schwarz of bench.py --config {cfg} "
-                          f"(profiles/ncu_traffic_{cfg}_r01.txt); cold cache"}
+                "source": f"ncu --set full --clock-control none (profiles/{note or 'ncu_traffic_' + cfg + '_r01.txt'}); "
+                          f"cold cache, mean over the captured launches"}
 print(json.dumps(res, indent=1))
