@@ -187,11 +187,16 @@ void L_tensor(iga2l_ctx *c, int dim, const Band1D &B, const double *in, double *
     c->launch_counter++;
     return;
   }
+  // shrinking transforms (restriction) run the last axis first, so that the contiguous-axis pass (the
+  // least efficient: inner = 1) works on the smallest intermediate; growing ones (prolongation) axis 0 first
+  const bool rev = B.rows < B.cols;
   const double *src = in;
-  for (int a = 0; a < dim; ++a) {
-    const bool last = (a == dim - 1);
-    double *dst = last ? out : (a % 2 == 0 ? t1 : t2);
-    const int64_t inner = ipow(B.rows, a), outer = ipow(B.cols, dim - 1 - a);
+  for (int k = 0; k < dim; ++k) {
+    const int a = rev ? dim - 1 - k : k;
+    const bool last = (k == dim - 1);
+    double *dst = last ? out : (k % 2 == 0 ? t1 : t2);
+    const int64_t inner = rev ? ipow(B.cols, a) : ipow(B.rows, a);
+    const int64_t outer = rev ? ipow(B.rows, dim - 1 - a) : ipow(B.cols, dim - 1 - a);
     launch_band_axis(src, dst, outer, B.cols, inner, B, last ? acc : 0, c->st);
     c->launch_counter++;
     src = dst;

@@ -1,5 +1,7 @@
 // Tensor-product band transfers: restriction d_q = (⊗R1) d and
 // prolongation x += (⊗R1)^T e on the fine level, the h<->2h transfers of the V-cycle.  See kernels.cuh.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -42,6 +44,90 @@ __global__ void __launch_bounds__(256) k_band_axis(const double *__restrict__ in
   }
   const double s = s0 + s1;
   const int64_t idx = (o * nr + (r - rlo)) * inner + i;
+  out[idx] = acc ? out[idx] + s : s;
+}
+
+// The same transform with a compile-time band width (v2: the generic kernel above was issue-bound at ~87%
+// of issue slots on C5's transfers): coefficients of the CTA's output row in registers, valid-column range
+// decided once per CTA (uniform branch), pointer increments instead of 64-bit products, and V = 2
+// consecutive inner outputs per thread by 16-byte loads when the inner extent is even.
+template <int W, int V>
+__global__ void __launch_bounds__(256) k_band_inner(const double *__restrict__ in, double *__restrict__ out, int nin,
+                                                    int64_t inner, const int *__restrict__ lo,
+                                                    const double *__restrict__ c, int acc, int clo, int chi, int coff,
+                                                    int rlo, int nr) {
+  const int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) * V;
+  if (i >= inner) return;
+  const int r = rlo + int(blockIdx.y);
+  const int64_t o = blockIdx.z;
+  const int l0 = lo[r];
+  const int kb = max(0, clo - l0), ke = min(W, chi - l0);     // valid band columns (uniform per CTA)
+  double cf[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) cf[k] = __ldg(c + int64_t(r) * W + k);
+  const double *src = in + (o * nin - coff + l0) * inner + i;
+  double s0[V], s1[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) s0[v] = s1[v] = 0.0;
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    if (k >= kb && k < ke) {
+      if constexpr (V == 2) {
+        const double2 t = __ldg(reinterpret_cast<const double2 *>(src + k * inner));
+        if (k & 1) { s1[0] = fma(cf[k], t.x, s1[0]); s1[1] = fma(cf[k], t.y, s1[1]); }
+        else { s0[0] = fma(cf[k], t.x, s0[0]); s0[1] = fma(cf[k], t.y, s0[1]); }
+      } else {
+        const double t = __ldg(src + k * inner);
+        if (k & 1) s1[0] = fma(cf[k], t, s1[0]); else s0[0] = fma(cf[k], t, s0[0]);
+      }
+    }
+  }
+  double *dst = out + (o * nr + (r - rlo)) * inner + i;
+  if constexpr (V == 2) {
+    double2 res = make_double2(s0[0] + s1[0], s0[1] + s1[1]);
+    if (acc) {
+      const double2 prev = *reinterpret_cast<const double2 *>(dst);
+      res.x += prev.x;
+      res.y += prev.y;
+    }
+    *reinterpret_cast<double2 *>(dst) = res;
+  } else {
+    const double s = s0[0] + s1[0];
+    *dst = acc ? *dst + s : s;
+  }
+}
+
+// inner == 1 (the contiguous axis): one thread per output row r of one outer slice.
+template <int W>
+__global__ void __launch_bounds__(128) k_band_rows(const double *__restrict__ in, double *__restrict__ out,
+                                                   int64_t outer, int nin, const int *__restrict__ lo,
+                                                   const double *__restrict__ c, int acc, int clo, int chi, int coff,
+                                                   int rlo, int rhi) {
+  const int r = rlo + int(blockIdx.x * blockDim.x + threadIdx.x);
+  const int64_t o = blockIdx.y + int64_t(gridDim.y) * blockIdx.z;
+  if (r >= rhi || o >= outer) return;
+  const int l0 = lo[r];
+  const double *src = in + o * nin - coff + l0;
+  const double *cr = c + int64_t(r) * W;
+  double s0 = 0.0, s1 = 0.0;
+  if (l0 >= clo && l0 + W <= chi) {                          // interior row: no column checks
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const double t = __ldg(cr + k) * __ldg(src + k);
+      if (k & 1) s1 += t; else s0 += t;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const int col = l0 + k;
+      if (col >= clo && col < chi) {
+        const double t = __ldg(cr + k) * __ldg(src + k);
+        if (k & 1) s1 += t; else s0 += t;
+      }
+    }
+  }
+  const double s = s0 + s1;
+  const int64_t idx = (o * (rhi - rlo) + (r - rlo));
   out[idx] = acc ? out[idx] + s : s;
 }
 
@@ -172,8 +258,33 @@ void launch_band_axis(const double *in, double *out, int64_t outer, int nin, int
   const int64_t total = outer * (rhi - rlo) * inner;
   if (total <= 0) return;
   const int nr = rhi - rlo;
+  const unsigned gy = unsigned(std::min<int64_t>(outer, 32768)), gz = unsigned((outer + gy - 1) / gy);
+  const bool v2 = inner % 2 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  bool done = false;
+  auto go = [&](auto wtag) {
+    constexpr int Wc = decltype(wtag)::value;
+    if (inner == 1) {
+      k_band_rows<Wc><<<dim3((nr + 127) / 128, gy, gz), 128, 0, st>>>(in, out, outer, nin, B.lo, B.c, accumulate, clo,
+                                                                        chi, coff, rlo, rhi);
+    } else if (v2) {
+      k_band_inner<Wc, 2><<<dim3(unsigned((inner / 2 + 255) / 256), unsigned(nr), unsigned(outer)), 256, 0, st>>>(
+          in, out, nin, inner, B.lo, B.c, accumulate, clo, chi, coff, rlo, nr);
+    } else {
+      k_band_inner<Wc, 1><<<dim3(unsigned((inner + 255) / 256), unsigned(nr), unsigned(outer)), 256, 0, st>>>(
+          in, out, nin, inner, B.lo, B.c, accumulate, clo, chi, coff, rlo, nr);
+    }
+    done = true;
+  };
+  switch (B.W) {
+#define IGA2L_BW(w_) case w_: go(std::integral_constant<int, w_>{}); break;
+    IGA2L_BW(1) IGA2L_BW(2) IGA2L_BW(3) IGA2L_BW(4) IGA2L_BW(5) IGA2L_BW(6) IGA2L_BW(7) IGA2L_BW(8)
+    IGA2L_BW(9) IGA2L_BW(10) IGA2L_BW(11) IGA2L_BW(12) IGA2L_BW(13) IGA2L_BW(14) IGA2L_BW(15) IGA2L_BW(16)
+#undef IGA2L_BW
+    default: break;
+  }
+  if (done) return;
   if (inner == 1) {
-    const unsigned gy = unsigned(std::min<int64_t>(outer, 32768)), gz = unsigned((outer + gy - 1) / gy);
     k_band_axis<<<dim3((nr + 127) / 128, gy, gz), 128, 0, st>>>(in, out, outer, nin, inner, B.W, B.lo, B.c,
                                                                 accumulate, clo, chi, coff, rlo, rhi);
   } else {
