@@ -10,7 +10,7 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libiga2l.so")
+LIB_PATH = os.environ.get("IGA2L_LIB") or os.path.join(_HERE, "libiga2l.so")   # IGA2L_LIB: A/B builds (dev)
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "iga2l.h")
 
 OK, EPARAM, ENUMERIC, NOTCONV, ECUDA, ENCCL, ENOMEM = range(7)
