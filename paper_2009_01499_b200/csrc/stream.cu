@@ -275,12 +275,6 @@ __global__ void __launch_bounds__(NT_, S3<P, TY, NT_>::MINB)
   }
 }
 
-// chunk the last axis so that about `target` CTAs run, chunks no shorter than `minlen` planes
-inline int chunks_for(int64_t tiles, int nz, int target, int minlen) {
-  int ch = int(std::max<int64_t>(1, (target + tiles - 1) / tiles));
-  return std::max(1, std::min(ch, nz / std::max(1, minlen)));
-}
-
 // A/B knob IGA2L_STREAM_CFG: 1 = TY 8 / 256 threads, 2 = TY 16 / 256 threads, 3 = TY 16 / 512 threads
 int stream_cfg() {                                   // read per call (tests switch it within one process)
   const char *e = std::getenv("IGA2L_STREAM_CFG");
