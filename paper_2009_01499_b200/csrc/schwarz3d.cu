@@ -295,6 +295,328 @@ __global__ void __launch_bounds__(B4<P, S>::NT) k_schwarz3d_v4(const __grid_cons
   }
 }
 
+// ---------------- v5: one WARP per block, window planes streamed in groups of G -----------------------
+// The same block step as v4 (r_B = b_B - (A x)_B by pencil passes x, y, z; δ by fast diagonalisation;
+// x_B += δ), reorganised so that a block needs ~10 KB of shared memory and no CTA barrier:
+//  * the window is read plane group by plane group straight from global memory (L2) into registers,
+//    one x-row per lane ((plane, row) tasks), never staged whole;
+//  * pass x -> Pa/Pb [S][G*Wn] (l-major: conflict-free stores), pass y per (plane, lx) pencil -> Pc/Pe
+//    [G][S][S] (aliasing Pa/Pb), pass z ACCUMULATES the group's planes into r[lz] held by lane (lx, ly);
+//  * on Toeplitz axes (A27) the symmetric band (k[t] = k[2p-t]) is applied to pair sums
+//    v[l+t] + v[l+2p-t] shared by K and M: 5 adds + 12 FMAs per output instead of 22 FMAs (p = 5);
+//  * the fast diagonalisation keeps (lx, ly) lanes with their S values of z in registers (the z
+//    transforms are register-local; x and y exchange through two 125-value buffers).
+// Smem offsets: conflict-free strides for the pass-y reads (TXP) and writes (PS); see the search below.
+template <int P, int S, int G>
+struct BW {
+  static constexpr int W = 2 * P + 1, Wn = S + 2 * P, w = (S - 1) / 2, S2 = S * S, S3 = S2 * S;
+  static constexpr int NG = Wn / G, TX = G * Wn, RX = (TX + 31) / 32, TY = G * S;
+  static_assert(Wn % G == 0 && TY <= 32 && S2 <= 32, "group shape");
+  static constexpr bool ok_txp(int t) {
+    for (int h = 0; h < 2; ++h)
+      for (int i = 16 * h; i < 16 * h + 16 && i < TY; ++i)
+        for (int k = i + 1; k < 16 * h + 16 && k < TY; ++k)
+          if (((i % S) * t + (i / S) * Wn) % 16 == ((k % S) * t + (k / S) * Wn) % 16) return false;
+    return true;
+  }
+  static constexpr int find_txp() {
+    for (int t = TX; t < TX + 64; ++t)
+      if (ok_txp(t)) return t;
+    return TX;
+  }
+  static constexpr int TXP = find_txp();
+  static constexpr int PS = S2 + ((S - S2 % 16) % 16 + 16) % 16;           // PS = S (mod 16), >= S2
+  static constexpr int AREA = (2 * S * TXP > 2 * G * PS ? 2 * S * TXP : 2 * G * PS);
+  static constexpr int TAB = (6 * S * W > 2 * S3 ? 6 * S * W : 2 * S3);   // Tk, Tm | F0, F1
+  static constexpr int OPA = 0, OPB = S * TXP, OPC = 0, OPE = G * PS, OT = AREA, OF = AREA,
+                       OVS = AREA + TAB, OLS = OVS + 3 * S2;
+  static constexpr int PERW = ((OLS + 3 * S + 1) / 2) * 2;                 // doubles per warp (16-byte multiple)
+};
+
+template <int P, int S, bool TOE>
+__device__ __forceinline__ void w_pass_x(const double (&v)[S + 2 * P], const double *Tk, const double *Tm,
+                                         const ToeP &tp, double *a, double *bo, int ostride) {
+  constexpr int W = 2 * P + 1;
+#pragma unroll
+  for (int l = 0; l < S; ++l) {
+    if constexpr (TOE) {
+      double ka = tp.k[P] * v[l + P], ma = tp.m[P] * v[l + P];
+#pragma unroll
+      for (int t = 0; t < P; ++t) {
+        const double s2 = v[l + t] + v[l + 2 * P - t];
+        ka = fma(tp.k[t], s2, ka);
+        ma = fma(tp.m[t], s2, ma);
+      }
+      a[l * ostride] = ka;
+      bo[l * ostride] = ma;
+    } else {
+      double ka = 0.0, ma = 0.0;
+#pragma unroll
+      for (int t = 0; t < W; ++t) {
+        ka = fma(Tk[l * W + t], v[l + t], ka);
+        ma = fma(Tm[l * W + t], v[l + t], ma);
+      }
+      a[l * ostride] = ka;
+      bo[l * ostride] = ma;
+    }
+  }
+}
+
+// pass y of one (plane, lx) pencil: Pc = My Pa + Ky Pb, Pe = My Pb
+template <int P, int S, bool TOE>
+__device__ __forceinline__ void w_pass_y(const double (&pa)[S + 2 * P], const double (&pb)[S + 2 * P], const double *Tk,
+                                         const double *Tm, const ToeP &tp, double *oc, double *oe) {
+  constexpr int W = 2 * P + 1;
+#pragma unroll
+  for (int l = 0; l < S; ++l) {
+    if constexpr (TOE) {
+      double c = tp.m[P] * pa[l + P], e = tp.m[P] * pb[l + P];
+      c = fma(tp.k[P], pb[l + P], c);
+#pragma unroll
+      for (int t = 0; t < P; ++t) {
+        const double sa = pa[l + t] + pa[l + 2 * P - t], sb = pb[l + t] + pb[l + 2 * P - t];
+        c = fma(tp.m[t], sa, c);
+        c = fma(tp.k[t], sb, c);
+        e = fma(tp.m[t], sb, e);
+      }
+      oc[l * S] = c;
+      oe[l * S] = e;
+    } else {
+      double c = 0.0, e = 0.0;
+#pragma unroll
+      for (int t = 0; t < W; ++t) {
+        c = fma(Tm[l * W + t], pa[l + t], c);
+        c = fma(Tk[l * W + t], pb[l + t], c);
+        e = fma(Tm[l * W + t], pb[l + t], e);
+      }
+      oc[l * S] = c;
+      oe[l * S] = e;
+    }
+  }
+}
+
+template <int P, int S, int G, int NW, int MINB, int LV>
+__global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_w(int n1, const double *__restrict__ K, const double *__restrict__ M,
+                                                        const double *__restrict__ Vt, const double *__restrict__ lamt,
+                                                        const double *__restrict__ b, double *__restrict__ x, int c0,
+                                                        int c1, int c2, int D, int nb0, int nb1, int nblk, int zoff,
+                                                        int tlo, int thi, const ToeP tp) {
+  using B = BW<P, S, G>;
+  constexpr int W = B::W, Wn = B::Wn, w = B::w, S2 = B::S2, TXP = B::TXP, PS = B::PS;
+  extern __shared__ __align__(16) double smw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = blockIdx.x * NW + wid;
+  if (g >= nblk) return;                                          // the whole warp: no CTA barrier is used
+  double *sw = smw + wid * B::PERW;
+  double *Pa = sw + B::OPA, *Pb = sw + B::OPB, *Pc = sw + B::OPC, *Pe = sw + B::OPE;
+  double *Tk = sw + B::OT, *Tm = sw + B::OT + 3 * S * W, *F0 = sw + B::OF, *F1 = sw + B::OF + B::S3;
+  double *Vs = sw + B::OVS, *Ls = sw + B::OLS;
+  const unsigned un = unsigned(n1);
+  const int cc[3] = {c0 + D * (g % nb0), c1 + D * ((g / nb0) % nb1), c2 + D * (g / (nb0 * nb1))};
+  const bool tv = tp.valid != 0;
+  bool toe[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) toe[a] = tv && cc[a] - w >= tlo && cc[a] + w <= thi;
+  const int ox = cc[0] - w - P, oy = cc[1] - w - P, oz = cc[2] - w - P;
+  const bool xin = ox >= 0 && ox + Wn <= n1;
+  // ---- band rows / FD tables of the boundary axes (zero rows outside the domain) ----
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (toe[a]) continue;
+    for (int i = lane; i < S * W; i += 32) {
+      const int l = i / W, t = i - l * W, gr = cc[a] - w + l;
+      const bool ok = unsigned(gr) < un;
+      Tk[a * S * W + i] = ok ? K[int64_t(gr) * W + t] : 0.0;
+      Tm[a * S * W + i] = ok ? M[int64_t(gr) * W + t] : 0.0;
+    }
+    for (int i = lane; i < S2; i += 32) Vs[a * S2 + i] = Vt[int64_t(cc[a]) * S2 + i];
+    if (lane < S) Ls[a * S + lane] = lamt[int64_t(cc[a]) * S + lane];
+  }
+  // ---- this lane's FD / update points (lx, ly, 0..S-1) and b_B there ----
+  const bool vl = lane < S2;
+  const int lx = vl ? lane % S : 0, ly = vl ? lane / S : 0;
+  const int gx = cc[0] - w + lx, gy = cc[1] - w + ly;
+  const bool xyok = vl && unsigned(gx) < un && unsigned(gy) < un;
+  __syncwarp();
+  double r[S];
+#pragma unroll
+  for (int lz = 0; lz < S; ++lz) r[lz] = 0.0;
+  // x-row of pass-x task t of group gi (zero outside the domain)
+  auto load_row = [&](int gi, int t, double (&v)[Wn]) {
+    const int jj = t / Wn, yy = t - jj * Wn;
+    const int gz = oz + gi * G + jj, gyy = oy + yy;
+    const bool rok = t < B::TX && unsigned(gz) < un && unsigned(gyy) < un;
+    const int64_t e0 = (int64_t(gz - zoff) * n1 + gyy) * n1 + ox;
+    if (LV > 1 && xin) {                                          // aligned LV-double vector loads + shift select
+      constexpr int NV = (Wn + 2 * LV - 2) / LV;                  // vectors covering [e0 & ~(LV-1), e0 + Wn)
+      double u[NV * LV];
+      const double *ap = x + (e0 & ~int64_t(LV - 1));
+      const int sh = int(e0 & (LV - 1));
+#pragma unroll
+      for (int c = 0; c < NV; ++c) {
+        if constexpr (LV == 4) {
+          if (rok)
+            asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                         : "=d"(u[4 * c]), "=d"(u[4 * c + 1]), "=d"(u[4 * c + 2]), "=d"(u[4 * c + 3])
+                         : "l"(ap + 4 * c));
+          else
+            u[4 * c] = u[4 * c + 1] = u[4 * c + 2] = u[4 * c + 3] = 0.0;
+        } else {
+          const double2 q = rok ? __ldg(reinterpret_cast<const double2 *>(ap) + c) : make_double2(0.0, 0.0);
+          u[2 * c] = q.x;
+          u[2 * c + 1] = q.y;
+        }
+      }
+      if constexpr (LV == 4) {
+        double u2[Wn + 1];
+#pragma unroll
+        for (int k = 0; k < Wn + 1; ++k) u2[k] = (sh & 2) ? u[k + 2] : u[k];
+#pragma unroll
+        for (int k = 0; k < Wn; ++k) v[k] = (sh & 1) ? u2[k + 1] : u2[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < Wn; ++k) v[k] = sh ? u[k + 1] : u[k];
+      }
+    } else {
+      const double *rp = x + e0;
+#pragma unroll
+      for (int k = 0; k < Wn; ++k) v[k] = (rok && (xin || unsigned(ox + k) < un)) ? rp[k] : 0.0;
+    }
+  };
+#pragma unroll
+  for (int gi = 0; gi < B::NG; ++gi) {
+    // ---- pass x over the group's (plane, row) tasks: Pa = Kx X, Pb = Mx X ----
+#pragma unroll 1
+    for (int rr = 0; rr < B::RX; ++rr) {
+      const int t = rr * 32 + lane;
+      double v[Wn];
+      load_row(gi, t, v);
+      if (t < B::TX) {
+        if (toe[0]) w_pass_x<P, S, true>(v, Tk, Tm, tp, Pa + t, Pb + t, TXP);
+        else w_pass_x<P, S, false>(v, Tk, Tm, tp, Pa + t, Pb + t, TXP);
+      }
+    }
+    __syncwarp();
+    // ---- pass y over the group's (plane, lx) pencils: Pc = My Pa + Ky Pb, Pe = My Pb (into Pa's area) ----
+    {
+      const bool act = lane < B::TY;
+      const int jj = act ? lane / S : 0, px = act ? lane - jj * S : 0;
+      double pa[Wn], pb[Wn];
+#pragma unroll
+      for (int k = 0; k < Wn; ++k) {
+        pa[k] = act ? Pa[px * TXP + jj * Wn + k] : 0.0;
+        pb[k] = act ? Pb[px * TXP + jj * Wn + k] : 0.0;
+      }
+      __syncwarp();
+      if (act) {
+        if (toe[1]) w_pass_y<P, S, true>(pa, pb, Tk + S * W, Tm + S * W, tp, Pc + jj * PS + px, Pe + jj * PS + px);
+        else w_pass_y<P, S, false>(pa, pb, Tk + S * W, Tm + S * W, tp, Pc + jj * PS + px, Pe + jj * PS + px);
+      }
+    }
+    __syncwarp();
+    // ---- pass z: r[lz] += Mz[lz][j-lz] Pc_j + Kz[lz][j-lz] Pe_j over the group's planes j ----
+    if (vl) {
+#pragma unroll
+      for (int jj = 0; jj < G; ++jj) {
+        const int j = gi * G + jj;
+        const double pc = Pc[jj * PS + lane], pe = Pe[jj * PS + lane];
+#pragma unroll
+        for (int lz = 0; lz < S; ++lz) {
+          const int t = j - lz;
+          if (t < 0 || t >= W) continue;
+          if (toe[2]) r[lz] = fma(tp.k[t], pe, fma(tp.m[t], pc, r[lz]));
+          else r[lz] = fma(Tk[2 * S * W + lz * W + t], pe, fma(Tm[2 * S * W + lz * W + t], pc, r[lz]));
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // ---- δ = (⊗V) Λ^{-1} (⊗V)^T (b_B - r), x_B += δ ----
+  auto Vax = [&](int a, int l, int j) { return toe[a] ? tp.v[l * S + j] : Vs[a * S2 + l * S + j]; };
+  auto Lax = [&](int a, int j) { return toe[a] ? tp.lam[j] : Ls[a * S + j]; };
+  double q[S];
+  if (vl) {
+#pragma unroll
+    for (int lz = 0; lz < S; ++lz) {
+      const int gz = cc[2] - w + lz;
+      const double bz = (xyok && unsigned(gz) < un) ? b[(int64_t(gz - zoff) * n1 + gy) * n1 + gx] : 0.0;
+      F0[lz * S2 + lane] = bz - r[lz];
+    }
+  }
+  __syncwarp();
+  if (vl) {                                                       // along x (transposed)
+    double vt[S];
+#pragma unroll
+    for (int l = 0; l < S; ++l) vt[l] = Vax(0, l, lx);
+#pragma unroll
+    for (int lz = 0; lz < S; ++lz) {
+      double a0 = 0.0;
+#pragma unroll
+      for (int l = 0; l < S; ++l) a0 = fma(vt[l], F0[lz * S2 + ly * S + l], a0);
+      F1[lz * S2 + lane] = a0;
+    }
+  }
+  __syncwarp();
+  if (vl) {                                                       // along y (transposed), z (transposed), Λ^{-1}, z
+    double vt[S];
+#pragma unroll
+    for (int l = 0; l < S; ++l) vt[l] = Vax(1, l, ly);
+#pragma unroll
+    for (int lz = 0; lz < S; ++lz) {
+      double a0 = 0.0;
+#pragma unroll
+      for (int l = 0; l < S; ++l) a0 = fma(vt[l], F1[lz * S2 + l * S + lx], a0);
+      q[lz] = a0;
+    }
+    const double lxy = Lax(0, lx) + Lax(1, ly);
+    double q3[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      double a0 = 0.0;
+#pragma unroll
+      for (int l = 0; l < S; ++l) a0 = fma(Vax(2, l, j), q[l], a0);
+      q3[j] = a0 / (lxy + Lax(2, j));
+    }
+#pragma unroll
+    for (int lz = 0; lz < S; ++lz) {
+      double a0 = 0.0;
+#pragma unroll
+      for (int l = 0; l < S; ++l) a0 = fma(Vax(2, lz, l), q3[l], a0);
+      F0[lz * S2 + lane] = a0;                                    // F0's last reads were before the barrier above
+    }
+  }
+  __syncwarp();
+  if (vl) {                                                       // along y
+    double vt[S];
+#pragma unroll
+    for (int l = 0; l < S; ++l) vt[l] = Vax(1, ly, l);
+#pragma unroll
+    for (int lz = 0; lz < S; ++lz) {
+      double a0 = 0.0;
+#pragma unroll
+      for (int l = 0; l < S; ++l) a0 = fma(vt[l], F0[lz * S2 + l * S + lx], a0);
+      F1[lz * S2 + lane] = a0;                                    // F1's last reads: two barriers ago
+    }
+  }
+  __syncwarp();
+  if (xyok) {                                                     // along x, and x_B += δ
+    double vt[S];
+#pragma unroll
+    for (int l = 0; l < S; ++l) vt[l] = Vax(0, lx, l);
+#pragma unroll
+    for (int lz = 0; lz < S; ++lz) {
+      double a0 = 0.0;
+#pragma unroll
+      for (int l = 0; l < S; ++l) a0 = fma(vt[l], F1[lz * S2 + ly * S + l], a0);
+      const int gz = cc[2] - w + lz;
+      if (unsigned(gz) < un) {
+        double *xp = x + (int64_t(gz - zoff) * n1 + gy) * n1 + gx;
+        *xp = *xp + a0;
+      }
+    }
+  }
+}
+
 // IGA2L_S3D_TMA=0: window by cp.async rows.  Read per launch (tests switch it within one process).
 inline bool env_on(const char *name) {
   const char *e = std::getenv(name);
@@ -328,11 +650,42 @@ bool try_schwarz3d(int p, int s, int64_t n1, const double *K, const double *M, c
   }
 }
 
+// launch of v5: NW warps (blocks) per CTA, at least MINB CTAs per SM, LV-double row loads
+template <int P, int S, int G, int NW, int MINB, int LV>
+void launch_w(int64_t n1, const double *K, const double *M, const double *V, const double *lam, const double *b,
+              double *x, int c0, int c1, int c2, int D, int nb0, int nb1, int nblk, int zoff, int tlo, int thi,
+              cudaStream_t st, const ToeP &tp) {
+  constexpr size_t sm = sizeof(double) * BW<P, S, G>::PERW * NW;
+  ensure_smem(k_schwarz3d_w<P, S, G, NW, MINB, LV>, sm);
+  k_schwarz3d_w<P, S, G, NW, MINB, LV><<<(nblk + NW - 1) / NW, 32 * NW, sm, st>>>(
+      int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nblk, zoff, tlo, thi, tp);
+}
+// v5 (warp per block) for the shapes of the 3D configs; IGA2L_S3D_WARP=0 selects v4.  4 warps (blocks) per CTA,
+// at most 128 registers (4 CTAs per SM).
+template <int P, int S, int G>
+bool try_schwarz3d_w(int p, int s, int64_t n1, const double *K, const double *M, const double *V, const double *lam,
+                     const double *b, double *x, int c0, int c1, int c2, int D, int nb0, int nb1, int nb2, int zoff,
+                     int tlo, int thi, cudaStream_t st, const ToeP *tpp) {
+  if (p != P || s != S || !env_on("IGA2L_S3D_WARP")) return false;
+  ToeP tp{};
+  if (tpp) tp = *tpp;
+  const int nblk = nb0 * nb1 * nb2;
+  // 32-byte row loads need a 32-byte aligned x (every torch / cudaMalloc allocation is)
+  if (reinterpret_cast<uintptr_t>(x) & 31)
+    launch_w<P, S, G, 4, 4, 1>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nblk, zoff, tlo, thi, st, tp);
+  else
+    launch_w<P, S, G, 4, 4, 4>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nblk, zoff, tlo, thi, st, tp);
+  return true;
+}
+
 }  // namespace
 
 bool launch_schwarz3d_colour(int p, int s, int64_t n1, const double *K, const double *M, const double *V,
                              const double *lam, const double *b, double *x, int c0, int c1, int f2, int D, int nb0,
                              int nb1, int nb2, int zoff, int tlo, int thi, cudaStream_t st, const ToeP *tp) {
+  if (try_schwarz3d_w<3, 3, 9>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, zoff, tlo, thi, st, tp) ||
+      try_schwarz3d_w<5, 5, 5>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, zoff, tlo, thi, st, tp))
+    return true;
   return try_schwarz3d<1, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, zoff, tlo, thi, st, tp) ||
          try_schwarz3d<2, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, zoff, tlo, thi, st, tp) ||
          try_schwarz3d<3, 3>(p, s, n1, K, M, V, lam, b, x, c0, c1, f2, D, nb0, nb1, nb2, zoff, tlo, thi, st, tp) ||

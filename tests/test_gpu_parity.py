@@ -301,26 +301,41 @@ def test_exact_coarse_fd_large():
 
 
 # ---- every kernel variant a knob selects gives the oracle's result ----
-@pytest.mark.parametrize("cfg", [PAR[7], PAR[8]], ids=["3d_p3", "3d_p5_q2"])
-def test_3d_sweep_variants_bitwise_equal(cfg, monkeypatch):
-    """3D colour kernel: window by TMA boxes (default) and by cp.async rows (IGA2L_S3D_TMA=0): the same
-    arithmetic in the same order -> bitwise equal sweeps, and equal to the oracle's multicolour sweep."""
+@pytest.mark.parametrize("cfg", [PAR[7], PAR[8], ("3d_p5_m24", 3, 5, 2, 24, 5, "vcycle", 2)],
+                         ids=["3d_p3", "3d_p5_q2", "3d_p5_m24"])
+def test_3d_sweep_variants(cfg, monkeypatch):
+    """3D colour kernels: v4 (CTA per block) with the window by TMA boxes and by cp.async rows
+    (IGA2L_S3D_TMA=0) -- the same arithmetic in the same order, bitwise equal; v5 (warp per block, the
+    default for (p, s) = (3, 3), (5, 5)) with 32-byte row loads and, on a misaligned x, 8-byte loads --
+    bitwise equal to each other; all equal to the oracle's multicolour sweep (m = 24 has interior blocks)."""
     name, d, p, q, m, s, coarse, hf = cfg
     ctx = make_ctx(d, p, q, m, s, coarse, hf)
     b, x0 = random_rhs(ctx.N), initial_guess(ctx.N)
-    outs = []
-    for env in ({}, {"IGA2L_S3D_TMA": "0"}):
-        monkeypatch.delenv("IGA2L_S3D_TMA", raising=False)
+    outs = {}
+    for key, env in (("v5", {}), ("v4", {"IGA2L_S3D_WARP": "0"}), ("v4rows", {"IGA2L_S3D_WARP": "0", "IGA2L_S3D_TMA": "0"})):
+        for k in ("IGA2L_S3D_WARP", "IGA2L_S3D_TMA"):
+            monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         xg = cu(x0)
         ctx.sweep(cu(b), xg)
-        outs.append(host(xg))
-    assert np.array_equal(outs[0], outs[1])
-    ora = oracle_for(*cfg)
+        outs[key] = host(xg)
+    monkeypatch.delenv("IGA2L_S3D_WARP", raising=False)
+    monkeypatch.delenv("IGA2L_S3D_TMA", raising=False)
+    buf = torch.zeros(ctx.N + 1, dtype=torch.float64, device=DEV)   # x at an 8-byte offset
+    buf[1:] = cu(x0)
+    ctx.sweep(cu(b), buf[1:])
+    outs["v5mis"] = host(buf[1:])
+    assert np.array_equal(outs["v4"], outs["v4rows"])
+    assert np.array_equal(outs["v5"], outs["v5mis"])
     xo = x0.copy()
-    ora.smoother.sweep(xo, b)
-    assert np.abs(outs[0] - xo).max() <= 1e-11 * np.abs(xo).max()
+    if m > 20:                                   # matrix-free Kronecker oracle (pinned == TwoLevel)
+        from oracle.kron import KronTwoLevel
+        KronTwoLevel(d, p, q, m, s).sweep(xo, b)
+    else:
+        oracle_for(*cfg).smoother.sweep(xo, b)
+    for key in ("v5", "v4"):
+        assert np.abs(outs[key] - xo).max() <= 1e-11 * np.abs(xo).max(), key
 
 
 @pytest.mark.parametrize("p,m", [(3, 20), (5, 12)])

@@ -34,3 +34,15 @@ for b in blocks:
     print(b["name"][:90], "| samples", tot, "| sass", len(data), "| executed", sum(f(r[i_ex]) for r in data))
     for r in sorted(data, key=lambda r: -f(r[i_s]))[:n]:
         print(f"  {f(r[i_s]):7.0f} {100*f(r[i_s])/max(tot,1):5.1f}% {r[i_ex]:>9} {r[i_src][:70]}")
+    # executed instructions and stall samples by opcode (predicate guards stripped)
+    ops = {}
+    for r in data:
+        toks = [t for t in r[i_src].split() if not t.startswith("@")]
+        op = toks[0].split(".")[0] if toks else "?"
+        e = ops.setdefault(op, [0.0, 0.0])
+        e[0] += f(r[i_ex])
+        e[1] += f(r[i_s])
+    tex = sum(v[0] for v in ops.values())
+    print("  by opcode (executed warp instructions, share; stall samples, share):")
+    for op, (ex, sa) in sorted(ops.items(), key=lambda kv: -kv[1][0])[:24]:
+        print(f"    {op:10s} {ex:12.0f} {100*ex/max(tex,1):5.1f}%  {sa:7.0f} {100*sa/max(tot,1):5.1f}%")
