@@ -242,7 +242,43 @@ void L_vcycle(iga2l_ctx *c, size_t l) {
   }
 }
 
+// 3D: centres per z-chunk of a last-axis colour class, so that the planes one chunk's blocks touch (x) stay
+// within ~mb MB of L2 across the class's D^2 colours (0: whole grid).  IGA2L_S3D_ZCHUNK_MB (read per call;
+// default 0 = off): measured SLOWER at C5 (48 MB: 194 vs 179 ms per sweep; the colour kernels are not bound
+// by the DRAM re-streaming, and the chunks' partial waves cost more than the L2 hits save).
+int zchunk_centres(const iga2l_ctx *c) {
+  const char *e = std::getenv("IGA2L_S3D_ZCHUNK_MB");
+  const double mb = (e && *e) ? std::atof(e) : 0.0;
+  const double plane = double(c->n1) * double(c->n1) * 8.0;
+  if (c->dim != 3 || mb <= 0.0 || 2.0 * plane * double(c->n1) <= 2.0 * mb * 1048576.0) return 0;
+  const int span = c->s + 2 * c->p;                              // planes of one block's window
+  const int planes = int(mb * 1048576.0 / plane);
+  return std::max(1, (planes - span) / c->D + 1);
+}
+
 void L_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
+  const int zc = zchunk_centres(c);
+  if (zc > 0) {
+    // Colour-major order inside each last-axis class, chunk by chunk: blocks of one class whose centres
+    // differ in z are >= D apart, hence A-decoupled across ALL the class's colours (reading A4), so this is
+    // the same sweep (bitwise) with each chunk's planes L2-resident while its D^2 colours run.
+    const int D = c->D, D2 = D * D;
+    for (int cls = c0 / D2; cls * D2 < c1; ++cls) {
+      const int a = std::max(c0, cls * D2), e = std::min(c1, (cls + 1) * D2);
+      const int nz = int((c->n1 - cls + D - 1) / D);               // centres of this class
+      const int nch = (nz + zc - 1) / zc, zcb = (nz + nch - 1) / nch;   // balanced chunks
+      for (int k0 = 0; k0 < nz; k0 += zcb) {
+        const SlabView sv{0, cls + D * k0, int(std::min<int64_t>(c->n1, cls + int64_t(D) * (k0 + zcb)))};
+        for (int col = a; col < e; ++col) {
+          if (!launch_schwarz_colour_fast(3, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, D, c->st, sv,
+                                          c->frags, &c->toe, c->ax))
+            launch_schwarz_colour(3, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, D, c->st, sv, c->ax);
+          c->launch_counter++;
+        }
+      }
+    }
+    return;
+  }
   for (int col = c0; col < c1; ++col) {
     if (!launch_schwarz_colour_fast(c->dim, c->p, c->s, c->n1, c->K1, c->M1, c->V, c->lam, b, x, col, c->D, c->st,
                                     kFull, c->frags, &c->toe, c->ax))

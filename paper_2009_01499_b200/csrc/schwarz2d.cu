@@ -410,7 +410,8 @@ __device__ __forceinline__ void mma_colour_block(double *__restrict__ X, int bid
                                                  const double *__restrict__ M, const double *__restrict__ Vt,
                                                  const double *__restrict__ lamt, const double *__restrict__ b,
                                                  double *__restrict__ x, int c0, int c1, int D, int nb0, int nblk,
-                                                 int zoff, const double *__restrict__ fb, int tlo, int thi, int ax) {
+                                                 int zoff, const double *__restrict__ fb, int tlo, int thi, int ax,
+                                                 int trig = -1) {
   using G = Mma2<P, S>;
   constexpr int Wn = G::Wn, w = G::w, MT = G::MT, WN4 = G::WN4, LDX = G::LDX;
   const int lane = threadIdx.x & 31;
@@ -419,17 +420,8 @@ __device__ __forceinline__ void mma_colour_block(double *__restrict__ X, int bid
   const int cx = c0 + D * j0, cy = c1 + D * j1;
   const int bx = cx - w, by = cy - w, ox = bx - P, oy = by - P;
   const unsigned un = unsigned(n1);
-  // zero-padded window through registers: every lane issues all its loads back to back, then stores
-  // (measured: 8-byte cp.async copies cost ~95 issue cycles per window row, 1.2-3k cycles per block)
-  constexpr int WT = MT * 8 * WN4, WI = (WT + 31) / 32;
-  double wv[WI];
-#pragma unroll
-  for (int k = 0; k < WI; ++k) {
-    const int i = lane + 32 * k, row = i / WN4, cc = i - row * WN4;
-    const int gx = ox + cc, gy = oy + row;
-    const bool ok = i < WT && row < Wn && cc < Wn && unsigned(gx) < un && unsigned(gy) < un;
-    wv[k] = ok ? x[(int64_t)(gy - zoff) * n1 + gx] : 0.0;
-  }
+  // operand fragments first: they do not depend on x, so under programmatic dependent launch (PDL) they
+  // load while the previous colour's grid is still running
   FragX<P, S> fx;
   FragY<P, S> fy;
   const bool interior = fb && cx - w >= tlo && cx + w <= thi && cy - w >= tlo && cy + w <= thi;
@@ -444,12 +436,27 @@ __device__ __forceinline__ void mma_colour_block(double *__restrict__ X, int bid
       build_fragy<P, S>(fy, n1, cy, K, M, Vt, lamt);
     }
   }
+  // x of the previous colour: wait for the prerequisite grid (no-op without PDL)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (trig == 3) asm volatile("griddepcontrol.launch_dependents;");   // IGA2L_PDL=4
+  // zero-padded window through registers: every lane issues all its loads back to back, then stores
+  // (measured: 8-byte cp.async copies cost ~95 issue cycles per window row, 1.2-3k cycles per block)
+  constexpr int WT = MT * 8 * WN4, WI = (WT + 31) / 32;
+  double wv[WI];
+#pragma unroll
+  for (int k = 0; k < WI; ++k) {
+    const int i = lane + 32 * k, row = i / WN4, cc = i - row * WN4;
+    const int gx = ox + cc, gy = oy + row;
+    const bool ok = i < WT && row < Wn && cc < Wn && unsigned(gx) < un && unsigned(gy) < un;
+    wv[k] = ok ? x[(int64_t)(gy - zoff) * n1 + gx] : 0.0;
+  }
 #pragma unroll
   for (int k = 0; k < WI; ++k) {
     const int i = lane + 32 * k, row = i / WN4, cc = i - row * WN4;
     if (i < WT) X[row * LDX + cc] = wv[k];
   }
   __syncwarp();
+  if (trig == 1) asm volatile("griddepcontrol.launch_dependents;");
   mma_block_f<P, S>(X, LDX, Pab, n1, cx, cy, fx, fy, b, zoff, [&](int ly, int lx, double v) {
     x[(int64_t)(by + ly - zoff) * n1 + bx + lx] = v;
   });
@@ -462,13 +469,26 @@ __global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma(int n1, const double
                                                             const double *__restrict__ lamt,
                                                             const double *__restrict__ b, double *__restrict__ x,
                                                             int c0, int c1, int D, int nb0, int nblk, int zoff,
-                                                            const double *__restrict__ fb, int tlo, int thi, int ax) {
+                                                            const double *__restrict__ fb, int tlo, int thi, int ax,
+                                                            int trig) {
   extern __shared__ double sm[];
+  // PDL: the next colour's grid may launch once every CTA of this one triggered (trig 0: at entry, 1: after the
+  // window is staged, else at exit); it waits (griddepcontrol.wait) for this grid's completion before it reads x
+  if (trig == 0) asm volatile("griddepcontrol.launch_dependents;");
   const int warp = threadIdx.x >> 5;
   const int bid = blockIdx.x * WPC + warp;
   if (bid >= nblk) return;                                   // whole warp exits together
   mma_colour_block<P, S>(sm + warp * Mma2<P, S>::PER, bid, n1, K, M, Vt, lamt, b, x, c0, c1, D, nb0, nblk, zoff, fb,
-                         tlo, thi, ax);
+                         tlo, thi, ax, trig);
+}
+
+// IGA2L_PDL (read per launch): 0 plain launches; else the colour kernels are launched with programmatic
+// stream serialisation and trigger their dependents at entry (1), once the window is staged (2, default:
+// C2 step 0.428 -> 0.365 ms, p = 5 chain 0.340 -> 0.282 ms), at exit (3: 0.392 ms) or right after their own
+// griddepcontrol.wait (4: 0.370 ms).  Entry triggers let every colour's grid launch at once (0.409 ms).
+inline int pdl_mode() {
+  const char *e = std::getenv("IGA2L_PDL");
+  return (e && *e) ? std::atoi(e) : 2;
 }
 
 template <int P, int S, int WPC>
@@ -478,8 +498,26 @@ void launch2d_mma(int64_t n1, const double *K, const double *M, const double *V,
   constexpr size_t sm = sizeof(double) * WPC * Mma2<P, S>::PER;
   ensure_smem(k_schwarz2d_mma<P, S, WPC>, sm);
   const int m = int(n1) - P + 2;
+  const int pm = pdl_mode();
+  if (pm > 0) {                                              // programmatic dependent launch (IGA2L_PDL)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((nblk + WPC - 1) / WPC);
+    cfg.blockDim = dim3(WPC * 32);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, k_schwarz2d_mma<P, S, WPC>, int(n1), K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff,
+                           fb, 2 * P - 1, m - 2 - P, ax, pm - 1) == cudaSuccess)
+      return;
+    cudaGetLastError();                                      // not launched: plain launch below
+  }
   k_schwarz2d_mma<P, S, WPC><<<(nblk + WPC - 1) / WPC, WPC * 32, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, D,
-                                                                           nb0, nblk, zoff, fb, 2 * P - 1, m - 2 - P, ax);
+                                                                           nb0, nblk, zoff, fb, 2 * P - 1, m - 2 - P, ax,
+                                                                           -1);
 }
 
 template <int P, int S>

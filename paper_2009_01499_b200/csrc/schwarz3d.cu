@@ -441,6 +441,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_w(int n1, const dou
   double r[S];
 #pragma unroll
   for (int lz = 0; lz < S; ++lz) r[lz] = 0.0;
+  asm volatile("griddepcontrol.wait;" ::: "memory");              // PDL: the previous colour's x (no-op otherwise)
   // x-row of pass-x task t of group gi (zero outside the domain)
   auto load_row = [&](int gi, int t, double (&v)[Wn]) {
     const int jj = t / Wn, yy = t - jj * Wn;
@@ -497,6 +498,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_w(int n1, const dou
       }
     }
     __syncwarp();
+    if (gi == 0) asm volatile("griddepcontrol.launch_dependents;");   // PDL: the next colour may launch
     // ---- pass y over the group's (plane, lx) pencils: Pc = My Pa + Ky Pb, Pe = My Pb (into Pa's area) ----
     {
       const bool act = lane < B::TY;
@@ -657,6 +659,23 @@ void launch_w(int64_t n1, const double *K, const double *M, const double *V, con
               cudaStream_t st, const ToeP &tp) {
   constexpr size_t sm = sizeof(double) * BW<P, S, G>::PERW * NW;
   ensure_smem(k_schwarz3d_w<P, S, G, NW, MINB, LV>, sm);
+  const char *e = std::getenv("IGA2L_PDL");
+  if (!(e && e[0] == '0')) {                                   // programmatic dependent launch (as 2D)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((nblk + NW - 1) / NW);
+    cfg.blockDim = dim3(32 * NW);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, k_schwarz3d_w<P, S, G, NW, MINB, LV>, int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0,
+                           nb1, nblk, zoff, tlo, thi, tp) == cudaSuccess)
+      return;
+    cudaGetLastError();
+  }
   k_schwarz3d_w<P, S, G, NW, MINB, LV><<<(nblk + NW - 1) / NW, 32 * NW, sm, st>>>(
       int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nblk, zoff, tlo, thi, tp);
 }

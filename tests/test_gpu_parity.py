@@ -338,6 +338,50 @@ def test_3d_sweep_variants(cfg, monkeypatch):
         assert np.abs(outs[key] - xo).max() <= 1e-11 * np.abs(xo).max(), key
 
 
+@pytest.mark.parametrize("cfg", [PAR[2], PAR[4], PAR[5]], ids=["2d_p3", "2d_p5", "2d_p8"])
+def test_2d_sweep_pdl_modes_bitwise(cfg, monkeypatch):
+    """2D DMMA colour kernels with programmatic dependent launch (IGA2L_PDL = 1, 2, 3, 4: trigger at entry,
+    after the window is staged, at exit, after the grid dependency wait) and without (0): the same arithmetic, bitwise equal sweeps; a
+    sweep in a CUDA graph (the iteration's launch mode) equal to the eager one."""
+    name, d, p, q, m, s, coarse, hf = cfg
+    ctx = make_ctx(d, p, q, m, s, coarse, hf)
+    b, x0 = cu(random_rhs(ctx.N)), cu(initial_guess(ctx.N))
+    outs = []
+    for v in ("0", "1", "2", "3", "4"):
+        monkeypatch.setenv("IGA2L_PDL", v)
+        x = x0.clone()
+        ctx.sweep(b, x)
+        outs.append(host(x))
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
+    monkeypatch.delenv("IGA2L_PDL", raising=False)
+    x = x0.clone()
+    ctx.sweep(b, x)
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=STREAM):
+        ctx.sweep(b, x)
+    x.copy_(x0)
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(outs[0], host(x))
+
+
+@pytest.mark.parametrize("mb", ["0.05", "0.2"])
+def test_3d_sweep_zchunk_schedule_bitwise(mb, monkeypatch):
+    """The z-chunked class schedule (IGA2L_S3D_ZCHUNK_MB) reorders colours only across A-decoupled blocks of
+    one last-axis class (reading A4): the swept iterate is bitwise the colour-major one."""
+    ctx = make_ctx(3, 5, 2, 24, 5, "vcycle", 2)
+    b, x0 = cu(random_rhs(ctx.N)), cu(initial_guess(ctx.N))
+    outs = []
+    for v in ("0", mb):
+        monkeypatch.setenv("IGA2L_S3D_ZCHUNK_MB", v)
+        x = x0.clone()
+        ctx.sweep(b, x)
+        outs.append(host(x))
+    assert np.array_equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("p,m", [(3, 20), (5, 12)])
 @pytest.mark.parametrize("env", [{"IGA2L_APPLY_STREAM": "0"}, {"IGA2L_STREAM_CFG": "1"}, {"IGA2L_STREAM_CFG": "2"},
                                  {"IGA2L_STREAM_CFG": "3"}], ids=["tiled", "cfg1", "cfg2", "cfg3"])
