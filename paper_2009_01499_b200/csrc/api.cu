@@ -815,8 +815,10 @@ int iga2l_setup_ex(int dim, int p, int q, int64_t n, int block, int overlap, con
   if (dim == 2 && !annulus) {   // interior-block fragments for the DMMA colour kernel (A27)
     const int nf = export_interior_frags(p, block, n1, c->K1, c->M1, c->V, c->lam, nullptr, nullptr);
     if (nf > 0) {
-      if ((rc = dalloc(c, &c->frags, nf))) return bail(rc);
+      const int nc = export_centre_frags(p, block, n1, c->K1, c->M1, c->V, c->lam, nullptr, nullptr);
+      if ((rc = dalloc(c, &c->frags, nf + std::max(nc, 0)))) return bail(rc);
       export_interior_frags(p, block, n1, c->K1, c->M1, c->V, c->lam, c->frags, nullptr);
+      if (nc > 0) export_centre_frags(p, block, n1, c->K1, c->M1, c->V, c->lam, c->frags + nf, nullptr);
       if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(IGA2L_ECUDA, "fragment export"));
     }
   }

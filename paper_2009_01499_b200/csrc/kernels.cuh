@@ -101,6 +101,10 @@ bool launch_schwarz3d_colour(int p, int s, int64_t n1, const double *K, const do
 // out == nullptr returns the number of doubles needed; -1 if no interior block or (p, s) not specialised.
 int export_interior_frags(int p, int s, int64_t n1, const double *K, const double *M, const double *V,
                           const double *lam, double *out, cudaStream_t st);
+// Operand fragments of every x-centre ([n1][NX][32]) then every y-centre ([n1][NY][32]) for k_schwarz2d_mmg,
+// written to out (device) right after the interior fragments; out == nullptr: count only; -1 if not specialised.
+int export_centre_frags(int p, int s, int64_t n1, const double *K, const double *M, const double *V,
+                        const double *lam, double *out, cudaStream_t st);
 // 2D tensor transfer out (+)= (By ⊗ B) in in one launch (in: B.cols^2, out: B.rows^2).
 // (optional: input rows valid in [iylo, iyhi) stored from iyoff; output rows [rylo, ryhi) stored from ryoff)
 // By: the y-axis band if it differs from the x-axis one (per-axis transfers of the quarter annulus).

@@ -285,10 +285,66 @@ __device__ __forceinline__ void build_fragy(FragY<P, S> &f, int n1, int cy, cons
   f.lam = r4 < S ? __ldg(lamt + (int64_t)cy * S + r4) : 1.0;
 }
 
+// Fragment accessors: operands held in registers (FragX/FragY) or read per use from memory in the
+// lane-major export layout ([k][32], FragX/FragY member order) -- the latter keeps a block's ~70 operand
+// registers free (k_schwarz2d_mmg).
+template <int P, int S>
+struct FxReg {
+  const FragX<P, S> &f;
+  __device__ double bx(int kt, int nt) const { return f.bxf[kt][nt]; }
+  __device__ double vb(int k) const { return f.vxb[k]; }
+  __device__ double vtb(int k) const { return f.vxtb[k]; }
+  __device__ double lam(int i) const { return f.lam[i]; }
+};
+template <int P, int S>
+struct FyReg {
+  const FragY<P, S> &f;
+  __device__ double ay(int k) const { return f.ayf[k]; }
+  __device__ double vta(int k) const { return f.vyta[k]; }
+  __device__ double va(int k) const { return f.vya[k]; }
+  __device__ double lam() const { return f.lam; }
+};
+template <int P, int S>
+struct FxMem {
+  const double *p;
+  int lane;
+  static constexpr int NTX = Mma2<P, S>::NTX, KT = Mma2<P, S>::KT, KF = Mma2<P, S>::KF;
+  __device__ double at(int k) const { return __ldg(p + k * 32 + lane); }
+  __device__ double bx(int kt, int nt) const { return at(kt * NTX + nt); }
+  __device__ double vb(int k) const { return at(KT * NTX + k); }
+  __device__ double vtb(int k) const { return at(KT * NTX + KF + k); }
+  __device__ double lam(int i) const { return at(KT * NTX + 2 * KF + i); }
+};
+template <int P, int S>
+struct FyMem {
+  const double *p;
+  int lane;
+  static constexpr int KY = Mma2<P, S>::KY, KF = Mma2<P, S>::KF;
+  __device__ double at(int k) const { return __ldg(p + k * 32 + lane); }
+  __device__ double ay(int k) const { return at(k); }
+  __device__ double vta(int k) const { return at(KY + k); }
+  __device__ double va(int k) const { return at(KY + KF + k); }
+  __device__ double lam() const { return at(KY + 2 * KF); }
+};
+
+// ALIAS: Pab overlays the window X (rows of Pab trail the rows of X that pass x has consumed); the block's
+// own x values are read before pass x.
+template <int P, int S, bool ALIAS = false, class FXA, class FYA, class OUT>
+__device__ __forceinline__ void mma_block_a(const double *Xw, int ldx, double *Pab, int n1, int cx, int cy,
+                                            const FXA &fx, const FYA &fy, const double *__restrict__ b, int zoff,
+                                            OUT out);
+
 template <int P, int S, class OUT>
 __device__ __forceinline__ void mma_block_f(const double *Xw, int ldx, double *Pab, int n1, int cx, int cy,
                                             const FragX<P, S> &fx, const FragY<P, S> &fy,
                                             const double *__restrict__ b, int zoff, OUT out) {
+  mma_block_a<P, S, false>(Xw, ldx, Pab, n1, cx, cy, FxReg<P, S>{fx}, FyReg<P, S>{fy}, b, zoff, out);
+}
+
+template <int P, int S, bool ALIAS, class FXA, class FYA, class OUT>
+__device__ __forceinline__ void mma_block_a(const double *Xw, int ldx, double *Pab, int n1, int cx, int cy,
+                                            const FXA &fx, const FYA &fy, const double *__restrict__ b, int zoff,
+                                            OUT out) {
   using G = Mma2<P, S>;
   constexpr int Wn = G::Wn, w = G::w, MT = G::MT, KT = G::KT, NTX = G::NTX, WN4 = G::WN4, LDP = G::LDP,
                 KY = G::KY, KF = G::KF;
@@ -299,9 +355,18 @@ __device__ __forceinline__ void mma_block_f(const double *Xw, int ldx, double *P
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const int j = 2 * q4 + i;
-    rden[i] = (r4 < S && j < S) ? 1.0 / (fx.lam[i] + fy.lam) : 0.0;
+    rden[i] = (r4 < S && j < S) ? 1.0 / (fx.lam(i) + fy.lam()) : 0.0;
     const int gx = bx + j, gy = by + r4;
     bb[i] = (r4 < S && j < S && unsigned(gx) < un && unsigned(gy) < un) ? __ldg(b + (int64_t)(gy - zoff) * n1 + gx) : 0.0;
+  }
+  double xc[2] = {0.0, 0.0};                                 // the block's own x (ALIAS: before Pab overlays X)
+  if constexpr (ALIAS) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int lx = 2 * q4 + i;
+      if (r4 < S && lx < S) xc[i] = Xw[(r4 + P) * ldx + lx + P];
+    }
+    __syncwarp();                                              // other lanes' Pab stores overwrite these rows
   }
   // ---- pass x ----
 #pragma unroll
@@ -313,7 +378,7 @@ __device__ __forceinline__ void mma_block_f(const double *Xw, int ldx, double *P
     for (int kt = 0; kt < KT; ++kt) {
       const double a = Xw[(8 * mt + r4) * ldx + 4 * kt + q4];
 #pragma unroll
-      for (int nt = 0; nt < NTX; ++nt) dmma(acc[nt][0], acc[nt][1], a, fx.bxf[kt][nt]);
+      for (int nt = 0; nt < NTX; ++nt) dmma(acc[nt][0], acc[nt][1], a, fx.bx(kt, nt));
     }
 #pragma unroll
     for (int nt = 0; nt < NTX; ++nt) {
@@ -330,33 +395,33 @@ __device__ __forceinline__ void mma_block_f(const double *Xw, int ldx, double *P
     const bool second = r >= WN4;
     const int rr = second ? r - WN4 : r;
     const double bv = (lx < S && rr < Wn) ? Pab[rr * LDP + (second ? S : 0) + lx] : 0.0;
-    if (kt & 1) dmma(s0, s1, fy.ayf[kt], bv);
-    else dmma(r0, r1, fy.ayf[kt], bv);
+    if (kt & 1) dmma(s0, s1, fy.ay(kt), bv);
+    else dmma(r0, r1, fy.ay(kt), bv);
   }
   r0 = (r4 < S && 2 * q4 < S) ? bb[0] - (r0 + s0) : 0.0;
   r1 = (r4 < S && 2 * q4 + 1 < S) ? bb[1] - (r1 + s1) : 0.0;
   // ---- FD: T = R Vx;  Z = Vy^T T ./ den;  U = Z Vx^T;  δ = Vy U ----
   double t0 = 0.0, t1 = 0.0;
 #pragma unroll
-  for (int kt = 0; kt < KF; ++kt) dmma(t0, t1, c_elem(r0, r1, r4, 4 * kt + q4), fx.vxb[kt]);
+  for (int kt = 0; kt < KF; ++kt) dmma(t0, t1, c_elem(r0, r1, r4, 4 * kt + q4), fx.vb(kt));
   double z0 = 0.0, z1 = 0.0;
 #pragma unroll
-  for (int kt = 0; kt < KF; ++kt) dmma(z0, z1, fy.vyta[kt], c_elem(t0, t1, 4 * kt + q4, r4));
+  for (int kt = 0; kt < KF; ++kt) dmma(z0, z1, fy.vta(kt), c_elem(t0, t1, 4 * kt + q4, r4));
   z0 *= rden[0];
   z1 *= rden[1];
   double u0 = 0.0, u1 = 0.0;
 #pragma unroll
-  for (int kt = 0; kt < KF; ++kt) dmma(u0, u1, c_elem(z0, z1, r4, 4 * kt + q4), fx.vxtb[kt]);
+  for (int kt = 0; kt < KF; ++kt) dmma(u0, u1, c_elem(z0, z1, r4, 4 * kt + q4), fx.vtb(kt));
   double e0 = 0.0, e1 = 0.0;
 #pragma unroll
-  for (int kt = 0; kt < KF; ++kt) dmma(e0, e1, fy.vya[kt], c_elem(u0, u1, 4 * kt + q4, r4));
+  for (int kt = 0; kt < KF; ++kt) dmma(e0, e1, fy.va(kt), c_elem(u0, u1, 4 * kt + q4, r4));
   // ---- x_B += δ ----
   const int ly = r4, gy = by + ly;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const int lx = 2 * q4 + i, gx = bx + lx;
     if (ly < S && lx < S && unsigned(gx) < un && unsigned(gy) < un)
-      out(ly, lx, Xw[(ly + P) * ldx + lx + P] + (i ? e1 : e0));
+      out(ly, lx, (ALIAS ? xc[i] : Xw[(ly + P) * ldx + lx + P]) + (i ? e1 : e0));
   }
 }
 
@@ -486,6 +551,81 @@ __global__ void __launch_bounds__(WPC * 32) k_schwarz2d_mma(int n1, const double
 // stream serialisation and trigger their dependents at entry (1), once the window is staged (2, default:
 // C2 step 0.428 -> 0.365 ms, p = 5 chain 0.340 -> 0.282 ms), at exit (3: 0.392 ms) or right after their own
 // griddepcontrol.wait (4: 0.370 ms).  Entry triggers let every colour's grid launch at once (0.409 ms).
+// ---- k_schwarz2d_mmg: the same block solve with the operand fragments read per use from memory ----------
+// (interior axes: the shared export, A27; boundary axes: the per-centre export) and Pab overlaying the
+// window: ~60 instead of ~125 registers and 4.7 KB of shared memory per block at p = 8, so a colour of C3's
+// 4692 blocks fits ONE wave (32 warps per SM) instead of two.  fb: [interior NX+NY][32] then
+// [n1][NX][32] (FragX per x-centre) then [n1][NY][32] (FragY per y-centre), export_centre_frags.
+template <int P, int S, int WPC, int MINB>
+__global__ void __launch_bounds__(WPC * 32, MINB) k_schwarz2d_mmg(int n1, const double *__restrict__ b,
+                                                                  double *__restrict__ x, int c0, int c1, int D,
+                                                                  int nb0, int nblk, int zoff,
+                                                                  const double *__restrict__ fb, int tlo, int thi,
+                                                                  int trig) {
+  using G = Mma2<P, S>;
+  constexpr int Wn = G::Wn, w = G::w, MT = G::MT, WN4 = G::WN4, LDX = G::LDX;
+  constexpr int NX = sizeof(FragX<P, S>) / sizeof(double), NY = sizeof(FragY<P, S>) / sizeof(double);
+  extern __shared__ double sm[];
+  if (trig == 0) asm volatile("griddepcontrol.launch_dependents;");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bid = blockIdx.x * WPC + warp;
+  if (bid >= nblk) return;
+  double *X = sm + warp * (MT * 8 * LDX);
+  const int j1 = bid / nb0, j0 = bid - j1 * nb0;
+  const int cx = c0 + D * j0, cy = c1 + D * j1;
+  const int bx = cx - w, by = cy - w, ox = bx - P, oy = by - P;
+  const unsigned un = unsigned(n1);
+  const double *fxall = fb + (NX + NY) * 32, *fyall = fxall + int64_t(n1) * NX * 32;
+  const bool ix = cx - w >= tlo && cx + w <= thi, iy = cy - w >= tlo && cy + w <= thi;
+  const FxMem<P, S> fx{ix ? fb : fxall + int64_t(cx) * NX * 32, lane};
+  const FyMem<P, S> fy{iy ? fb + NX * 32 : fyall + int64_t(cy) * NY * 32, lane};
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (trig == 3) asm volatile("griddepcontrol.launch_dependents;");
+  constexpr int WT = MT * 8 * WN4, WI = (WT + 31) / 32;
+  double wv[WI];
+#pragma unroll
+  for (int k = 0; k < WI; ++k) {
+    const int i = lane + 32 * k, row = i / WN4, cc = i - row * WN4;
+    const int gx = ox + cc, gy = oy + row;
+    const bool ok = i < WT && row < Wn && cc < Wn && unsigned(gx) < un && unsigned(gy) < un;
+    wv[k] = ok ? x[(int64_t)(gy - zoff) * n1 + gx] : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < WI; ++k) {
+    const int i = lane + 32 * k, row = i / WN4, cc = i - row * WN4;
+    if (i < WT) X[row * LDX + cc] = wv[k];
+  }
+  __syncwarp();
+  if (trig == 1) asm volatile("griddepcontrol.launch_dependents;");
+  mma_block_a<P, S, true>(X, LDX, X, n1, cx, cy, fx, fy, b, zoff, [&](int ly, int lx, double v) {
+    x[(int64_t)(by + ly - zoff) * n1 + bx + lx] = v;
+  });
+}
+
+template <int P, int S>
+__global__ void k_export_cfrags(int n1, const double *__restrict__ K, const double *__restrict__ M,
+                                const double *__restrict__ Vt, const double *__restrict__ lamt, double *outx,
+                                double *outy) {
+  const int c = blockIdx.x, lane = threadIdx.x;
+  FragX<P, S> fx;
+  FragY<P, S> fy;
+  build_fragx<P, S>(fx, n1, c, K, M, Vt, lamt);
+  build_fragy<P, S>(fy, n1, c, K, M, Vt, lamt);
+  const double *a = reinterpret_cast<const double *>(&fx), *d = reinterpret_cast<const double *>(&fy);
+  constexpr int NX = sizeof(FragX<P, S>) / sizeof(double), NY = sizeof(FragY<P, S>) / sizeof(double);
+#pragma unroll
+  for (int k = 0; k < NX; ++k) outx[(int64_t(c) * NX + k) * 32 + lane] = a[k];
+#pragma unroll
+  for (int k = 0; k < NY; ++k) outy[(int64_t(c) * NY + k) * 32 + lane] = d[k];
+}
+
+// IGA2L_MMG (read per launch): 1 / 0 force / forbid k_schwarz2d_mmg; default: when the colour has more
+// blocks than one wave of k_schwarz2d_mma (16 one-warp blocks per SM) and the centre fragments exist
+inline int mmg_mode() {
+  const char *e = std::getenv("IGA2L_MMG");
+  return (e && *e) ? std::atoi(e) : -1;
+}
+
 inline int pdl_mode() {
   const char *e = std::getenv("IGA2L_PDL");
   return (e && *e) ? std::atoi(e) : 2;
@@ -495,10 +635,30 @@ template <int P, int S, int WPC>
 void launch2d_mma(int64_t n1, const double *K, const double *M, const double *V, const double *lam, const double *b,
                   double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st, const double *fb,
                   int ax) {
-  constexpr size_t sm = sizeof(double) * WPC * Mma2<P, S>::PER;
-  ensure_smem(k_schwarz2d_mma<P, S, WPC>, sm);
   const int m = int(n1) - P + 2;
   const int pm = pdl_mode();
+  const int mg = mmg_mode();
+  if (fb && !ax && (mg == 1 || (mg < 0 && nblk > 148 * 16))) {   // fragments from memory (k_schwarz2d_mmg)
+    constexpr int MW = 8, MB = 4;
+    constexpr size_t smg = sizeof(double) * MW * Mma2<P, S>::MT * 8 * Mma2<P, S>::LDX;
+    ensure_smem(k_schwarz2d_mmg<P, S, MW, MB>, smg);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((nblk + MW - 1) / MW);
+    cfg.blockDim = dim3(MW * 32);
+    cfg.dynamicSmemBytes = smg;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pm > 0 ? 1 : 0;
+    if (cudaLaunchKernelEx(&cfg, k_schwarz2d_mmg<P, S, MW, MB>, int(n1), b, x, c0, c1, D, nb0, nblk, zoff, fb, 2 * P - 1,
+                           m - 2 - P, pm > 0 ? pm - 1 : -1) == cudaSuccess)
+      return;
+    cudaGetLastError();
+  }
+  constexpr size_t sm = sizeof(double) * WPC * Mma2<P, S>::PER;
+  ensure_smem(k_schwarz2d_mma<P, S, WPC>, sm);
   if (pm > 0) {                                              // programmatic dependent launch (IGA2L_PDL)
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((nblk + WPC - 1) / WPC);
@@ -592,6 +752,21 @@ bool launch_schwarz_colour_fast(int dim, int p, int s, int64_t n1, const double 
          try_schwarz2d_mma<6, 5>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb, ax) ||
          try_schwarz2d_mma<7, 7>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb, ax) ||
          try_schwarz2d_mma<8, 7>(p, s, n1, K, M, V, lam, b, x, c0, f1, D, nb0, nblk, z, st, fb, ax);
+}
+
+int export_centre_frags(int p, int s, int64_t n1, const double *K, const double *M, const double *V,
+                        const double *lam, double *out, cudaStream_t st) {
+#define IGA2L_EXPC(P_, S_)                                                                                  \
+  if (p == P_ && s == S_) {                                                                                 \
+    constexpr int NX = sizeof(FragX<P_, S_>) / sizeof(double), NY = sizeof(FragY<P_, S_>) / sizeof(double); \
+    if (out)                                                                                                \
+      k_export_cfrags<P_, S_><<<int(n1), 32, 0, st>>>(int(n1), K, M, V, lam, out, out + n1 * NX * 32);    \
+    return int(n1 * (NX + NY) * 32);                                                                        \
+  }
+  IGA2L_EXPC(1, 3) IGA2L_EXPC(2, 3) IGA2L_EXPC(3, 3) IGA2L_EXPC(4, 3) IGA2L_EXPC(5, 5) IGA2L_EXPC(6, 5)
+  IGA2L_EXPC(7, 7) IGA2L_EXPC(8, 7)
+#undef IGA2L_EXPC
+  return -1;
 }
 
 int export_interior_frags(int p, int s, int64_t n1, const double *K, const double *M, const double *V,

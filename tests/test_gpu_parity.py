@@ -367,6 +367,26 @@ def test_2d_sweep_pdl_modes_bitwise(cfg, monkeypatch):
     assert np.array_equal(outs[0], host(x))
 
 
+@pytest.mark.parametrize("cfg", [PAR[2], PAR[3], PAR[4], PAR[5]], ids=["2d_p3", "2d_p4", "2d_p5", "2d_p8"])
+def test_2d_sweep_mmg_bitwise(cfg, monkeypatch):
+    """k_schwarz2d_mmg (operand fragments read per use from the interior / per-centre exports, Pab over the
+    window; the default for colours larger than one wave) and k_schwarz2d_mma (fragments in registers): the
+    same DMMA sequence on the same operands -> bitwise equal sweeps, equal to the oracle's sweep."""
+    name, d, p, q, m, s, coarse, hf = cfg
+    ctx = make_ctx(d, p, q, m, s, coarse, hf)
+    b, x0 = random_rhs(ctx.N), initial_guess(ctx.N)
+    outs = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("IGA2L_MMG", v)
+        x = cu(x0)
+        ctx.sweep(cu(b), x)
+        outs.append(host(x))
+    assert np.array_equal(outs[0], outs[1])
+    xo = x0.copy()
+    oracle_for(*cfg).smoother.sweep(xo, b)
+    assert np.abs(outs[1] - xo).max() <= 1e-11 * np.abs(xo).max()
+
+
 @pytest.mark.parametrize("mb", ["0.05", "0.2"])
 def test_3d_sweep_zchunk_schedule_bitwise(mb, monkeypatch):
     """The z-chunked class schedule (IGA2L_S3D_ZCHUNK_MB) reorders colours only across A-decoupled blocks of
