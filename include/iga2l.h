@@ -129,6 +129,21 @@ int iga2l_residual_norm(iga2l_ctx *ctx, const double *b, const double *x, double
 int iga2l_iterate(iga2l_ctx *ctx, const double *b, double *x, int iters, double *res_hist);
 
 /*
+ * Torus LFA run: the spectral radius of the two-grid error operator
+ * E = (I - P A_q^+ R A_p) S_p of the multicolour method (reading A4) on the dim = 2, n x n
+ * PERIODIC grid, by `iters` power iterations with the library's kernels from a seeded mean-zero start
+ * (the constant, E 1 = 1, projected out: LFA excludes it).  h_factor 1: exact degree-q level on the
+ * same mesh (Table 1's ρ_2g); 2: aggressive, degree q on H = 2h (Table 3's ρ_2g^ag).  With n = nk (s + p),
+ * nk even, the torus frequencies are the Bloch quasi-momenta of an nk^2 LFA grid.  Synchronous; allocates
+ * and frees its own device memory on the current device.
+ * rho (host): geometric mean of the last quarter of the norm ratios; ratios (host, NULL or `iters`
+ * doubles): every ratio.  Errors: IGA2L_EPARAM (dim != 2, n not a multiple of s + p or < 2(s + p), n /
+ * h_factor < 2q + 1, iters outside 4..100000, ...), IGA2L_ENUMERIC, IGA2L_ECUDA, IGA2L_ENOMEM.
+ */
+int iga2l_lfa_torus(int dim, int p, int q, int n, int block, int h_factor, int iters, unsigned long long seed,
+                    double *rho, double *ratios);
+
+/*
  * Iterate until ||b - A x_k|| <= rtol ||b - A x_0|| or maxit iterations.
  * iters_out / relres_out (host, may be NULL) receive the count and ||r_k||/||r_0||.
  * Returns IGA2L_NOTCONV (outputs valid) if maxit was reached, IGA2L_ENUMERIC on NaN/Inf.

@@ -61,6 +61,7 @@ def lib():
         "iga2l_apply": (i, [vp, vp, vp]),
         "iga2l_residual_norm": (i, [vp, vp, vp, P(d)]),
         "iga2l_iterate": (i, [vp, vp, vp, i, vp]),
+        "iga2l_lfa_torus": (i, [i, i, i, i, i, i, i, ctypes.c_ulonglong, vp, vp]),
         "iga2l_solve": (i, [vp, vp, vp, d, i, P(i), P(d)]),
         "iga2l_sweep": (i, [vp, vp, vp, i, i]),
         "iga2l_defect_restrict": (i, [vp, vp, vp, vp]),
@@ -180,6 +181,16 @@ def host_annulus_load(p, m):
     b = np.zeros((m + p - 2) ** 2)
     _check(lib().iga2l_host_annulus_load(p, m, _ptr(b)))
     return b
+
+
+def lfa_torus(p, q, n, block, h_factor=1, iters=200, seed=0, dim=2, return_ratios=False):
+    """iga2l_lfa_torus: spectral radius of the two-grid error operator on the n x n torus (power iteration
+    with the library's kernels; see the header)."""
+    rho = ctypes.c_double()
+    rat = (ctypes.c_double * iters)()
+    _check(lib().iga2l_lfa_torus(dim, p, q, n, block, h_factor, iters, seed, ctypes.byref(rho),
+                                 ctypes.cast(rat, ctypes.c_void_p)))
+    return (rho.value, list(rat)) if return_ratios else rho.value
 
 
 class Context:

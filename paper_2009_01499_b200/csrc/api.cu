@@ -1040,6 +1040,13 @@ int iga2l_iterate(iga2l_ctx *c, const double *b, double *x, int iters, double *r
   return stage_out(c, x, sx, c->N);
 }
 
+int iga2l_lfa_torus(int dim, int p, int q, int n, int block, int h_factor, int iters, unsigned long long seed,
+                    double *rho, double *ratios) {
+  std::string err;
+  const int rc = lfa_torus_run(dim, p, q, n, block, h_factor, iters, seed, rho, ratios, &err);
+  return rc ? fail(rc, err) : IGA2L_OK;
+}
+
 int iga2l_solve(iga2l_ctx *c, const double *b, double *x, double rtol, int maxit, int *iters_out,
                 double *relres_out) {
   if (int rc = check_ctx(c)) return rc;

@@ -87,7 +87,7 @@ __global__ void k_eig_divide(double *__restrict__ T, const double *__restrict__ 
        idx += (int64_t)gridDim.x * blockDim.x) {
     double den = lam[idx % n] + lam[lys + (idx / n) % n];
     if (dim == 3) den += lam[idx / ((int64_t)n * n)];
-    T[idx] /= den;
+    T[idx] = den != 0.0 ? T[idx] / den : 0.0;   // den == 0 only for the constant mode of a torus (pseudo-inverse)
   }
 }
 

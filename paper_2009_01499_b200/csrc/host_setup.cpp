@@ -560,4 +560,60 @@ bool band_fd_tables(int q, int n, const double *Kb, const double *Mb, std::vecto
   return true;
 }
 
+bool periodic_fd_tables(int q, int n, const double *krow, const double *mrow, std::vector<double> &V,
+                        std::vector<double> &lam) {
+  // circulant K, M (row i: column (i + t - q) mod n holds krow[t], mrow[t]); M = L L^T (dense Cholesky:
+  // the periodic factor fills in), C = L^{-1} K L^{-T} = Q Λ Q^T, V = L^{-T} Q.  K annihilates constants,
+  // so one λ vanishes: it is returned as exactly 0 (the caller's solve uses the pseudo-inverse).
+  const int W = 2 * q + 1;
+  if (n < W) return false;
+  std::vector<double> Kd((size_t)n * n, 0.0), L((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int t = 0; t < W; ++t) {
+      const int j = ((i + t - q) % n + n) % n;
+      Kd[(size_t)i * n + j] += krow[t];
+      L[(size_t)i * n + j] += mrow[t];
+    }
+  if (!cholesky(L, n)) return false;
+  auto fwd = [&](std::vector<double> &B) {            // B <- L^{-1} B (dense lower L)
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) {
+        double sacc = B[(size_t)i * n + j];
+        for (int k = 0; k < i; ++k) sacc -= L[(size_t)i * n + k] * B[(size_t)k * n + j];
+        B[(size_t)i * n + j] = sacc / L[(size_t)i * n + i];
+      }
+  };
+  fwd(Kd);
+  std::vector<double> C((size_t)n * n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) C[(size_t)i * n + j] = Kd[(size_t)j * n + i];
+  fwd(C);
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j) {
+      const double av = 0.5 * (C[(size_t)i * n + j] + C[(size_t)j * n + i]);
+      C[(size_t)i * n + j] = C[(size_t)j * n + i] = av;
+    }
+  std::vector<double> Q;
+  sym_eigen(C, n, Q, lam);
+  double mx = 0.0;
+  for (double l : lam) mx = std::max(mx, std::fabs(l));
+  int nz = 0;
+  for (double &l : lam)
+    if (std::fabs(l) <= 1e-10 * mx) {
+      l = 0.0;
+      ++nz;
+    } else if (l < 0.0) {
+      return false;
+    }
+  if (nz != 1) return false;
+  V = Q;
+  for (int j = 0; j < n; ++j)
+    for (int i = n - 1; i >= 0; --i) {
+      double sacc = V[(size_t)i * n + j];
+      for (int k = i + 1; k < n; ++k) sacc -= L[(size_t)k * n + i] * V[(size_t)k * n + j];
+      V[(size_t)i * n + j] = sacc / L[(size_t)i * n + i];
+    }
+  return true;
+}
+
 }  // namespace iga2l

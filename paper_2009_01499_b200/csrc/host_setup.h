@@ -61,6 +61,11 @@ bool coarse_fd_tables(int q, int64_t m, std::vector<double> &V, std::vector<doub
 // The same from given band tables (bandwidth 2q+1, n rows): K V = M V Λ, V^T M V = I.
 bool band_fd_tables(int q, int n, const double *K, const double *M, std::vector<double> &V, std::vector<double> &lam);
 
+// The same on the n-point TORUS (circulant K, M from one interior band row each, bandwidth 2q+1): the one
+// vanishing eigenvalue (constants) is returned as exactly 0.  False unless M is SPD and exactly one λ vanishes.
+bool periodic_fd_tables(int q, int n, const double *krow, const double *mrow, std::vector<double> &V,
+                        std::vector<double> &lam);
+
 // Dense inverse of the d-dim operator Σ_a ⊗ (K on axis a, M elsewhere) from band tables of
 // degree q (bandwidth 2q+1) on n points per axis.  Returns false if not SPD.  Row-major N x N.
 // ays > 0: per-axis tables, axis a's rows at K[a * ays ...] (the quarter annulus, A = My ⊗ Kx + Ky ⊗ Mx).

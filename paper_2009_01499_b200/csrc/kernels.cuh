@@ -10,6 +10,7 @@
 // memory (2D: 4(2p+1) FMAs/DOF; 3D: 7(2p+1) FMAs/DOF).
 #pragma once
 #include <cstdint>
+#include <string>
 #include <cuda_runtime.h>
 
 namespace iga2l {
@@ -166,6 +167,11 @@ void launch_dgemm(const double *A, const double *B, double *C, int M, int N, int
 // ax = 1 (2D): per-axis decompositions, V [2][n][n], lam [2][n] (x then y; the quarter annulus).
 int launch_coarse_fd(int dim, int n, const double *V, const double *lam, const double *d, double *e, double *t1,
                      double *t2, cudaStream_t st, int ax = 0);
+
+// Torus LFA run (torus.cu): spectral radius of the 2D two-grid error operator on the n x n torus by power
+// iteration with the hot-path kernels.  Returns an IGA2L code; *err set on failure.
+int lfa_torus_run(int dim, int p, int q, int n, int s, int hf, int iters, unsigned long long seed, double *rho,
+                  double *ratios, std::string *err);
 
 // y += x (fixed-order sums of the slab partial coarse vectors in local multi-slab mode)
 void launch_axpy(double *y, const double *x, int64_t n, cudaStream_t st);

@@ -1,0 +1,293 @@
+// Torus LFA run: the two-grid error operator of Algorithm 1 on an n x n
+// PERIODIC grid, applied by the hot-path kernels and power-iterated for its spectral radius.
+//
+// Local Fourier analysis reads the method on the infinite uniform grid, where every operator is
+// a convolution; on the n-point torus the same operators are circulant, and the torus spectrum is the LFA
+// symbol sampled at θ = 2πk/n.  With n = nk (s + p) (nk even) those frequencies are exactly the nk^2 Bloch
+// quasi-momenta the oracle's block LFA (`oracle/lfa.py: rho_2g`, `rho_2g_ag`) samples, so the measured ρ
+// pins the analysis at scale.
+//
+//   E = (I - P A_c^+ R A_p) S_p        (same h, q: Table 1's setting; or H = 2h, Table 3's)
+//
+// * S_p: the multicolour Schwarz sweep (reading A4) by the colour kernels of the Dirichlet path, run on a
+//   padded grid of n + 2G points per axis (G = 2w + p) whose band tables are the interior (Toeplitz, A27)
+//   rows everywhere; after each colour the ghost layers are refreshed from their periodic images.  A block
+//   centred in a ghost layer is the periodic image of a real block of the same colour (n % D == 0) and
+//   writes the same update into the real points it covers; blocks whose windows leave the padded grid
+//   only write ghost points, which the refresh overwrites.
+// * A_p: the residual kernel on the padded grid (b = 0); R = D^{-1} M_c (lumped, A6) and, for
+//   H = 2h, composed with the knot-insertion restriction (A8/A9): periodic band transfers; P = R^T.
+// * A_c^+: Kronecker fast diagonalisation with the circulant 1D eigen-decompositions;
+//   the constant mode (A_c 1 = 0) gets 0 (pseudo-inverse, as LFA excludes θ = 0's constant).
+// * Power iteration from a seeded random mean-zero start; the mean (the constant, E 1 = 1) is projected
+//   out after every application.  ρ = geometric mean of the last quarter of the norm ratios.
+// 2D (the paper's setting; in 3D the rediscretised 2h operator differs from h's by a factor 2 and the
+// padded sweep is the same construction).
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "host_setup.h"
+#include "kernels.cuh"
+
+namespace iga2l {
+namespace {
+
+// ghost layers of an np x np padded array (real block [G, G+n)^2) from their periodic images
+__global__ void k_ghost2d(double *__restrict__ x, int n, int G) {
+  const int np = n + 2 * G;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)np * np;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = int(idx % np), j = int(idx / np);
+    const bool gi = i < G || i >= G + n, gj = j < G || j >= G + n;
+    if (!gi && !gj) continue;
+    const int si = G + ((i - G) % n + n) % n, sj = G + ((j - G) % n + n) % n;
+    x[idx] = x[(int64_t)sj * np + si];
+  }
+}
+
+// compact n x n <-> real block of the padded array; mode 0: pad = c, 1: c = pad
+__global__ void k_pad2d(double *__restrict__ pad, double *__restrict__ c, int n, int G, int mode) {
+  const int np = n + 2 * G;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)n * n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = int(idx % n), j = int(idx / n);
+    double *pp = pad + (int64_t)(j + G) * np + i + G;
+    if (mode == 0) *pp = c[idx];
+    else c[idx] = *pp;
+  }
+}
+
+// periodic band transfer along one axis of a 2D array (x fastest).  Forward (restriction R):
+//   out[i] = Σ_k c[k] in[(ratio i + o0 + k) mod nin], i < nout;
+// transpose (prolongation R^T): out[j] = Σ_{i, k: ratio i + o0 + k ≡ j} c[k] in[i], j < nout (= nin_fwd).
+__global__ void k_pband(const double *__restrict__ in, double *__restrict__ out, int nin, int nout, int other,
+                        int axis, const double *__restrict__ c, int W, int o0, int ratio, int transpose,
+                        int accumulate) {
+  const int64_t total = (int64_t)nout * other;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int a = int(idx % (axis == 0 ? nout : other)), bb = int(idx / (axis == 0 ? nout : other));
+    const int o = axis == 0 ? a : bb, t = axis == 0 ? bb : a;   // o: index along the axis, t: the other one
+    auto at = [&](int k) { return axis == 0 ? in[(int64_t)t * nin + k] : in[(int64_t)k * other + t]; };
+    double acc = 0.0;
+    if (!transpose) {
+      for (int k = 0; k < W; ++k) acc = fma(c[k], at(((ratio * o + o0 + k) % nin + nin) % nin), acc);
+    } else {
+      for (int k = 0; k < W; ++k) {
+        const int r = o - o0 - k;                               // = ratio * i (mod ratio * nin)
+        const int rm = ((r % (ratio * nin)) + ratio * nin) % (ratio * nin);
+        if (rm % ratio) continue;
+        acc = fma(c[k], at(rm / ratio), acc);
+      }
+    }
+    double *op = out + (axis == 0 ? (int64_t)t * nout + o : (int64_t)o * other + t);
+    *op = accumulate ? *op + acc : acc;
+  }
+}
+
+// sum and sum of squares of v[0..N) (one CTA, fixed order)
+__global__ void k_sums(const double *__restrict__ v, int64_t N, double *out) {
+  __shared__ double red[32];
+  double s = 0.0, q = 0.0;
+  for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+    s += v[i];
+    q = fma(v[i], v[i], q);
+  }
+  s = block_sum(s, red);
+  __syncthreads();
+  q = block_sum(q, red);
+  if (threadIdx.x == 0) {
+    out[0] = s;
+    out[1] = q;
+  }
+}
+
+// v = (v - mean) * scale
+__global__ void k_shift_scale(double *__restrict__ v, int64_t N, double mean, double scale) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = (v[i] - mean) * scale;
+}
+
+uint64_t splitmix(uint64_t &st) {
+  uint64_t z = (st += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+struct DevBuf {
+  std::vector<void *> ptrs;
+  ~DevBuf() {
+    for (void *p : ptrs) cudaFree(p);
+  }
+  template <typename T>
+  T *get(size_t n, cudaError_t *e) {
+    void *p = nullptr;
+    *e = cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T));
+    if (*e == cudaSuccess) ptrs.push_back(p);
+    return static_cast<T *>(p);
+  }
+};
+
+}  // namespace
+
+int lfa_torus_run(int dim, int p, int q, int n, int s, int hf, int iters, unsigned long long seed, double *rho,
+                  double *ratios, std::string *err) {
+  auto bad = [&](const std::string &m) {
+    *err = m;
+    return 1;   // IGA2L_EPARAM
+  };
+  if (dim != 2) return bad("the torus run is 2D (dim must be 2)");
+  if (p < 1 || p > 8) return bad("p must be in 1..8");
+  if (q < 1 || q > 2 || q > p) return bad("q must satisfy 1 <= q <= min(p, 2)");
+  if (s != 1 && s != 3 && s != 5 && s != 7) return bad("block must be 1, 3, 5 or 7");
+  if (hf != 1 && hf != 2) return bad("h_factor must be 1 (same h) or 2 (aggressive)");
+  const int D = s + p, w = (s - 1) / 2, W = 2 * p + 1;
+  if (n % D != 0 || n < 2 * D) return bad("n must be a multiple of s + p and at least 2 (s + p)");
+  if (n % hf != 0 || n / hf < 2 * q + 1) return bad("n / h_factor must be an integer >= 2q + 1");
+  if (iters < 4 || iters > 100000) return bad("iters must be in 4..100000");
+  if (!rho) return bad("rho is NULL");
+  // ---- interior (Toeplitz, A27) rows from a Dirichlet grid large enough to have them ----
+  const int64_t mb = 4 * (2 * p + s + 8);
+  std::vector<double> Kb, Mb, Kq, Mq;
+  band_tables(p, mb, Kb, Mb);
+  band_tables(q, mb, Kq, Mq);
+  int64_t lo, hi;
+  toeplitz_rows(p, mb, &lo, &hi);
+  const int64_t rp = (lo + hi) / 2;
+  toeplitz_rows(q, mb, &lo, &hi);
+  const int64_t rq = (lo + hi) / 2;
+  const BandOp R1 = degree_restriction(p, q, mb);
+  const int64_t ir = R1.rows / 2;                         // an interior row: cols ir - q + k, k = 0..p+q
+  // R on the torus (q-function i and p-function j numbered by the cell their support starts in):
+  // row i couples p-columns j = i + k - p with R1's interior coefficients (same h); for H = 2h the knot-
+  // insertion restriction (A8/A9) is folded in: row J = Σ_k' 2^{-q} C(q+1, k') (row 2J + k' at h).
+  std::vector<double> rc;
+  int o0 = -p, ratio = 1;
+  {
+    std::vector<double> r1(R1.W);
+    for (int k = 0; k < R1.W; ++k) r1[k] = R1.c[ir * R1.W + k];
+    if (hf == 1) {
+      rc = r1;
+    } else {
+      ratio = 2;
+      rc.assign(R1.W + q + 1, 0.0);                        // offsets -p .. q + 1 + q
+      double binom = 1.0;
+      for (int kk = 0; kk <= q + 1; ++kk) {
+        const double wgt = binom / double(1 << q);
+        for (int k = 0; k < R1.W; ++k) rc[kk + k] += wgt * r1[k];
+        binom = binom * double(q + 1 - kk) / double(kk + 1);
+      }
+    }
+  }
+  // ---- padded p-grid tables ----
+  const int G = 2 * w + p, np = n + 2 * G;
+  std::vector<double> K((size_t)np * W, 0.0), M((size_t)np * W, 0.0);
+  for (int i = 0; i < np; ++i)
+    for (int t = 0; t < W; ++t) {
+      const int j = i + t - p;
+      if (j < 0 || j >= np) continue;
+      K[(size_t)i * W + t] = Kb[rp * W + t];
+      M[(size_t)i * W + t] = Mb[rp * W + t];
+    }
+  std::vector<double> V, lam;
+  if (!fd_tables(p, s, np, K, M, V, lam)) return bad("block matrices not SPD");
+  ToeP tp{};
+  for (int t = 0; t < W; ++t) {
+    tp.k[t] = Kb[rp * W + t];
+    tp.m[t] = Mb[rp * W + t];
+  }
+  const int cref = np / 2;
+  for (int i = 0; i < s * s; ++i) tp.v[i] = V[(size_t)cref * s * s + i];
+  for (int j = 0; j < s; ++j) tp.lam[j] = lam[(size_t)cref * s + j];
+  tp.valid = 1;
+  // ---- coarse level on the torus ----
+  const int nc = n / hf, Wq = 2 * q + 1;
+  std::vector<double> Vc, lamc;
+  if (!periodic_fd_tables(q, nc, &Kq[rq * Wq], &Mq[rq * Wq], Vc, lamc)) return bad("coarse torus operator");
+  // ---- device ----
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaSuccess;
+  DevBuf buf;
+  const int64_t NP = (int64_t)np * np, N = (int64_t)n * n, NC = (int64_t)nc * nc;
+  double *dK = buf.get<double>(K.size(), &e), *dM = buf.get<double>(M.size(), &e);
+  double *dV = buf.get<double>(V.size(), &e), *dlam = buf.get<double>(lam.size(), &e);
+  double *dVc = buf.get<double>(Vc.size(), &e), *dlamc = buf.get<double>(lamc.size(), &e);
+  double *drc = buf.get<double>(rc.size(), &e);
+  double *xp = buf.get<double>(NP, &e), *zp = buf.get<double>(NP, &e), *rpad = buf.get<double>(NP, &e);
+  double *ec = buf.get<double>(N, &e), *rr = buf.get<double>(N, &e), *tf = buf.get<double>(N, &e);
+  double *dc = buf.get<double>(NC, &e), *xc = buf.get<double>(NC, &e), *t1 = buf.get<double>(NC, &e),
+         *t2 = buf.get<double>(NC, &e), *tc = buf.get<double>((int64_t)nc * n, &e);
+  double *dsum = buf.get<double>(2, &e);
+  const int nfr = export_interior_frags(p, s, np, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+  double *dfb = nfr > 0 ? buf.get<double>(nfr, &e) : nullptr;
+  const int npart = apply_num_partials(2, p, np);
+  double *dpart = buf.get<double>(npart, &e);
+  if (e != cudaSuccess) return (*err = "cudaMalloc failed", 6);
+  auto up = [&](double *d, const std::vector<double> &h) {
+    return cudaMemcpy(d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice);
+  };
+  if (up(dK, K) || up(dM, M) || up(dV, V) || up(dlam, lam) || up(dVc, Vc) || up(dlamc, lamc) || up(drc, rc) ||
+      cudaMemset(zp, 0, NP * sizeof(double)))
+    return (*err = "upload failed", 4);
+  if (dfb) export_interior_frags(p, s, np, dK, dM, dV, dlam, dfb, st);
+  // ---- seeded mean-zero start ----
+  std::vector<double> h0(N);
+  uint64_t sst = seed;
+  double mean = 0.0;
+  for (auto &v : h0) {
+    v = 2.0 * (double(splitmix(sst) >> 11) * (1.0 / 9007199254740992.0)) - 1.0;
+    mean += v;
+  }
+  mean /= double(N);
+  for (auto &v : h0) v -= mean;
+  if (up(ec, h0)) return (*err = "upload failed", 4);
+  const int gN = grid_for(N, 256), gNP = grid_for(NP, 256);
+  std::vector<double> hist;
+  double prev = 0.0;
+  for (int it = 0; it <= iters; ++it) {
+    // normalise (and project out the constant)
+    k_sums<<<1, 1024, 0, st>>>(ec, N, dsum);
+    double hs[2];
+    if (cudaMemcpy(hs, dsum, sizeof(hs), cudaMemcpyDeviceToHost) != cudaSuccess) return (*err = "sums", 4);
+    const double mu = hs[0] / double(N), nrm = std::sqrt(std::max(hs[1] - hs[0] * mu, 0.0));
+    if (!(nrm > 0.0) || !std::isfinite(nrm)) return (*err = "power iteration vector vanished or not finite", 2);
+    if (it > 0) hist.push_back(nrm / prev);
+    if (it == iters) break;
+    k_shift_scale<<<gN, 256, 0, st>>>(ec, N, mu, 1.0 / nrm);
+    prev = 1.0;
+    // x (padded, ghosts) = e
+    k_pad2d<<<gN, 256, 0, st>>>(xp, ec, n, G, 0);
+    k_ghost2d<<<gNP, 256, 0, st>>>(xp, n, G);
+    // S_p: colour by colour, ghosts refreshed after each
+    for (int col = 0; col < D * D; ++col) {
+      if (!launch_schwarz_colour_fast(2, p, s, np, dK, dM, dV, dlam, zp, xp, col, D, st, kFull, dfb, &tp))
+        launch_schwarz_colour(2, p, s, np, dK, dM, dV, dlam, zp, xp, col, D, st, kFull);
+      k_ghost2d<<<gNP, 256, 0, st>>>(xp, n, G);
+    }
+    // r = 0 - A_p x (real block), d_c = R r, e_c = A_c^+ d_c, e = x + R^T e_c
+    int nparts = 0;
+    launch_apply(2, p, np, dK, dM, xp, zp, rpad, nullptr, 1, st, &nparts, kFull, &tp);
+    k_pad2d<<<gN, 256, 0, st>>>(rpad, rr, n, G, 1);
+    k_pband<<<grid_for((int64_t)nc * n, 256), 256, 0, st>>>(rr, tc, n, nc, n, 0, drc, int(rc.size()), o0, ratio, 0, 0);
+    k_pband<<<grid_for(NC, 256), 256, 0, st>>>(tc, dc, n, nc, nc, 1, drc, int(rc.size()), o0, ratio, 0, 0);
+    launch_coarse_fd(2, nc, dVc, dlamc, dc, xc, t1, t2, st);
+    k_pband<<<grid_for((int64_t)nc * n, 256), 256, 0, st>>>(xc, tc, nc, n, nc, 1, drc, int(rc.size()), o0, ratio, 1, 0);
+    k_pband<<<grid_for(N, 256), 256, 0, st>>>(tc, tf, nc, n, n, 0, drc, int(rc.size()), o0, ratio, 1, 0);
+    k_pad2d<<<gN, 256, 0, st>>>(xp, ec, n, G, 1);
+    launch_axpy(ec, tf, N, st);
+    if ((e = cudaGetLastError()) != cudaSuccess) return (*err = std::string("kernel launch: ") + cudaGetErrorString(e), 4);
+  }
+  (void)dpart;
+  const int tail = std::max(2, int(hist.size()) / 4);
+  double lg = 0.0;
+  for (int k = int(hist.size()) - tail; k < int(hist.size()); ++k) lg += std::log(hist[k]);
+  *rho = std::exp(lg / tail);
+  if (ratios)
+    for (size_t k = 0; k < hist.size(); ++k) ratios[k] = hist[k];
+  return 0;
+}
+
+}  // namespace iga2l
