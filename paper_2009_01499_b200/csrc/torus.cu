@@ -87,6 +87,44 @@ __global__ void k_pband(const double *__restrict__ in, double *__restrict__ out,
   }
 }
 
+// degree-q operator on the n x n torus, direct (2q+1)^2 stencil A = K ⊗ M + M ⊗ K (row stencils k, m)
+__device__ __forceinline__ double torus_ax(const double *__restrict__ x, int n, int q, const double *k,
+                                           const double *m, int i, int j, double *diag) {
+  double acc = 0.0;
+  for (int b = -q; b <= q; ++b) {
+    const int jj = ((j + b) % n + n) % n;
+    for (int a = -q; a <= q; ++a) {
+      const int ii = ((i + a) % n + n) % n;
+      acc = fma(k[a + q] * m[b + q] + m[a + q] * k[b + q], x[(int64_t)jj * n + ii], acc);
+    }
+  }
+  *diag = 2.0 * k[q] * m[q];
+  return acc;
+}
+struct QRows {
+  double k[5], m[5];
+};
+// one colour (c0, c1) of the (q+1)^2-colour Gauss-Seidel (reading A11): points (q+1) apart do not couple
+__global__ void k_torus_gs(double *__restrict__ x, const double *__restrict__ b, int n, int q, QRows r, int c0,
+                           int c1) {
+  const int st = q + 1, na = n / st;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)na * na;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = c0 + st * int(idx % na), j = c1 + st * int(idx / na);
+    double dg;
+    const double ax = torus_ax(x, n, q, r.k, r.m, i, j, &dg);
+    x[(int64_t)j * n + i] += (b[(int64_t)j * n + i] - ax) / dg;
+  }
+}
+__global__ void k_torus_resid(double *__restrict__ rr, const double *__restrict__ b, const double *__restrict__ x,
+                              int n, int q, QRows r) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)n * n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    double dg;
+    rr[idx] = b[idx] - torus_ax(x, n, q, r.k, r.m, int(idx % n), int(idx / n), &dg);
+  }
+}
+
 // sum and sum of squares of v[0..N) (one CTA, fixed order)
 __global__ void k_sums(const double *__restrict__ v, int64_t N, double *out) {
   __shared__ double red[32];
@@ -143,10 +181,13 @@ int lfa_torus_run(int dim, int p, int q, int n, int s, int hf, int iters, unsign
   if (p < 1 || p > 8) return bad("p must be in 1..8");
   if (q < 1 || q > 2 || q > p) return bad("q must satisfy 1 <= q <= min(p, 2)");
   if (s != 1 && s != 3 && s != 5 && s != 7) return bad("block must be 1, 3, 5 or 7");
-  if (hf != 1 && hf != 2) return bad("h_factor must be 1 (same h) or 2 (aggressive)");
+  if (hf < 1 || hf > 3) return bad("h_factor must be 1 (two-grid, same h), 2 (aggressive) or 3 (three-grid)");
+  const bool three = hf == 3;
+  if (three && (n % 2 || n % (q + 1) || n / 2 < 2 * q + 1))
+    return bad("three-grid: n must be even, a multiple of q + 1, and n / 2 >= 2q + 1");
   const int D = s + p, w = (s - 1) / 2, W = 2 * p + 1;
   if (n % D != 0 || n < 2 * D) return bad("n must be a multiple of s + p and at least 2 (s + p)");
-  if (n % hf != 0 || n / hf < 2 * q + 1) return bad("n / h_factor must be an integer >= 2q + 1");
+  if (hf == 2 && (n % 2 != 0 || n / 2 < 2 * q + 1)) return bad("aggressive: n must be even and n / 2 >= 2q + 1");
   if (iters < 4 || iters > 100000) return bad("iters must be in 4..100000");
   if (!rho) return bad("rho is NULL");
   // ---- interior (Toeplitz, A27) rows from a Dirichlet grid large enough to have them ----
@@ -169,7 +210,7 @@ int lfa_torus_run(int dim, int p, int q, int n, int s, int hf, int iters, unsign
   {
     std::vector<double> r1(R1.W);
     for (int k = 0; k < R1.W; ++k) r1[k] = R1.c[ir * R1.W + k];
-    if (hf == 1) {
+    if (hf != 2) {
       rc = r1;
     } else {
       ratio = 2;
@@ -204,9 +245,26 @@ int lfa_torus_run(int dim, int p, int q, int n, int s, int hf, int iters, unsign
   for (int j = 0; j < s; ++j) tp.lam[j] = lam[(size_t)cref * s + j];
   tp.valid = 1;
   // ---- coarse level on the torus ----
-  const int nc = n / hf, Wq = 2 * q + 1;
+  const int nc = hf == 2 ? n / 2 : n, Wq = 2 * q + 1;
+  const int nfd = three ? n / 2 : nc;                    // the exactly solved level
   std::vector<double> Vc, lamc;
-  if (!periodic_fd_tables(q, nc, &Kq[rq * Wq], &Mq[rq * Wq], Vc, lamc)) return bad("coarse torus operator");
+  if (!periodic_fd_tables(q, nfd, &Kq[rq * Wq], &Mq[rq * Wq], Vc, lamc)) return bad("coarse torus operator");
+  // three-grid: the q-level system by one two-grid cycle from 0 -- (q+1)^2-colour GS (A11),
+  // residual, knot-insertion restriction P_m^T (A8), exact 2h solve (2D: the rediscretised 2h stencil equals
+  // h's, A10), P_m, GS
+  QRows qr{};
+  for (int t = 0; t < Wq; ++t) {
+    qr.k[t] = Kq[rq * Wq + t];
+    qr.m[t] = Mq[rq * Wq + t];
+  }
+  std::vector<double> pm(q + 2);
+  {
+    double binom = 1.0;
+    for (int kk = 0; kk <= q + 1; ++kk) {
+      pm[kk] = binom / double(1 << q);
+      binom = binom * double(q + 1 - kk) / double(kk + 1);
+    }
+  }
   // ---- device ----
   cudaStream_t st = nullptr;
   cudaError_t e = cudaSuccess;
@@ -215,7 +273,11 @@ int lfa_torus_run(int dim, int p, int q, int n, int s, int hf, int iters, unsign
   double *dK = buf.get<double>(K.size(), &e), *dM = buf.get<double>(M.size(), &e);
   double *dV = buf.get<double>(V.size(), &e), *dlam = buf.get<double>(lam.size(), &e);
   double *dVc = buf.get<double>(Vc.size(), &e), *dlamc = buf.get<double>(lamc.size(), &e);
-  double *drc = buf.get<double>(rc.size(), &e);
+  double *drc = buf.get<double>(rc.size(), &e), *dpm = buf.get<double>(pm.size(), &e);
+  const int64_t N2 = (int64_t)(n / 2) * (n / 2);
+  double *qx = buf.get<double>(three ? (int64_t)n * n : 1, &e), *qr2 = buf.get<double>(three ? (int64_t)n * n : 1, &e),
+         *qt = buf.get<double>(three ? (int64_t)n * n : 1, &e), *d2 = buf.get<double>(three ? N2 : 1, &e),
+         *e2 = buf.get<double>(three ? N2 : 1, &e);
   double *xp = buf.get<double>(NP, &e), *zp = buf.get<double>(NP, &e), *rpad = buf.get<double>(NP, &e);
   double *ec = buf.get<double>(N, &e), *rr = buf.get<double>(N, &e), *tf = buf.get<double>(N, &e);
   double *dc = buf.get<double>(NC, &e), *xc = buf.get<double>(NC, &e), *t1 = buf.get<double>(NC, &e),
@@ -230,6 +292,7 @@ int lfa_torus_run(int dim, int p, int q, int n, int s, int hf, int iters, unsign
     return cudaMemcpy(d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice);
   };
   if (up(dK, K) || up(dM, M) || up(dV, V) || up(dlam, lam) || up(dVc, Vc) || up(dlamc, lamc) || up(drc, rc) ||
+      up(dpm, pm) ||
       cudaMemset(zp, 0, NP * sizeof(double)))
     return (*err = "upload failed", 4);
   if (dfb) export_interior_frags(p, s, np, dK, dM, dV, dlam, dfb, st);
@@ -273,7 +336,22 @@ int lfa_torus_run(int dim, int p, int q, int n, int s, int hf, int iters, unsign
     k_pad2d<<<gN, 256, 0, st>>>(rpad, rr, n, G, 1);
     k_pband<<<grid_for((int64_t)nc * n, 256), 256, 0, st>>>(rr, tc, n, nc, n, 0, drc, int(rc.size()), o0, ratio, 0, 0);
     k_pband<<<grid_for(NC, 256), 256, 0, st>>>(tc, dc, n, nc, nc, 1, drc, int(rc.size()), o0, ratio, 0, 0);
-    launch_coarse_fd(2, nc, dVc, dlamc, dc, xc, t1, t2, st);
+    if (!three) {
+      launch_coarse_fd(2, nc, dVc, dlamc, dc, xc, t1, t2, st);
+    } else {                                              // xc = B_q dc (one q-level two-grid cycle from 0)
+      const int gq = grid_for(NC, 256), st1 = q + 1, h2 = n / 2;
+      cudaMemsetAsync(xc, 0, NC * sizeof(double), st);
+      for (int col = 0; col < st1 * st1; ++col)
+        k_torus_gs<<<gq, 256, 0, st>>>(xc, dc, n, q, qr, col % st1, col / st1);
+      k_torus_resid<<<gq, 256, 0, st>>>(qr2, dc, xc, n, q, qr);
+      k_pband<<<grid_for((int64_t)h2 * n, 256), 256, 0, st>>>(qr2, qt, n, h2, n, 0, dpm, q + 2, 0, 2, 0, 0);
+      k_pband<<<grid_for(N2, 256), 256, 0, st>>>(qt, d2, n, h2, h2, 1, dpm, q + 2, 0, 2, 0, 0);
+      launch_coarse_fd(2, h2, dVc, dlamc, d2, e2, t1, t2, st);
+      k_pband<<<grid_for((int64_t)h2 * n, 256), 256, 0, st>>>(e2, qt, h2, n, h2, 1, dpm, q + 2, 0, 2, 1, 0);
+      k_pband<<<grid_for(NC, 256), 256, 0, st>>>(qt, xc, h2, n, n, 0, dpm, q + 2, 0, 2, 1, 1);
+      for (int col = 0; col < st1 * st1; ++col)
+        k_torus_gs<<<gq, 256, 0, st>>>(xc, dc, n, q, qr, col % st1, col / st1);
+    }
     k_pband<<<grid_for((int64_t)nc * n, 256), 256, 0, st>>>(xc, tc, nc, n, nc, 1, drc, int(rc.size()), o0, ratio, 1, 0);
     k_pband<<<grid_for(N, 256), 256, 0, st>>>(tc, tf, nc, n, n, 0, drc, int(rc.size()), o0, ratio, 1, 0);
     k_pad2d<<<gN, 256, 0, st>>>(xp, ec, n, G, 1);

@@ -40,6 +40,16 @@ def test_torus_aggressive_equals_block_lfa(p, q, s, nk):
     assert abs(got - ref) <= 0.01 * ref, (got, ref)
 
 
+@pytest.mark.parametrize("p,q,s,nk", [(2, 1, 3, 2), (3, 1, 3, 2), (4, 1, 3, 2), (8, 2, 7, 2)], ids=["p2", "p3", "p4", "p8q2"])
+def test_torus_three_grid_equals_block_lfa(p, q, s, nk):
+    """Table 2's setting (q-level by one two-grid cycle, (q+1)^2-colour GS, exact 2h): == ρ_3g(nk)."""
+    L = lfa._cell(p, q, s)
+    n = nk * L
+    ref = lfa.rho_3g(p, q, s, 2, nk=nk)
+    got = pkg.lfa_torus(p, q, n, s, h_factor=3, iters=400, seed=3)
+    assert abs(got - ref) <= 0.01 * ref, (got, ref)
+
+
 def test_torus_seed_independent_and_errors():
     a = pkg.lfa_torus(3, 1, 24, 3, iters=300, seed=3)
     b = pkg.lfa_torus(3, 1, 24, 3, iters=300, seed=4)

@@ -38,6 +38,19 @@ for p in range(2, 6):
         print(f"{p:2d} {q:2d} {s:2d} {nk:3d} {n:4d} {got:9.5f} {ref:9.5f} {abs(got - ref) / ref:9.2e} {dt:6.2f}",
               flush=True)
 print()
+print("three-grid, q-level by one two-grid cycle (Table 2's setting): torus rho vs block LFA rho_3g")
+for p in (2, 3, 4, 5, 8):
+    s, q = S[p], (2 if p == 8 else 1)
+    L = lfa._cell(p, q, s)
+    for nk in (2,):
+        n = nk * L
+        t0 = time.time()
+        got = pkg.lfa_torus(p, q, n, s, h_factor=3, iters=400, seed=2)
+        dt = time.time() - t0
+        ref = lfa.rho_3g(p, q, s, 2, nk=nk)
+        print(f"{p:2d} {q:2d} {s:2d} {nk:3d} {n:4d} {got:9.5f} {ref:9.5f} {abs(got - ref) / ref:9.2e} {dt:6.2f}",
+              flush=True)
+print()
 print("at scale (the torus alone, no oracle): n = 32 L")
 for p in (3, 5, 8):
     s = S[p]
