@@ -443,12 +443,16 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_w(int n1, const dou
   for (int lz = 0; lz < S; ++lz) r[lz] = 0.0;
   asm volatile("griddepcontrol.wait;" ::: "memory");              // PDL: the previous colour's x (no-op otherwise)
   // x-row of pass-x task t of group gi (zero outside the domain)
-  auto load_row = [&](int gi, int t, double (&v)[Wn]) {
+  // pass-x task t of group gi: window row (plane gi G + t / Wn, row t % Wn) -> Pa, Pb.  Rows inside the
+  // domain in y and z, with the whole window inside in x (every interior block): LV-double vector loads and
+  // the parity shift; rows outside the domain give zero rows (no loads).
+  auto task_x = [&](int gi, int t) {
     const int jj = t / Wn, yy = t - jj * Wn;
     const int gz = oz + gi * G + jj, gyy = oy + yy;
-    const bool rok = t < B::TX && unsigned(gz) < un && unsigned(gyy) < un;
+    const bool rok = unsigned(gz) < un && unsigned(gyy) < un;
     const int64_t e0 = (int64_t(gz - zoff) * n1 + gyy) * n1 + ox;
-    if (LV > 1 && xin) {                                          // aligned LV-double vector loads + shift select
+    double v[Wn];
+    if (rok && xin && LV > 1) {
       constexpr int NV = (Wn + 2 * LV - 2) / LV;                  // vectors covering [e0 & ~(LV-1), e0 + Wn)
       double u[NV * LV];
       const double *ap = x + (e0 & ~int64_t(LV - 1));
@@ -456,14 +460,11 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_w(int n1, const dou
 #pragma unroll
       for (int c = 0; c < NV; ++c) {
         if constexpr (LV == 4) {
-          if (rok)
-            asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
-                         : "=d"(u[4 * c]), "=d"(u[4 * c + 1]), "=d"(u[4 * c + 2]), "=d"(u[4 * c + 3])
-                         : "l"(ap + 4 * c));
-          else
-            u[4 * c] = u[4 * c + 1] = u[4 * c + 2] = u[4 * c + 3] = 0.0;
+          asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                       : "=d"(u[4 * c]), "=d"(u[4 * c + 1]), "=d"(u[4 * c + 2]), "=d"(u[4 * c + 3])
+                       : "l"(ap + 4 * c));
         } else {
-          const double2 q = rok ? __ldg(reinterpret_cast<const double2 *>(ap) + c) : make_double2(0.0, 0.0);
+          const double2 q = __ldg(reinterpret_cast<const double2 *>(ap) + c);
           u[2 * c] = q.x;
           u[2 * c + 1] = q.y;
         }
@@ -478,11 +479,17 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_w(int n1, const dou
 #pragma unroll
         for (int k = 0; k < Wn; ++k) v[k] = sh ? u[k + 1] : u[k];
       }
-    } else {
+    } else if (rok) {
       const double *rp = x + e0;
 #pragma unroll
-      for (int k = 0; k < Wn; ++k) v[k] = (rok && (xin || unsigned(ox + k) < un)) ? rp[k] : 0.0;
+      for (int k = 0; k < Wn; ++k) v[k] = (xin || unsigned(ox + k) < un) ? rp[k] : 0.0;
+    } else {
+#pragma unroll
+      for (int l = 0; l < S; ++l) Pa[l * TXP + t] = Pb[l * TXP + t] = 0.0;
+      return;
     }
+    if (toe[0]) w_pass_x<P, S, true>(v, Tk, Tm, tp, Pa + t, Pb + t, TXP);
+    else w_pass_x<P, S, false>(v, Tk, Tm, tp, Pa + t, Pb + t, TXP);
   };
 #pragma unroll
   for (int gi = 0; gi < B::NG; ++gi) {
@@ -490,12 +497,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_w(int n1, const dou
 #pragma unroll 1
     for (int rr = 0; rr < B::RX; ++rr) {
       const int t = rr * 32 + lane;
-      double v[Wn];
-      load_row(gi, t, v);
-      if (t < B::TX) {
-        if (toe[0]) w_pass_x<P, S, true>(v, Tk, Tm, tp, Pa + t, Pb + t, TXP);
-        else w_pass_x<P, S, false>(v, Tk, Tm, tp, Pa + t, Pb + t, TXP);
-      }
+      if (t < B::TX) task_x(gi, t);
     }
     __syncwarp();
     if (gi == 0) asm volatile("griddepcontrol.launch_dependents;");   // PDL: the next colour may launch
@@ -690,10 +692,14 @@ bool try_schwarz3d_w(int p, int s, int64_t n1, const double *K, const double *M,
   if (tpp) tp = *tpp;
   const int nblk = nb0 * nb1 * nb2;
   // 32-byte row loads need a 32-byte aligned x (every torch / cudaMalloc allocation is)
+  // row loads: 16 bytes at p = 5 (170.5 vs 173.3 us per C5 colour with 32), 32 bytes at p = 3 (25.96 vs 26.20 us
+  // per C4 colour); 8 bytes when x is not 32-byte aligned.  More CTAs per SM (96 / 80 registers) measured
+  // slower (173.3 us).
   if (reinterpret_cast<uintptr_t>(x) & 31)
     launch_w<P, S, G, 4, 4, 1>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nblk, zoff, tlo, thi, st, tp);
   else
-    launch_w<P, S, G, 4, 4, 4>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nblk, zoff, tlo, thi, st, tp);
+    launch_w<P, S, G, 4, 4, (P == 5 ? 2 : 4)>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nblk, zoff, tlo, thi,
+                                               st, tp);
   return true;
 }
 

@@ -52,7 +52,7 @@ def timing(name, reps):
     x = x0.clone()
     ncol = ctx.info().colours
     res = {}
-    for env in ("0", "1"):
+    for env, lv in (("0", "-"), ("1", "-")):
         os.environ["IGA2L_S3D_WARP"] = env
         ctx.sweep(b, x)                          # first launch outside capture (lazy module loading)
         g = torch.cuda.CUDAGraph()
@@ -62,7 +62,7 @@ def timing(name, reps):
         x.copy_(x0)
         g.replay()
         torch.cuda.synchronize()
-        res[env] = x.clone()
+        res[(env, lv)] = x.clone()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
         for _ in range(reps):
@@ -70,7 +70,7 @@ def timing(name, reps):
         e1.record(st)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
-        d = (res[env] - res["0"]).abs().max().item() / res["0"].abs().max().item()
+        d = (res[(env, lv)] - res[("0", "-")]).abs().max().item() / res[("0", "-")].abs().max().item()
         print(f"{name} IGA2L_S3D_WARP={env}: sweep {ms:.3f} ms, {1000 * ms / ncol:.2f} us/colour"
               f" (graph); max|x - x_v4|/max|x| {d:.2e}", flush=True)
         del g
