@@ -130,15 +130,15 @@ int iga2l_iterate(iga2l_ctx *ctx, const double *b, double *x, int iters, double 
 
 /*
  * Torus LFA run: the spectral radius of the two-grid error operator
- * E = (I - P A_q^+ R A_p) S_p of the multicolour method (reading A4) on the dim = 2, n x n
+ * E = (I - P A_q^+ R A_p) S_p of the multicolour method (reading A4) on the n^dim (dim 2 or 3)
  * PERIODIC grid, by `iters` power iterations with the library's kernels from a seeded mean-zero start
  * (the constant, E 1 = 1, projected out: LFA excludes it).  h_factor 1: exact degree-q level on the
  * same mesh (Table 1's ρ_2g); 2: aggressive, degree q on H = 2h (Table 3's ρ_2g^ag); 3: three-grid, the
- * degree-q level by one two-grid cycle ((q+1)^2-colour GS, exact 2h solve; Table 2's ρ_3g).  With n = nk (s + p),
+ * degree-q level by one two-grid cycle ((q+1)^2-colour GS, exact 2h solve; Table 2's ρ_3g; 2D).  With n = nk (s + p),
  * nk even, the torus frequencies are the Bloch quasi-momenta of an nk^2 LFA grid.  Synchronous; allocates
  * and frees its own device memory on the current device.
  * rho (host): geometric mean of the last quarter of the norm ratios; ratios (host, NULL or `iters`
- * doubles): every ratio.  Errors: IGA2L_EPARAM (dim != 2, n not a multiple of s + p or < 2(s + p), n /
+ * doubles): every ratio.  Errors: IGA2L_EPARAM (dim not 2/3, n not a multiple of s + p or < 2(s + p), n /
  * h_factor < 2q + 1, iters outside 4..100000, ...), IGA2L_ENUMERIC, IGA2L_ECUDA, IGA2L_ENOMEM.
  */
 int iga2l_lfa_torus(int dim, int p, int q, int n, int block, int h_factor, int iters, unsigned long long seed,

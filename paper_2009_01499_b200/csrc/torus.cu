@@ -21,8 +21,8 @@
 //   the constant mode (A_c 1 = 0) gets 0 (pseudo-inverse, as LFA excludes θ = 0's constant).
 // * Power iteration from a seeded random mean-zero start; the mean (the constant, E 1 = 1) is projected
 //   out after every application.  ρ = geometric mean of the last quarter of the norm ratios.
-// 2D (the paper's setting; in 3D the rediscretised 2h operator differs from h's by a factor 2 and the
-// padded sweep is the same construction).
+// 2D and 3D (the padded sweep is the same construction; in 3D the rediscretised 2h operator is twice h's
+// stencil, A10); the three-grid mode is 2D.
 #include <cmath>
 #include <string>
 #include <vector>
@@ -34,56 +34,75 @@
 namespace iga2l {
 namespace {
 
-// ghost layers of an np x np padded array (real block [G, G+n)^2) from their periodic images
-__global__ void k_ghost2d(double *__restrict__ x, int n, int G) {
+// ghost layers of an np^dim padded array (real block [G, G+n)^dim) from their periodic images
+__global__ void k_ghost(double *__restrict__ x, int dim, int n, int G) {
   const int np = n + 2 * G;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)np * np;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int i = int(idx % np), j = int(idx / np);
-    const bool gi = i < G || i >= G + n, gj = j < G || j >= G + n;
-    if (!gi && !gj) continue;
-    const int si = G + ((i - G) % n + n) % n, sj = G + ((j - G) % n + n) % n;
-    x[idx] = x[(int64_t)sj * np + si];
+  const int64_t tot = dim == 3 ? (int64_t)np * np * np : (int64_t)np * np;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = int(idx % np), j = int((idx / np) % np), k = dim == 3 ? int(idx / ((int64_t)np * np)) : G;
+    const bool gh = i < G || i >= G + n || j < G || j >= G + n || k < G || k >= G + n;
+    if (!gh) continue;
+    const int si = G + ((i - G) % n + n) % n, sj = G + ((j - G) % n + n) % n, sk = G + ((k - G) % n + n) % n;
+    x[idx] = x[dim == 3 ? ((int64_t)sk * np + sj) * np + si : (int64_t)sj * np + si];
   }
 }
 
-// compact n x n <-> real block of the padded array; mode 0: pad = c, 1: c = pad
-__global__ void k_pad2d(double *__restrict__ pad, double *__restrict__ c, int n, int G, int mode) {
+// compact n^dim <-> real block of the padded array; mode 0: pad = c, 1: c = pad
+__global__ void k_pad(double *__restrict__ pad, double *__restrict__ c, int dim, int n, int G, int mode) {
   const int np = n + 2 * G;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)n * n;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int i = int(idx % n), j = int(idx / n);
-    double *pp = pad + (int64_t)(j + G) * np + i + G;
+  const int64_t tot = dim == 3 ? (int64_t)n * n * n : (int64_t)n * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = int(idx % n), j = int((idx / n) % n), k = dim == 3 ? int(idx / ((int64_t)n * n)) : 0;
+    double *pp = pad + (dim == 3 ? ((int64_t)(k + G) * np + j + G) * np + i + G : (int64_t)(j + G) * np + i + G);
     if (mode == 0) *pp = c[idx];
     else c[idx] = *pp;
   }
 }
 
-// periodic band transfer along one axis of a 2D array (x fastest).  Forward (restriction R):
-//   out[i] = Σ_k c[k] in[(ratio i + o0 + k) mod nin], i < nout;
-// transpose (prolongation R^T): out[j] = Σ_{i, k: ratio i + o0 + k ≡ j} c[k] in[i], j < nout (= nin_fwd).
-__global__ void k_pband(const double *__restrict__ in, double *__restrict__ out, int nin, int nout, int other,
-                        int axis, const double *__restrict__ c, int W, int o0, int ratio, int transpose,
+// periodic band transfer along one axis, [outer][nin][inner] -> [outer][nout][inner].  Forward (restriction R):
+//   out[i] = Σ_k c[k] in[(ratio i + o0 + k) mod nin];
+// transpose (prolongation R^T): out[j] = Σ_{i, k: ratio i + o0 + k ≡ j} c[k] in[i].
+__global__ void k_pband(const double *__restrict__ in, double *__restrict__ out, int nin, int nout, int64_t outer,
+                        int64_t inner, const double *__restrict__ c, int W, int o0, int ratio, int transpose,
                         int accumulate) {
-  const int64_t total = (int64_t)nout * other;
+  const int64_t total = outer * nout * inner;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int a = int(idx % (axis == 0 ? nout : other)), bb = int(idx / (axis == 0 ? nout : other));
-    const int o = axis == 0 ? a : bb, t = axis == 0 ? bb : a;   // o: index along the axis, t: the other one
-    auto at = [&](int k) { return axis == 0 ? in[(int64_t)t * nin + k] : in[(int64_t)k * other + t]; };
+    const int64_t t = idx % inner, ob = idx / inner;
+    const int o = int(ob % nout);
+    const int64_t u = ob / nout;
+    const double *src = in + u * nin * inner + t;
     double acc = 0.0;
     if (!transpose) {
-      for (int k = 0; k < W; ++k) acc = fma(c[k], at(((ratio * o + o0 + k) % nin + nin) % nin), acc);
+      for (int k = 0; k < W; ++k) acc = fma(c[k], src[(int64_t)(((ratio * o + o0 + k) % nin + nin) % nin) * inner], acc);
     } else {
       for (int k = 0; k < W; ++k) {
         const int r = o - o0 - k;                               // = ratio * i (mod ratio * nin)
         const int rm = ((r % (ratio * nin)) + ratio * nin) % (ratio * nin);
         if (rm % ratio) continue;
-        acc = fma(c[k], at(rm / ratio), acc);
+        acc = fma(c[k], src[(int64_t)(rm / ratio) * inner], acc);
       }
     }
-    double *op = out + (axis == 0 ? (int64_t)t * nout + o : (int64_t)o * other + t);
-    *op = accumulate ? *op + acc : acc;
+    out[idx] = accumulate ? out[idx] + acc : acc;
+  }
+}
+
+// d-dim periodic transfer, axis by axis (x first): n_in^d -> n_out^d through tmp0/tmp1 (n_max^d each)
+void pband_nd(int dim, const double *in, double *out, int nin, int nout, const double *c, int W, int o0, int ratio,
+              int transpose, int accumulate, double *tmp0, double *tmp1, cudaStream_t st) {
+  int64_t sz[3] = {nin, nin, dim == 3 ? nin : 1};
+  const double *src = in;
+  for (int a = 0; a < dim; ++a) {
+    const bool last = a == dim - 1;
+    double *dst = last ? out : (a % 2 == 0 ? tmp0 : tmp1);
+    int64_t inner = 1, outer = 1;
+    for (int b = 0; b < a; ++b) inner *= sz[b];
+    for (int b = a + 1; b < dim; ++b) outer *= sz[b];
+    const int64_t tot = outer * nout * inner;
+    k_pband<<<grid_for(tot, 256), 256, 0, st>>>(src, dst, nin, nout, outer, inner, c, W, o0, ratio, transpose,
+                                                last ? accumulate : 0);
+    sz[a] = nout;
+    src = dst;
   }
 }
 
@@ -177,12 +196,13 @@ int lfa_torus_run(int dim, int p, int q, int n, int s, int hf, int iters, unsign
     *err = m;
     return 1;   // IGA2L_EPARAM
   };
-  if (dim != 2) return bad("the torus run is 2D (dim must be 2)");
+  if (dim != 2 && dim != 3) return bad("dim must be 2 or 3");
   if (p < 1 || p > 8) return bad("p must be in 1..8");
   if (q < 1 || q > 2 || q > p) return bad("q must satisfy 1 <= q <= min(p, 2)");
   if (s != 1 && s != 3 && s != 5 && s != 7) return bad("block must be 1, 3, 5 or 7");
   if (hf < 1 || hf > 3) return bad("h_factor must be 1 (two-grid, same h), 2 (aggressive) or 3 (three-grid)");
   const bool three = hf == 3;
+  if (three && dim != 2) return bad("the three-grid torus run is 2D");
   if (three && (n % 2 || n % (q + 1) || n / 2 < 2 * q + 1))
     return bad("three-grid: n must be even, a multiple of q + 1, and n / 2 >= 2q + 1");
   const int D = s + p, w = (s - 1) / 2, W = 2 * p + 1;
@@ -249,6 +269,8 @@ int lfa_torus_run(int dim, int p, int q, int n, int s, int hf, int iters, unsign
   const int nfd = three ? n / 2 : nc;                    // the exactly solved level
   std::vector<double> Vc, lamc;
   if (!periodic_fd_tables(q, nfd, &Kq[rq * Wq], &Mq[rq * Wq], Vc, lamc)) return bad("coarse torus operator");
+  if (dim == 3 && hf == 2)                               // rediscretised on 2h: K/2 (x) 2M (x) 2M = 2 (K M M)
+    for (double &l : lamc) l *= 2.0;
   // three-grid: the q-level system by one two-grid cycle from 0 -- (q+1)^2-colour GS (A11),
   // residual, knot-insertion restriction P_m^T (A8), exact 2h solve (2D: the rediscretised 2h stencil equals
   // h's, A10), P_m, GS
@@ -269,24 +291,22 @@ int lfa_torus_run(int dim, int p, int q, int n, int s, int hf, int iters, unsign
   cudaStream_t st = nullptr;
   cudaError_t e = cudaSuccess;
   DevBuf buf;
-  const int64_t NP = (int64_t)np * np, N = (int64_t)n * n, NC = (int64_t)nc * nc;
+  auto pw = [&](int64_t a) { return dim == 3 ? a * a * a : a * a; };
+  const int64_t NP = pw(np), N = pw(n), NC = pw(nc);
   double *dK = buf.get<double>(K.size(), &e), *dM = buf.get<double>(M.size(), &e);
   double *dV = buf.get<double>(V.size(), &e), *dlam = buf.get<double>(lam.size(), &e);
   double *dVc = buf.get<double>(Vc.size(), &e), *dlamc = buf.get<double>(lamc.size(), &e);
   double *drc = buf.get<double>(rc.size(), &e), *dpm = buf.get<double>(pm.size(), &e);
   const int64_t N2 = (int64_t)(n / 2) * (n / 2);
-  double *qx = buf.get<double>(three ? (int64_t)n * n : 1, &e), *qr2 = buf.get<double>(three ? (int64_t)n * n : 1, &e),
-         *qt = buf.get<double>(three ? (int64_t)n * n : 1, &e), *d2 = buf.get<double>(three ? N2 : 1, &e),
+  double *qr2 = buf.get<double>(three ? (int64_t)n * n : 1, &e), *d2 = buf.get<double>(three ? N2 : 1, &e),
          *e2 = buf.get<double>(three ? N2 : 1, &e);
   double *xp = buf.get<double>(NP, &e), *zp = buf.get<double>(NP, &e), *rpad = buf.get<double>(NP, &e);
   double *ec = buf.get<double>(N, &e), *rr = buf.get<double>(N, &e), *tf = buf.get<double>(N, &e);
   double *dc = buf.get<double>(NC, &e), *xc = buf.get<double>(NC, &e), *t1 = buf.get<double>(NC, &e),
-         *t2 = buf.get<double>(NC, &e), *tc = buf.get<double>((int64_t)nc * n, &e);
+         *t2 = buf.get<double>(NC, &e), *tc = buf.get<double>(N, &e), *td = buf.get<double>(N, &e);
   double *dsum = buf.get<double>(2, &e);
-  const int nfr = export_interior_frags(p, s, np, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+  const int nfr = dim == 2 ? export_interior_frags(p, s, np, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr) : -1;
   double *dfb = nfr > 0 ? buf.get<double>(nfr, &e) : nullptr;
-  const int npart = apply_num_partials(2, p, np);
-  double *dpart = buf.get<double>(npart, &e);
   if (e != cudaSuccess) return (*err = "cudaMalloc failed", 6);
   auto up = [&](double *d, const std::vector<double> &h) {
     return cudaMemcpy(d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice);
@@ -322,43 +342,39 @@ int lfa_torus_run(int dim, int p, int q, int n, int s, int hf, int iters, unsign
     k_shift_scale<<<gN, 256, 0, st>>>(ec, N, mu, 1.0 / nrm);
     prev = 1.0;
     // x (padded, ghosts) = e
-    k_pad2d<<<gN, 256, 0, st>>>(xp, ec, n, G, 0);
-    k_ghost2d<<<gNP, 256, 0, st>>>(xp, n, G);
+    k_pad<<<gN, 256, 0, st>>>(xp, ec, dim, n, G, 0);
+    k_ghost<<<gNP, 256, 0, st>>>(xp, dim, n, G);
     // S_p: colour by colour, ghosts refreshed after each
-    for (int col = 0; col < D * D; ++col) {
-      if (!launch_schwarz_colour_fast(2, p, s, np, dK, dM, dV, dlam, zp, xp, col, D, st, kFull, dfb, &tp))
-        launch_schwarz_colour(2, p, s, np, dK, dM, dV, dlam, zp, xp, col, D, st, kFull);
-      k_ghost2d<<<gNP, 256, 0, st>>>(xp, n, G);
+    const int ncol = dim == 3 ? D * D * D : D * D;
+    for (int col = 0; col < ncol; ++col) {
+      if (!launch_schwarz_colour_fast(dim, p, s, np, dK, dM, dV, dlam, zp, xp, col, D, st, kFull, dfb, &tp))
+        launch_schwarz_colour(dim, p, s, np, dK, dM, dV, dlam, zp, xp, col, D, st, kFull);
+      k_ghost<<<gNP, 256, 0, st>>>(xp, dim, n, G);
     }
     // r = 0 - A_p x (real block), d_c = R r, e_c = A_c^+ d_c, e = x + R^T e_c
     int nparts = 0;
-    launch_apply(2, p, np, dK, dM, xp, zp, rpad, nullptr, 1, st, &nparts, kFull, &tp);
-    k_pad2d<<<gN, 256, 0, st>>>(rpad, rr, n, G, 1);
-    k_pband<<<grid_for((int64_t)nc * n, 256), 256, 0, st>>>(rr, tc, n, nc, n, 0, drc, int(rc.size()), o0, ratio, 0, 0);
-    k_pband<<<grid_for(NC, 256), 256, 0, st>>>(tc, dc, n, nc, nc, 1, drc, int(rc.size()), o0, ratio, 0, 0);
+    launch_apply(dim, p, np, dK, dM, xp, zp, rpad, nullptr, 1, st, &nparts, kFull, &tp);
+    k_pad<<<gN, 256, 0, st>>>(rpad, rr, dim, n, G, 1);
+    pband_nd(dim, rr, dc, n, nc, drc, int(rc.size()), o0, ratio, 0, 0, tc, td, st);
     if (!three) {
-      launch_coarse_fd(2, nc, dVc, dlamc, dc, xc, t1, t2, st);
+      launch_coarse_fd(dim, nc, dVc, dlamc, dc, xc, t1, t2, st);
     } else {                                              // xc = B_q dc (one q-level two-grid cycle from 0)
       const int gq = grid_for(NC, 256), st1 = q + 1, h2 = n / 2;
       cudaMemsetAsync(xc, 0, NC * sizeof(double), st);
       for (int col = 0; col < st1 * st1; ++col)
         k_torus_gs<<<gq, 256, 0, st>>>(xc, dc, n, q, qr, col % st1, col / st1);
       k_torus_resid<<<gq, 256, 0, st>>>(qr2, dc, xc, n, q, qr);
-      k_pband<<<grid_for((int64_t)h2 * n, 256), 256, 0, st>>>(qr2, qt, n, h2, n, 0, dpm, q + 2, 0, 2, 0, 0);
-      k_pband<<<grid_for(N2, 256), 256, 0, st>>>(qt, d2, n, h2, h2, 1, dpm, q + 2, 0, 2, 0, 0);
+      pband_nd(2, qr2, d2, n, h2, dpm, q + 2, 0, 2, 0, 0, tc, td, st);
       launch_coarse_fd(2, h2, dVc, dlamc, d2, e2, t1, t2, st);
-      k_pband<<<grid_for((int64_t)h2 * n, 256), 256, 0, st>>>(e2, qt, h2, n, h2, 1, dpm, q + 2, 0, 2, 1, 0);
-      k_pband<<<grid_for(NC, 256), 256, 0, st>>>(qt, xc, h2, n, n, 0, dpm, q + 2, 0, 2, 1, 1);
+      pband_nd(2, e2, xc, h2, n, dpm, q + 2, 0, 2, 1, 1, tc, td, st);
       for (int col = 0; col < st1 * st1; ++col)
         k_torus_gs<<<gq, 256, 0, st>>>(xc, dc, n, q, qr, col % st1, col / st1);
     }
-    k_pband<<<grid_for((int64_t)nc * n, 256), 256, 0, st>>>(xc, tc, nc, n, nc, 1, drc, int(rc.size()), o0, ratio, 1, 0);
-    k_pband<<<grid_for(N, 256), 256, 0, st>>>(tc, tf, nc, n, n, 0, drc, int(rc.size()), o0, ratio, 1, 0);
-    k_pad2d<<<gN, 256, 0, st>>>(xp, ec, n, G, 1);
+    pband_nd(dim, xc, tf, nc, n, drc, int(rc.size()), o0, ratio, 1, 0, tc, td, st);
+    k_pad<<<gN, 256, 0, st>>>(xp, ec, dim, n, G, 1);
     launch_axpy(ec, tf, N, st);
     if ((e = cudaGetLastError()) != cudaSuccess) return (*err = std::string("kernel launch: ") + cudaGetErrorString(e), 4);
   }
-  (void)dpart;
   const int tail = std::max(2, int(hist.size()) / 4);
   double lg = 0.0;
   for (int k = int(hist.size()) - tail; k < int(hist.size()); ++k) lg += std::log(hist[k]);

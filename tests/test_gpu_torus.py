@@ -57,4 +57,14 @@ def test_torus_seed_independent_and_errors():
     with pytest.raises(pkg.IgaError):
         pkg.lfa_torus(3, 1, 25, 3)                       # n not a multiple of s + p
     with pytest.raises(pkg.IgaError):
-        pkg.lfa_torus(3, 1, 24, 3, dim=3)                # 2D only
+        pkg.lfa_torus(3, 1, 24, 3, h_factor=3, dim=3)    # the three-grid run is 2D
+
+
+@pytest.mark.parametrize("p,s,hf", [(2, 3, 1), (3, 3, 1), (3, 3, 2)], ids=["p2", "p3", "p3_ag"])
+def test_torus_3d_equals_block_lfa(p, s, hf):
+    """3D (reading A25; no paper value): the torus run == the oracle's 3D block LFA on the nk = 2 grid."""
+    L = (s + p) if hf == 1 else lfa._cell(p, 1, s)
+    n = 2 * L
+    ref = (lfa.rho_2g if hf == 1 else lfa.rho_2g_ag)(p, 1, s, 3, nk=2)
+    got = pkg.lfa_torus(p, 1, n, s, h_factor=hf, iters=300, seed=4, dim=3)
+    assert abs(got - ref) <= 0.01 * ref, (got, ref)

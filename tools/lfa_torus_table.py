@@ -51,6 +51,24 @@ for p in (2, 3, 4, 5, 8):
         print(f"{p:2d} {q:2d} {s:2d} {nk:3d} {n:4d} {got:9.5f} {ref:9.5f} {abs(got - ref) / ref:9.2e} {dt:6.2f}",
               flush=True)
 print()
+print("3D (reading A25, no paper values): torus vs the oracle's 3D block LFA, nk = 2")
+for p, s, hf in ((2, 3, 1), (3, 3, 1), (3, 3, 2), (4, 3, 1)):
+    L = (s + p) if hf == 1 else lfa._cell(p, 1, s)
+    n = 2 * L
+    t0 = time.time()
+    got = pkg.lfa_torus(p, 1, n, s, h_factor=hf, iters=300, seed=4, dim=3)
+    dt = time.time() - t0
+    ref = (lfa.rho_2g if hf == 1 else lfa.rho_2g_ag)(p, 1, s, 3, nk=2)
+    print(f"{p:2d}  1 {s:2d}   2 {n:4d} {got:9.5f} {ref:9.5f} {abs(got - ref) / ref:9.2e} {dt:6.2f}  (h_factor {hf})",
+          flush=True)
+print("3D predictions beyond the oracle's reach (torus only): C4's and C5's (p, s), aggressive 2h like the configs")
+for p, s, q, nk in ((3, 3, 1, 4), (5, 5, 1, 2), (5, 5, 2, 2)):
+    L = lfa._cell(p, q, s)
+    n = nk * L
+    t0 = time.time()
+    got = pkg.lfa_torus(p, q, n, s, h_factor=2, iters=300, seed=5, dim=3)
+    print(f"{p:2d} {q:2d} {s:2d} {nk:3d} {n:4d} {got:9.5f}  ({time.time() - t0:.1f} s, {n ** 3} DOF)", flush=True)
+print()
 print("at scale (the torus alone, no oracle): n = 32 L")
 for p in (3, 5, 8):
     s = S[p]
