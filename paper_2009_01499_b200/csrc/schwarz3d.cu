@@ -405,14 +405,14 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_w(int n1, const dou
   constexpr int W = B::W, Wn = B::Wn, w = B::w, S2 = B::S2, TXP = B::TXP, PS = B::PS;
   extern __shared__ __align__(16) double smw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int g = blockIdx.x * NW + wid;
-  if (g >= nblk) return;                                          // the whole warp: no CTA barrier is used
+  const int j0 = blockIdx.x * NW + wid;                           // grid (ceil(nb0 / NW), nb1, nb2)
+  if (j0 >= nb0) return;                                          // the whole warp: no CTA barrier is used
   double *sw = smw + wid * B::PERW;
   double *Pa = sw + B::OPA, *Pb = sw + B::OPB, *Pc = sw + B::OPC, *Pe = sw + B::OPE;
   double *Tk = sw + B::OT, *Tm = sw + B::OT + 3 * S * W, *F0 = sw + B::OF, *F1 = sw + B::OF + B::S3;
   double *Vs = sw + B::OVS, *Ls = sw + B::OLS;
   const unsigned un = unsigned(n1);
-  const int cc[3] = {c0 + D * (g % nb0), c1 + D * ((g / nb0) % nb1), c2 + D * (g / (nb0 * nb1))};
+  const int cc[3] = {c0 + D * j0, c1 + D * int(blockIdx.y), c2 + D * int(blockIdx.z)};
   const bool tv = tp.valid != 0;
   bool toe[3];
 #pragma unroll
@@ -504,12 +504,13 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_w(int n1, const dou
     // ---- pass y over the group's (plane, lx) pencils: Pc = My Pa + Ky Pb, Pe = My Pb (into Pa's area) ----
     {
       const bool act = lane < B::TY;
-      const int jj = act ? lane / S : 0, px = act ? lane - jj * S : 0;
+      const int jj = act ? lane / S : 0, px = act ? lane - jj * S : 0;   // idle lanes read pencil 0 (unused)
+      const double *pap = Pa + px * TXP + jj * Wn, *pbp = Pb + px * TXP + jj * Wn;
       double pa[Wn], pb[Wn];
 #pragma unroll
       for (int k = 0; k < Wn; ++k) {
-        pa[k] = act ? Pa[px * TXP + jj * Wn + k] : 0.0;
-        pb[k] = act ? Pb[px * TXP + jj * Wn + k] : 0.0;
+        pa[k] = pap[k];
+        pb[k] = pbp[k];
       }
       __syncwarp();
       if (act) {
@@ -520,101 +521,125 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_w(int n1, const dou
     __syncwarp();
     // ---- pass z: r[lz] += Mz[lz][j-lz] Pc_j + Kz[lz][j-lz] Pe_j over the group's planes j ----
     if (vl) {
+      if (toe[2]) {
 #pragma unroll
-      for (int jj = 0; jj < G; ++jj) {
-        const int j = gi * G + jj;
-        const double pc = Pc[jj * PS + lane], pe = Pe[jj * PS + lane];
+        for (int jj = 0; jj < G; ++jj) {
+          const double pc = Pc[jj * PS + lane], pe = Pe[jj * PS + lane];
 #pragma unroll
-        for (int lz = 0; lz < S; ++lz) {
-          const int t = j - lz;
-          if (t < 0 || t >= W) continue;
-          if (toe[2]) r[lz] = fma(tp.k[t], pe, fma(tp.m[t], pc, r[lz]));
-          else r[lz] = fma(Tk[2 * S * W + lz * W + t], pe, fma(Tm[2 * S * W + lz * W + t], pc, r[lz]));
+          for (int lz = 0; lz < S; ++lz) {
+            const int t = gi * G + jj - lz;
+            if (t >= 0 && t < W) r[lz] = fma(tp.k[t], pe, fma(tp.m[t], pc, r[lz]));
+          }
+        }
+      } else {
+        const double *tk = Tk + 2 * S * W, *tm = Tm + 2 * S * W;
+#pragma unroll
+        for (int jj = 0; jj < G; ++jj) {
+          const double pc = Pc[jj * PS + lane], pe = Pe[jj * PS + lane];
+#pragma unroll
+          for (int lz = 0; lz < S; ++lz) {
+            const int t = gi * G + jj - lz;
+            if (t >= 0 && t < W) r[lz] = fma(tk[lz * W + t], pe, fma(tm[lz * W + t], pc, r[lz]));
+          }
         }
       }
     }
     __syncwarp();
   }
   // ---- δ = (⊗V) Λ^{-1} (⊗V)^T (b_B - r), x_B += δ ----
-  auto Vax = [&](int a, int l, int j) { return toe[a] ? tp.v[l * S + j] : Vs[a * S2 + l * S + j]; };
-  auto Lax = [&](int a, int j) { return toe[a] ? tp.lam[j] : Ls[a * S + j]; };
-  double q[S];
-  if (vl) {
+  // this lane's FD operands (x, y), loaded once: Toeplitz axes from the kernel parameter (A27), others from Vs, Ls
+  double vxt[S], vxn[S], vyt[S], vyn[S], lxy = 0.0;
+  if (toe[0]) {
 #pragma unroll
-    for (int lz = 0; lz < S; ++lz) {
-      const int gz = cc[2] - w + lz;
-      const double bz = (xyok && unsigned(gz) < un) ? b[(int64_t(gz - zoff) * n1 + gy) * n1 + gx] : 0.0;
-      F0[lz * S2 + lane] = bz - r[lz];
-    }
+    for (int l = 0; l < S; ++l) { vxt[l] = tp.v[l * S + lx]; vxn[l] = tp.v[lx * S + l]; }
+    lxy = tp.lam[lx];
+  } else {
+#pragma unroll
+    for (int l = 0; l < S; ++l) { vxt[l] = Vs[l * S + lx]; vxn[l] = Vs[lx * S + l]; }
+    lxy = Ls[lx];
   }
-  __syncwarp();
-  if (vl) {                                                       // along x (transposed)
-    double vt[S];
+  if (toe[1]) {
 #pragma unroll
-    for (int l = 0; l < S; ++l) vt[l] = Vax(0, l, lx);
+    for (int l = 0; l < S; ++l) { vyt[l] = tp.v[l * S + ly]; vyn[l] = tp.v[ly * S + l]; }
+    lxy += tp.lam[ly];
+  } else {
 #pragma unroll
-    for (int lz = 0; lz < S; ++lz) {
-      double a0 = 0.0;
-#pragma unroll
-      for (int l = 0; l < S; ++l) a0 = fma(vt[l], F0[lz * S2 + ly * S + l], a0);
-      F1[lz * S2 + lane] = a0;
-    }
+    for (int l = 0; l < S; ++l) { vyt[l] = Vs[S2 + l * S + ly]; vyn[l] = Vs[S2 + ly * S + l]; }
+    lxy += Ls[S + ly];
   }
-  __syncwarp();
-  if (vl) {                                                       // along y (transposed), z (transposed), Λ^{-1}, z
-    double vt[S];
-#pragma unroll
-    for (int l = 0; l < S; ++l) vt[l] = Vax(1, l, ly);
-#pragma unroll
-    for (int lz = 0; lz < S; ++lz) {
-      double a0 = 0.0;
-#pragma unroll
-      for (int l = 0; l < S; ++l) a0 = fma(vt[l], F1[lz * S2 + l * S + lx], a0);
-      q[lz] = a0;
-    }
-    const double lxy = Lax(0, lx) + Lax(1, ly);
+  // z: the lane's S values are register-local; V_z, λ_z are uniform (constant bank when Toeplitz)
+  auto zfd = [&](auto vz, auto lz_, const double (&qi)[S], double (&qo)[S]) {
     double q3[S];
 #pragma unroll
     for (int j = 0; j < S; ++j) {
       double a0 = 0.0;
 #pragma unroll
-      for (int l = 0; l < S; ++l) a0 = fma(Vax(2, l, j), q[l], a0);
-      q3[j] = a0 / (lxy + Lax(2, j));
+      for (int l = 0; l < S; ++l) a0 = fma(vz(l, j), qi[l], a0);
+      q3[j] = a0 / (lxy + lz_(j));
     }
 #pragma unroll
     for (int lz = 0; lz < S; ++lz) {
       double a0 = 0.0;
 #pragma unroll
-      for (int l = 0; l < S; ++l) a0 = fma(Vax(2, lz, l), q3[l], a0);
-      F0[lz * S2 + lane] = a0;                                    // F0's last reads were before the barrier above
+      for (int l = 0; l < S; ++l) a0 = fma(vz(lz, l), q3[l], a0);
+      qo[lz] = a0;
+    }
+  };
+  // the block's points of this lane: column (gx, gy), planes cc[2] - w + lz
+  const int64_t col0 = (int64_t(cc[2] - w - zoff) * n1 + gy) * n1 + gx, pl = int64_t(n1) * n1;
+  double q[S];
+  if (vl) {
+#pragma unroll
+    for (int lz = 0; lz < S; ++lz) {
+      const int gz = cc[2] - w + lz;
+      const double bz = (xyok && unsigned(gz) < un) ? b[col0 + lz * pl] : 0.0;
+      F0[lz * S2 + lane] = bz - r[lz];
     }
   }
   __syncwarp();
-  if (vl) {                                                       // along y
-    double vt[S];
-#pragma unroll
-    for (int l = 0; l < S; ++l) vt[l] = Vax(1, ly, l);
+  if (vl) {                                                       // along x (transposed)
 #pragma unroll
     for (int lz = 0; lz < S; ++lz) {
       double a0 = 0.0;
 #pragma unroll
-      for (int l = 0; l < S; ++l) a0 = fma(vt[l], F0[lz * S2 + l * S + lx], a0);
+      for (int l = 0; l < S; ++l) a0 = fma(vxt[l], F0[lz * S2 + ly * S + l], a0);
+      F1[lz * S2 + lane] = a0;
+    }
+  }
+  __syncwarp();
+  if (vl) {                                                       // along y (transposed), z (transposed), Λ^{-1}, z
+#pragma unroll
+    for (int lz = 0; lz < S; ++lz) {
+      double a0 = 0.0;
+#pragma unroll
+      for (int l = 0; l < S; ++l) a0 = fma(vyt[l], F1[lz * S2 + l * S + lx], a0);
+      q[lz] = a0;
+    }
+    double qo[S];
+    if (toe[2]) zfd([&](int l, int j) { return tp.v[l * S + j]; }, [&](int j) { return tp.lam[j]; }, q, qo);
+    else zfd([&](int l, int j) { return Vs[2 * S2 + l * S + j]; }, [&](int j) { return Ls[2 * S + j]; }, q, qo);
+#pragma unroll
+    for (int lz = 0; lz < S; ++lz) F0[lz * S2 + lane] = qo[lz];   // F0's last reads were before the barrier above
+  }
+  __syncwarp();
+  if (vl) {                                                       // along y
+#pragma unroll
+    for (int lz = 0; lz < S; ++lz) {
+      double a0 = 0.0;
+#pragma unroll
+      for (int l = 0; l < S; ++l) a0 = fma(vyn[l], F0[lz * S2 + l * S + lx], a0);
       F1[lz * S2 + lane] = a0;                                    // F1's last reads: two barriers ago
     }
   }
   __syncwarp();
   if (xyok) {                                                     // along x, and x_B += δ
-    double vt[S];
-#pragma unroll
-    for (int l = 0; l < S; ++l) vt[l] = Vax(0, lx, l);
 #pragma unroll
     for (int lz = 0; lz < S; ++lz) {
       double a0 = 0.0;
 #pragma unroll
-      for (int l = 0; l < S; ++l) a0 = fma(vt[l], F1[lz * S2 + ly * S + l], a0);
-      const int gz = cc[2] - w + lz;
-      if (unsigned(gz) < un) {
-        double *xp = x + (int64_t(gz - zoff) * n1 + gy) * n1 + gx;
+      for (int l = 0; l < S; ++l) a0 = fma(vxn[l], F1[lz * S2 + ly * S + l], a0);
+      if (unsigned(cc[2] - w + lz) < un) {
+        double *xp = x + col0 + lz * pl;
         *xp = *xp + a0;
       }
     }
@@ -664,7 +689,7 @@ void launch_w(int64_t n1, const double *K, const double *M, const double *V, con
   const char *e = std::getenv("IGA2L_PDL");
   if (!(e && e[0] == '0')) {                                   // programmatic dependent launch (as 2D)
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((nblk + NW - 1) / NW);
+    cfg.gridDim = dim3((nb0 + NW - 1) / NW, nb1, nblk / (nb0 * nb1));
     cfg.blockDim = dim3(32 * NW);
     cfg.dynamicSmemBytes = sm;
     cfg.stream = st;
@@ -678,7 +703,7 @@ void launch_w(int64_t n1, const double *K, const double *M, const double *V, con
       return;
     cudaGetLastError();
   }
-  k_schwarz3d_w<P, S, G, NW, MINB, LV><<<(nblk + NW - 1) / NW, 32 * NW, sm, st>>>(
+  k_schwarz3d_w<P, S, G, NW, MINB, LV><<<dim3((nb0 + NW - 1) / NW, nb1, nblk / (nb0 * nb1)), 32 * NW, sm, st>>>(
       int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nblk, zoff, tlo, thi, tp);
 }
 // v5 (warp per block) for the shapes of the 3D configs; IGA2L_S3D_WARP=0 selects v4.  4 warps (blocks) per CTA,
