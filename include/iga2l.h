@@ -204,6 +204,11 @@ int iga2l_host_restriction_1d(int p, int q, int64_t m, int h_factor, double *R);
  * (SURVEY §8(f) row 1).  ENUMERIC if M or K is not SPD. */
 int iga2l_host_coarse_fd(int q, int64_t m, double *V, double *lam);
 
+/* The same for the degree-q level on the n-point TORUS (the torus LFA run's exact second level, 1 <= q <= 2,
+ * 2q+1 <= n <= 4096): circulant K, M from the interior band rows; the constant's eigenvalue is exactly 0
+ * (the run applies the pseudo-inverse).  V: host n*n, lam: host n.  ENUMERIC unless exactly one λ vanishes. */
+int iga2l_host_periodic_fd(int q, int n, double *V, double *lam);
+
 /* Host-only helpers of the quarter annulus (no GPU needed):
  *  tables: per-axis constrained band tables, K and M each [2][n1][2p+1] (axis 0 = ξ: ∫R'R'/s, ∫R R s;
  *          axis 1 = η: ∫N'N' ρ/ρ', ∫N N ρ'/ρ), so that A = My ⊗ Kx + Ky ⊗ Mx;

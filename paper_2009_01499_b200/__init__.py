@@ -61,6 +61,7 @@ def lib():
         "iga2l_apply": (i, [vp, vp, vp]),
         "iga2l_residual_norm": (i, [vp, vp, vp, P(d)]),
         "iga2l_iterate": (i, [vp, vp, vp, i, vp]),
+        "iga2l_host_periodic_fd": (i, [i, i, vp, vp]),
         "iga2l_lfa_torus": (i, [i, i, i, i, i, i, i, ctypes.c_ulonglong, vp, vp]),
         "iga2l_solve": (i, [vp, vp, vp, d, i, P(i), P(d)]),
         "iga2l_sweep": (i, [vp, vp, vp, i, i]),
@@ -131,6 +132,15 @@ def host_coarse_fd(q, m):
     V = np.zeros(n * n)
     lam = np.zeros(n)
     _check(lib().iga2l_host_coarse_fd(q, m, _ptr(V), _ptr(lam)))
+    return V.reshape(n, n), lam
+
+
+def host_periodic_fd(q, n):
+    """1D generalised eigen-decomposition of the degree-q level on the n-point torus (host-only)."""
+    import numpy as np
+    V = np.zeros(n * n)
+    lam = np.zeros(n)
+    _check(lib().iga2l_host_periodic_fd(q, n, _ptr(V), _ptr(lam)))
     return V.reshape(n, n), lam
 
 

@@ -1184,6 +1184,20 @@ int iga2l_host_coarse_fd(int q, int64_t m, double *V, double *lam) {
   return IGA2L_OK;
 }
 
+int iga2l_host_periodic_fd(int q, int n, double *V, double *lam) {
+  if (q < 1 || q > 2 || n < 2 * q + 1 || n > 4096 || !V || !lam) return fail(IGA2L_EPARAM, "host_periodic_fd arguments");
+  const int64_t mb = 4 * (2 * q + 8);
+  std::vector<double> Kb, Mb, v, l;
+  band_tables(q, mb, Kb, Mb);
+  int64_t lo, hi;
+  toeplitz_rows(q, mb, &lo, &hi);
+  const int64_t r = (lo + hi) / 2, W = 2 * q + 1;
+  if (!periodic_fd_tables(q, n, &Kb[r * W], &Mb[r * W], v, l)) return fail(IGA2L_ENUMERIC, "periodic coarse operator");
+  std::memcpy(V, v.data(), v.size() * sizeof(double));
+  std::memcpy(lam, l.data(), l.size() * sizeof(double));
+  return IGA2L_OK;
+}
+
 int iga2l_host_band_tables(int p, int64_t m, double *K, double *M) {
   if (p < 0 || p > 8 || m < 1 || m + p - 2 < 1 || !K || !M) return fail(IGA2L_EPARAM, "host_band_tables arguments");
   std::vector<double> k, mm;

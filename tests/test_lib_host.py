@@ -95,6 +95,43 @@ def test_host_coarse_fd_diagonalises_the_oracle_matrices(q, m):
     assert np.abs(E.ravel() - ref).max() <= 1e-11 * np.abs(ref).max()
 
 
+@pytest.mark.parametrize("q,n", [(1, 7), (1, 24), (2, 12), (2, 30)])
+def test_host_periodic_fd_diagonalises_the_circulant_pencil(q, n):
+    """The torus LFA run's exact second level (iga2l_host_periodic_fd): against the oracle's convolution
+    stencils (oracle.lfa.stencils_1d, h = 1; the library's tables carry another h, so both are compared up to
+    one scale): V diagonalises the circulant pencil (V^T M V ∝ I, V^T K V ∝ diag(λ)); the spectrum equals
+    the closed form k̂(θ_j)/m̂(θ_j), θ_j = 2πj/n (circulant symbols); exactly one λ is 0, with a constant
+    eigenvector."""
+    import numpy as np
+    from oracle.lfa import stencils_1d
+    V, lam = pkg.host_periodic_fd(q, n)
+    _, _, kq, mq, _ = stencils_1d(q, q)
+    K, M = np.zeros((n, n)), np.zeros((n, n))
+    for i in range(n):
+        for d, v in kq.items():
+            K[i, (i + d) % n] += v
+        for d, v in mq.items():
+            M[i, (i + d) % n] += v
+    VMV, VKV = V.T @ M @ V, V.T @ K @ V
+    c = VMV[0, 0]
+    assert np.abs(VMV - c * np.eye(n)).max() <= 1e-12 * c
+    assert np.abs(VKV - np.diag(np.diag(VKV))).max() <= 1e-11 * np.abs(VKV).max()
+    assert np.sum(lam == 0.0) == 1
+    nz = lam != 0.0
+    ratio = np.diag(VKV)[nz] / lam[nz]
+    assert np.abs(ratio / ratio[0] - 1).max() <= 1e-11
+    th = 2 * np.pi * np.arange(n) / n
+    khat = sum(v * np.cos(d * th) for d, v in kq.items())
+    mhat = sum(v * np.cos(d * th) for d, v in mq.items())
+    closed = np.sort(khat / mhat)
+    got = np.sort(lam)
+    assert abs(closed[0]) <= 1e-13 and got[0] == 0.0
+    assert np.abs(got[1:] / got[-1] - closed[1:] / closed[-1]).max() <= 1e-12
+    j0 = int(np.argmin(np.abs(lam)))
+    v0 = V[:, j0]
+    assert np.abs(v0 - v0.mean()).max() <= 1e-12 * np.abs(v0).max()
+
+
 # ---- quarter annulus (P:433-479): the library's host setup against the oracle's 2D assembly ----
 def _dense_band(B, p):
     n1, W = B.shape
