@@ -685,7 +685,9 @@ bool try_schwarz2d_mma(int p, int s, int64_t n1, const double *K, const double *
                        const double *b, double *x, int c0, int c1, int D, int nb0, int nblk, int zoff, cudaStream_t st,
                        const double *fb, int ax) {
   if (p != P || s != S) return false;
-  constexpr int wpc = S >= 5 ? 1 : 4;   // warps (blocks) per CTA, measured best (profiles/variants_wpc_r01.txt)
+  // warps (blocks) per CTA: 1 for s >= 5 (profiles/variants_wpc_r01.txt); 2 for s = 3 under programmatic
+  // dependent launch (C2 step 0.3987 vs 0.4024 ms with 4, p = 3 alone 0.153 vs 0.160 ms; same box)
+  constexpr int wpc = S >= 5 ? 1 : 2;
   launch2d_mma<P, S, wpc>(n1, K, M, V, lam, b, x, c0, c1, D, nb0, nblk, zoff, st, fb, ax);
   return true;
 }
