@@ -1,6 +1,8 @@
 // 3D multicolour Schwarz colour kernel (reading A4, A25): one CTA per block, register-blocked
 // pencil passes for the sum-factorised block residual, then fast diagonalisation.  See kernels.cuh.
 #include <cuda.h>
+#include <type_traits>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -646,6 +648,296 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_w(int n1, const dou
   }
 }
 
+// ---- 3D Schwarz colour kernel, z-chain variant (IGA2L_S3D_CHAIN = L > 0) ----
+// For s = p (both 3D configs) the window length Wn = s + 2p is 3G and the colour spacing D = s + p is 2G with
+// G = (s + p) / 2: the windows of the same-colour blocks (cx, cy, c2 + D k) along z overlap by one plane group
+// (planes oz_k + 2G .. oz_k + 3G are the first group of block k + 1).  One warp runs a segment of L such blocks
+// in ascending z: every plane group passes x and y once and its pass z accumulates into the one or two blocks
+// whose window holds it (2L + 1 groups per segment instead of 3L; the pass-x/y arithmetic and the per-point
+// operation order are those of k_schwarz3d_w, so the result is bitwise equal).  A block's update is written as
+// soon as its last group is accumulated: no later group of the segment reads its points (A4: a same-colour
+// window never holds another block's points), so the segment order is free.  z band rows / FD tables of
+// non-Toeplitz blocks sit in two slots (block parity); the F buffers do not alias the tables (they are reused).
+template <int P, int S>
+struct BZ {
+  using B = BW<P, S, (S + P) / 2>;
+  static constexpr int G = (S + P) / 2, W = B::W, S2 = B::S2, S3 = B::S3;
+  static_assert(B::Wn == 3 * G && B::NG == 3, "z-chain needs s = p");
+  static constexpr int OT = B::AREA;                      // Tk[4 S W]: x, y, z slot 0, z slot 1; Tm after it
+  static constexpr int OTM = OT + 4 * S * W, OF = OTM + 4 * S * W, OVS = OF + 2 * S3, OLS = OVS + 4 * S2;
+  static constexpr int PERW = ((OLS + 4 * S + 1) / 2) * 2;
+};
+
+template <int P, int S, int NW, int MINB, int LV>
+__global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_zc(int n1, const double *__restrict__ K, const double *__restrict__ M,
+                                                         const double *__restrict__ Vt, const double *__restrict__ lamt,
+                                                         const double *__restrict__ b, double *__restrict__ x, int c0,
+                                                         int c1, int c2, int D, int nb0, int nb2, int L, int zoff,
+                                                         int tlo, int thi, const ToeP tp) {
+  using Z = BZ<P, S>;
+  using B = typename Z::B;
+  constexpr int G = Z::G, W = B::W, Wn = B::Wn, w = B::w, S2 = B::S2, TXP = B::TXP, PS = B::PS;
+  extern __shared__ __align__(16) double smw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int j0 = blockIdx.x * NW + wid;
+  if (j0 >= nb0) return;                                          // the whole warp: no CTA barrier is used
+  double *sw = smw + wid * Z::PERW;
+  double *Pa = sw + B::OPA, *Pb = sw + B::OPB, *Pc = sw + B::OPC, *Pe = sw + B::OPE;
+  double *Tk = sw + Z::OT, *Tm = sw + Z::OTM, *F0 = sw + Z::OF, *F1 = sw + Z::OF + Z::S3;
+  double *Vs = sw + Z::OVS, *Ls = sw + Z::OLS;
+  const unsigned un = unsigned(n1);
+  const int k0 = int(blockIdx.z) * L, k1 = min(nb2, k0 + L);
+  const int cx = c0 + D * j0, cy = c1 + D * int(blockIdx.y);
+  const bool tv = tp.valid != 0;
+  const bool toex = tv && cx - w >= tlo && cx + w <= thi, toey = tv && cy - w >= tlo && cy + w <= thi;
+  const int ox = cx - w - P, oy = cy - w - P;
+  const bool xin = ox >= 0 && ox + Wn <= n1;
+  // band rows / FD tables of a boundary axis a (0, 1; z: 2 + slot) centred at c
+  auto load_tab = [&](int a, int c) {
+    for (int i = lane; i < S * W; i += 32) {
+      const int l = i / W, t = i - l * W, gr = c - w + l;
+      const bool ok = unsigned(gr) < un;
+      Tk[a * S * W + i] = ok ? K[int64_t(gr) * W + t] : 0.0;
+      Tm[a * S * W + i] = ok ? M[int64_t(gr) * W + t] : 0.0;
+    }
+    for (int i = lane; i < S2; i += 32) Vs[a * S2 + i] = Vt[int64_t(c) * S2 + i];
+    if (lane < S) Ls[a * S + lane] = lamt[int64_t(c) * S + lane];
+  };
+  auto toe_z = [&](int k) { const int cz = c2 + D * k; return tv && cz - w >= tlo && cz + w <= thi; };
+  if (!toex) load_tab(0, cx);
+  if (!toey) load_tab(1, cy);
+  if (!toe_z(k0)) load_tab(2, c2 + D * k0);
+  const bool vl = lane < S2;
+  const int lx = vl ? lane % S : 0, ly = vl ? lane / S : 0;
+  const int gx = cx - w + lx, gy = cy - w + ly;
+  const bool xyok = vl && unsigned(gx) < un && unsigned(gy) < un;
+  __syncwarp();
+  double vxt[S], vxn[S], vyt[S], vyn[S], lxy = 0.0;
+  if (toex) {
+#pragma unroll
+    for (int l = 0; l < S; ++l) { vxt[l] = tp.v[l * S + lx]; vxn[l] = tp.v[lx * S + l]; }
+    lxy = tp.lam[lx];
+  } else {
+#pragma unroll
+    for (int l = 0; l < S; ++l) { vxt[l] = Vs[l * S + lx]; vxn[l] = Vs[lx * S + l]; }
+    lxy = Ls[lx];
+  }
+  if (toey) {
+#pragma unroll
+    for (int l = 0; l < S; ++l) { vyt[l] = tp.v[l * S + ly]; vyn[l] = tp.v[ly * S + l]; }
+    lxy += tp.lam[ly];
+  } else {
+#pragma unroll
+    for (int l = 0; l < S; ++l) { vyt[l] = Vs[S2 + l * S + ly]; vyn[l] = Vs[S2 + ly * S + l]; }
+    lxy += Ls[S + ly];
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");              // PDL: the previous colour's x (no-op otherwise)
+  // pass x and y of the G planes from absolute plane gzb: Pc/Pe[jj][lane] for the block column (lx, ly)
+  auto group_xy = [&](int gzb) {
+    auto task_x = [&](int t) {
+      const int jj = t / Wn, yy = t - jj * Wn;
+      const int gz = gzb + jj, gyy = oy + yy;
+      const bool rok = unsigned(gz) < un && unsigned(gyy) < un;
+      const int64_t e0 = (int64_t(gz - zoff) * n1 + gyy) * n1 + ox;
+      double v[Wn];
+      if (rok && xin && LV > 1) {
+        constexpr int NV = (Wn + 2 * LV - 2) / LV;
+        double u[NV * LV];
+        const double *ap = x + (e0 & ~int64_t(LV - 1));
+        const int sh = int(e0 & (LV - 1));
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+          if constexpr (LV == 4) {
+            asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                         : "=d"(u[4 * c]), "=d"(u[4 * c + 1]), "=d"(u[4 * c + 2]), "=d"(u[4 * c + 3])
+                         : "l"(ap + 4 * c));
+          } else {
+            const double2 q = __ldg(reinterpret_cast<const double2 *>(ap) + c);
+            u[2 * c] = q.x;
+            u[2 * c + 1] = q.y;
+          }
+        }
+        if constexpr (LV == 4) {
+          double u2[Wn + 1];
+#pragma unroll
+          for (int k = 0; k < Wn + 1; ++k) u2[k] = (sh & 2) ? u[k + 2] : u[k];
+#pragma unroll
+          for (int k = 0; k < Wn; ++k) v[k] = (sh & 1) ? u2[k + 1] : u2[k];
+        } else {
+#pragma unroll
+          for (int k = 0; k < Wn; ++k) v[k] = sh ? u[k + 1] : u[k];
+        }
+      } else if (rok) {
+        const double *rp = x + e0;
+#pragma unroll
+        for (int k = 0; k < Wn; ++k) v[k] = (xin || unsigned(ox + k) < un) ? rp[k] : 0.0;
+      } else {
+#pragma unroll
+        for (int l = 0; l < S; ++l) Pa[l * TXP + t] = Pb[l * TXP + t] = 0.0;
+        return;
+      }
+      if (toex) w_pass_x<P, S, true>(v, Tk, Tm, tp, Pa + t, Pb + t, TXP);
+      else w_pass_x<P, S, false>(v, Tk, Tm, tp, Pa + t, Pb + t, TXP);
+    };
+#pragma unroll 1
+    for (int rr = 0; rr < B::RX; ++rr) {
+      const int t = rr * 32 + lane;
+      if (t < B::TX) task_x(t);
+    }
+    __syncwarp();
+    const bool act = lane < B::TY;
+    const int jj = act ? lane / S : 0, px = act ? lane - jj * S : 0;
+    const double *pap = Pa + px * TXP + jj * Wn, *pbp = Pb + px * TXP + jj * Wn;
+    double pa[Wn], pb[Wn];
+#pragma unroll
+    for (int k = 0; k < Wn; ++k) {
+      pa[k] = pap[k];
+      pb[k] = pbp[k];
+    }
+    __syncwarp();
+    if (act) {
+      if (toey) w_pass_y<P, S, true>(pa, pb, Tk + S * W, Tm + S * W, tp, Pc + jj * PS + px, Pe + jj * PS + px);
+      else w_pass_y<P, S, false>(pa, pb, Tk + S * W, Tm + S * W, tp, Pc + jj * PS + px, Pe + jj * PS + px);
+    }
+    __syncwarp();
+  };
+  // pass z of the current group into r: the group starts R planes into the block's window (compile time)
+  auto acc_z = [&](auto Rc, double (&r)[S], bool toe, int slot) {
+    constexpr int R = decltype(Rc)::value;
+    if (!vl) return;
+    if (toe) {
+#pragma unroll
+      for (int jj = 0; jj < G; ++jj) {
+        const double pc = Pc[jj * PS + lane], pe = Pe[jj * PS + lane];
+#pragma unroll
+        for (int lz = 0; lz < S; ++lz) {
+          const int t = R + jj - lz;
+          if (t >= 0 && t < W) r[lz] = fma(tp.k[t], pe, fma(tp.m[t], pc, r[lz]));
+        }
+      }
+    } else {
+      const double *tk = Tk + (2 + slot) * S * W, *tm = Tm + (2 + slot) * S * W;
+#pragma unroll
+      for (int jj = 0; jj < G; ++jj) {
+        const double pc = Pc[jj * PS + lane], pe = Pe[jj * PS + lane];
+#pragma unroll
+        for (int lz = 0; lz < S; ++lz) {
+          const int t = R + jj - lz;
+          if (t >= 0 && t < W) r[lz] = fma(tk[lz * W + t], pe, fma(tm[lz * W + t], pc, r[lz]));
+        }
+      }
+    }
+  };
+  // δ = (⊗V) Λ^{-1} (⊗V)^T (b_B - r), x_B += δ for block k (z tables in slot)
+  auto solve = [&](int k, const double (&r)[S], bool toe, int slot) {
+    const int cz = c2 + D * k;
+    const int64_t col0 = (int64_t(cz - w - zoff) * n1 + gy) * n1 + gx, pl = int64_t(n1) * n1;
+    if (vl) {
+#pragma unroll
+      for (int lz = 0; lz < S; ++lz) {
+        const int gz = cz - w + lz;
+        const double bz = (xyok && unsigned(gz) < un) ? b[col0 + lz * pl] : 0.0;
+        F0[lz * S2 + lane] = bz - r[lz];
+      }
+    }
+    __syncwarp();
+    if (vl) {
+#pragma unroll
+      for (int lz = 0; lz < S; ++lz) {
+        double a0 = 0.0;
+#pragma unroll
+        for (int l = 0; l < S; ++l) a0 = fma(vxt[l], F0[lz * S2 + ly * S + l], a0);
+        F1[lz * S2 + lane] = a0;
+      }
+    }
+    __syncwarp();
+    double q[S], qo[S];
+    if (vl) {
+#pragma unroll
+      for (int lz = 0; lz < S; ++lz) {
+        double a0 = 0.0;
+#pragma unroll
+        for (int l = 0; l < S; ++l) a0 = fma(vyt[l], F1[lz * S2 + l * S + lx], a0);
+        q[lz] = a0;
+      }
+      const double *vz = Vs + (2 + slot) * S2, *lzs = Ls + (2 + slot) * S;
+      double q3[S];
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        double a0 = 0.0;
+#pragma unroll
+        for (int l = 0; l < S; ++l) a0 = fma(toe ? tp.v[l * S + j] : vz[l * S + j], q[l], a0);
+        q3[j] = a0 / (lxy + (toe ? tp.lam[j] : lzs[j]));
+      }
+#pragma unroll
+      for (int lz = 0; lz < S; ++lz) {
+        double a0 = 0.0;
+#pragma unroll
+        for (int l = 0; l < S; ++l) a0 = fma(toe ? tp.v[lz * S + l] : vz[lz * S + l], q3[l], a0);
+        qo[lz] = a0;
+      }
+#pragma unroll
+      for (int lz = 0; lz < S; ++lz) F0[lz * S2 + lane] = qo[lz];   // F0's last reads were before the barrier above
+    }
+    __syncwarp();
+    if (vl) {
+#pragma unroll
+      for (int lz = 0; lz < S; ++lz) {
+        double a0 = 0.0;
+#pragma unroll
+        for (int l = 0; l < S; ++l) a0 = fma(vyn[l], F0[lz * S2 + l * S + lx], a0);
+        F1[lz * S2 + lane] = a0;
+      }
+    }
+    __syncwarp();
+    if (xyok) {
+#pragma unroll
+      for (int lz = 0; lz < S; ++lz) {
+        double a0 = 0.0;
+#pragma unroll
+        for (int l = 0; l < S; ++l) a0 = fma(vxn[l], F1[lz * S2 + ly * S + l], a0);
+        if (unsigned(cz - w + lz) < un) {
+          double *xp = x + col0 + lz * pl;
+          *xp = *xp + a0;
+        }
+      }
+    }
+    __syncwarp();                                                 // F1's reads are done before the next solve
+  };
+  using C0 = std::integral_constant<int, 0>;
+  using CG = std::integral_constant<int, G>;
+  using C2G = std::integral_constant<int, 2 * G>;
+  double rc[S];
+#pragma unroll
+  for (int lz = 0; lz < S; ++lz) rc[lz] = 0.0;
+  bool tc = toe_z(k0);
+  group_xy(c2 + D * k0 - w - P);
+  asm volatile("griddepcontrol.launch_dependents;");              // PDL: the next colour may launch
+  acc_z(C0{}, rc, tc, 0);
+  __syncwarp();
+#pragma unroll 1
+  for (int k = k0; k < k1; ++k) {
+    const int slot = (k - k0) & 1, oz = c2 + D * k - w - P;
+    group_xy(oz + G);
+    acc_z(CG{}, rc, tc, slot);
+    const bool nx = k + 1 < k1;
+    const bool tn = nx && toe_z(k + 1);
+    if (nx && !tn) load_tab(2 + (slot ^ 1), c2 + D * (k + 1));   // the other slot: its last reader was block k-1
+    __syncwarp();
+    group_xy(oz + 2 * G);
+    acc_z(C2G{}, rc, tc, slot);
+    double rn[S];
+#pragma unroll
+    for (int lz = 0; lz < S; ++lz) rn[lz] = 0.0;
+    if (nx) acc_z(C0{}, rn, tn, slot ^ 1);
+    __syncwarp();
+    solve(k, rc, tc, slot);
+#pragma unroll
+    for (int lz = 0; lz < S; ++lz) rc[lz] = rn[lz];
+    tc = tn;
+  }
+}
+
 // IGA2L_S3D_TMA=0: window by cp.async rows.  Read per launch (tests switch it within one process).
 inline bool env_on(const char *name) {
   const char *e = std::getenv(name);
@@ -706,6 +998,34 @@ void launch_w(int64_t n1, const double *K, const double *M, const double *V, con
   k_schwarz3d_w<P, S, G, NW, MINB, LV><<<dim3((nb0 + NW - 1) / NW, nb1, nblk / (nb0 * nb1)), 32 * NW, sm, st>>>(
       int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nblk, zoff, tlo, thi, tp);
 }
+// z-chain variant: NW warps per CTA, grid (ceil(nb0 / NW), nb1, ceil(nb2 / L)), PDL as v5
+template <int P, int S, int NW, int MINB, int LV>
+void launch_zc(int64_t n1, const double *K, const double *M, const double *V, const double *lam, const double *b,
+               double *x, int c0, int c1, int c2, int D, int nb0, int nb1, int nb2, int L, int zoff, int tlo, int thi,
+               cudaStream_t st, const ToeP &tp) {
+  constexpr size_t sm = sizeof(double) * BZ<P, S>::PERW * NW;
+  ensure_smem(k_schwarz3d_zc<P, S, NW, MINB, LV>, sm);
+  const dim3 grid((nb0 + NW - 1) / NW, nb1, (nb2 + L - 1) / L);
+  const char *e = std::getenv("IGA2L_PDL");
+  if (!(e && e[0] == '0')) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(32 * NW);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, k_schwarz3d_zc<P, S, NW, MINB, LV>, int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0,
+                           nb2, L, zoff, tlo, thi, tp) == cudaSuccess)
+      return;
+    cudaGetLastError();
+  }
+  k_schwarz3d_zc<P, S, NW, MINB, LV><<<grid, 32 * NW, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb2, L,
+                                                                zoff, tlo, thi, tp);
+}
 // v5 (warp per block) for the shapes of the 3D configs; IGA2L_S3D_WARP=0 selects v4.  4 warps (blocks) per CTA,
 // at most 128 registers (4 CTAs per SM).
 template <int P, int S, int G>
@@ -716,6 +1036,15 @@ bool try_schwarz3d_w(int p, int s, int64_t n1, const double *K, const double *M,
   ToeP tp{};
   if (tpp) tp = *tpp;
   const int nblk = nb0 * nb1 * nb2;
+  if constexpr (P == S) {
+    const char *ce = std::getenv("IGA2L_S3D_CHAIN");              // z-chain segments of L blocks (0: off)
+    const int L = ce ? std::atoi(ce) : 0;
+    if (L > 0 && !(reinterpret_cast<uintptr_t>(x) & 31)) {
+      launch_zc<P, S, 4, 4, (P == 5 ? 2 : 4)>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, L, zoff, tlo, thi,
+                                             st, tp);
+      return true;
+    }
+  }
   // 32-byte row loads need a 32-byte aligned x (every torch / cudaMalloc allocation is)
   // row loads: 16 bytes at p = 5 (170.5 vs 173.3 us per C5 colour with 32), 32 bytes at p = 3 (25.96 vs 26.20 us
   // per C4 colour); 8 bytes when x is not 32-byte aligned.  More CTAs per SM (96 / 80 registers) measured

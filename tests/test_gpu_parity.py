@@ -402,6 +402,35 @@ def test_3d_sweep_zchunk_schedule_bitwise(mb, monkeypatch):
     assert np.array_equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("p,q,m", [(3, 1, 8), (3, 1, 20), (5, 2, 10), (5, 2, 24)])
+def test_3d_sweep_zchain_bitwise(p, q, m, monkeypatch):
+    """The z-chain colour kernel (IGA2L_S3D_CHAIN = L: one warp sweeps L same-colour blocks along z, each plane
+    group's pass x / y shared by the two blocks whose windows hold it) performs v5's arithmetic per point in
+    the same order: bitwise equal sweeps for every segment length, incl. segments longer than the column and
+    the misaligned-x fallback; and equal to the oracle's sweep."""
+    ctx = make_ctx(3, p, q, m, p, "vcycle", 2)
+    b, x0 = cu(random_rhs(ctx.N)), cu(initial_guess(ctx.N))
+    outs = {}
+    for L in ("0", "1", "2", "3", "64"):
+        monkeypatch.setenv("IGA2L_S3D_CHAIN", L)
+        x = x0.clone()
+        ctx.sweep(b, x)
+        outs[L] = host(x)
+    buf = torch.zeros(ctx.N + 1, dtype=torch.float64, device=DEV)   # x at an 8-byte offset: v5's fallback
+    buf[1:] = x0
+    ctx.sweep(b, buf[1:])
+    outs["mis"] = host(buf[1:])
+    for L, o in outs.items():
+        assert np.array_equal(outs["0"], o), L
+    xo = host(x0)
+    if m > 20:                                   # matrix-free Kronecker oracle (pinned == TwoLevel)
+        from oracle.kron import KronTwoLevel
+        KronTwoLevel(3, p, q, m, p).sweep(xo, host(b))
+    else:
+        oracle_for(f"3d_p{p}", 3, p, q, m, p, "vcycle", 2).smoother.sweep(xo, host(b))
+    assert np.abs(outs["2"] - xo).max() <= 1e-11 * np.abs(xo).max()
+
+
 @pytest.mark.parametrize("p,m", [(3, 20), (5, 12)])
 @pytest.mark.parametrize("env", [{"IGA2L_APPLY_STREAM": "0"}, {"IGA2L_STREAM_CFG": "1"}, {"IGA2L_STREAM_CFG": "2"},
                                  {"IGA2L_STREAM_CFG": "3"}], ids=["tiled", "cfg1", "cfg2", "cfg3"])

@@ -1,0 +1,83 @@
+"""A/B of the 3D z-chain colour kernel (IGA2L_S3D_CHAIN = L, segments of L same-colour blocks along z) against
+v5 (L = 0): bitwise agreement of one sweep at small and config sizes, and the time of full sweeps replayed
+from CUDA graphs (as in the iteration).  python tools/zchain_ab.py [configs...]   (default: C4 C5)"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2009_01499_b200 as pkg  # noqa: E402
+from synthetic_inputs import CONFIGS, initial_guess, random_rhs  # noqa: E402
+
+LS = [int(v) for v in os.environ.get("ZC_LS", "0,1,2,3,4,6,8,32").split(",")]
+
+
+def agree(p, q, m, s):
+    ctx = pkg.Context(3, p, q, m, s, coarse_mode=pkg.COARSE_VCYCLE, coarse_h_factor=2)
+    b = torch.tensor(random_rhs(ctx.N, seed=1), device="cuda")
+    x0 = torch.tensor(initial_guess(ctx.N), device="cuda")
+    ok = True
+    ref = None
+    for L in LS:
+        os.environ["IGA2L_S3D_CHAIN"] = str(L)
+        x = x0.clone()
+        ctx.sweep(b, x)
+        torch.cuda.synchronize()
+        if ref is None:
+            ref = x
+        eq = torch.equal(x, ref)
+        ok &= eq
+        print(f"agree p={p} m={m} L={L}: bitwise {eq}", flush=True)
+    ctx.close()
+    return ok
+
+
+def timing(name, reps):
+    c = CONFIGS[name]
+    st = torch.cuda.Stream()
+    torch.cuda.set_stream(st)
+    ctx = pkg.Context(3, c["p"], c["q"], c["m"], c["s"], coarse_mode=pkg.COARSE_VCYCLE, coarse_h_factor=2,
+                      stream=st.cuda_stream)
+    b = torch.empty(ctx.N, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    ctx.rhs_sine(b)
+    x0 = torch.tensor(initial_guess(ctx.N), device="cuda")
+    x = x0.clone()
+    ncol = ctx.info().colours
+    ref = None
+    for L in LS:
+        os.environ["IGA2L_S3D_CHAIN"] = str(L)
+        ctx.sweep(b, x)
+        g = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=st):
+            ctx.sweep(b, x)
+        x.copy_(x0)
+        g.replay()
+        torch.cuda.synchronize()
+        if ref is None:
+            ref = x.clone()
+        eq = torch.equal(x, ref)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            g.replay()
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        print(f"{name} IGA2L_S3D_CHAIN={L}: sweep {ms:.3f} ms, {1000 * ms / ncol:.2f} us/colour (graph); "
+              f"bitwise equal to L=0: {eq}", flush=True)
+        del g
+    os.environ.pop("IGA2L_S3D_CHAIN", None)
+    ctx.close()
+
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or ["C4", "C5"]
+    ok = True
+    for p, q, m, s in [(3, 1, 8, 3), (3, 1, 20, 3), (5, 2, 10, 5), (5, 2, 32, 5), (3, 1, 48, 3)]:
+        ok &= agree(p, q, m, s)
+    for n in names:
+        timing(n, 3 if n == "C5" else 20)
+    print("AGREE_OK" if ok else "AGREE_FAIL")
