@@ -2,6 +2,7 @@
 // Contract: include/iga2l.h.  Paper: arXiv 2009.01499 (P:<line> = /root/reference/PAPER.md).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost nothing without a profiler attached
 #include <nccl.h>   // types only; the library is dlopen'ed (the process may already hold torch's copy)
 
 #include <algorithm>
@@ -288,15 +289,34 @@ void L_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
   }
 }
 
+// NVTX range for the host-side scope of an API call or phase (profiler timelines; a no-op otherwise)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 // One iteration of Algorithm 1, ν1 = 1, ν2 = 0.
 void L_iteration(iga2l_ctx *c, const double *b, double *x, bool with_norm) {
-  L_sweep(c, b, x, 0, c->colours);                           // u^1 = u^0 + S_p(b - A_p u^0)
-  L_apply(c, x, b, c->r, nullptr, 1);                        // d_p = b - A_p u^1
+  {
+    NvtxRange r("iga2l: Schwarz sweep (D^d colours)");
+    L_sweep(c, b, x, 0, c->colours);                         // u^1 = u^0 + S_p(b - A_p u^0)
+  }
   const Band1D *Ry = c->ax ? &c->Ry.b : nullptr, *RTy = c->ax ? &c->RTy.b : nullptr;
-  L_tensor(c, c->dim, c->R.b, c->r, c->lev[0].b, c->t1, c->t2, 0, Ry);   // d_q = I_p^q d_p
-  L_vcycle(c, 0);                                            // A_q e_q = d_q (exact or one V(1,1))
-  L_tensor(c, c->dim, c->RT.b, c->lev[0].x, x, c->t1, c->t2, 1, RTy);     // u^1 += I_q^p e_q
+  {
+    NvtxRange r("iga2l: defect + restriction");
+    L_apply(c, x, b, c->r, nullptr, 1);                      // d_p = b - A_p u^1
+    L_tensor(c, c->dim, c->R.b, c->r, c->lev[0].b, c->t1, c->t2, 0, Ry);   // d_q = I_p^q d_p
+  }
+  {
+    NvtxRange r("iga2l: second level");
+    L_vcycle(c, 0);                                          // A_q e_q = d_q (exact or one V(1,1))
+  }
+  {
+    NvtxRange r("iga2l: prolongation");
+    L_tensor(c, c->dim, c->RT.b, c->lev[0].x, x, c->t1, c->t2, 1, RTy);   // u^1 += I_q^p e_q
+  }
   if (with_norm) {
+    NvtxRange r("iga2l: residual norm");
     L_norm(c, x, b, true);
   }
 }
@@ -374,7 +394,10 @@ int run_iterations(iga2l_ctx *c, const double *b, double *x, int iters, bool wit
     g->x = x;
     g->norm = int(with_norm);
   }
-  for (int k = 0; k < iters; ++k) CU(cudaGraphLaunch(g->exec, c->st));
+  for (int k = 0; k < iters; ++k) {
+    NvtxRange r("iga2l: iteration (graph launch)");
+    CU(cudaGraphLaunch(g->exec, c->st));
+  }
   return IGA2L_OK;
 }
 
@@ -1003,6 +1026,7 @@ int iga2l_residual_norm(iga2l_ctx *c, const double *b, const double *x, double *
 }
 
 int iga2l_iterate(iga2l_ctx *c, const double *b, double *x, int iters, double *res_hist) {
+  NvtxRange nvtx_("iga2l_iterate");
   if (int rc = check_ctx(c)) return rc;
   if (iters < 0) return fail(IGA2L_EPARAM, "iters must be >= 0");
   if (int rc = ensure_staging(c)) return rc;
@@ -1049,6 +1073,7 @@ int iga2l_lfa_torus(int dim, int p, int q, int n, int block, int h_factor, int i
 
 int iga2l_solve(iga2l_ctx *c, const double *b, double *x, double rtol, int maxit, int *iters_out,
                 double *relres_out) {
+  NvtxRange nvtx_("iga2l_solve");
   if (int rc = check_ctx(c)) return rc;
   if (!(rtol > 0.0) || maxit < 0) return fail(IGA2L_EPARAM, "rtol must be > 0 and maxit >= 0");
   if (int rc = ensure_staging(c)) return rc;
@@ -1092,6 +1117,7 @@ int iga2l_solve(iga2l_ctx *c, const double *b, double *x, double rtol, int maxit
 }
 
 int iga2l_sweep(iga2l_ctx *c, const double *b, double *x, int c0, int c1) {
+  NvtxRange nvtx_("iga2l_sweep");
   if (int rc = check_ctx(c)) return rc;
   if (c->nranks > 1) return fail(IGA2L_EPARAM, "phase entry points are single-domain only (nranks == 1)");
   if (c0 < 0 || c1 < c0 || c1 > c->colours) return fail(IGA2L_EPARAM, "colour range must satisfy 0 <= begin <= end <= D^d");

@@ -657,36 +657,54 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_w(int n1, const dou
 // operation order are those of k_schwarz3d_w, so the result is bitwise equal).  A block's update is written as
 // soon as its last group is accumulated: no later group of the segment reads its points (A4: a same-colour
 // window never holds another block's points), so the segment order is free.  z band rows / FD tables of
-// non-Toeplitz blocks sit in two slots (block parity); the F buffers do not alias the tables (they are reused).
-template <int P, int S>
+// non-Toeplitz blocks sit in two slots (block parity); the solve buffers F0/F1 overlay the pass buffers, not the
+// tables (the x/y tables serve every block of the segment).
+template <int P, int S, int GP>
 struct BZ {
-  using B = BW<P, S, (S + P) / 2>;
-  static constexpr int G = (S + P) / 2, W = B::W, S2 = B::S2, S3 = B::S3;
-  static_assert(B::Wn == 3 * G && B::NG == 3, "z-chain needs s = p");
-  static constexpr int OT = B::AREA;                      // Tk[4 S W]: x, y, z slot 0, z slot 1; Tm after it
-  static constexpr int OTM = OT + 4 * S * W, OF = OTM + 4 * S * W, OVS = OF + 2 * S3, OLS = OVS + 4 * S2;
+  static constexpr int G = (S + P) / 2, W = 2 * P + 1, Wn = S + 2 * P, w = (S - 1) / 2, S2 = S * S, S3 = S2 * S;
+  static_assert(Wn == 3 * G && (GP == G || GP == 2 * G), "z-chain needs s = p");
+  static constexpr int TX = GP * Wn, TY = GP * S;
+  static_assert(TY <= 32 && S2 <= 32, "group shape");
+  static constexpr bool ok_txp(int t) {
+    for (int h = 0; h < 2; ++h)
+      for (int i = 16 * h; i < 16 * h + 16 && i < TY; ++i)
+        for (int k = i + 1; k < 16 * h + 16 && k < TY; ++k)
+          if (((i % S) * t + (i / S) * Wn) % 16 == ((k % S) * t + (k / S) * Wn) % 16) return false;
+    return true;
+  }
+  static constexpr int find_txp() {
+    for (int t = TX; t < TX + 64; ++t)
+      if (ok_txp(t)) return t;
+    return TX;
+  }
+  static constexpr int TXP = find_txp();
+  static constexpr int PS = S2 + ((S - S2 % 16) % 16 + 16) % 16;
+  static constexpr int A1 = (2 * S * TXP > 2 * GP * PS ? 2 * S * TXP : 2 * GP * PS);
+  static constexpr int AREA = (A1 > 2 * S3 ? A1 : 2 * S3);   // Pa/Pb | Pc/Pe | F0/F1 (the solve's buffers)
+  static constexpr int OPA = 0, OPB = S * TXP, OPC = 0, OPE = GP * PS, OF = 0;
+  static constexpr int OT = AREA;                           // Tk[4 S W]: x, y, z slot 0, z slot 1; Tm after it
+  static constexpr int OTM = OT + 4 * S * W, OVS = OTM + 4 * S * W, OLS = OVS + 4 * S2;
   static constexpr int PERW = ((OLS + 4 * S + 1) / 2) * 2;
 };
 
-template <int P, int S, int NW, int MINB, int LV>
+template <int P, int S, int GP, int NW, int MINB, int LV>
 __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_zc(int n1, const double *__restrict__ K, const double *__restrict__ M,
                                                          const double *__restrict__ Vt, const double *__restrict__ lamt,
                                                          const double *__restrict__ b, double *__restrict__ x, int c0,
                                                          int c1, int c2, int D, int nb0, int nb2, int L, int zoff,
                                                          int tlo, int thi, const ToeP tp) {
-  using Z = BZ<P, S>;
-  using B = typename Z::B;
-  constexpr int G = Z::G, W = B::W, Wn = B::Wn, w = B::w, S2 = B::S2, TXP = B::TXP, PS = B::PS;
+  using Z = BZ<P, S, GP>;
+  constexpr int G = Z::G, W = Z::W, Wn = Z::Wn, w = Z::w, S2 = Z::S2, TXP = Z::TXP, PS = Z::PS;
   extern __shared__ __align__(16) double smw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int j0 = blockIdx.x * NW + wid;
   if (j0 >= nb0) return;                                          // the whole warp: no CTA barrier is used
   double *sw = smw + wid * Z::PERW;
-  double *Pa = sw + B::OPA, *Pb = sw + B::OPB, *Pc = sw + B::OPC, *Pe = sw + B::OPE;
+  double *Pa = sw + Z::OPA, *Pb = sw + Z::OPB, *Pc = sw + Z::OPC, *Pe = sw + Z::OPE;
   double *Tk = sw + Z::OT, *Tm = sw + Z::OTM, *F0 = sw + Z::OF, *F1 = sw + Z::OF + Z::S3;
   double *Vs = sw + Z::OVS, *Ls = sw + Z::OLS;
   const unsigned un = unsigned(n1);
-  const int k0 = int(blockIdx.z) * L, k1 = min(nb2, k0 + L);
+  const int k0 = int(blockIdx.z) * L, k1 = min(nb2, k0 + L);       // segment blockIdx.z: L blocks (the last short)
   const int cx = c0 + D * j0, cy = c1 + D * int(blockIdx.y);
   const bool tv = tp.valid != 0;
   const bool toex = tv && cx - w >= tlo && cx + w <= thi, toey = tv && cy - w >= tlo && cy + w <= thi;
@@ -712,28 +730,10 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_zc(int n1, const do
   const int gx = cx - w + lx, gy = cy - w + ly;
   const bool xyok = vl && unsigned(gx) < un && unsigned(gy) < un;
   __syncwarp();
-  double vxt[S], vxn[S], vyt[S], vyn[S], lxy = 0.0;
-  if (toex) {
-#pragma unroll
-    for (int l = 0; l < S; ++l) { vxt[l] = tp.v[l * S + lx]; vxn[l] = tp.v[lx * S + l]; }
-    lxy = tp.lam[lx];
-  } else {
-#pragma unroll
-    for (int l = 0; l < S; ++l) { vxt[l] = Vs[l * S + lx]; vxn[l] = Vs[lx * S + l]; }
-    lxy = Ls[lx];
-  }
-  if (toey) {
-#pragma unroll
-    for (int l = 0; l < S; ++l) { vyt[l] = tp.v[l * S + ly]; vyn[l] = tp.v[ly * S + l]; }
-    lxy += tp.lam[ly];
-  } else {
-#pragma unroll
-    for (int l = 0; l < S; ++l) { vyt[l] = Vs[S2 + l * S + ly]; vyn[l] = Vs[S2 + ly * S + l]; }
-    lxy += Ls[S + ly];
-  }
   asm volatile("griddepcontrol.wait;" ::: "memory");              // PDL: the previous colour's x (no-op otherwise)
-  // pass x and y of the G planes from absolute plane gzb: Pc/Pe[jj][lane] for the block column (lx, ly)
-  auto group_xy = [&](int gzb) {
+  // pass x and y of NP (compile time) planes from absolute plane gzb: Pc/Pe[jj][lane] for the column (lx, ly)
+  auto group_xy = [&](auto NPc, int gzb) {
+    constexpr int NP = decltype(NPc)::value, TX = NP * Wn, RX = (TX + 31) / 32, TY = NP * S;
     auto task_x = [&](int t) {
       const int jj = t / Wn, yy = t - jj * Wn;
       const int gz = gzb + jj, gyy = oy + yy;
@@ -780,12 +780,12 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_zc(int n1, const do
       else w_pass_x<P, S, false>(v, Tk, Tm, tp, Pa + t, Pb + t, TXP);
     };
 #pragma unroll 1
-    for (int rr = 0; rr < B::RX; ++rr) {
+    for (int rr = 0; rr < RX; ++rr) {
       const int t = rr * 32 + lane;
-      if (t < B::TX) task_x(t);
+      if (t < TX) task_x(t);
     }
     __syncwarp();
-    const bool act = lane < B::TY;
+    const bool act = lane < TY;
     const int jj = act ? lane / S : 0, px = act ? lane - jj * S : 0;
     const double *pap = Pa + px * TXP + jj * Wn, *pbp = Pb + px * TXP + jj * Wn;
     double pa[Wn], pb[Wn];
@@ -801,13 +801,14 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_zc(int n1, const do
     }
     __syncwarp();
   };
-  // pass z of the current group into r: the group starts R planes into the block's window (compile time)
-  auto acc_z = [&](auto Rc, double (&r)[S], bool toe, int slot) {
-    constexpr int R = decltype(Rc)::value;
+  // pass z of the NP planes just passed into r: plane jj is window plane R + jj of r's block (compile time)
+  auto acc_z = [&](auto NPc, auto Rc, double (&r)[S], bool toe, int slot) {
+    constexpr int NP = decltype(NPc)::value, R = decltype(Rc)::value;
     if (!vl) return;
     if (toe) {
 #pragma unroll
-      for (int jj = 0; jj < G; ++jj) {
+      for (int jj = 0; jj < NP; ++jj) {
+        if (R + jj < 0 || R + jj - (S - 1) >= W) continue;
         const double pc = Pc[jj * PS + lane], pe = Pe[jj * PS + lane];
 #pragma unroll
         for (int lz = 0; lz < S; ++lz) {
@@ -818,7 +819,8 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_zc(int n1, const do
     } else {
       const double *tk = Tk + (2 + slot) * S * W, *tm = Tm + (2 + slot) * S * W;
 #pragma unroll
-      for (int jj = 0; jj < G; ++jj) {
+      for (int jj = 0; jj < NP; ++jj) {
+        if (R + jj < 0 || R + jj - (S - 1) >= W) continue;
         const double pc = Pc[jj * PS + lane], pe = Pe[jj * PS + lane];
 #pragma unroll
         for (int lz = 0; lz < S; ++lz) {
@@ -828,9 +830,28 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_zc(int n1, const do
       }
     }
   };
-  // δ = (⊗V) Λ^{-1} (⊗V)^T (b_B - r), x_B += δ for block k (z tables in slot)
+  // δ = (⊗V) Λ^{-1} (⊗V)^T (b_B - r), x_B += δ for block k (z tables in slot); F0/F1 overlay Pa..Pe
   auto solve = [&](int k, const double (&r)[S], bool toe, int slot) {
     const int cz = c2 + D * k;
+    double vxt[S], vxn[S], vyt[S], vyn[S], lxy = 0.0;
+    if (toex) {
+#pragma unroll
+      for (int l = 0; l < S; ++l) { vxt[l] = tp.v[l * S + lx]; vxn[l] = tp.v[lx * S + l]; }
+      lxy = tp.lam[lx];
+    } else {
+#pragma unroll
+      for (int l = 0; l < S; ++l) { vxt[l] = Vs[l * S + lx]; vxn[l] = Vs[lx * S + l]; }
+      lxy = Ls[lx];
+    }
+    if (toey) {
+#pragma unroll
+      for (int l = 0; l < S; ++l) { vyt[l] = tp.v[l * S + ly]; vyn[l] = tp.v[ly * S + l]; }
+      lxy += tp.lam[ly];
+    } else {
+#pragma unroll
+      for (int l = 0; l < S; ++l) { vyt[l] = Vs[S2 + l * S + ly]; vyn[l] = Vs[S2 + ly * S + l]; }
+      lxy += Ls[S + ly];
+    }
     const int64_t col0 = (int64_t(cz - w - zoff) * n1 + gy) * n1 + gx, pl = int64_t(n1) * n1;
     if (vl) {
 #pragma unroll
@@ -851,8 +872,25 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_zc(int n1, const do
       }
     }
     __syncwarp();
-    double q[S], qo[S];
+    auto zfd = [&](auto vz, auto lz_, const double (&qi)[S], double (&qo)[S]) {
+      double q3[S];
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+        double a0 = 0.0;
+#pragma unroll
+        for (int l = 0; l < S; ++l) a0 = fma(vz(l, j), qi[l], a0);
+        q3[j] = a0 / (lxy + lz_(j));
+      }
+#pragma unroll
+      for (int lz = 0; lz < S; ++lz) {
+        double a0 = 0.0;
+#pragma unroll
+        for (int l = 0; l < S; ++l) a0 = fma(vz(lz, l), q3[l], a0);
+        qo[lz] = a0;
+      }
+    };
     if (vl) {
+      double q[S], qo[S];
 #pragma unroll
       for (int lz = 0; lz < S; ++lz) {
         double a0 = 0.0;
@@ -860,21 +898,10 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_zc(int n1, const do
         for (int l = 0; l < S; ++l) a0 = fma(vyt[l], F1[lz * S2 + l * S + lx], a0);
         q[lz] = a0;
       }
-      const double *vz = Vs + (2 + slot) * S2, *lzs = Ls + (2 + slot) * S;
-      double q3[S];
-#pragma unroll
-      for (int j = 0; j < S; ++j) {
-        double a0 = 0.0;
-#pragma unroll
-        for (int l = 0; l < S; ++l) a0 = fma(toe ? tp.v[l * S + j] : vz[l * S + j], q[l], a0);
-        q3[j] = a0 / (lxy + (toe ? tp.lam[j] : lzs[j]));
-      }
-#pragma unroll
-      for (int lz = 0; lz < S; ++lz) {
-        double a0 = 0.0;
-#pragma unroll
-        for (int l = 0; l < S; ++l) a0 = fma(toe ? tp.v[lz * S + l] : vz[lz * S + l], q3[l], a0);
-        qo[lz] = a0;
+      if (toe) zfd([&](int l, int j) { return tp.v[l * S + j]; }, [&](int j) { return tp.lam[j]; }, q, qo);
+      else {
+        const double *vz = Vs + (2 + slot) * S2, *lzs = Ls + (2 + slot) * S;
+        zfd([&](int l, int j) { return vz[l * S + j]; }, [&](int j) { return lzs[j]; }, q, qo);
       }
 #pragma unroll
       for (int lz = 0; lz < S; ++lz) F0[lz * S2 + lane] = qo[lz];   // F0's last reads were before the barrier above
@@ -902,34 +929,41 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_zc(int n1, const do
         }
       }
     }
-    __syncwarp();                                                 // F1's reads are done before the next solve
+    __syncwarp();                                                 // F1's reads are done before Pa/Pb are rewritten
   };
-  using C0 = std::integral_constant<int, 0>;
   using CG = std::integral_constant<int, G>;
-  using C2G = std::integral_constant<int, 2 * G>;
+  using CGP = std::integral_constant<int, GP>;
   double rc[S];
 #pragma unroll
   for (int lz = 0; lz < S; ++lz) rc[lz] = 0.0;
   bool tc = toe_z(k0);
-  group_xy(c2 + D * k0 - w - P);
+  group_xy(CG{}, c2 + D * k0 - w - P);                            // the first block's first plane group
   asm volatile("griddepcontrol.launch_dependents;");              // PDL: the next colour may launch
-  acc_z(C0{}, rc, tc, 0);
+  acc_z(CG{}, std::integral_constant<int, 0>{}, rc, tc, 0);
   __syncwarp();
 #pragma unroll 1
   for (int k = k0; k < k1; ++k) {
     const int slot = (k - k0) & 1, oz = c2 + D * k - w - P;
-    group_xy(oz + G);
-    acc_z(CG{}, rc, tc, slot);
     const bool nx = k + 1 < k1;
     const bool tn = nx && toe_z(k + 1);
-    if (nx && !tn) load_tab(2 + (slot ^ 1), c2 + D * (k + 1));   // the other slot: its last reader was block k-1
-    __syncwarp();
-    group_xy(oz + 2 * G);
-    acc_z(C2G{}, rc, tc, slot);
     double rn[S];
+    if (nx && !tn) load_tab(2 + (slot ^ 1), c2 + D * (k + 1));   // the other slot: its last reader was block k-1
+    if constexpr (GP == 2 * G) {                                  // planes oz + G .. oz + 3G in one group
+      group_xy(CGP{}, oz + G);
+      acc_z(CGP{}, CG{}, rc, tc, slot);
 #pragma unroll
-    for (int lz = 0; lz < S; ++lz) rn[lz] = 0.0;
-    if (nx) acc_z(C0{}, rn, tn, slot ^ 1);
+      for (int lz = 0; lz < S; ++lz) rn[lz] = 0.0;
+      if (nx) acc_z(CGP{}, std::integral_constant<int, -G>{}, rn, tn, slot ^ 1);
+    } else {                                                      // two groups of G planes
+      group_xy(CG{}, oz + G);
+      acc_z(CG{}, CG{}, rc, tc, slot);
+      __syncwarp();
+      group_xy(CG{}, oz + 2 * G);
+      acc_z(CG{}, std::integral_constant<int, 2 * G>{}, rc, tc, slot);
+#pragma unroll
+      for (int lz = 0; lz < S; ++lz) rn[lz] = 0.0;
+      if (nx) acc_z(CG{}, std::integral_constant<int, 0>{}, rn, tn, slot ^ 1);
+    }
     __syncwarp();
     solve(k, rc, tc, slot);
 #pragma unroll
@@ -998,13 +1032,33 @@ void launch_w(int64_t n1, const double *K, const double *M, const double *V, con
   k_schwarz3d_w<P, S, G, NW, MINB, LV><<<dim3((nb0 + NW - 1) / NW, nb1, nblk / (nb0 * nb1)), 32 * NW, sm, st>>>(
       int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nblk, zoff, tlo, thi, tp);
 }
-// z-chain variant: NW warps per CTA, grid (ceil(nb0 / NW), nb1, ceil(nb2 / L)), PDL as v5
-template <int P, int S, int NW, int MINB, int LV>
+// Segment length of the z-chain: a wave-quantised makespan model, ceil(warps / resident warp slots) waves of
+// (2 L + 1) plane groups each.  C5 (nb = 26): L = 4, 7 segments, 4732 warps = two full waves (model 18 vs 24 for
+// v5; measured 153.5 vs 162.7 us per colour, same box; L = 3 157.7, 2 161.6, 9 164.2, 5 170.2, 6 187.7).  Segments of
+// near-equal length measured slower (169 us at 7 segments) and were dropped.
+inline int zchain_length(int nb0, int nb1, int nb2) {
+  static int slots = 0;
+  if (!slots) {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    slots = sms * 16;                                             // 4 CTAs x 4 warps per SM
+  }
+  const int64_t cols = int64_t(nb0) * nb1;
+  int best = 1;
+  int64_t bc = -1;
+  for (int L = 1; L <= nb2; ++L) {
+    const int64_t segs = (nb2 + L - 1) / L, c = ((cols * segs + slots - 1) / slots) * (2 * L + 1);
+    if (bc < 0 || c < bc) { bc = c; best = L; }
+  }
+  return best;
+}
+// z-chain variant: NW warps per CTA, grid (ceil(nb0 / NW), nb1, ceil(nb2 / L)) for segments of L blocks, PDL as v5
+template <int P, int S, int GP, int NW, int MINB, int LV>
 void launch_zc(int64_t n1, const double *K, const double *M, const double *V, const double *lam, const double *b,
                double *x, int c0, int c1, int c2, int D, int nb0, int nb1, int nb2, int L, int zoff, int tlo, int thi,
                cudaStream_t st, const ToeP &tp) {
-  constexpr size_t sm = sizeof(double) * BZ<P, S>::PERW * NW;
-  ensure_smem(k_schwarz3d_zc<P, S, NW, MINB, LV>, sm);
+  constexpr size_t sm = sizeof(double) * BZ<P, S, GP>::PERW * NW;
+  ensure_smem(k_schwarz3d_zc<P, S, GP, NW, MINB, LV>, sm);
   const dim3 grid((nb0 + NW - 1) / NW, nb1, (nb2 + L - 1) / L);
   const char *e = std::getenv("IGA2L_PDL");
   if (!(e && e[0] == '0')) {
@@ -1018,12 +1072,12 @@ void launch_zc(int64_t n1, const double *K, const double *M, const double *V, co
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, k_schwarz3d_zc<P, S, NW, MINB, LV>, int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0,
+    if (cudaLaunchKernelEx(&cfg, k_schwarz3d_zc<P, S, GP, NW, MINB, LV>, int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0,
                            nb2, L, zoff, tlo, thi, tp) == cudaSuccess)
       return;
     cudaGetLastError();
   }
-  k_schwarz3d_zc<P, S, NW, MINB, LV><<<grid, 32 * NW, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb2, L,
+  k_schwarz3d_zc<P, S, GP, NW, MINB, LV><<<grid, 32 * NW, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb2, L,
                                                                 zoff, tlo, thi, tp);
 }
 // v5 (warp per block) for the shapes of the 3D configs; IGA2L_S3D_WARP=0 selects v4.  4 warps (blocks) per CTA,
@@ -1037,11 +1091,26 @@ bool try_schwarz3d_w(int p, int s, int64_t n1, const double *K, const double *M,
   if (tpp) tp = *tpp;
   const int nblk = nb0 * nb1 * nb2;
   if constexpr (P == S) {
-    const char *ce = std::getenv("IGA2L_S3D_CHAIN");              // z-chain segments of L blocks (0: off)
-    const int L = ce ? std::atoi(ce) : 0;
+    // z-chain (IGA2L_S3D_CHAIN): "0" off, L > 0 segments of L blocks, unset / "auto": zchain_length's L at p = 5
+    // (v5 measured faster at p = 3, C4: 25.6 vs 29.3 us per colour at the best L, same box)
+    const char *ce = std::getenv("IGA2L_S3D_CHAIN");
+    int L = 0;
+    if (ce && ce[0] >= '0' && ce[0] <= '9') {
+      L = std::atoi(ce);
+    } else if (P == 5) {
+      L = zchain_length(nb0, nb1, nb2);
+      if (L <= 1) L = 0;                                          // one block per warp: v5 is that, faster
+    }
     if (L > 0 && !(reinterpret_cast<uintptr_t>(x) & 31)) {
-      launch_zc<P, S, 4, 4, (P == 5 ? 2 : 4)>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, L, zoff, tlo, thi,
-                                             st, tp);
+      constexpr int GZ = (S + P) / 2, GP = (2 * GZ * S <= 32 ? 2 * GZ : GZ);   // 2G-plane groups where they fit a warp
+      const char *lv = std::getenv("IGA2L_S3D_CHAIN_LV");         // A/B: row load width (doubles)
+      if (lv && lv[0] == '1')
+        launch_zc<P, S, GP, 4, 4, 1>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, L, zoff, tlo, thi, st, tp);
+      else if (lv && lv[0] == '4')
+        launch_zc<P, S, GP, 4, 4, 4>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, L, zoff, tlo, thi, st, tp);
+      else
+        launch_zc<P, S, GP, 4, 4, (P == 5 ? 2 : 4)>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, L, zoff, tlo,
+                                                   thi, st, tp);
       return true;
     }
   }

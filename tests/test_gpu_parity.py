@@ -312,8 +312,9 @@ def test_3d_sweep_variants(cfg, monkeypatch):
     ctx = make_ctx(d, p, q, m, s, coarse, hf)
     b, x0 = random_rhs(ctx.N), initial_guess(ctx.N)
     outs = {}
-    for key, env in (("v5", {}), ("v4", {"IGA2L_S3D_WARP": "0"}), ("v4rows", {"IGA2L_S3D_WARP": "0", "IGA2L_S3D_TMA": "0"})):
-        for k in ("IGA2L_S3D_WARP", "IGA2L_S3D_TMA"):
+    for key, env in (("v5", {"IGA2L_S3D_CHAIN": "0"}), ("v4", {"IGA2L_S3D_WARP": "0"}),
+                     ("v4rows", {"IGA2L_S3D_WARP": "0", "IGA2L_S3D_TMA": "0"})):
+        for k in ("IGA2L_S3D_WARP", "IGA2L_S3D_TMA", "IGA2L_S3D_CHAIN"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
@@ -404,15 +405,18 @@ def test_3d_sweep_zchunk_schedule_bitwise(mb, monkeypatch):
 
 @pytest.mark.parametrize("p,q,m", [(3, 1, 8), (3, 1, 20), (5, 2, 10), (5, 2, 24)])
 def test_3d_sweep_zchain_bitwise(p, q, m, monkeypatch):
-    """The z-chain colour kernel (IGA2L_S3D_CHAIN = L: one warp sweeps L same-colour blocks along z, each plane
+    """The z-chain colour kernel (IGA2L_S3D_CHAIN = L: one warp sweeps ~L same-colour blocks along z, each plane
     group's pass x / y shared by the two blocks whose windows hold it) performs v5's arithmetic per point in
     the same order: bitwise equal sweeps for every segment length, incl. segments longer than the column and
     the misaligned-x fallback; and equal to the oracle's sweep."""
     ctx = make_ctx(3, p, q, m, p, "vcycle", 2)
     b, x0 = cu(random_rhs(ctx.N)), cu(initial_guess(ctx.N))
     outs = {}
-    for L in ("0", "1", "2", "3", "64"):
-        monkeypatch.setenv("IGA2L_S3D_CHAIN", L)
+    for L in ("0", "1", "2", "3", "64", "auto"):
+        if L == "auto":
+            monkeypatch.delenv("IGA2L_S3D_CHAIN", raising=False)     # the default (chain at p = 5, v5 at p = 3)
+        else:
+            monkeypatch.setenv("IGA2L_S3D_CHAIN", L)
         x = x0.clone()
         ctx.sweep(b, x)
         outs[L] = host(x)

@@ -1,4 +1,4 @@
-"""A/B of the 3D z-chain colour kernel (IGA2L_S3D_CHAIN = L, segments of L same-colour blocks along z) against
+"""A/B of the 3D z-chain colour kernel (IGA2L_S3D_CHAIN = L, segments of about L same-colour blocks along z; "auto" = the default) against
 v5 (L = 0): bitwise agreement of one sweep at small and config sizes, and the time of full sweeps replayed
 from CUDA graphs (as in the iteration).  python tools/zchain_ab.py [configs...]   (default: C4 C5)"""
 import os
@@ -10,7 +10,14 @@ import torch  # noqa: E402
 import paper_2009_01499_b200 as pkg  # noqa: E402
 from synthetic_inputs import CONFIGS, initial_guess, random_rhs  # noqa: E402
 
-LS = [int(v) for v in os.environ.get("ZC_LS", "0,1,2,3,4,6,8,32").split(",")]
+LS = os.environ.get("ZC_LS", "0,auto,2,3,4,6").split(",")
+
+
+def setL(L):
+    if L == "auto":
+        os.environ.pop("IGA2L_S3D_CHAIN", None)
+    else:
+        os.environ["IGA2L_S3D_CHAIN"] = L
 
 
 def agree(p, q, m, s):
@@ -20,7 +27,7 @@ def agree(p, q, m, s):
     ok = True
     ref = None
     for L in LS:
-        os.environ["IGA2L_S3D_CHAIN"] = str(L)
+        setL(L)
         x = x0.clone()
         ctx.sweep(b, x)
         torch.cuda.synchronize()
@@ -33,7 +40,10 @@ def agree(p, q, m, s):
     return ok
 
 
-def timing(name, reps):
+def timing(name, reps, rounds=5):
+    """One graph per variant (knobs are read at capture), replayed round-robin `rounds` times x `reps` sweeps:
+    the same box, interleaved, median per variant.  Variant "LvK": segments of L blocks with K-double row loads."""
+    import statistics
     c = CONFIGS[name]
     st = torch.cuda.Stream()
     torch.cuda.set_stream(st)
@@ -45,9 +55,11 @@ def timing(name, reps):
     x0 = torch.tensor(initial_guess(ctx.N), device="cuda")
     x = x0.clone()
     ncol = ctx.info().colours
-    ref = None
+    graphs, ref = {}, None
     for L in LS:
-        os.environ["IGA2L_S3D_CHAIN"] = str(L)
+        base, _, lv = L.partition("v")              # "4v1": L = 4 with 8-byte row loads
+        setL(base)
+        os.environ["IGA2L_S3D_CHAIN_LV"] = lv or "0"
         ctx.sweep(b, x)
         g = torch.cuda.CUDAGraph()
         torch.cuda.synchronize()
@@ -58,18 +70,25 @@ def timing(name, reps):
         torch.cuda.synchronize()
         if ref is None:
             ref = x.clone()
-        eq = torch.equal(x, ref)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        for _ in range(reps):
-            g.replay()
-        e1.record(st)
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / reps
-        print(f"{name} IGA2L_S3D_CHAIN={L}: sweep {ms:.3f} ms, {1000 * ms / ncol:.2f} us/colour (graph); "
-              f"bitwise equal to L=0: {eq}", flush=True)
-        del g
+        print(f"{name} {L}: bitwise equal to {LS[0]}: {torch.equal(x, ref)}", flush=True)
+        graphs[L] = g
     os.environ.pop("IGA2L_S3D_CHAIN", None)
+    os.environ.pop("IGA2L_S3D_CHAIN_LV", None)
+    times = {L: [] for L in LS}
+    for _ in range(rounds):
+        for L in LS:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(reps):
+                graphs[L].replay()
+            e1.record(st)
+            torch.cuda.synchronize()
+            times[L].append(e0.elapsed_time(e1) / reps)
+    for L in LS:
+        ms = statistics.median(times[L])
+        print(f"{name} IGA2L_S3D_CHAIN={L}: sweep {ms:.3f} ms, {1000 * ms / ncol:.2f} us/colour (graph, median of "
+              f"{rounds} interleaved rounds; min {1000 * min(times[L]) / ncol:.2f})", flush=True)
+    del graphs
     ctx.close()
 
 
@@ -79,5 +98,5 @@ if __name__ == "__main__":
     for p, q, m, s in [(3, 1, 8, 3), (3, 1, 20, 3), (5, 2, 10, 5), (5, 2, 32, 5), (3, 1, 48, 3)]:
         ok &= agree(p, q, m, s)
     for n in names:
-        timing(n, 3 if n == "C5" else 20)
+        timing(n, 1 if n == "C5" else 10)
     print("AGREE_OK" if ok else "AGREE_FAIL")
