@@ -456,7 +456,9 @@ def main():
     else:
         roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic, "traffic_kernel": traffic_kernel,
-                    "kernel": "k_schwarz3d_w (v5: FP64 FMA block solves, one warp per block, one launch per colour)",
+                    "kernel": ("k_schwarz3d_zc (z-chain: one warp per segment of same-colour blocks along z, FP64 FMA "
+                               "block solves, one launch per colour)" if ctxs[0].p == 5 else
+                               "k_schwarz3d_w (v5: FP64 FMA block solves, one warp per block, one launch per colour)"),
                     "peak_source": "derived 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md)", "note": note}
     roofline["hbm_kernels"] = {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                                for k, v in kr.items() if k not in ("sweep", "hbm_peak_GBps", "hbm_peak_source")}
