@@ -420,6 +420,13 @@ def test_3d_sweep_zchain_bitwise(p, q, m, monkeypatch):
         x = x0.clone()
         ctx.sweep(b, x)
         outs[L] = host(x)
+    monkeypatch.setenv("IGA2L_S3D_CHAIN", "2")
+    for lv in ("1", "4"):                        # row-load width A/B knob
+        monkeypatch.setenv("IGA2L_S3D_CHAIN_LV", lv)
+        x = x0.clone()
+        ctx.sweep(b, x)
+        outs["lv" + lv] = host(x)
+    monkeypatch.delenv("IGA2L_S3D_CHAIN_LV", raising=False)
     buf = torch.zeros(ctx.N + 1, dtype=torch.float64, device=DEV)   # x at an 8-byte offset: v5's fallback
     buf[1:] = x0
     ctx.sweep(b, buf[1:])
