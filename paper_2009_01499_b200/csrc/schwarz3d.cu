@@ -687,7 +687,7 @@ struct BZ {
   static constexpr int PERW = ((OLS + 4 * S + 1) / 2) * 2;
 };
 
-template <int P, int S, int GP, int NW, int MINB, int LV, bool ONEG>
+template <int P, int S, int GP, int NW, int MINB, int LV>
 __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_zc(int n1, const double *__restrict__ K, const double *__restrict__ M,
                                                          const double *__restrict__ Vt, const double *__restrict__ lamt,
                                                          const double *__restrict__ b, double *__restrict__ x, int c0,
@@ -937,7 +937,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_zc(int n1, const do
 #pragma unroll
   for (int lz = 0; lz < S; ++lz) rc[lz] = 0.0;
   bool tc = toe_z(k0);
-  if constexpr (ONEG && GP == G) {
+  if constexpr (GP == G) {
     // one loop over the segment's 2 (k1 - k0) + 1 plane groups (a single inlined copy of the passes): group g
     // is plane group g / 2 of block k0 + g / 2 - 1 (even g > 0: its last, R = 2G) and the first of block
     // k0 + g / 2 (even g, R = 0); odd g is the middle group (R = G) of block k0 + (g - 1) / 2
@@ -970,7 +970,8 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_zc(int n1, const do
     }
     return;
   }
-  group_xy(CG{}, c2 + D * k0 - w - P);                            // the first block's first plane group
+  // GP == 2G (p = 3 shape): the first group of G planes, then per block one group of 2G planes (oz + G .. oz + 3G)
+  group_xy(CG{}, c2 + D * k0 - w - P);
   asm volatile("griddepcontrol.launch_dependents;");              // PDL: the next colour may launch
   acc_z(CG{}, std::integral_constant<int, 0>{}, rc, tc, 0);
   __syncwarp();
@@ -981,22 +982,11 @@ __global__ void __launch_bounds__(32 * NW, MINB) k_schwarz3d_zc(int n1, const do
     const bool tn = nx && toe_z(k + 1);
     double rn[S];
     if (nx && !tn) load_tab(2 + (slot ^ 1), c2 + D * (k + 1));   // the other slot: its last reader was block k-1
-    if constexpr (GP == 2 * G) {                                  // planes oz + G .. oz + 3G in one group
-      group_xy(CGP{}, oz + G);
-      acc_z(CGP{}, CG{}, rc, tc, slot);
+    group_xy(CGP{}, oz + G);
+    acc_z(CGP{}, CG{}, rc, tc, slot);
 #pragma unroll
-      for (int lz = 0; lz < S; ++lz) rn[lz] = 0.0;
-      if (nx) acc_z(CGP{}, std::integral_constant<int, -G>{}, rn, tn, slot ^ 1);
-    } else {                                                      // two groups of G planes
-      group_xy(CG{}, oz + G);
-      acc_z(CG{}, CG{}, rc, tc, slot);
-      __syncwarp();
-      group_xy(CG{}, oz + 2 * G);
-      acc_z(CG{}, std::integral_constant<int, 2 * G>{}, rc, tc, slot);
-#pragma unroll
-      for (int lz = 0; lz < S; ++lz) rn[lz] = 0.0;
-      if (nx) acc_z(CG{}, std::integral_constant<int, 0>{}, rn, tn, slot ^ 1);
-    }
+    for (int lz = 0; lz < S; ++lz) rn[lz] = 0.0;
+    if (nx) acc_z(CGP{}, std::integral_constant<int, -G>{}, rn, tn, slot ^ 1);
     __syncwarp();
     solve(k, rc, tc, slot);
 #pragma unroll
@@ -1086,12 +1076,12 @@ inline int zchain_length(int nb0, int nb1, int nb2) {
   return best;
 }
 // z-chain variant: NW warps per CTA, grid (ceil(nb0 / NW), nb1, ceil(nb2 / L)) for segments of L blocks, PDL as v5
-template <int P, int S, int GP, int NW, int MINB, int LV, bool ONEG = false>
+template <int P, int S, int GP, int NW, int MINB, int LV>
 void launch_zc(int64_t n1, const double *K, const double *M, const double *V, const double *lam, const double *b,
                double *x, int c0, int c1, int c2, int D, int nb0, int nb1, int nb2, int L, int zoff, int tlo, int thi,
                cudaStream_t st, const ToeP &tp) {
   constexpr size_t sm = sizeof(double) * BZ<P, S, GP>::PERW * NW;
-  ensure_smem(k_schwarz3d_zc<P, S, GP, NW, MINB, LV, ONEG>, sm);
+  ensure_smem(k_schwarz3d_zc<P, S, GP, NW, MINB, LV>, sm);
   const dim3 grid((nb0 + NW - 1) / NW, nb1, (nb2 + L - 1) / L);
   const char *e = std::getenv("IGA2L_PDL");
   if (!(e && e[0] == '0')) {
@@ -1105,12 +1095,12 @@ void launch_zc(int64_t n1, const double *K, const double *M, const double *V, co
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, k_schwarz3d_zc<P, S, GP, NW, MINB, LV, ONEG>, int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0,
+    if (cudaLaunchKernelEx(&cfg, k_schwarz3d_zc<P, S, GP, NW, MINB, LV>, int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0,
                            nb2, L, zoff, tlo, thi, tp) == cudaSuccess)
       return;
     cudaGetLastError();
   }
-  k_schwarz3d_zc<P, S, GP, NW, MINB, LV, ONEG><<<grid, 32 * NW, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb2, L,
+  k_schwarz3d_zc<P, S, GP, NW, MINB, LV><<<grid, 32 * NW, sm, st>>>(int(n1), K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb2, L,
                                                                 zoff, tlo, thi, tp);
 }
 // v5 (warp per block) for the shapes of the 3D configs; IGA2L_S3D_WARP=0 selects v4.  4 warps (blocks) per CTA,
@@ -1141,9 +1131,6 @@ bool try_schwarz3d_w(int p, int s, int64_t n1, const double *K, const double *M,
         launch_zc<P, S, GP, 4, 4, 1>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, L, zoff, tlo, thi, st, tp);
       else if (lv && lv[0] == '4')
         launch_zc<P, S, GP, 4, 4, 4>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, L, zoff, tlo, thi, st, tp);
-      else if (lv && lv[0] == 'g')                                // A/B: the single-loop schedule
-        launch_zc<P, S, GP, 4, 4, (P == 5 ? 2 : 4), true>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, L, zoff,
-                                                         tlo, thi, st, tp);
       else
         launch_zc<P, S, GP, 4, 4, (P == 5 ? 2 : 4)>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, L, zoff, tlo,
                                                    thi, st, tp);
