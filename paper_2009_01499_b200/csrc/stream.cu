@@ -15,6 +15,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -171,34 +173,48 @@ __global__ void __launch_bounds__(NT_, S3<P, TY, NT_>::MINB)
         phase ^= 1u << s;
         const double *X = stage + s * WY * ROW;
         const int pbase = int(int64_t(gi - zoff) * plane + int64_t(y0 - P) * n1 + (x0 - P));
-        for (int task = tid; task < WY * (TX / 2); task += NT) {   // pass x: (row, 2 outputs)
-          const int wy = task / (TX / 2), l0 = (task - wy * (TX / 2)) * 2;
-          const int sh = (pbase + wy * n1) & 1;                     // row start parity (see S3::BOX)
-          double v[2 + 2 * P];
-#pragma unroll
-          for (int k = 0; k < 2 + 2 * P; ++k) v[k] = X[wy * ROW + sh + l0 + k];
+        // pass x: a task is (row, 2 outputs); a warp takes two rows of EQUAL start parity (rows wy, wy + 2), so
+        // the parity shift is warp-uniform and the window comes in by 16-byte loads at a 16-byte lane stride
+        // (conflict-free quarter-warps) from the even element at or below the first needed one
+        constexpr int HC = (WY + 1) / 2, TC = (HC + 1) / 2;          // rows per parity class, warp tasks per class
+        for (int wt = tid >> 5; wt < 2 * TC; wt += NT / 32) {
+          const int cls = wt / TC, wy = cls + 2 * (2 * (wt - cls * TC) + ((tid >> 4) & 1)), l0 = (tid & 15) * 2;
+          if (wy >= WY) continue;
+          const double2 *Xr = reinterpret_cast<const double2 *>(X + wy * ROW + l0);
           double a0 = 0.0, a1 = 0.0, m0 = 0.0, m1 = 0.0;
-          if (toex) {
+          auto row = [&](auto shc) {
+            constexpr int SH = decltype(shc)::value, NV = (2 + 2 * P + SH + 1) / 2;
+            double v[2 * NV];
 #pragma unroll
-            for (int t = 0; t < W; ++t) {
-              a0 = fma(tp.k[t], v[t], a0);
-              a1 = fma(tp.k[t], v[t + 1], a1);
-              m0 = fma(tp.m[t], v[t], m0);
-              m1 = fma(tp.m[t], v[t + 1], m1);
+            for (int k = 0; k < NV; ++k) {
+              const double2 t2 = Xr[k];
+              v[2 * k] = t2.x;
+              v[2 * k + 1] = t2.y;
             }
-          } else {
+            if (toex) {
 #pragma unroll
-            for (int t = 0; t < W; ++t) {
-              a0 = fma(ckx[l0 * W + t], v[t], a0);
-              a1 = fma(ckx[(l0 + 1) * W + t], v[t + 1], a1);
-              m0 = fma(cmx[l0 * W + t], v[t], m0);
-              m1 = fma(cmx[(l0 + 1) * W + t], v[t + 1], m1);
+              for (int t = 0; t < W; ++t) {
+                a0 = fma(tp.k[t], v[SH + t], a0);
+                a1 = fma(tp.k[t], v[SH + t + 1], a1);
+                m0 = fma(tp.m[t], v[SH + t], m0);
+                m1 = fma(tp.m[t], v[SH + t + 1], m1);
+              }
+            } else {
+#pragma unroll
+              for (int t = 0; t < W; ++t) {
+                a0 = fma(ckx[l0 * W + t], v[SH + t], a0);
+                a1 = fma(ckx[(l0 + 1) * W + t], v[SH + t + 1], a1);
+                m0 = fma(cmx[l0 * W + t], v[SH + t], m0);
+                m1 = fma(cmx[(l0 + 1) * W + t], v[SH + t + 1], m1);
+              }
             }
-          }
-          pa[wy * TX + l0] = a0;
-          pa[wy * TX + l0 + 1] = a1;
-          pb[wy * TX + l0] = m0;
-          pb[wy * TX + l0 + 1] = m1;
+          };
+          if ((pbase + cls * n1) & 1)             // row start parity (see S3::BOX); equal for rows cls, cls + 2, ...
+            row(std::integral_constant<int, 1>{});
+          else
+            row(std::integral_constant<int, 0>{});
+          *reinterpret_cast<double2 *>(pa + wy * TX + l0) = make_double2(a0, a1);
+          *reinterpret_cast<double2 *>(pb + wy * TX + l0) = make_double2(m0, m1);
         }
       }
       __syncthreads();                        // Pa/Pb ready; stage s consumed
