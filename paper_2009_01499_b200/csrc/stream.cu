@@ -79,25 +79,25 @@ namespace {
 // 3D: work = (x,y) tiles of TX x TY outputs times the z planes, linearised tile-major; a persistent CTA
 // takes one contiguous segment of it (a few tiles' z ranges, so no wave quantisation and a z-halo only
 // at segment ends).  Thread (lx, ly0) owns the OY outputs (lx, ly0 .. ly0+OY-1) of every output plane.
-template <int P, int TY, int NT_>
+template <int P, int TY, int NT_, int MB = 0>
 struct S3 {
   // BOX = WX + 2: TMA row starts must be 16-byte aligned, so a row is loaded from the even element at or
   // below its first needed element and read with a shift of 0 or 1 (odd n1 alternates the parity)
   static constexpr int TX = 32, W = 2 * P + 1, WX = TX + 2 * P, BOX = WX + 2, ROW = ((BOX + 15) / 16) * 16;
   static constexpr int WY = TY + 2 * P;
-  static constexpr int NS = 4, NT = NT_, OY = TX * TY / NT, MINB = 65536 / (NT * 128) > 0 ? 65536 / (NT * 128) : 1;
+  static constexpr int NS = 4, NT = NT_, OY = TX * TY / NT;
+  static constexpr int MINB = MB ? MB : (65536 / (NT * 128) > 0 ? 65536 / (NT * 128) : 1);
   static constexpr int NDBL = NS * WY * ROW + 4 * WY * TX + 2 * TX * W + 2 * TY * W;
   static constexpr size_t SMEM = sizeof(double) * (NDBL + 32) + 8 * NS;
-  static_assert(WY <= 32, "one TMA row per lane of warp 0");
 };
 
-template <int P, int TY, int NT_>
-__global__ void __launch_bounds__(NT_, S3<P, TY, NT_>::MINB)
+template <int P, int TY, int NT_, int MB = 0>
+__global__ void __launch_bounds__(NT_, S3<P, TY, NT_, MB>::MINB)
     k_apply3d_tma(const __grid_constant__ CUtensorMap xmap, int n1, const double *__restrict__ K,
                   const double *__restrict__ M, const double *__restrict__ b, double *__restrict__ y,
                   double *__restrict__ partial, int mode, int zoff, int zlo0, int nz, int64_t work, int tlo,
                   int thi, const ToeP tp) {
-  using A = S3<P, TY, NT_>;
+  using A = S3<P, TY, NT_, MB>;
   constexpr int TX = A::TX, W = A::W, ROW = A::ROW, WY = A::WY, NS = A::NS, NT = A::NT, OY = A::OY;
   extern __shared__ __align__(128) double sm[];
   double *stage = sm;                         // [NS][WY][ROW]  input plane windows
@@ -141,16 +141,18 @@ __global__ void __launch_bounds__(NT_, S3<P, TY, NT_>::MINB)
     }
     __syncthreads();
     const int gs = zlo - P, ge = zhi + P;     // input planes [gs, ge)
-    auto issue = [&](int gi, int s) {         // warp 0: plane gi's WY window rows into stage s
+    // plane gi's WY window rows into stage s: lane 0 of warp w issues rows w, w + NT/32, ... (a TMA issue is
+    // per thread, so one issuing warp would be WY issues late at every plane's CTA barrier: 24% of the stall
+    // samples); the expect-tx arrival may follow some of the copies' complete-tx (the count is signed)
+    auto issue = [&](int gi, int s) {
       if (unsigned(gi) >= unsigned(n1)) return;
       if (tid == 0) mbar_expect_tx(&bar[s], WY * A::BOX * 8);
-      __syncwarp();
-      if (tid < WY)
-        tma_load_1d(stage + (s * WY + tid) * ROW, &xmap,
-                    int(int64_t(gi - zoff) * plane + int64_t(y0 - P + tid) * n1 + (x0 - P)) & ~1, &bar[s]);
+      if ((tid & 31) == 0)
+        for (int r = tid >> 5; r < WY; r += NT / 32)
+          tma_load_1d(stage + (s * WY + r) * ROW, &xmap,
+                      int(int64_t(gi - zoff) * plane + int64_t(y0 - P + r) * n1 + (x0 - P)) & ~1, &bar[s]);
     };
-    if (tid < 32)
-      for (int k = 0; k < NS && gs + k < ge; ++k) issue(gs + k, (it + k) % NS);
+    for (int k = 0; k < NS && gs + k < ge; ++k) issue(gs + k, (it + k) % NS);
     double acc[W][OY];
 #pragma unroll
     for (int j = 0; j < W; ++j)
@@ -218,7 +220,7 @@ __global__ void __launch_bounds__(NT_, S3<P, TY, NT_>::MINB)
         }
       }
       __syncthreads();                        // Pa/Pb ready; stage s consumed
-      if (tid < 32 && gi + NS < ge) issue(gi + NS, s);
+      if (gi + NS < ge) issue(gi + NS, s);
       double c[OY], e[OY];
 #pragma unroll
       for (int o = 0; o < OY; ++o) c[o] = e[o] = 0.0;
@@ -291,16 +293,17 @@ __global__ void __launch_bounds__(NT_, S3<P, TY, NT_>::MINB)
   }
 }
 
-// A/B knob IGA2L_STREAM_CFG: 1 = TY 8 / 256 threads, 2 = TY 16 / 256 threads, 3 = TY 16 / 512 threads
+// A/B knob IGA2L_STREAM_CFG: 1 = TY 8 / 256 threads, 2 = TY 16 / 256 threads, 3 = TY 16 / 512 threads,
+// 4 / 5 = TY 8 / 256 threads at 3 / 4 CTAs per SM (80 / 64 registers)
 int stream_cfg() {                                   // read per call (tests switch it within one process)
   const char *e = std::getenv("IGA2L_STREAM_CFG");
   return e ? std::atoi(e) : 0;
 }
 
-template <int P, int TY, int NT>
+template <int P, int TY, int NT, int MB = 0>
 bool go_stream3d(int64_t n1, const double *K, const double *M, const double *x, const double *b, double *y,
                  double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv, const ToeP *tpp, bool count) {
-  using A = S3<P, TY, NT>;
+  using A = S3<P, TY, NT, MB>;
   const int nz = sv.zhi - sv.zlo;
   const int64_t tiles = ((n1 + A::TX - 1) / A::TX) * ((n1 + TY - 1) / TY), work = tiles * nz;
   // persistent: MINB CTAs per SM; segments no shorter than 8p planes (z halo <= 25%)
@@ -313,8 +316,8 @@ bool go_stream3d(int64_t n1, const double *K, const double *M, const double *x, 
   ToeP tp{};
   if (tpp) tp = *tpp;
   const int m = int(n1) - P + 2;
-  ensure_smem(k_apply3d_tma<P, TY, NT>, A::SMEM);
-  k_apply3d_tma<P, TY, NT><<<grid, NT, A::SMEM, st>>>(map, int(n1), K, M, b, y, partial, mode, sv.zoff, sv.zlo, nz,
+  ensure_smem(k_apply3d_tma<P, TY, NT, MB>, A::SMEM);
+  k_apply3d_tma<P, TY, NT, MB><<<grid, NT, A::SMEM, st>>>(map, int(n1), K, M, b, y, partial, mode, sv.zoff, sv.zlo, nz,
                                                       work, 2 * P - 1, m - 2 - P, tp);
   return true;
 }
@@ -323,18 +326,25 @@ template <int P>
 bool try_stream3d(int p, int64_t n1, const double *K, const double *M, const double *x, const double *b, double *y,
                   double *partial, int mode, cudaStream_t st, int *nparts, SlabView sv, const ToeP *tpp, bool count) {
   if (p != P) return false;
-  // measured (C4 p = 3, C5 p = 5): TY 8 / 256 threads for p <= 4, TY 16 / 256 threads above
+  // measured (C4 p = 3, C5 p = 5): TY 8 / 256 threads at 3 CTAs per SM (80 registers) for p <= 4 (C4 65.5 us; 2 CTAs
+  // 70.7, 4 CTAs at 64 registers 84), TY 16 / 256 threads at 2 CTAs per SM above (C5 510 us; TY 8 at 3 CTAs 613,
+  // 512 threads 583)
   if (count) {                                        // partial-buffer sizing: the most any config writes
     int a = 0, c = 0, d = 0;
     go_stream3d<P, 8, 256>(n1, K, M, x, b, y, partial, mode, st, &a, sv, tpp, true);
     go_stream3d<P, 16, 256>(n1, K, M, x, b, y, partial, mode, st, &c, sv, tpp, true);
     go_stream3d<P, 16, 512>(n1, K, M, x, b, y, partial, mode, st, &d, sv, tpp, true);
-    if (nparts) *nparts = std::max(a, std::max(c, d));
+    int e = 0, f = 0;
+    go_stream3d<P, 8, 256, 3>(n1, K, M, x, b, y, partial, mode, st, &e, sv, tpp, true);
+    go_stream3d<P, 8, 256, 4>(n1, K, M, x, b, y, partial, mode, st, &f, sv, tpp, true);
+    if (nparts) *nparts = std::max(std::max(a, e), std::max(c, std::max(d, f)));
     return true;
   }
-  const int cfg = stream_cfg() ? stream_cfg() : (P <= 4 ? 1 : 2);
+  const int cfg = stream_cfg() ? stream_cfg() : (P <= 4 ? 4 : 2);
   if (cfg == 1) return go_stream3d<P, 8, 256>(n1, K, M, x, b, y, partial, mode, st, nparts, sv, tpp, count);
   if (cfg == 2) return go_stream3d<P, 16, 256>(n1, K, M, x, b, y, partial, mode, st, nparts, sv, tpp, count);
+  if (cfg == 4) return go_stream3d<P, 8, 256, 3>(n1, K, M, x, b, y, partial, mode, st, nparts, sv, tpp, count);
+  if (cfg == 5) return go_stream3d<P, 8, 256, 4>(n1, K, M, x, b, y, partial, mode, st, nparts, sv, tpp, count);
   return go_stream3d<P, 16, 512>(n1, K, M, x, b, y, partial, mode, st, nparts, sv, tpp, count);
 }
 

@@ -444,7 +444,8 @@ def test_3d_sweep_zchain_bitwise(p, q, m, monkeypatch):
 
 @pytest.mark.parametrize("p,m", [(3, 20), (5, 12)])
 @pytest.mark.parametrize("env", [{"IGA2L_APPLY_STREAM": "0"}, {"IGA2L_STREAM_CFG": "1"}, {"IGA2L_STREAM_CFG": "2"},
-                                 {"IGA2L_STREAM_CFG": "3"}], ids=["tiled", "cfg1", "cfg2", "cfg3"])
+                                 {"IGA2L_STREAM_CFG": "3"}, {"IGA2L_STREAM_CFG": "4"}, {"IGA2L_STREAM_CFG": "5"}],
+                         ids=["tiled", "cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
 def test_3d_apply_variants(p, m, env, monkeypatch):
     """3D residual: the tiled kernel and every streaming configuration against the assembled operator,
     and the residual norm over exactly the partials each variant writes."""

@@ -32,8 +32,15 @@ for b in blocks:
             return 0.0
     tot = sum(f(r[i_s]) for r in data)
     print(b["name"][:90], "| samples", tot, "| sass", len(data), "| executed", sum(f(r[i_ex]) for r in data))
+    # per-reason stall columns (stall_barrier, stall_long_sb, ...), when the report's source page has them
+    reasons = [(i, h) for i, h in enumerate(hdr) if h.lower().startswith("stall_") and "not_issued" not in h.lower()]
     for r in sorted(data, key=lambda r: -f(r[i_s]))[:n]:
-        print(f"  {f(r[i_s]):7.0f} {100*f(r[i_s])/max(tot,1):5.1f}% {r[i_ex]:>9} {r[i_src][:70]}")
+        why = sorted(((f(r[i]), h) for i, h in reasons if f(r[i]) > 0), reverse=True)[:3]
+        print(f"  {f(r[i_s]):7.0f} {100*f(r[i_s])/max(tot,1):5.1f}% {r[i_ex]:>9} {r[i_src][:70]}",
+              " ".join(f"{h.split()[0]}={v:.0f}" for v, h in why))
+    if reasons:
+        tots = sorted(((sum(f(r[i]) for r in data), h) for i, h in reasons), reverse=True)
+        print("  stall reasons (all samples):", ", ".join(f"{h.split()[0]} {100*v/max(tot,1):.1f}%" for v, h in tots if v > 0))
     # executed instructions and stall samples by opcode (predicate guards stripped)
     ops = {}
     for r in data:
