@@ -87,8 +87,9 @@ struct S3 {
   static constexpr int WY = TY + 2 * P;
   static constexpr int NS = 4, NT = NT_, OY = TX * TY / NT;
   static constexpr int MINB = MB ? MB : (65536 / (NT * 128) > 0 ? 65536 / (NT * 128) : 1);
-  static constexpr int NDBL = NS * WY * ROW + 4 * WY * TX + 2 * TX * W + 2 * TY * W;
-  static constexpr size_t SMEM = sizeof(double) * (NDBL + 32) + 8 * NS;
+  static constexpr int NB = 4;                 // Pa/Pb ring: pass x of plane g + 1 may run beside pass y/z of plane g - 2
+  static constexpr int NDBL = NS * WY * ROW + 2 * NB * WY * TX + 2 * TX * W + 2 * TY * W;
+  static constexpr size_t SMEM = sizeof(double) * (NDBL + 32) + 8 * (NS + 2);
 };
 
 template <int P, int TY, int NT_, int MB = 0>
@@ -101,18 +102,21 @@ __global__ void __launch_bounds__(NT_, S3<P, TY, NT_, MB>::MINB)
   constexpr int TX = A::TX, W = A::W, ROW = A::ROW, WY = A::WY, NS = A::NS, NT = A::NT, OY = A::OY;
   extern __shared__ __align__(128) double sm[];
   double *stage = sm;                         // [NS][WY][ROW]  input plane windows
-  double *Pa = stage + NS * WY * ROW;         // [2][WY][TX]    K_x X
-  double *Pb = Pa + 2 * WY * TX;              // [2][WY][TX]    M_x X
-  double *ckx = Pb + 2 * WY * TX, *cmx = ckx + TX * W;   // band rows of the tile's x rows (boundary tiles)
+  double *Pa = stage + NS * WY * ROW;         // [NB][WY][TX]   K_x X
+  double *Pb = Pa + A::NB * WY * TX;          // [NB][WY][TX]   M_x X
+  double *ckx = Pb + A::NB * WY * TX, *cmx = ckx + TX * W;   // band rows of the tile's x rows (boundary tiles)
   double *cky = cmx + TX * W, *cmy = cky + TY * W;       // ... and y rows
   double *red = cmy + TY * W;                 // [32] block reduction scratch
   uint64_t *bar = reinterpret_cast<uint64_t *>(red + 32);
+  uint64_t *px = bar + NS;                    // [2] "pass x of plane n done by every warp" (n & 1), see the plane loop
   const int tid = threadIdx.x;
   const bool tv = tp.valid != 0;
   const int64_t plane = int64_t(n1) * n1;
   const int ntx = (n1 + TX - 1) / TX;
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
+    mbar_init(&px[0], NT / 32);
+    mbar_init(&px[1], NT / 32);
     mbar_fence_init();
   }
   double sq = 0.0;
@@ -158,19 +162,26 @@ __global__ void __launch_bounds__(NT_, S3<P, TY, NT_, MB>::MINB)
     for (int j = 0; j < W; ++j)
 #pragma unroll
       for (int o = 0; o < OY; ++o) acc[j][o] = 0.0;
-    for (int gi = gs; gi < ge; ++gi, ++it) {
-      const int s = it % NS, buf = it & 1;
-      const bool live = unsigned(gi) < unsigned(n1);
-      const int go = gi - P;                  // output plane completed by this input plane
-      const bool out = go >= zlo && go < zhi;
+    // Software pipeline without a CTA barrier: iteration gq runs pass x of plane gq (stage A) and then pass y / z of
+    // plane gq - 1 (stage B).  A warp arrives on px[n & 1] after its pass x of the CTA's n-th plane and waits for
+    // that phase only one stage later, so warps drift by up to one plane instead of meeting at every plane; the
+    // Pa/Pb ring of NB = 4 keeps the plane a leading warp writes (n + 1) apart from the one a trailing warp still
+    // reads (n - 2); a TMA stage is refilled after the wait that proves every warp has passed it in x.
+    for (int gq = gs; gq <= ge; ++gq) {
+      const int gi = gq - 1;                  // stage B's plane
+      const int go = gi - P;                  // output plane completed by input plane gi
+      const bool out = gq > gs && go >= zlo && go < zhi;
       double bv[OY];
 #pragma unroll
       for (int o = 0; o < OY; ++o) {          // prefetch b (used after the passes)
         const int gy = y0 + ly0 + o;
         bv[o] = (mode && out && gx < n1 && gy < n1) ? b[int64_t(go - zoff) * plane + int64_t(gy) * n1 + gx] : 0.0;
       }
-      double *pa = Pa + buf * WY * TX, *pb = Pb + buf * WY * TX;
-      if (live) {
+      if (gq < ge) {                          // ---- stage A: pass x of plane gq ----
+      const int s = it % NS;
+      double *pa = Pa + (it % A::NB) * WY * TX, *pb = Pb + (it % A::NB) * WY * TX;
+      if (unsigned(gq) < unsigned(n1)) {
+        const int gi = gq;
         mbar_wait(&bar[s], (phase >> s) & 1u);
         phase ^= 1u << s;
         const double *X = stage + s * WY * ROW;
@@ -219,8 +230,16 @@ __global__ void __launch_bounds__(NT_, S3<P, TY, NT_, MB>::MINB)
           *reinterpret_cast<double2 *>(pb + wy * TX + l0) = make_double2(m0, m1);
         }
       }
-      __syncthreads();                        // Pa/Pb ready; stage s consumed
-      if (gi + NS < ge) issue(gi + NS, s);
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&px[it & 1]);
+      ++it;
+      }
+      if (gq == gs) continue;                 // ---- stage B: pass y / z of plane gi = gq - 1 ----
+      const int itb = it - (gq < ge ? 2 : 1);  // ring position of plane gi
+      mbar_wait(&px[itb & 1], unsigned(itb >> 1) & 1u);   // Pa/Pb of plane gi ready; its stage consumed by every warp
+      if (gi + NS < ge) issue(gi + NS, itb % NS);
+      const bool live = unsigned(gi) < unsigned(n1);
+      const double *pa = Pa + (itb % A::NB) * WY * TX, *pb = Pb + (itb % A::NB) * WY * TX;
       double c[OY], e[OY];
 #pragma unroll
       for (int o = 0; o < OY; ++o) c[o] = e[o] = 0.0;
