@@ -2,7 +2,9 @@
 //
 // The grid is swept along its LAST axis (z).  A CTA owns a tile of the other axes and a
 // chunk of last-axis planes; every input plane window (tile + p-wide halo) is loaded by 1D TMA row copies
-// into a ring of shared-memory stages (mbarrier completion), contracted along the in-plane axes
+// into a ring of shared-memory stages (mbarrier completion; lane 0 of every warp issues its share of the rows),
+// contracted along the in-plane axes without a CTA barrier (pass x of plane g beside pass y / z of plane g - 1,
+// split-phase mbarriers between them)
 // (sum factorisation, band coefficients of Toeplitz tiles as constant-bank operands, reading A27), and
 // the last-axis contraction is accumulated in a REGISTER ring of 2p+1 partial output planes: input plane
 // g contributes tap 2p-j to output plane g-p+j, and output plane g-p is complete after plane g.
