@@ -461,3 +461,20 @@ def test_3d_apply_variants(p, m, env, monkeypatch):
     rn = ctx.residual_norm(cu(b), cu(x))
     assert abs(rn - np.linalg.norm(b - ref)) <= 1e-12 * np.linalg.norm(b - ref)
 
+
+@pytest.mark.parametrize("p", [1, 2, 4, 6, 7, 8])
+@pytest.mark.parametrize("m", [9, 37])
+def test_3d_apply_every_degree(p, m):
+    """The streaming 3D residual kernel is instantiated for p = 1..8 (the q-level residuals use p = 1, 2): every
+    degree the configs do not exercise against the oracle's Kronecker operator, one tile (m = 9) and several
+    tiles with ragged tails in x, y and the z segments (m = 37)."""
+    from oracle.kron import KronOperator
+    ctx = make_ctx(3, p, 1, m, 3 if p <= 4 else (5 if p <= 6 else 7), "exact", 1)
+    x, b = initial_guess(ctx.N, seed=4), random_rhs(ctx.N, seed=5)
+    y = torch.empty(ctx.N, dtype=torch.float64, device=DEV)
+    ctx.apply(cu(x), y)
+    ref = KronOperator(p, m, 3).apply(x)
+    assert np.abs(host(y) - ref).max() <= 1e-13 * np.abs(ref).max()
+    rn = ctx.residual_norm(cu(b), cu(x))
+    assert abs(rn - np.linalg.norm(b - ref)) <= 1e-12 * np.linalg.norm(b - ref)
+
