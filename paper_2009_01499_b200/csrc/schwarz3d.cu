@@ -1131,8 +1131,15 @@ bool try_schwarz3d_w(int p, int s, int64_t n1, const double *K, const double *M,
         launch_zc<P, S, GP, 4, 4, 1>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, L, zoff, tlo, thi, st, tp);
       else if (lv && lv[0] == '4')
         launch_zc<P, S, GP, 4, 4, 4>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, L, zoff, tlo, thi, st, tp);
-      else
+      else if (const char *nw = std::getenv("IGA2L_S3D_NW"); nw && nw[0] == '4')   // A/B: warps per CTA
         launch_zc<P, S, GP, 4, 4, (P == 5 ? 2 : 4)>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, L, zoff, tlo,
+                                                   thi, st, tp);
+      else if (nw && nw[0] == '1')
+        launch_zc<P, S, GP, 1, 16, (P == 5 ? 2 : 4)>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, L, zoff, tlo,
+                                                    thi, st, tp);
+      else   // 2 warps per CTA: C5's 26 block columns fill 13 CTAs (4 per CTA leave 2 of 28 warp slots idle): 140.2 vs
+             // 144.5 us per colour, same box (1 per CTA 143.2)
+        launch_zc<P, S, GP, 2, 8, (P == 5 ? 2 : 4)>(n1, K, M, V, lam, b, x, c0, c1, c2, D, nb0, nb1, nb2, L, zoff, tlo,
                                                    thi, st, tp);
       return true;
     }

@@ -427,6 +427,12 @@ def test_3d_sweep_zchain_bitwise(p, q, m, monkeypatch):
         ctx.sweep(b, x)
         outs["lv" + lv] = host(x)
     monkeypatch.delenv("IGA2L_S3D_CHAIN_LV", raising=False)
+    for nw in ("4", "1"):                        # warps per CTA A/B knob (default 2)
+        monkeypatch.setenv("IGA2L_S3D_NW", nw)
+        x = x0.clone()
+        ctx.sweep(b, x)
+        outs["nw" + nw] = host(x)
+    monkeypatch.delenv("IGA2L_S3D_NW", raising=False)
     buf = torch.zeros(ctx.N + 1, dtype=torch.float64, device=DEV)   # x at an 8-byte offset: v5's fallback
     buf[1:] = x0
     ctx.sweep(b, buf[1:])

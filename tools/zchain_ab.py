@@ -14,6 +14,11 @@ LS = os.environ.get("ZC_LS", "0,auto,2,3,4,6").split(",")
 
 
 def setL(L):
+    if L.endswith(":nw4") or L.endswith(":nw1"):   # "auto:nw4": 4 warps (blocks' segments) per CTA instead of 2
+        os.environ["IGA2L_S3D_NW"] = L[-1]
+        L = L[:-4]
+    else:
+        os.environ.pop("IGA2L_S3D_NW", None)
     if L == "auto":
         os.environ.pop("IGA2L_S3D_CHAIN", None)
     else:
@@ -57,8 +62,8 @@ def timing(name, reps, rounds=5):
     ncol = ctx.info().colours
     graphs, ref = {}, None
     for L in LS:
-        base, _, lv = L.partition("v")              # "4v1": L = 4 with 8-byte row loads
-        setL(base)
+        base, _, lv = L.partition(":")[0].partition("v")   # "4v1": L = 4 with 8-byte row loads
+        setL(base + (":" + L.partition(":")[2] if ":" in L else ""))
         os.environ["IGA2L_S3D_CHAIN_LV"] = lv or "0"
         ctx.sweep(b, x)
         g = torch.cuda.CUDAGraph()
@@ -74,6 +79,7 @@ def timing(name, reps, rounds=5):
         graphs[L] = g
     os.environ.pop("IGA2L_S3D_CHAIN", None)
     os.environ.pop("IGA2L_S3D_CHAIN_LV", None)
+    os.environ.pop("IGA2L_S3D_NW", None)
     times = {L: [] for L in LS}
     for _ in range(rounds):
         for L in LS:
